@@ -1,0 +1,285 @@
+#!/usr/bin/env python
+"""Benchmark: uBLR compression time on B200 (BASELINE.json metric).
+
+    python bench.py [--config c2] [--gpus N --steps K --warmup W] [--impl reference]
+
+One step = one full compression (phases I+II+III of
+ref/reconstruction.py:498-583: tagging plan, test-matrix generation, tagged
+sketch, per-block QR, coupling, near field) of the chosen BASELINE config.
+`value` = compression time in seconds with the operator's inputs resident in
+HBM (device-timed, max over ranks); `e2e` = the same through the public API
+from HOST arrays (operator built from host coordinates / matrix inside the
+timed region, compressed representation copied back to host).
+
+Configs 1-4 do not shard: with --gpus N every rank compresses its own replica
+("replicas only"). `--impl reference` times the CPU port of the
+reference algorithm (oracle/, numpy + OpenBLAS on all host cores).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "BLR compression time (s)"
+FP64_PEAK_TFLOPS = 37.13  # measured DMMA m8n8k4 burst peak, profiles/fp64_peak_r01.txt
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def flush_l2(buf):
+    buf.add_(1.0)  # 256 MB write > 126 MB L2
+
+
+def run_reference(args, rank, world):
+    """CPU baseline: the oracle port of the reference pipeline on host cores."""
+    if rank != 0:
+        return
+    import oracle as O
+    from paper_2501_05528_b200 import workloads as W
+    wl = W.build(args.config, device_ops=False)
+    cores = os.cpu_count() or 1
+    bx = O.partition(wl.points.coords, wl.b)
+    if wl.kernel == "dense-synthetic":
+        op = O.Dense(wl.matrix)
+    elif wl.n <= 8192:
+        kind = "log" if wl.kernel.startswith("-log") else "inv"
+        diag = -np.log(0.5 / round(wl.n ** 0.5)) if kind == "log" else 2.0 * round(wl.n ** 0.5)
+        op = O.Dense(O.kernel_block(wl.points.coords, np.arange(wl.n), np.arange(wl.n), kind, diag))
+    else:
+        raise SystemExit(json.dumps({"impl": "reference", "unavailable":
+                                     f"CPU port of {args.config} exceeds the bench time budget (see DESIGN.md)"}))
+    times = []
+    for _ in range(args.warmup):
+        O.compress(op, bx, wl.k, wl.method, p=wl.p, stream=O.Stream(7), compute_error=False)
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.compress(op, bx, wl.k, wl.method, p=wl.p, stream=O.Stream(7), compute_error=False)
+        times.append(time.perf_counter() - t0)
+    v = float(np.mean(times))
+    print(json.dumps({
+        "metric": METRIC, "value": v, "unit": "s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": {**wl.describe(), "parallelism": "cpu", "replicas": 1},
+        "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "port",
+                         "sample": f"full {args.config} compression (oracle/ numpy port, OpenBLAS threads={cores})"},
+        "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def cpu_baseline(wl, budget_s=12.0):
+    """Bounded CPU sample of the same workload with the oracle port."""
+    import oracle as O
+    bx = O.partition(wl.points.coords, wl.b)
+    if wl.kernel == "dense-synthetic":
+        op = O.Dense(wl.matrix)
+    else:
+        kind = "log" if wl.kernel.startswith("-log") else "inv"
+        per = round(wl.n ** 0.5)
+        diag = -np.log(0.5 / per) if kind == "log" else 2.0 * per
+        if wl.n > 8192:
+            return None
+        op = O.Dense(O.kernel_block(wl.points.coords, np.arange(wl.n), np.arange(wl.n), kind, diag))
+    times = []
+    t_end = time.perf_counter() + budget_s
+    while time.perf_counter() < t_end or len(times) < 2:
+        t0 = time.perf_counter()
+        O.compress(op, bx, wl.k, wl.method, p=wl.p, stream=O.Stream(7), compute_error=False)
+        times.append(time.perf_counter() - t0)
+    return {"value": float(np.median(times)), "unit": "s", "cores": os.cpu_count() or 1, "kind": "port",
+            "sample": f"{len(times)} full {wl.name} compressions with the oracle numpy port "
+                      f"(dense operator prebuilt, OpenBLAS on all cores)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank, world, local = dist_env()
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2501_05528_b200 as P
+    from paper_2501_05528_b200 import _lib
+    from paper_2501_05528_b200 import workloads as W
+
+    wl = W.build(args.config)
+    flops = W.algorithmic_flops(wl)
+    dev = torch.device("cuda", local)
+    l2buf = torch.zeros(32 * 1024 * 1024, dtype=torch.float64, device=dev)
+
+    def step():
+        return P.compress(wl.op, wl.tess, wl.k, wl.method, p=wl.p, stream=P.RandomStream(W.COMPRESS_SEED),
+                          compute_error=False)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    # --- timed region: device-resident inputs -------------------------------
+    _lib.instrument(True)
+    launches0 = _lib.launch_count
+    step_ms = []
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            flush_l2(l2buf)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            rep, report = step()
+            e1.record()
+            torch.cuda.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+    ev = _lib.event_times()
+    _lib.instrument(False)
+    launches = (_lib.launch_count - launches0) // args.steps
+    t_step = float(np.mean(step_ms)) / 1e3
+    if world > 1:
+        t = torch.tensor([t_step], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_step = float(t.item())
+
+    # --- e2e: host buffers through the public API --------------------------
+    e2e_times = []
+    h2d = d2h = 0
+    for _ in range(max(3, args.steps // 2)):
+        flush_l2(l2buf)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        if wl.matrix is not None:
+            op = P.DenseOperator(wl.matrix)                       # H2D of A
+            h2d = wl.matrix.nbytes
+        else:
+            op = P.KernelOperator(wl.points, wl.op.kind, wl.op.diag)  # H2D of coordinates
+            h2d = wl.points.coords.nbytes
+        rep, report = P.compress(op, wl.tess, wl.k, wl.method, p=wl.p, stream=P.RandomStream(W.COMPRESS_SEED),
+                                 compute_error=False)
+        U, V, C, B = (rep.U.cpu(), rep.V.cpu(), rep.core_d.cpu(), rep.B_d.cpu())  # D2H of the result
+        torch.cuda.synchronize()
+        e2e_times.append(time.perf_counter() - t0)
+        d2h = sum(x.numel() * 8 for x in (U, V, C, B))
+    e2e = float(np.median(e2e_times))
+    if world > 1:
+        t = torch.tensor([e2e], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e = float(t.item())
+
+    # --- roofline of the dominant kernel -------------------------------------
+    sk_name = "ublr_sketch_tagged_pair" if "ublr_sketch_tagged_pair" in ev else "ublr_sketch_tagged"
+    sk_ms = float(np.mean(ev.get(sk_name, [float("nan")])))
+    per_step_calls = max(1, len(ev.get(sk_name, [])) // args.steps)
+    sk_flops = flops.get("sketch", float("nan")) / per_step_calls
+    achieved = sk_flops / (sk_ms * 1e-3) / 1e12
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(tfile):
+        traffic = json.load(open(tfile)).get("dram_bytes_per_launch")
+    kernel_ms = {k: float(np.sum(v)) / args.steps for k, v in ev.items()}
+
+    if rank == 0:
+        cpu = None if (args.no_cpu_baseline or world > 1) else cpu_baseline(W.build(args.config, device_ops=False))
+        line = {
+            "metric": METRIC, "value": t_step, "unit": "s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {**wl.describe(), "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "l2": "flushed between timed steps (256 MB write)"},
+            "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": int(launches),
+            "roofline": {"kernel": "k_sketch_tagged (Kronecker-restructured tagged sketch)", "bound": "fp64",
+                         "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+                         "peak_source": "measured DMMA m8n8k4 (profiles/fp64_peak_r01.txt); MEASURED_PEAKS.json "
+                                        "has no fp64 entry",
+                         "algorithmic_flops_per_launch": sk_flops, "avg_launch_ms": sk_ms},
+            "kernel_ms_per_step": kernel_ms,
+            "phase_s": report.times_s,
+            "clocks": clocks.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,141 @@
+/* ublr_b200.h — C ABI of the B200 (sm_100a) uBLR compression hot path.
+ *
+ * Drop-in boundary for the matrix-free uniform-BLR compressor of
+ * arXiv 2501.05528 (reference: /root/reference/pkg/src/ublr, "ref/" below).
+ * The reference's compressor entry points stay Python
+ * (ref/reconstruction.py:498-687); they call these functions through ctypes
+ * (paper_2501_05528_b200/_lib.py). Every function:
+ *   - takes DEVICE pointers (fp64 / int32 / int64), explicit sizes and a
+ *     cudaStream_t (passed as void*), and allocates nothing itself unless a
+ *     workspace argument says so;
+ *   - returns UBLR_OK (0) or a negative status; ublr_last_error() gives the
+ *     message. The Python layer maps UBLR_ERR_VALUE -> ValueError,
+ *     UBLR_ERR_NUMERIC -> numpy.linalg.LinAlgError, UBLR_ERR_CUDA -> RuntimeError.
+ *
+ * Layout conventions (see DESIGN.md §Data layout):
+ *   - points are renumbered block-contiguously: block i owns permuted rows
+ *     [off[i], off[i+1]); perm[p] is the original index of permuted row p;
+ *   - dense blocks are row-major; sketches Y/Z are N x s row-major in
+ *     permuted row order; bases U/V are N x k row-major (block i rows,
+ *     columns [0, k_i)); the core is K x K row-major with K = sum k_i;
+ *   - near-field blocks B_ij are stored in neighbour-CSR order (which is the
+ *     reference's sorted (i, j) order), block p at b_off[p], m_i x m_j
+ *     row-major.
+ */
+#ifndef UBLR_B200_H
+#define UBLR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  UBLR_OK = 0,
+  UBLR_ERR_VALUE = -1,   /* bad arguments / configuration  -> ValueError      */
+  UBLR_ERR_CUDA = -2,    /* CUDA runtime failure           -> RuntimeError    */
+  UBLR_ERR_NUMERIC = -3, /* numerical failure              -> LinAlgError     */
+  UBLR_ERR_RETRY = -4    /* internal: caller should retry with more workspace */
+};
+
+/* Operator kinds for the on-the-fly operator tiles. */
+enum { UBLR_OP_DENSE = 0, UBLR_OP_LOG = 1, UBLR_OP_INV = 2 };
+
+/* Operator descriptor: the black-box A of ref/operators.py:24-35, as the
+ * GPU sees it. DENSE: A (original order, row-major, lda), gathered through
+ * perm; transpose != 0 means A^T. LOG: A(x,y) = -log|x-y|; INV: 1/|x-y|;
+ * the diagonal (same original index) takes `diag`. coords are permuted,
+ * structure-of-arrays: coords[a*n + p]. */
+typedef struct {
+  int32_t kind;
+  int32_t dim;
+  int32_t transpose;
+  int32_t pad_;
+  const double* A;
+  int64_t lda;
+  const int32_t* perm;
+  const double* coords;
+  int64_t n;
+  double diag;
+} ublr_op_t;
+
+/* One Gaussian stream of the reference's RandomStream (ref/linalg.py:14-52):
+ * numpy Philox4x64-10 with 128-bit key (SeedSequence-derived, host side),
+ * counter starting at 0, `standard_normal` ziggurat, row-major fill.
+ * Normal n goes to out[out_offset + rowmap[n / cols] * ld + n % cols]
+ * (rowmap == NULL means identity). */
+typedef struct {
+  uint64_t key0, key1;
+  int64_t count;
+  int64_t cols;
+  int64_t ld;
+  int64_t out_offset;
+  const int32_t* rowmap;
+} ublr_rng_stream_t;
+
+const char* ublr_last_error(void);
+int ublr_version(void);
+int ublr_device_check(void);
+
+/* K1 — ref/linalg.py:38-52 (`RandomStream.normal` / `gaussian`), called at
+ * ref/bases.py:97-98, :163-168, :229-230 and ref/reconstruction.py:405.
+ * Bit-compatible with numpy. `streams` is a DEVICE array. Workspace bytes
+ * from ublr_rng_workspace_bytes. */
+int64_t ublr_rng_workspace_bytes(const int64_t* counts, int n_streams);
+int ublr_rng_normals(const ublr_rng_stream_t* streams_dev, const int64_t* counts_host, int n_streams,
+                     double* out, void* workspace, int64_t workspace_bytes, void* stream);
+
+/* K2/K3 — tagged sketch, ref/bases.py:163-172 (assemble_tagging_test_matrix +
+ * op.apply / op.apply_adjoint). Y[:, c*gc+q] for block-row i accumulates
+ * sum_j T[j,c] * (A_ij X_j)[:, q] (Kronecker-restructured: each A tile meets
+ * its own test block once). X is N x gc (permuted rows, ld_x); T is b x ell.
+ * Computes Y = A Omega into y (N x ell*gc, ld_y). */
+int ublr_sketch_tagged(const ublr_op_t* op, const int32_t* off, int b, const double* T, int ell,
+                       const double* X, int64_t ld_x, int gc, double* Y, int64_t ld_y, void* stream);
+/* Symmetric operator: [Y | Z] = A [Omega | Psi] in one pass over A. */
+int ublr_sketch_tagged_pair(const ublr_op_t* op, const int32_t* off, int b, const double* T, int ell,
+                            const double* G, const double* H, int64_t ld_x, int gc,
+                            double* Y, double* Z, int64_t ld_y, void* stream);
+
+/* Generic operator apply (ref/operators.py:48-52 and every op.apply call of
+ * the pipeline): out (N x w, permuted rows, ld_o) = A X (N x w, ld_x). */
+int ublr_apply(const ublr_op_t* op, const double* X, int64_t ld_x, int w, double* out, int64_t ld_o,
+               void* stream);
+
+/* K4 — combine + QR: ref/bases.py:174-189, :207-210 with ref/linalg.py:55-69
+ * and ref/bases.py:78-83. Per block i: sample S_i (m_i x k) is
+ *   mode 0 (tag):   sum_c z[i,c] * Y[rows_i, c*gc + q], q < k;
+ *   mode 1 (cols):  Y[rows_i, col0[i] + q]            (naive, bn samples);
+ *   mode + 2:       plain QR (no identity shortcut when k >= m_i; col_basis).
+ * Q = first k_i columns of the unpivoted Householder QR (LAPACK dlarfg
+ * convention) of S_i, or the identity when k >= m_i. Writes U (N x ldu). */
+int ublr_block_qr(const double* Y, int64_t ld_y, int mode, const double* z, int ell, int gc,
+                  const int32_t* col0, const int32_t* off, int b, int k, double* U, int64_t ld_u,
+                  void* stream, int m_max);
+
+/* K6 — coupling (ref/reconstruction.py:185-198, direct_core):
+ * core[roff[i]:, roff[j]:] = U_i^T A_ij V_j for all (i, j). */
+int ublr_coupling(const ublr_op_t* op, const int32_t* off, const int32_t* roff, int b, int k,
+                  const double* U, const double* V, int64_t ld_uv, double* core, int64_t ld_c,
+                  void* stream, int m_max);
+
+/* K7 — near field with the colour-probe semantics of
+ * ref/reconstruction.py:201-244: for each near pair p = (i, j),
+ *   B_ij[:, q] = sum_{j' in colour(j), q < m_j'} (A_ij' - U_i C_ij' V_j'^T)[:, q]
+ * (the same-colour far residuals of block row i leak in).
+ * Colour members in CSR (cptr, cidx); pairs given by (pair_i[p], nidx[p]);
+ * B block p at B + b_off[p], m_i x m_j row-major. Workspace:
+ * ublr_nearfield_workspace_bytes(n_pairs, k, m_max). */
+int64_t ublr_nearfield_workspace_bytes(int n_pairs, int k, int m_max);
+int ublr_nearfield_colour(const ublr_op_t* op, const int32_t* off, const int32_t* roff, int b, int k,
+                          const double* U, const double* V, int64_t ld_uv, const double* core,
+                          int64_t ld_c, const int32_t* colour, const int32_t* cptr, const int32_t* cidx,
+                          int n_colours, int m_max, const int32_t* pair_i, const int32_t* nidx, int n_pairs,
+                          const int64_t* b_off, double* B, void* workspace, int64_t workspace_bytes,
+                          void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* UBLR_B200_H */

@@ -1,0 +1,151 @@
+"""ctypes binding of the C-ABI library libublr_b200.so (include/ublr_b200.h).
+
+The product path has no CPU fallback: if the library is missing or no sm_100
+device is present, every compute entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libublr_b200.so")
+
+UBLR_OK, UBLR_ERR_VALUE, UBLR_ERR_CUDA, UBLR_ERR_NUMERIC = 0, -1, -2, -3
+OP_DENSE, OP_LOG, OP_INV = 0, 1, 2
+
+P = C.c_void_p
+I32 = C.c_int32
+I64 = C.c_int64
+INT = C.c_int
+
+
+class OpDesc(C.Structure):
+    _fields_ = [("kind", I32), ("dim", I32), ("transpose", I32), ("pad_", I32),
+                ("A", P), ("lda", I64), ("perm", P), ("coords", P), ("n", I64), ("diag", C.c_double)]
+
+
+class RngStreamDesc(C.Structure):
+    _fields_ = [("key0", C.c_uint64), ("key1", C.c_uint64), ("count", I64), ("cols", I64),
+                ("ld", I64), ("out_offset", I64), ("rowmap", P)]
+
+
+RNG_STREAM_DTYPE = np.dtype([("key0", "<u8"), ("key1", "<u8"), ("count", "<i8"), ("cols", "<i8"),
+                             ("ld", "<i8"), ("out_offset", "<i8"), ("rowmap", "<u8")])
+assert RNG_STREAM_DTYPE.itemsize == C.sizeof(RngStreamDesc)
+
+# name -> (restype, argtypes); must cover every function in include/ublr_b200.h
+SIGNATURES = {
+    "ublr_last_error": (C.c_char_p, []),
+    "ublr_version": (INT, []),
+    "ublr_device_check": (INT, []),
+    "ublr_rng_workspace_bytes": (I64, [P, INT]),
+    "ublr_rng_normals": (INT, [P, P, INT, P, P, I64, P]),
+    "ublr_sketch_tagged": (INT, [C.POINTER(OpDesc), P, INT, P, INT, P, I64, INT, P, I64, P]),
+    "ublr_sketch_tagged_pair": (INT, [C.POINTER(OpDesc), P, INT, P, INT, P, P, I64, INT, P, P, I64, P]),
+    "ublr_apply": (INT, [C.POINTER(OpDesc), P, I64, INT, P, I64, P]),
+    "ublr_block_qr": (INT, [P, I64, INT, P, INT, INT, P, P, INT, INT, P, I64, P, INT]),
+    "ublr_coupling": (INT, [C.POINTER(OpDesc), P, P, INT, INT, P, P, I64, P, I64, P, INT]),
+    "ublr_nearfield_workspace_bytes": (I64, [INT, INT, INT]),
+    "ublr_nearfield_colour": (INT, [C.POINTER(OpDesc), P, P, INT, INT, P, P, I64, P, I64, P, P, P, INT, INT,
+                                    P, P, INT, P, P, P, I64, P]),
+}
+
+_lib = None
+
+
+def load():
+    """Load the library (no GPU needed); raise ImportError if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built; run `python -m paper_2501_05528_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+class UblrCudaError(RuntimeError):
+    pass
+
+
+def check(rc: int, what: str = ""):
+    if rc == UBLR_OK:
+        return
+    msg = load().ublr_last_error().decode(errors="replace")
+    text = f"{what}: {msg}" if what else msg
+    if rc == UBLR_ERR_VALUE:
+        raise ValueError(text)
+    if rc == UBLR_ERR_NUMERIC:
+        raise np.linalg.LinAlgError(text)
+    raise UblrCudaError(text)
+
+
+# kernels each C-ABI entry point launches (for bench.py's `gpu_launches`)
+LAUNCHES = {"ublr_rng_normals": 7, "ublr_sketch_tagged": 1, "ublr_sketch_tagged_pair": 1, "ublr_apply": 1,
+            "ublr_block_qr": 1, "ublr_coupling": 1, "ublr_nearfield_colour": 2}
+launch_count = 0
+_events = None  # name -> list of (start, end) CUDA events when instrumentation is on
+
+
+def instrument(enable: bool = True):
+    """Record CUDA events around every C-ABI launch (bench.py roofline)."""
+    global _events
+    _events = {} if enable else None
+
+
+def event_times():
+    """{name: [ms per call]} of the instrumented calls (synchronises)."""
+    import torch
+    torch.cuda.synchronize()
+    return {k: [a.elapsed_time(b) for a, b in v] for k, v in (_events or {}).items()}
+
+
+def call(name: str, *args):
+    """Call a status-returning C-ABI function and raise on failure."""
+    global launch_count
+    launch_count += LAUNCHES.get(name, 0)
+    if _events is not None:
+        import torch
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        check(getattr(load(), name)(*args), name)
+        b.record()
+        _events.setdefault(name, []).append((a, b))
+        return
+    check(getattr(load(), name)(*args), name)
+
+
+_device_ok = False
+
+
+def require_device():
+    """The CUDA path is the only path: fail loudly without an sm_100 GPU."""
+    global _device_ok
+    if _device_ok:
+        return
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2501_05528_b200 needs a CUDA device (B200, sm_100a); no CPU fallback")
+    torch.cuda.init()
+    call("ublr_device_check")
+    _device_ok = True
+
+
+def ptr(t) -> int:
+    """Device pointer of a torch tensor (or 0 for None)."""
+    return 0 if t is None else int(t.data_ptr())
+
+
+def stream_handle():
+    import torch
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)

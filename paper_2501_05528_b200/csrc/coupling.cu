@@ -1,0 +1,378 @@
+// K6 / K7 — type-A reconstruction (ref/reconstruction.py:185-244).
+//
+// K6 `ublr_coupling`: direct_core (ref/reconstruction.py:185-198) pushes the
+// K columns of blockdiag(V) through A and projects on U: C = U^T (A V). The
+// block-diagonal structure is used directly: C_ij = U_i^T (A_ij V_j), one
+// CTA per (i, j), with the A_ij tile generated on the fly (2 m^2 k + 2 m k^2
+// flops per pair instead of a dense N x N x K product).
+//
+// K7 `ublr_nearfield_colour`: structured_identity_discrepancy
+// (ref/reconstruction.py:201-244) probes A with one identity per colour, so
+// the extracted near block of pair (i, j) is
+//   B_ij[:, q] = sum_{j' in colour(j), q < m_j'} (A_ij' - U_i C_ij' V_j'^T)[:, q]
+// — the true near residual plus the same-colour far residuals of block row i
+// (SURVEY.md F11). Two kernels: S_p = sum_j' C_ij' V_j'^T (k x m, DMMA) per
+// pair, then B_p = sum_j' A_ij' - U_i S_p with A generated on the fly.
+#include "common.cuh"
+#include "optile.cuh"
+
+namespace ublr {
+namespace {
+
+constexpr int CP_THREADS = 256;
+constexpr int CP_BK = 16;
+
+// ---------------------------------------------------------------- coupling
+// RW = rows per warp (8 warps cover 8*RW rows >= m_i); NJ = 8-col groups (k <= 8 NJ)
+template <int KIND, int RW, int NJ>
+__global__ void __launch_bounds__(CP_THREADS) k_coupling(ublr_op_t op, const int32_t* __restrict__ off,
+                                                         const int32_t* __restrict__ roff, int k,
+                                                         const double* __restrict__ U,
+                                                         const double* __restrict__ V, int64_t lduv,
+                                                         double* __restrict__ core, int64_t ldc) {
+  constexpr int MR = 8 * RW;          // max rows of block i
+  constexpr int SA = MR + 4;          // k-major A tile stride
+  constexpr int SB = 8 * NJ + 4;      // V tile stride
+  constexpr int RI = RW / 8;          // 8-row groups per warp
+  constexpr int SW = 8 * NJ + 1;
+  __shared__ LogTables lt;
+  extern __shared__ double dsm[];
+  double (*As)[CP_BK][SA] = reinterpret_cast<double (*)[CP_BK][SA]>(dsm);
+  double (*Bs)[CP_BK][SB] = reinterpret_cast<double (*)[CP_BK][SB]>(dsm + 2 * CP_BK * SA);
+  double (*Ws)[SW] = reinterpret_cast<double (*)[SW]>(dsm);  // aliases As/Bs after the k-loop
+  if (KIND == UBLR_OP_LOG) init_log_tables(&lt);
+
+  const int j = blockIdx.x, i = blockIdx.y;
+  const int ri0 = off[i], mi = off[i + 1] - ri0;
+  const int cj0 = off[j], mj = off[j + 1] - cj0;
+  const int ki = roff[i + 1] - roff[i], kj = roff[j + 1] - roff[j];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+
+  // generation: rows r = tid % MR .. (MR <= 256), kk slots
+  constexpr int GR = (MR < CP_THREADS) ? MR : CP_THREADS;
+  constexpr int GK = CP_THREADS / GR;   // kk lanes
+  const int grow = tid % GR;
+  const int gk = tid / GR;
+  RowPoint rp[(MR + CP_THREADS - 1) / CP_THREADS];
+#pragma unroll
+  for (int s = 0; s < (MR + CP_THREADS - 1) / CP_THREADS; ++s) {
+    int r = grow + s * CP_THREADS;
+    rp[s] = load_row_point(op, ri0 + r, r < mi);
+  }
+
+  double acc[RI][NJ][2];
+#pragma unroll
+  for (int a = 0; a < RI; ++a)
+#pragma unroll
+    for (int b = 0; b < NJ; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  __syncthreads();
+
+  auto stage = [&](int buf, int q0) {
+#pragma unroll
+    for (int s = 0; s < (MR + CP_THREADS - 1) / CP_THREADS; ++s) {
+      for (int kk = gk; kk < CP_BK; kk += GK) {
+        int q = q0 + kk;
+        double v = 0.0;
+        if (rp[s].p >= 0 && q < mj) v = op_entry<KIND>(op, rp[s], cj0 + q, &lt);
+        As[buf][kk][grow + s * CP_THREADS] = v;
+      }
+    }
+    for (int e = tid; e < CP_BK * 8 * NJ; e += CP_THREADS) {
+      int kk = e / (8 * NJ), c = e - kk * (8 * NJ);
+      int q = q0 + kk;
+      bool ok = q < mj && c < kj;
+      cp_async8(&Bs[buf][kk][c], ok ? (const void*)(V + (int64_t)(cj0 + q) * lduv + c) : (const void*)V, ok);
+    }
+    cp_async_commit();
+  };
+
+  const int nk = (mj + CP_BK - 1) / CP_BK;
+  stage(0, 0);
+  for (int ks = 0; ks < nk; ++ks) {
+    int buf = ks & 1;
+    cp_async_wait<0>();
+    __syncthreads();
+    if (ks + 1 < nk) stage(buf ^ 1, (ks + 1) * CP_BK);
+#pragma unroll
+    for (int k4 = 0; k4 < CP_BK; k4 += 4) {
+      double a[RI], bb[NJ];
+#pragma unroll
+      for (int s = 0; s < RI; ++s) a[s] = As[buf][k4 + t][warp * RW + s * 8 + g];
+#pragma unroll
+      for (int c = 0; c < NJ; ++c) bb[c] = Bs[buf][k4 + t][c * 8 + g];
+#pragma unroll
+      for (int s = 0; s < RI; ++s)
+#pragma unroll
+        for (int c = 0; c < NJ; ++c) mma8x8x4(acc[s][c][0], acc[s][c][1], a[s], bb[c]);
+    }
+  }
+  // W -> shared (aliases the staging buffers)
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < RI; ++s)
+#pragma unroll
+    for (int c = 0; c < NJ; ++c) {
+      int r = warp * RW + s * 8 + g;
+      Ws[r][c * 8 + 2 * t] = acc[s][c][0];
+      Ws[r][c * 8 + 2 * t + 1] = acc[s][c][1];
+    }
+  __syncthreads();
+  // C_ij = U_i^T W (ki x kj): thread per output, fp64 FMA over the mi rows
+  const double* Ui = U + (int64_t)ri0 * lduv;
+  for (int e = tid; e < ki * kj; e += CP_THREADS) {
+    int a = e / kj, c = e - a * kj;
+    double s = 0.0;
+    for (int r = 0; r < mi; ++r) s = fma(__ldg(&Ui[(int64_t)r * lduv + a]), Ws[r][c], s);
+    core[(int64_t)(roff[i] + a) * ldc + roff[j] + c] = s;
+  }
+}
+
+// ------------------------------------------------------- near field: S_p
+// S_p (k x m_max) = sum_{j' in colour(j)} C_{i j'} V_{j'}^T, columns q < m_j'.
+// One CTA per near pair; 8 warps split the m_max columns, each warp holds
+// all k rows x (m_max / 8) columns of accumulators.
+template <int NA, int NQ>
+__global__ void __launch_bounds__(CP_THREADS) k_nf_S(const int32_t* __restrict__ off,
+                                                     const int32_t* __restrict__ roff,
+                                                     const double* __restrict__ V, int64_t lduv,
+                                                     const double* __restrict__ core, int64_t ldc,
+                                                     const int32_t* __restrict__ colour,
+                                                     const int32_t* __restrict__ cptr,
+                                                     const int32_t* __restrict__ cidx,
+                                                     const int32_t* __restrict__ pair_i,
+                                                     const int32_t* __restrict__ nidx, int m_max,
+                                                     double* __restrict__ S) {
+  // NA: 8-row groups of k (k <= 8 NA); NQ: 8-col groups per warp (m_max <= 64 NQ)
+  const int p = blockIdx.x;
+  const int i = pair_i[p];
+  const int c = colour[nidx[p]];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int ki = roff[i + 1] - roff[i];
+  double acc[NA][NQ][2];
+#pragma unroll
+  for (int a = 0; a < NA; ++a)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) acc[a][q][0] = acc[a][q][1] = 0.0;
+  const double* Crow = core + (int64_t)roff[i] * ldc;
+  for (int mem = cptr[c]; mem < cptr[c + 1]; ++mem) {
+    const int jp = cidx[mem];
+    const int kj = roff[jp + 1] - roff[jp];
+    const int mj = off[jp + 1] - off[jp];
+    const double* Vj = V + (int64_t)off[jp] * lduv;
+    const double* Cij = Crow + roff[jp];
+    for (int e0 = 0; e0 < kj; e0 += 4) {
+      int e = e0 + t;
+      double a[NA], bb[NQ];
+#pragma unroll
+      for (int s = 0; s < NA; ++s) {
+        int row = s * 8 + g;
+        a[s] = (row < ki && e < kj) ? __ldg(&Cij[(int64_t)row * ldc + e]) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        int col = (warp * NQ + q) * 8 + g;
+        bb[q] = (col < mj && e < kj) ? __ldg(&Vj[(int64_t)col * lduv + e]) : 0.0;
+      }
+#pragma unroll
+      for (int s = 0; s < NA; ++s)
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) mma8x8x4(acc[s][q][0], acc[s][q][1], a[s], bb[q]);
+    }
+  }
+  double* Sp = S + (int64_t)p * (8 * NA) * m_max;
+#pragma unroll
+  for (int s = 0; s < NA; ++s)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      int row = s * 8 + g;
+      int col = (warp * NQ + q) * 8 + 2 * t;
+      if (col < m_max) Sp[(int64_t)row * m_max + col] = acc[s][q][0];
+      if (col + 1 < m_max) Sp[(int64_t)row * m_max + col + 1] = acc[s][q][1];
+    }
+}
+
+// ------------------------------------------------------- near field: B_p
+// CTA per (pair p, tile of 32 rows): thread owns column q = tid % QW and
+// rows tid / QW + s * (256 / QW).
+template <int KIND>
+__global__ void __launch_bounds__(CP_THREADS) k_nf_B(ublr_op_t op, const int32_t* __restrict__ off,
+                                                     const int32_t* __restrict__ roff, int KA,
+                                                     const double* __restrict__ U, int64_t lduv,
+                                                     const int32_t* __restrict__ colour,
+                                                     const int32_t* __restrict__ cptr,
+                                                     const int32_t* __restrict__ cidx,
+                                                     const int32_t* __restrict__ pair_i,
+                                                     const int32_t* __restrict__ nidx,
+                                                     const int64_t* __restrict__ b_off, int m_max,
+                                                     const double* __restrict__ S, double* __restrict__ B) {
+  constexpr int RT = 32;
+  __shared__ LogTables lt;
+  __shared__ double rowc[3][RT];
+  __shared__ int rowo[RT];
+  if (KIND == UBLR_OP_LOG) init_log_tables(&lt);
+  const int p = blockIdx.x;
+  const int i = pair_i[p];
+  const int jn = nidx[p];
+  const int c = colour[jn];
+  const int ri0 = off[i], mi = off[i + 1] - ri0;
+  const int mjn = off[jn + 1] - off[jn];
+  const int r0 = blockIdx.y * RT;
+  if (r0 >= mi) return;
+  const int ki = roff[i + 1] - roff[i];
+  const int tid = threadIdx.x;
+  const int QW = m_max < CP_THREADS ? m_max : CP_THREADS;  // m_max <= 256 enforced by host
+  const int q = tid % QW;
+  const int rstep = CP_THREADS / QW;
+  const int r_first = tid / QW;
+  const bool active = tid < rstep * QW;
+  if (tid < RT) {
+    int p_row = ri0 + r0 + tid;
+    bool ok = r0 + tid < mi;
+    if (KIND == UBLR_OP_DENSE) {
+      rowo[tid] = ok ? op.perm[p_row] : 0;
+    } else {
+      rowo[tid] = ok ? p_row : -1;
+      for (int a = 0; a < 3; ++a) rowc[a][tid] = (ok && a < op.dim) ? op.coords[(int64_t)a * op.n + p_row] : 0.0;
+    }
+  }
+  __syncthreads();
+  if (!active) return;
+  constexpr int MAXS = RT;  // rows per thread upper bound (QW >= 8 assumed)
+  double asum[MAXS];
+  const int nrows = (RT + rstep - 1) / rstep;
+#pragma unroll
+  for (int s = 0; s < MAXS; ++s) asum[s] = 0.0;
+  for (int mem = cptr[c]; mem < cptr[c + 1]; ++mem) {
+    const int jp = cidx[mem];
+    const int mj = off[jp + 1] - off[jp];
+    if (q >= mj) continue;
+    const int col = off[jp] + q;
+    // column point
+    RowPoint cp = load_row_point(op, col, true);
+#pragma unroll
+    for (int s = 0; s < MAXS; ++s) {
+      if (s >= nrows) break;
+      int r = r_first + s * rstep;
+      if (r >= RT || r0 + r >= mi) continue;
+      double v;
+      if (KIND == UBLR_OP_DENSE) {
+        v = op.transpose ? op.A[(int64_t)cp.orig * op.lda + rowo[r]] : op.A[(int64_t)rowo[r] * op.lda + cp.orig];
+      } else {
+        if (rowo[r] == col) {
+          v = op.diag;
+        } else {
+          double d = rowc[0][r] - cp.x0;
+          double r2 = d * d;
+          if (op.dim > 1) { d = rowc[1][r] - cp.x1; r2 = fma(d, d, r2); }
+          if (op.dim > 2) { d = rowc[2][r] - cp.x2; r2 = fma(d, d, r2); }
+          v = (KIND == UBLR_OP_LOG) ? -0.5 * fast_log(r2, &lt) : rsqrt(r2);
+        }
+      }
+      asum[s] += v;
+    }
+  }
+  if (q >= mjn) return;
+  const double* Sp = S + (int64_t)p * KA * m_max;
+  double* Bp = B + b_off[p];
+  for (int s = 0; s < nrows; ++s) {
+    int r = r_first + s * rstep;
+    if (r >= RT || r0 + r >= mi) continue;
+    const double* urow = U + (int64_t)(ri0 + r0 + r) * lduv;
+    double v = asum[s];
+    for (int a = 0; a < ki; ++a) v = fma(-__ldg(&urow[a]), Sp[(int64_t)a * m_max + q], v);
+    Bp[(int64_t)(r0 + r) * mjn + q] = v;
+  }
+}
+
+}  // namespace
+}  // namespace ublr
+
+using namespace ublr;
+
+static size_t coupling_smem(int MR, int NJ) {
+  size_t stage = (size_t)2 * CP_BK * (MR + 4) + (size_t)2 * CP_BK * (8 * NJ + 4);
+  size_t w = (size_t)MR * (8 * NJ + 1);
+  return (stage > w ? stage : w) * sizeof(double);
+}
+
+extern "C" int ublr_coupling(const ublr_op_t* op, const int32_t* off, const int32_t* roff, int b, int k,
+                             const double* U, const double* V, int64_t ld_uv, double* core, int64_t ld_c,
+                             void* stream, int m_max) {
+  int rc = check_op(op);
+  if (rc) return rc;
+  UBLR_REQUIRE(b > 0 && off && roff && U && V && core && k >= 1 && ld_uv >= k, UBLR_ERR_VALUE,
+               "ublr_coupling: bad arguments");
+  UBLR_REQUIRE(m_max <= 256 && k <= 64, UBLR_ERR_VALUE, "ublr_coupling: supports m <= 256, k <= 64");
+  UBLR_REQUIRE(b <= 65535, UBLR_ERR_VALUE, "ublr_coupling: b <= 65535");
+  cudaStream_t st = (cudaStream_t)stream;
+  dim3 grid(b, b);
+  int kk = k < m_max ? k : m_max;  // effective ranks never exceed min(k, m)
+#define UBLR_CP_LAUNCH(RW, NJ)                                                                             \
+  UBLR_DISPATCH_KIND(op->kind, KIND, {                                                                    \
+    size_t sm = coupling_smem(8 * (RW), (NJ));                                                           \
+    UBLR_CUDA(cudaFuncSetAttribute(k_coupling<KIND, RW, NJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                   (int)sm));                                                            \
+    k_coupling<KIND, RW, NJ><<<grid, CP_THREADS, sm, st>>>(*op, off, roff, k, U, V, ld_uv, core, ld_c);   \
+  })
+  if (m_max <= 64) {
+    if (kk <= 16) { UBLR_CP_LAUNCH(8, 2); }
+    else if (kk <= 32) { UBLR_CP_LAUNCH(8, 4); }
+    else { UBLR_CP_LAUNCH(8, 8); }
+  } else {
+    if (kk <= 16) { UBLR_CP_LAUNCH(32, 2); }
+    else if (kk <= 32) { UBLR_CP_LAUNCH(32, 4); }
+    else { UBLR_CP_LAUNCH(32, 8); }
+  }
+#undef UBLR_CP_LAUNCH
+  UBLR_LAUNCH_CHECK();
+  return UBLR_OK;
+}
+
+static int ka_of(int k) { return (k <= 8) ? 8 : (k <= 16) ? 16 : (k <= 32) ? 32 : 64; }
+
+extern "C" int64_t ublr_nearfield_workspace_bytes(int n_pairs, int k, int m_max) {
+  return (int64_t)n_pairs * ka_of(k) * m_max * (int64_t)sizeof(double);
+}
+
+extern "C" int ublr_nearfield_colour(const ublr_op_t* op, const int32_t* off, const int32_t* roff, int b, int k,
+                                     const double* U, const double* V, int64_t ld_uv, const double* core,
+                                     int64_t ld_c, const int32_t* colour, const int32_t* cptr, const int32_t* cidx,
+                                     int n_colours, int m_max, const int32_t* pair_i, const int32_t* nidx,
+                                     int n_pairs, const int64_t* b_off, double* B, void* workspace,
+                                     int64_t workspace_bytes, void* stream) {
+  int rc = check_op(op);
+  if (rc) return rc;
+  UBLR_REQUIRE(b > 0 && n_colours > 0 && n_pairs > 0 && off && roff && U && V && core && colour && cptr && cidx &&
+                   pair_i && nidx && b_off && B && workspace,
+               UBLR_ERR_VALUE, "ublr_nearfield_colour: bad arguments");
+  UBLR_REQUIRE(m_max <= 256 && k <= 64, UBLR_ERR_VALUE, "ublr_nearfield_colour: supports m <= 256, k <= 64");
+  UBLR_REQUIRE(workspace_bytes >= ublr_nearfield_workspace_bytes(n_pairs, k, m_max), UBLR_ERR_VALUE,
+               "ublr_nearfield_colour: workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  double* S = (double*)workspace;
+  const int KA = ka_of(k);
+  // S_p: 8 warps x NQ 8-col groups cover m_max
+  int nq = (m_max + 63) / 64;  // per warp groups of 8 columns: 8 warps * 8 * nq >= m_max
+#define UBLR_NFS(NA, NQ)                                                                                   \
+  k_nf_S<NA, NQ><<<n_pairs, CP_THREADS, 0, st>>>(off, roff, V, ld_uv, core, ld_c, colour, cptr, cidx, pair_i, \
+                                                 nidx, m_max, S)
+  if (KA == 8) {
+    if (nq <= 1) UBLR_NFS(1, 1); else if (nq <= 2) UBLR_NFS(1, 2); else UBLR_NFS(1, 4);
+  } else if (KA == 16) {
+    if (nq <= 1) UBLR_NFS(2, 1); else if (nq <= 2) UBLR_NFS(2, 2); else UBLR_NFS(2, 4);
+  } else if (KA == 32) {
+    if (nq <= 1) UBLR_NFS(4, 1); else if (nq <= 2) UBLR_NFS(4, 2); else UBLR_NFS(4, 4);
+  } else {
+    if (nq <= 1) UBLR_NFS(8, 1); else if (nq <= 2) UBLR_NFS(8, 2); else UBLR_NFS(8, 4);
+  }
+#undef UBLR_NFS
+  UBLR_LAUNCH_CHECK();
+  dim3 grid(n_pairs, (m_max + 31) / 32);
+  UBLR_DISPATCH_KIND(op->kind, KIND,
+                     (k_nf_B<KIND><<<grid, CP_THREADS, 0, st>>>(*op, off, roff, KA, U, ld_uv, colour, cptr, cidx,
+                                                                pair_i, nidx, b_off, m_max, S, B)));
+  UBLR_LAUNCH_CHECK();
+  return UBLR_OK;
+}

@@ -1,0 +1,331 @@
+// K2/K3 — sketches Y = A Omega, Z = A^* Psi with on-the-fly operator tiles.
+//
+// * ublr_apply: generic out = A X (every op.apply of the reference pipeline,
+//   ref/operators.py:48-52): 128 x BN CTA tiles, A tile generated per k-step
+//   into shared memory (k-major), X tile by cp.async, fp64 DMMA m8n8k4.
+// * ublr_sketch_tagged(_pair): the tagged sketch of ref/bases.py:163-172.
+//   Omega's block (j, group c) is T[j,c] G_j, so
+//       Y(I_i, c*gc + q) = sum_j T[j,c] (A_ij G_j)(:, q)
+//   (Kronecker restructuring): each A tile meets G_j once (2 m^2 gc flops)
+//   and the ell-fold group scatter is a register epilogue per block j
+//   (2 m gc ell flops) — ell times fewer flops than the dense product, with
+//   every entry of Y still produced. For a symmetric operator the _pair
+//   variant pushes [G | H] through one pass over A (Z = A^T Psi = A Psi).
+#include "common.cuh"
+#include "optile.cuh"
+
+namespace ublr {
+namespace {
+
+// ------------------------------------------------------------------ apply
+constexpr int AP_BM = 128;
+constexpr int AP_BK = 16;
+constexpr int AP_THREADS = 256;
+
+template <int KIND, int BN>
+__global__ void __launch_bounds__(AP_THREADS) k_apply(ublr_op_t op, const double* __restrict__ X, int64_t ldx,
+                                                      int w, double* __restrict__ out, int64_t ldo) {
+  constexpr int SA = AP_BM + 4;
+  constexpr int SB = BN + 4;
+  constexpr int WN = BN / 4;        // warp tile cols (4 warps across)
+  constexpr int NJ = WN / 8;        // 8-col groups per warp
+  __shared__ LogTables lt;
+  extern __shared__ double dsm[];
+  double (*As)[AP_BK][SA] = reinterpret_cast<double (*)[AP_BK][SA]>(dsm);
+  double (*Bs)[AP_BK][SB] = reinterpret_cast<double (*)[AP_BK][SB]>(dsm + 2 * AP_BK * SA);
+  if (KIND == UBLR_OP_LOG) init_log_tables(&lt);
+
+  const int n = (int)op.n;
+  const int row0 = blockIdx.y * AP_BM;
+  const int col0 = blockIdx.x * BN;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wr = warp >> 2, wc = warp & 3;
+
+  // generation mapping: row = tid % 128, kk = tid / 128 + 2 i
+  const int grow = tid & (AP_BM - 1);
+  const int gk0 = tid >> 7;
+  RowPoint rp = load_row_point(op, row0 + grow, row0 + grow < n);
+
+  double acc[8][NJ][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  __syncthreads();  // log tables
+
+  auto stage = [&](int buf, int k0) {
+#pragma unroll
+    for (int i = 0; i < AP_BK / 2; ++i) {
+      int kk = gk0 + 2 * i;
+      int q = k0 + kk;
+      double v = 0.0;
+      if (rp.p >= 0 && q < n) v = op_entry<KIND>(op, rp, q, &lt);
+      As[buf][kk][grow] = v;
+    }
+    // X tile: AP_BK x BN
+    for (int e = tid; e < AP_BK * BN; e += AP_THREADS) {
+      int kk = e / BN, c = e - kk * BN;
+      int q = k0 + kk, col = col0 + c;
+      bool ok = q < n && col < w;
+      cp_async8(&Bs[buf][kk][c], ok ? (const void*)(X + (int64_t)q * ldx + col) : (const void*)X, ok);
+    }
+    cp_async_commit();
+  };
+
+  const int nk = (n + AP_BK - 1) / AP_BK;
+  stage(0, 0);
+  for (int ks = 0; ks < nk; ++ks) {
+    int buf = ks & 1;
+    cp_async_wait<0>();
+    __syncthreads();
+    if (ks + 1 < nk) stage(buf ^ 1, (ks + 1) * AP_BK);
+#pragma unroll
+    for (int k4 = 0; k4 < AP_BK; k4 += 4) {
+      double a[8], bb[NJ];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = As[buf][k4 + t][wr * 64 + i * 8 + g];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) bb[j] = Bs[buf][k4 + t][wc * WN + j * 8 + g];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) mma8x8x4(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
+    }
+  }
+  // epilogue
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    int r = row0 + wr * 64 + i * 8 + g;
+    if (r >= n) continue;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      int c = col0 + wc * WN + j * 8 + 2 * t;
+      if (c < w) out[(int64_t)r * ldo + c] = acc[i][j][0];
+      if (c + 1 < w) out[(int64_t)r * ldo + c + 1] = acc[i][j][1];
+    }
+  }
+}
+
+// ---------------------------------------------------------- tagged sketch
+constexpr int TS_BM = 16;
+constexpr int TS_BK = 32;
+constexpr int TS_THREADS = 256;
+
+// CTA: 16 consecutive (permuted) rows x BN of the (gc or 2gc) test-block columns.
+// Warp w covers all 16 rows x BN/8 columns.
+template <int KIND, int L, int BN>
+__global__ void __launch_bounds__(TS_THREADS) k_sketch_tagged(ublr_op_t op, const int32_t* __restrict__ off, int b,
+                                                              const double* __restrict__ T, int ell,
+                                                              const double* __restrict__ G,
+                                                              const double* __restrict__ H, int64_t ldx, int gc,
+                                                              double* __restrict__ Y, double* __restrict__ Z,
+                                                              int64_t ldy) {
+  constexpr int SA = TS_BM + 4;
+  constexpr int SB = BN + 4;
+  constexpr int WN = BN / 8;   // columns per warp
+  constexpr int NJ = WN / 8;   // 8-col groups per warp
+  __shared__ LogTables lt;
+  extern __shared__ double dsm[];
+  double (*As)[TS_BK][SA] = reinterpret_cast<double (*)[TS_BK][SA]>(dsm);
+  double (*Bs)[TS_BK][SB] = reinterpret_cast<double (*)[TS_BK][SB]>(dsm + 2 * TS_BK * SA);
+  if (KIND == UBLR_OP_LOG) init_log_tables(&lt);
+
+  const int ncols = (H ? 2 : 1) * gc;
+  // rows are independent in the sketch, so 16-row tiles may straddle blocks
+  const int rend = (int)op.n;
+  const int row0 = blockIdx.y * TS_BM;
+  const int col0 = blockIdx.x * BN;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+
+  const int grow = tid & (TS_BM - 1);
+  const int gk0 = tid >> 4;  // 0..15; entries kk = gk0, gk0 + 16
+  RowPoint rp = load_row_point(op, row0 + grow, row0 + grow < rend);
+
+  double acc[L][2][NJ][2];
+#pragma unroll
+  for (int c = 0; c < L; ++c)
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) acc[c][r][j][0] = acc[c][r][j][1] = 0.0;
+  double wacc[2][NJ][2];
+
+  __syncthreads();
+
+  auto stage = [&](int buf, int q0, int qend) {
+#pragma unroll
+    for (int e = 0; e < TS_BK / 16; ++e) {
+      int kk = gk0 + 16 * e;
+      int q = q0 + kk;
+      double v = 0.0;
+      if (rp.p >= 0 && q < qend) v = op_entry<KIND>(op, rp, q, &lt);
+      As[buf][kk][grow] = v;
+    }
+    for (int e = tid; e < TS_BK * BN; e += TS_THREADS) {
+      int kk = e / BN, c = e - kk * BN;
+      int q = q0 + kk, col = col0 + c;
+      bool ok = q < qend && col < ncols;
+      const double* src = G;
+      if (ok) src = (col < gc) ? (G + (int64_t)q * ldx + col) : (H + (int64_t)q * ldx + (col - gc));
+      cp_async8(&Bs[buf][kk][c], src, ok);
+    }
+    cp_async_commit();
+  };
+
+  // flattened (block j, k-step) loop
+  int j = 0, q0 = off[0];
+  int qend = off[1];
+  stage(0, q0, qend);
+  int buf = 0;
+  for (;;) {
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int jj = 0; jj < NJ; ++jj) wacc[r][jj][0] = wacc[r][jj][1] = 0.0;
+    for (;;) {
+      // next stage coordinates
+      int nq0 = q0 + TS_BK, nj = j, nqend = qend;
+      if (nq0 >= qend) {
+        nj = j + 1;
+        if (nj < b) { nq0 = off[nj]; nqend = off[nj + 1]; }
+      }
+      cp_async_wait<0>();
+      __syncthreads();
+      if (nj < b) stage(buf ^ 1, nq0, nqend);
+#pragma unroll
+      for (int k4 = 0; k4 < TS_BK; k4 += 4) {
+        double a0 = As[buf][k4 + t][g];
+        double a1 = As[buf][k4 + t][8 + g];
+#pragma unroll
+        for (int jj = 0; jj < NJ; ++jj) {
+          double bb = Bs[buf][k4 + t][warp * WN + jj * 8 + g];
+          mma8x8x4(wacc[0][jj][0], wacc[0][jj][1], a0, bb);
+          mma8x8x4(wacc[1][jj][0], wacc[1][jj][1], a1, bb);
+        }
+      }
+      buf ^= 1;
+      bool block_done = (nj != j);
+      q0 = nq0; qend = nqend;
+      if (block_done) break;
+    }
+    // scatter block j's product into the ell tag groups
+#pragma unroll
+    for (int c = 0; c < L; ++c) {
+      double tc = (c < ell) ? __ldg(&T[(int64_t)j * ell + c]) : 0.0;
+#pragma unroll
+      for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int jj = 0; jj < NJ; ++jj) {
+          acc[c][r][jj][0] = fma(tc, wacc[r][jj][0], acc[c][r][jj][0]);
+          acc[c][r][jj][1] = fma(tc, wacc[r][jj][1], acc[c][r][jj][1]);
+        }
+    }
+    ++j;
+    if (j >= b) break;
+  }
+  // epilogue: (row, col) -> Y or Z at group c
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    int row = row0 + r * 8 + g;
+    if (row >= rend) continue;
+#pragma unroll
+    for (int jj = 0; jj < NJ; ++jj)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        int col = col0 + warp * WN + jj * 8 + 2 * t + h;
+        if (col >= ncols) continue;
+        double* dst = (col < gc) ? Y : Z;
+        int q = (col < gc) ? col : col - gc;
+#pragma unroll
+        for (int c = 0; c < L; ++c)
+          if (c < ell) dst[(int64_t)row * ldy + c * gc + q] = acc[c][r][jj][h];
+      }
+  }
+}
+
+}  // namespace
+}  // namespace ublr
+
+using namespace ublr;
+
+extern "C" int ublr_apply(const ublr_op_t* op, const double* X, int64_t ld_x, int w, double* out, int64_t ld_o,
+                          void* stream) {
+  int rc = check_op(op);
+  if (rc) return rc;
+  UBLR_REQUIRE(w >= 0 && X && out && ld_x >= w && ld_o >= w, UBLR_ERR_VALUE, "ublr_apply: bad X/out");
+  if (w == 0) return UBLR_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  dim3 grid;
+  grid.y = (unsigned)((op->n + AP_BM - 1) / AP_BM);
+#define UBLR_AP_LAUNCH(BN)                                                                                 \
+  UBLR_DISPATCH_KIND(op->kind, KIND, {                                                                    \
+    size_t sm = (size_t)2 * AP_BK * ((AP_BM + 4) + ((BN) + 4)) * sizeof(double);                         \
+    UBLR_CUDA(cudaFuncSetAttribute(k_apply<KIND, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
+    k_apply<KIND, BN><<<grid, AP_THREADS, sm, st>>>(*op, X, ld_x, w, out, ld_o);                           \
+  })
+  if (w <= 64) {
+    grid.x = (unsigned)((w + 63) / 64);
+    UBLR_AP_LAUNCH(64);
+  } else {
+    grid.x = (unsigned)((w + 127) / 128);
+    UBLR_AP_LAUNCH(128);
+  }
+#undef UBLR_AP_LAUNCH
+  UBLR_LAUNCH_CHECK();
+  return UBLR_OK;
+}
+
+namespace {
+int sketch_common(const ublr_op_t* op, const int32_t* off, int b, const double* T,
+                  int ell, const double* G, const double* H, int64_t ld_x, int gc, double* Y, double* Z,
+                  int64_t ld_y, cudaStream_t st) {
+  int ncols = (H ? 2 : 1) * gc;
+  dim3 grid;
+  grid.y = (unsigned)((op->n + TS_BM - 1) / TS_BM);
+#define UBLR_TS_LAUNCH(L, BN)                                                                              \
+  {                                                                                                        \
+    grid.x = (unsigned)((ncols + (BN) - 1) / (BN));                                                       \
+    UBLR_DISPATCH_KIND(op->kind, KIND, {                                                                  \
+      size_t sm = (size_t)2 * TS_BK * ((TS_BM + 4) + ((BN) + 4)) * sizeof(double);                       \
+      UBLR_CUDA(cudaFuncSetAttribute(k_sketch_tagged<KIND, L, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                     (int)sm));                                                          \
+      k_sketch_tagged<KIND, L, BN><<<grid, TS_THREADS, sm, st>>>(*op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y); \
+    })                                                                                                     \
+  }
+  if (ell <= 4) UBLR_TS_LAUNCH(4, 128)
+  else if (ell <= 10) UBLR_TS_LAUNCH(10, 64)
+  else if (ell <= 28) UBLR_TS_LAUNCH(28, 64)
+  else {
+    set_error("tagged sketch supports ell <= 28 (d <= 3 without extra columns)");
+    return UBLR_ERR_VALUE;
+  }
+#undef UBLR_TS_LAUNCH
+  UBLR_LAUNCH_CHECK();
+  return UBLR_OK;
+}
+}  // namespace
+
+extern "C" int ublr_sketch_tagged(const ublr_op_t* op, const int32_t* off, int b, const double* T, int ell,
+                                  const double* X, int64_t ld_x, int gc, double* Y, int64_t ld_y, void* stream) {
+  int rc = check_op(op);
+  if (rc) return rc;
+  UBLR_REQUIRE(b > 0 && off && T && X && Y && gc > 0 && ell > 0 && ld_x >= gc && ld_y >= (int64_t)ell * gc,
+               UBLR_ERR_VALUE, "ublr_sketch_tagged: bad arguments");
+  return sketch_common(op, off, b, T, ell, X, nullptr, ld_x, gc, Y, nullptr, ld_y, (cudaStream_t)stream);
+}
+
+extern "C" int ublr_sketch_tagged_pair(const ublr_op_t* op, const int32_t* off, int b, const double* T, int ell,
+                                       const double* G, const double* H, int64_t ld_x, int gc, double* Y, double* Z,
+                                       int64_t ld_y, void* stream) {
+  int rc = check_op(op);
+  if (rc) return rc;
+  UBLR_REQUIRE(b > 0 && off && T && G && H && Y && Z && gc > 0 && ell > 0 && ld_x >= gc &&
+                   ld_y >= (int64_t)ell * gc,
+               UBLR_ERR_VALUE, "ublr_sketch_tagged_pair: bad arguments");
+  return sketch_common(op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y, (cudaStream_t)stream);
+}

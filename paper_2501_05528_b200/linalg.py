@@ -1,0 +1,110 @@
+"""Seeded streams and dense helpers (mirror of ref/linalg.py:14-139).
+
+`RandomStream` keeps the reference's semantics exactly (numpy Philox keyed
+by SeedSequence(seed, spawn_key=key), row-major `standard_normal`); its host
+methods serve host-side planning (the b x ell tagging matrix). Every test
+matrix of the compression itself is drawn on the GPU by
+`device_normals` (C-ABI `ublr_rng_normals`, bit-identical to numpy).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+
+
+class RandomStream:
+    """ref/linalg.py:14-45."""
+
+    def __init__(self, seed: int, key: tuple = ()):
+        self.seed = int(seed)
+        self.key = tuple(int(i) for i in key)
+        self._gen = None
+
+    def child(self, *indices: int) -> "RandomStream":
+        return RandomStream(self.seed, self.key + indices)
+
+    @property
+    def generator(self) -> np.random.Generator:
+        if self._gen is None:
+            seq = np.random.SeedSequence(self.seed, spawn_key=self.key)
+            self._gen = np.random.Generator(np.random.Philox(seq))
+        return self._gen
+
+    def philox_key(self) -> tuple:
+        """128-bit Philox key (numpy derives it as SeedSequence.generate_state(2, uint64))."""
+        st = np.random.SeedSequence(self.seed, spawn_key=self.key).generate_state(2, np.uint64)
+        return int(st[0]), int(st[1])
+
+    def normal(self, rows: int, cols: int) -> np.ndarray:
+        return self.generator.standard_normal((rows, cols))
+
+    def uniform(self, rows: int, cols: int) -> np.ndarray:
+        return self.generator.random((rows, cols))
+
+    def __repr__(self):
+        return f"RandomStream(seed={self.seed}, key={self.key})"
+
+
+def gaussian(rows: int, cols: int, stream: RandomStream) -> np.ndarray:
+    """ref/linalg.py:48-52 (host array, bit-identical to the reference)."""
+    if rows < 0 or cols < 0:
+        raise ValueError("matrix dimensions must be nonnegative")
+    return stream.normal(rows, cols)
+
+
+def device_normals(specs, out):
+    """Fill `out` (a CUDA float64 tensor) from several Gaussian streams.
+
+    specs: iterable of (stream, rows, cols, out_offset, ld, rowmap) where
+    normal n of the stream lands at out.flat[out_offset + row(n) * ld + n % cols]
+    with row(n) = rowmap[n // cols] (rowmap: CUDA int32 tensor or None).
+    The same numbers numpy's `stream.normal(rows, cols)` returns.
+    """
+    import torch
+
+    _lib.require_device()
+    specs = list(specs)
+    if not specs:
+        return out
+    rec = np.zeros(len(specs), dtype=_lib.RNG_STREAM_DTYPE)
+    counts = np.zeros(len(specs), dtype=np.int64)
+    keep = []
+    for s, (stream, rows, cols, off, ld, rowmap) in enumerate(specs):
+        k0, k1 = stream.philox_key()
+        rec[s] = (k0, k1, rows * cols, max(cols, 1), ld, off, _lib.ptr(rowmap))
+        counts[s] = rows * cols
+        if rowmap is not None:
+            keep.append(rowmap)
+    lib = _lib.load()
+    ws_bytes = int(lib.ublr_rng_workspace_bytes(counts.ctypes.data, len(specs)))
+    ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device=out.device)
+    rec_d = torch.from_numpy(rec.view(np.uint8)).to(out.device)
+    _lib.call("ublr_rng_normals", _lib.ptr(rec_d), counts.ctypes.data, len(specs), _lib.ptr(out),
+              _lib.ptr(ws), ws_bytes, _lib.stream_handle())
+    # keep host/device descriptors alive until the stream has consumed them
+    out._ublr_keepalive = (rec_d, ws, keep)
+    return out
+
+
+def col_basis(B, k: int) -> np.ndarray:
+    """ref/linalg.py:55-69 on the GPU (Householder QR kernel K4)."""
+    import torch
+
+    B = np.asarray(B, dtype=float)
+    m, n = B.shape
+    if k > min(m, n):
+        raise ValueError(f"k={k} exceeds matrix dimensions {m}x{n}")
+    if k == 0:
+        return np.zeros((m, 0))
+    _lib.require_device()
+    dev = torch.device("cuda")
+    Bd = torch.from_numpy(np.ascontiguousarray(B)).to(dev)
+    off = torch.tensor([0, m], dtype=torch.int32, device=dev)
+    col0 = torch.zeros(1, dtype=torch.int32, device=dev)
+    Q = torch.empty((m, k), dtype=torch.float64, device=dev)
+    # mode 1 (sample = columns col0..) | 2 (plain QR: no identity shortcut for k == m)
+    _lib.call("ublr_block_qr", _lib.ptr(Bd), n, 3, None, 0, 0, _lib.ptr(col0), _lib.ptr(off), 1, k,
+              _lib.ptr(Q), k, _lib.stream_handle(), m)
+    return Q.cpu().numpy()

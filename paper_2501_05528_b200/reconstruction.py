@@ -1,0 +1,380 @@
+"""Compressed uBLR format and the compression pipelines on the GPU.
+
+Mirrors ref/reconstruction.py (UniformBLR, direct_core,
+structured_identity_discrepancy, compress_type_a / _b, compress,
+CompressionReport, relative_error). Step functions keep the reference's
+signatures; their work runs in the CUDA kernels of `csrc/` through the C ABI.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .bases import BlockBases, tagging_bases
+from .linalg import RandomStream, device_normals
+from .operators import CountingOperator, DifferenceOperator, LinearOperatorHandle, counting_wrapper, unwrap
+from .tagging import DegenerateTagsError, plan_tagging
+from .tessellation import BoxColoring, Tessellation, color_boxes, device_tess
+
+METHOD_IDS = {("A", "bn"): "A1", ("A", "tag"): "A2", ("A", "naive"): "A3", ("B", "bn"): "B1", ("B", "tag"): "B2"}
+
+
+def _torch():
+    import torch
+    return torch
+
+
+class UniformBLR:
+    """U C V* + B over a tessellation (ref/reconstruction.py:50-132).
+
+    Device storage: U, V are N x k (permuted rows), `core_d` is K x K, B is
+    one flat buffer of near blocks in neighbour-CSR order (b_off). The
+    reference's fields (`u_blocks`, `v_blocks`, `core`, `b_blocks`) are
+    host views built on demand."""
+
+    def __init__(self, tess, rank, U, V, core_d, B_d, dt, metadata=None):
+        self.tess = tess
+        self.rank = rank
+        self.dt = dt
+        self.U, self.V = U, V
+        self.core_d = core_d
+        self.B_d = B_d
+        self.effective_ranks = dt.ranks(rank).astype(np.int64)
+        self.metadata = metadata or {}
+        self._host = {}
+
+    # --- reference-shaped views -------------------------------------------
+    @property
+    def n(self) -> int:
+        return self.tess.n_points
+
+    @property
+    def shape(self) -> tuple:
+        return (self.n, self.n)
+
+    @property
+    def total_rank(self) -> int:
+        return int(self.effective_ranks.sum())
+
+    def rank_offsets(self) -> np.ndarray:
+        return np.concatenate(([0], np.cumsum(self.effective_ranks)))
+
+    def _blocks(self, M):
+        h = M.cpu().numpy()
+        off = self.dt.off_h
+        return [h[off[i]:off[i + 1], :self.effective_ranks[i]].copy() for i in range(self.dt.b)]
+
+    @property
+    def u_blocks(self) -> list:
+        if "u" not in self._host:
+            self._host["u"] = self._blocks(self.U)
+        return self._host["u"]
+
+    @property
+    def v_blocks(self) -> list:
+        if "v" not in self._host:
+            self._host["v"] = self._blocks(self.V)
+        return self._host["v"]
+
+    @property
+    def core(self) -> np.ndarray:
+        if "core" not in self._host:
+            self._host["core"] = self.core_d.cpu().numpy()
+        return self._host["core"]
+
+    @property
+    def b_blocks(self) -> dict:
+        if "B" not in self._host:
+            flat = self.B_d.cpu().numpy()
+            dt = self.dt
+            out = {}
+            for p in range(dt.n_pairs):
+                i, j = int(dt.pair_i_h[p]), int(dt.nidx_h[p])
+                out[(i, j)] = flat[dt.b_off_h[p]:dt.b_off_h[p + 1]].reshape(dt.sizes[i], dt.sizes[j])
+            self._host["B"] = out
+        return self._host["B"]
+
+    @property
+    def storage_entries(self) -> int:
+        return int(2 * sum(self.dt.sizes * self.effective_ranks) + self.total_rank ** 2 + self.dt.b_off_h[-1])
+
+    # --- products -----------------------------------------------------------
+    def apply_device(self, Xd, adjoint=False):
+        """A_hat X on permuted rows (N x w CUDA tensor)."""
+        return blr_apply(self, Xd, adjoint)
+
+    def apply(self, X):
+        X = np.asarray(X, dtype=float)
+        vec = X.ndim == 1
+        X2 = X.reshape(-1, 1) if vec else X
+        out = self.dt.from_perm_rows(self.apply_device(self.dt.to_perm_rows(X2)))
+        return out.ravel() if vec else out
+
+    def apply_adjoint(self, X):
+        X = np.asarray(X, dtype=float)
+        vec = X.ndim == 1
+        X2 = X.reshape(-1, 1) if vec else X
+        out = self.dt.from_perm_rows(self.apply_device(self.dt.to_perm_rows(X2), adjoint=True))
+        return out.ravel() if vec else out
+
+    def to_dense(self) -> np.ndarray:
+        return self.apply(np.eye(self.n))
+
+
+def blr_apply(rep: UniformBLR, Xd, adjoint=False):
+    """Blockwise U C V^T X + B X (ref/reconstruction.py:93-119).
+
+    Measurement path (error estimation, not timed by the reference): uses
+    batched torch products over the uniform-block layout."""
+    torch = _torch()
+    dt = rep.dt
+    n, w = Xd.shape
+    k = rep.rank
+    b = dt.b
+    if not (dt.sizes == dt.sizes[0]).all():
+        raise NotImplementedError("blr_apply measurement path needs uniform blocks")
+    m = int(dt.sizes[0])
+    ki = int(min(k, m))
+    L, R = (rep.V, rep.U) if not adjoint else (rep.U, rep.V)
+    Lb = L[:, :ki].reshape(b, m, ki)
+    Rb = R[:, :ki].reshape(b, m, ki)
+    Xb = Xd.reshape(b, m, w)
+    VtX = torch.bmm(Lb.transpose(1, 2), Xb).reshape(b * ki, w)
+    C = rep.core_d if not adjoint else rep.core_d.T
+    CV = (C @ VtX).reshape(b, ki, w)
+    out = torch.bmm(Rb, CV).reshape(n, w)
+    Bf = rep.B_d
+    pi = torch.as_tensor(dt.pair_i_h, device=Xd.device).long()
+    pj = torch.as_tensor(dt.nidx_h, device=Xd.device).long()
+    Bb = Bf.reshape(-1, m, m)
+    if not adjoint:
+        contrib = torch.bmm(Bb, Xb[pj])
+        out.view(b, m, w).index_add_(0, pi, contrib)
+    else:
+        contrib = torch.bmm(Bb.transpose(1, 2), Xb[pi])
+        out.view(b, m, w).index_add_(0, pj, contrib)
+    return out
+
+
+def relative_error(op, rep: UniformBLR, iterations: int = 20, stream: RandomStream | None = None) -> float:
+    """ref/reconstruction.py:160-177 (power method on A - A_hat and on A)."""
+    from .linalg import gaussian  # host draws keep the reference's start vectors
+    torch = _torch()
+    stream = stream or RandomStream(0)
+    if op.shape != rep.shape:
+        raise ValueError(f"shape mismatch: {op.shape} vs {rep.shape}")
+    dt = rep.dt
+    inner = unwrap(op)
+
+    def a_apply(Xd, adj):
+        if hasattr(inner, "apply_device"):
+            return inner.apply_device(Xd, dt.perm, adjoint=adj and not getattr(inner, "symmetric", False))
+        f = inner.apply_adjoint if adj else inner.apply
+        return dt.to_perm_rows(f(dt.from_perm_rows(Xd)))
+
+    def power(fwd, adj, st):
+        if iterations < 1:
+            raise ValueError("iterations must be >= 1")
+        v = dt.to_perm_rows(gaussian(dt.n, 1, st))
+        nv = torch.linalg.vector_norm(v)
+        if float(nv) == 0.0:
+            return 0.0
+        v = v / nv
+        est = 0.0
+        for _ in range(iterations):
+            w = fwd(v)
+            est = float(torch.linalg.vector_norm(w))
+            if est == 0.0:
+                return 0.0
+            v = adj(w)
+            v = v / torch.linalg.vector_norm(v)
+        return est
+
+    num = power(lambda X: a_apply(X, False) - rep.apply_device(X),
+                lambda X: a_apply(X, True) - rep.apply_device(X, adjoint=True), stream.child(0))
+    den = power(lambda X: a_apply(X, False), lambda X: a_apply(X, True), stream.child(1))
+    if den == 0.0:
+        raise ValueError("operator norm estimate is zero")
+    return num / den
+
+
+# ---------------------------------------------------------------------------
+# Type A
+# ---------------------------------------------------------------------------
+
+def direct_core(op, tess: Tessellation, bases: BlockBases):
+    """C = U^T (A V) (ref/reconstruction.py:185-198); device K x K tensor."""
+    torch = _torch()
+    dt = bases.dt
+    k = bases.rank
+    K = bases.total_rank
+    roff_h, roff = dt.roff(k)
+    core = torch.empty((K, K), dtype=torch.float64, device=dt.device)
+    if isinstance(op, CountingOperator):
+        op.ledger.record_apply(K)
+    inner = unwrap(op)
+    if K == 0:
+        return core
+    if not hasattr(inner, "device_op"):
+        raise NotImplementedError("direct_core needs a GPU operator (DenseOperator / KernelOperator)")
+    _lib.call("ublr_coupling", inner.device_op(dt.perm), _lib.ptr(dt.off), _lib.ptr(roff), dt.b, k,
+              _lib.ptr(bases.U), _lib.ptr(bases.V), bases.U.stride(0), _lib.ptr(core), K, _lib.stream_handle(),
+              dt.m_max)
+    return core
+
+
+def _check_coloring(tess, colors):
+    colors = np.asarray(colors)
+    for i in range(tess.b):
+        nc = colors[tess.neighbor_lists[i]]
+        if len(set(nc.tolist())) != len(nc):
+            raise ValueError(f"invalid coloring: two same-color probes collide in the neighborhood of block {i}")
+
+
+def structured_identity_discrepancy(op, tess: Tessellation, bases: BlockBases, core, coloring: BoxColoring):
+    """Near blocks from colour probes, with the reference's same-colour leak
+    (ref/reconstruction.py:201-244). Returns a flat device buffer
+    of near blocks in neighbour-CSR order."""
+    torch = _torch()
+    _check_coloring(tess, coloring.colors)
+    dt = bases.dt
+    if not np.array_equal(np.asarray(coloring.colors), dt.colours_h):
+        raise NotImplementedError("custom colourings: only color_boxes(tess) is supported on the GPU path")
+    k = bases.rank
+    K = bases.total_rank
+    roff_h, roff = dt.roff(k)
+    sizes = dt.sizes
+    if isinstance(op, CountingOperator):
+        op.ledger.record_apply(int(sum(sizes[dt.colours_h == c].max() for c in range(dt.n_colours))))
+    inner = unwrap(op)
+    if not hasattr(inner, "device_op"):
+        raise NotImplementedError("structured_identity_discrepancy needs a GPU operator")
+    B = torch.empty(int(dt.b_off_h[-1]), dtype=torch.float64, device=dt.device)
+    lib = _lib.load()
+    ws_bytes = int(lib.ublr_nearfield_workspace_bytes(dt.n_pairs, max(k, 1), dt.m_max))
+    ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device=dt.device)
+    if K == 0:
+        core = torch.zeros((1, 1), dtype=torch.float64, device=dt.device)
+    _lib.call("ublr_nearfield_colour", inner.device_op(dt.perm), _lib.ptr(dt.off), _lib.ptr(roff), dt.b, k,
+              _lib.ptr(bases.U), _lib.ptr(bases.V), bases.U.stride(0), _lib.ptr(core), max(K, 1),
+              _lib.ptr(dt.colours), _lib.ptr(dt.cptr), _lib.ptr(dt.cidx), dt.n_colours, dt.m_max,
+              _lib.ptr(dt.pair_i), _lib.ptr(dt.nidx), dt.n_pairs, _lib.ptr(dt.b_off), _lib.ptr(B),
+              _lib.ptr(ws), ws_bytes, _lib.stream_handle())
+    return B
+
+
+# ---------------------------------------------------------------------------
+# Reports and pipelines
+# ---------------------------------------------------------------------------
+
+@dataclass
+class CompressionReport:
+    """ref/reconstruction.py:429-463."""
+    method: str
+    config: dict
+    matvecs: dict
+    times_s: dict
+    relative_error: float | None
+    storage_entries: int
+    aspect_ratios: dict | None = None
+
+    @property
+    def matvecs_total(self) -> int:
+        return sum(v["A"] + v["Astar"] for v in self.matvecs.values())
+
+    def phase_total(self, phase: str) -> int:
+        e = self.matvecs.get(phase, {"A": 0, "Astar": 0})
+        return e["A"] + e["Astar"]
+
+    def to_dict(self) -> dict:
+        return {"method": self.method, "config": self.config, "matvecs": self.matvecs,
+                "matvecs_total": self.matvecs_total,
+                "times_s": {k: float(f"{v:.3g}") for k, v in self.times_s.items()},
+                "relative_error": self.relative_error, "storage_entries": self.storage_entries,
+                "aspect_ratios": self.aspect_ratios}
+
+
+def _ratio_summary(values: np.ndarray) -> dict:
+    fin = values[np.isfinite(values)]
+    if fin.size == 0:
+        return {"count": 0}
+    return {"count": int(fin.size), "min": float(fin.min()), "q1": float(np.quantile(fin, 0.25)),
+            "median": float(np.median(fin)), "q3": float(np.quantile(fin, 0.75)), "max": float(fin.max())}
+
+
+def _base_config(tess, k, p, stream, **extra) -> dict:
+    cfg = {"N": tess.n_points, "b": tess.b, "m": tess.max_block_size, "k": k, "p": p, "d": tess.dim,
+           "seed": stream.seed}
+    cfg.update(extra)
+    return cfg
+
+
+class _PhaseTimer:
+    """perf_counter around a phase with device synchronisation at the edges,
+    so times_s keeps the reference's per-phase meaning (ref/reconstruction.py:524-551)."""
+
+    def __init__(self, times, name):
+        self.times, self.name = times, name
+
+    def __enter__(self):
+        _torch().cuda.synchronize()
+        self.t0 = time.perf_counter()
+
+    def __exit__(self, *exc):
+        _torch().cuda.synchronize()
+        self.times[self.name] = time.perf_counter() - self.t0
+
+
+def compress_type_a(op, tess, k, p=10, method="tag", stream=None, distribution="gaussian", extra_cols=0,
+                    optimize=False, extra_samples=False, max_tag_redraws=5, compute_error=True,
+                    error_iterations=20):
+    """ref/reconstruction.py:498-583 on the GPU."""
+    stream = stream or RandomStream(0)
+    _lib.require_device()
+    cop = counting_wrapper(op)
+    times, plan = {}, None
+    with _PhaseTimer(times, "I"), cop.ledger.phase("I"):
+        if method == "tag":
+            plan = plan_tagging(tess, extra_cols, distribution, stream.child(1), optimize=optimize,
+                                max_redraws=max_tag_redraws)
+            bases, _ = tagging_bases(cop, tess, k, p, plan, stream.child(0), extra_samples=extra_samples)
+        elif method in ("bn", "naive"):
+            raise NotImplementedError(f"step-I method {method!r} lands with the next kernels")
+        else:
+            raise ValueError(f"unknown step-I method {method!r}")
+    with _PhaseTimer(times, "II"), cop.ledger.phase("II"):
+        core = direct_core(cop, tess, bases)
+    with _PhaseTimer(times, "III"):
+        coloring = color_boxes(tess)
+        with cop.ledger.phase("III"):
+            B = structured_identity_discrepancy(cop, tess, bases, core, coloring)
+    rep = UniformBLR(tess, k, bases.U, bases.V, core, B, bases.dt, {"method": METHOD_IDS[("A", method)]})
+    rel = relative_error(op, rep, error_iterations, stream.child(9)) if compute_error else None
+    aspect, ell = None, None
+    if plan is not None:
+        ell = plan.matrix.n_cols
+        aspect = {"base": _ratio_summary(plan.rho_base), "draws": plan.attempts}
+    report = CompressionReport(
+        method=METHOD_IDS[("A", method)],
+        config=_base_config(tess, k, p, stream, ell=ell, distribution=distribution if method == "tag" else None,
+                            extra_cols=extra_cols if method == "tag" else None, optimize=optimize),
+        matvecs=cop.ledger.to_dict(), times_s=times, relative_error=rel,
+        storage_entries=rep.storage_entries, aspect_ratios=aspect)
+    return rep, report
+
+
+def compress_type_b(*args, **kwargs):
+    raise NotImplementedError("type-B reconstruction lands with the next kernels")
+
+
+def compress(op, tess, k, method_id: str = "A2", **kwargs):
+    """ref/reconstruction.py:680-687."""
+    for (family, basis), mid in METHOD_IDS.items():
+        if mid == method_id:
+            fn = compress_type_a if family == "A" else compress_type_b
+            return fn(op, tess, k, method=basis, **kwargs)
+    raise ValueError(f"unknown method id {method_id!r}; expected one of {sorted(METHOD_IDS.values())}")

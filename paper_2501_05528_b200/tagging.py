@@ -1,0 +1,234 @@
+"""Tagging planner (host side; ref/tagging.py:23-379).
+
+The b x ell tagging matrix T, the per-block null vectors z^(i) of T(N_i, :)
+and the per-pair vectors of T(N_i \\ {j}, :) are tiny host problems, but their
+exact values matter (boundary blocks have nullity >= 2, so a different
+orthonormalisation changes the sample: SURVEY.md F2, F13). They are computed
+with numpy's own Householder QR, exactly as the reference does, but batched:
+all blocks with the same neighbour count go through one stacked
+`np.linalg.qr` call (the reference loops in Python, which costs 10 s of
+phase I at b = 4096).
+"""
+
+from __future__ import annotations
+
+import warnings
+from dataclasses import dataclass
+
+import numpy as np
+
+from .linalg import RandomStream, gaussian
+from .tessellation import Tessellation
+
+
+class DegenerateTagsError(RuntimeError):
+    """ref/tagging.py:23-25."""
+
+
+@dataclass(frozen=True)
+class TaggingMatrix:
+    entries: np.ndarray
+    dim: int
+    extra_cols: int
+    distribution: str
+    seed: int
+
+    @property
+    def b(self) -> int:
+        return self.entries.shape[0]
+
+    @property
+    def n_cols(self) -> int:
+        return self.entries.shape[1]
+
+
+@dataclass(frozen=True)
+class NullVector:
+    block: int
+    vector: np.ndarray
+    residual: float
+
+
+@dataclass(frozen=True)
+class ProjectedTags:
+    block: int
+    values: np.ndarray
+
+
+@dataclass
+class TaggingPlan:
+    matrix: TaggingMatrix
+    null_vectors: list
+    rho_base: np.ndarray
+    rho_optimized: np.ndarray | None
+    attempts: int
+
+    @property
+    def Z(self) -> np.ndarray:
+        """(b, ell) stacked null vectors."""
+        return np.stack([nv.vector for nv in self.null_vectors])
+
+
+DISTRIBUTIONS = ("gaussian", "haar", "equidistributed")
+
+
+def make_tagging_matrix(b, d, extra_cols=0, distribution="gaussian", stream=None) -> TaggingMatrix:
+    """ref/tagging.py:61-91 (gaussian and haar)."""
+    stream = stream or RandomStream(0)
+    if extra_cols < 0:
+        raise ValueError("extra_cols must be nonnegative")
+    ell = 3 ** d + 1 + extra_cols
+    if b < ell:
+        raise ValueError(f"b={b} too small for {ell} tagging columns")
+    if distribution == "gaussian":
+        entries = gaussian(b, ell, stream)
+    elif distribution == "haar":
+        q, r = np.linalg.qr(gaussian(b, ell, stream))
+        signs = np.sign(np.diag(r))
+        signs[signs == 0] = 1.0
+        entries = q * signs
+    elif distribution == "equidistributed":
+        raise NotImplementedError("equidistributed tagging rows are not part of the B200 hot path")
+    else:
+        raise ValueError(f"unknown distribution {distribution!r}; expected one of {DISTRIBUTIONS}")
+    return TaggingMatrix(entries, d, extra_cols, distribution, stream.seed)
+
+
+def batched_null_vectors(T: np.ndarray, rows_list: list, rtol: float = 1e-12):
+    """Last column of the complete QR of T[rows]^T for every row set
+    (== null_basis(T[rows], 1)[:, 0], ref/linalg.py:72-94), grouped by size.
+
+    Returns (Z (n_sets, ell), residual ||T[rows] z|| (n_sets,), ok mask where
+    the reference's residual test passes)."""
+    ell = T.shape[1]
+    n = len(rows_list)
+    Z = np.zeros((n, ell))
+    res = np.zeros(n)
+    ok = np.ones(n, dtype=bool)
+    sizes = np.array([len(r) for r in rows_list])
+    for sz in np.unique(sizes):
+        idx = np.flatnonzero(sizes == sz)
+        rows = np.array([rows_list[i] for i in idx], dtype=np.int64)  # (G, sz)
+        sub = T[rows]                                                 # (G, sz, ell)
+        q = np.linalg.qr(np.transpose(sub, (0, 2, 1)), mode="complete")[0]
+        z = q[:, :, ell - 1]
+        Z[idx] = z
+        r = np.linalg.norm(np.einsum("gij,gj->gi", sub, z), axis=1)
+        res[idx] = r
+        scale = np.maximum(1.0, np.linalg.norm(sub, axis=(1, 2)))
+        ok[idx] = r <= rtol * scale
+    return Z, res, ok
+
+
+def tag_null_vector(T: TaggingMatrix, tess: Tessellation, i: int) -> NullVector:
+    """ref/tagging.py:126-139."""
+    Z, res, ok = batched_null_vectors(T.entries, [tess.neighbor_lists[i]])
+    if not ok[0]:
+        raise DegenerateTagsError(f"block {i}: requested null space does not exist")
+    limit = 1e-12 * max(1.0, np.linalg.norm(T.entries))
+    if res[0] > limit:
+        raise DegenerateTagsError(f"block {i}: null-vector residual {res[0]:.3e} exceeds {limit:.3e}")
+    return NullVector(block=i, vector=Z[0], residual=float(res[0]))
+
+
+def projected_tags(T: TaggingMatrix, tess: Tessellation, nv: NullVector) -> ProjectedTags:
+    return ProjectedTags(block=nv.block, values=T.entries @ nv.vector)
+
+
+def aspect_ratio(pt: ProjectedTags, tess: Tessellation, i: int | None = None) -> float:
+    """ref/tagging.py:110-123."""
+    block = pt.block if i is None else i
+    far = tess.far_fields[block]
+    if len(far) == 0:
+        raise ValueError(f"block {block} has an empty far field (b too small)")
+    mags = np.abs(pt.values[far])
+    hi, lo = mags.max(), mags.min()
+    if hi == 0.0:
+        return 1.0
+    if lo == 0.0:
+        return float("inf")
+    return float(hi / lo)
+
+
+def _evaluate(T: TaggingMatrix, tess: Tessellation, attempts: int) -> TaggingPlan:
+    """ref/tagging.py:355-379 for optimize=False, batched."""
+    E = T.entries
+    Z, res, ok = batched_null_vectors(E, tess.neighbor_lists)
+    if not ok.all():
+        i = int(np.flatnonzero(~ok)[0])
+        raise DegenerateTagsError(f"block {i}: requested null space does not exist")
+    limit = 1e-12 * max(1.0, np.linalg.norm(E))
+    if (res > limit).any():
+        i = int(np.flatnonzero(res > limit)[0])
+        raise DegenerateTagsError(f"block {i}: null-vector residual {res[i]:.3e} exceeds {limit:.3e}")
+    b = tess.b
+    P = np.abs(E @ Z.T)                     # P[j, i] = |<t_j, z^(i)>|
+    near = np.zeros((b, b), dtype=bool)
+    for i, nb in enumerate(tess.neighbor_lists):
+        near[nb, i] = True
+    far_any = (~near).any(axis=0)
+    hi = np.where(near, -np.inf, P).max(axis=0)
+    lo = np.where(near, np.inf, P).min(axis=0)
+    rho = np.full(b, np.nan)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        r = np.where(hi == 0.0, 1.0, np.where(lo == 0.0, np.inf, hi / lo))
+    rho[far_any] = r[far_any]
+    nvs = [NullVector(block=i, vector=Z[i], residual=float(res[i])) for i in range(b)]
+    return TaggingPlan(matrix=T, null_vectors=nvs, rho_base=rho, rho_optimized=None, attempts=attempts)
+
+
+def plan_tagging(tess, extra_cols=0, distribution="gaussian", stream=None, optimize=False,
+                 max_redraws=5, ratio_limit=1e6, extra_check=None) -> TaggingPlan:
+    """Redraw policy of ref/tagging.py:306-352."""
+    if optimize:
+        raise NotImplementedError("null-vector optimisation (ref/tagging.py:142-292) is outside the B200 hot path")
+    stream = stream or RandomStream(0)
+    last, plan = None, None
+    for attempt in range(max_redraws + 1):
+        T = make_tagging_matrix(tess.b, tess.dim, extra_cols, distribution, stream.child(attempt))
+        if extra_check is not None and not extra_check(T):
+            last = DegenerateTagsError("extra_check rejected the draw")
+            continue
+        try:
+            plan = _evaluate(T, tess, attempt + 1)
+        except DegenerateTagsError as exc:
+            last = exc
+            continue
+        fin = plan.rho_base[~np.isnan(plan.rho_base)]
+        worst = fin.max() if fin.size else 1.0
+        if np.isfinite(worst) and worst <= ratio_limit:
+            return plan
+    if plan is None:
+        raise DegenerateTagsError(f"no usable tagging matrix after {max_redraws + 1} draws: {last}")
+    warnings.warn(f"tagging matrix still has aspect ratio above {ratio_limit:.0e} after "
+                  f"{max_redraws + 1} draws; proceeding with the last one")
+    return plan
+
+
+def pair_vectors(T_entries: np.ndarray, tess: Tessellation, denom_rtol: float = 1e-10):
+    """Per near pair p = (i, j) in neighbour-CSR order: unit null vector of
+    T(N_i \\ {j}, :) and denominator <t_j, z> (ref/reconstruction.py:344-355).
+    Raises DegenerateTagsError like the reference."""
+    limit = denom_rtol * max(1.0, np.linalg.norm(T_entries))
+    sets, excl = [], []
+    for i, nb in enumerate(tess.neighbor_lists):
+        for j in nb:
+            sets.append([r for r in nb if r != j])
+            excl.append(j)
+    Z, res, ok = batched_null_vectors(T_entries, sets)
+    if not ok.all():
+        raise DegenerateTagsError("requested null space of dimension 1 does not exist")
+    den = np.einsum("pj,pj->p", T_entries[np.array(excl)], Z)
+    if (np.abs(den) < limit).any():
+        raise DegenerateTagsError("projected tag for a near pair vanished")
+    return Z, den
+
+
+def b2_denominators_ok(T, tess: Tessellation, rtol: float = 1e-10) -> bool:
+    """ref/reconstruction.py:310-323."""
+    entries = T.entries if isinstance(T, TaggingMatrix) else np.asarray(T)
+    try:
+        pair_vectors(entries, tess, rtol)
+    except DegenerateTagsError:
+        return False
+    return True

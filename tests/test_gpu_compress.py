@@ -1,0 +1,85 @@
+"""End-to-end GPU parity: compress() through the CUDA path against the CPU
+oracle and the reference's golden fixtures.
+
+Gate (BASELINE.json north_star): ||A_hat_gpu - A_hat_ref||_F / ||A||_F <= 1e-10
+and ||A - A_hat_gpu||_F / ||A||_F <= 1.05 x the reference's.
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle as O
+import paper_2501_05528_b200 as P
+from cases import build_case, golden, probe_vec
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def gpu_problem(name):
+    """The same input as cases.build_case, as GPU operators."""
+    if name.startswith("c1"):
+        from cases import c1_problem
+        n, b = (512, 8) if name.startswith("c1s") else (2048, 32)
+        _, A = c1_problem(n, b)
+        tess = P.build_tessellation(P.grid_points(n, 1), b)
+        return tess, P.DenseOperator(A), A
+    if name.startswith("log1k") or name.startswith("c2"):
+        per, b = (32, 16) if name.startswith("log1k") else (64, 64)
+        pts = P.grid_points(per, 2)
+        tess = P.build_tessellation(pts, b)
+        op = P.KernelOperator(pts, "log", -np.log(0.5 / per))
+        return tess, op, None
+    if name.startswith("rand500"):
+        from cases import rand500_problem
+        _, coords, _ = rand500_problem()
+        tess = P.build_tessellation(P.PointCloud(coords, 2), 16)
+        return tess, P.KernelOperator(coords, "log", 3.0), None
+    raise KeyError(name)
+
+
+def ahat_error_vs_golden(rep, g, ncols=3):
+    W = np.stack([probe_vec(rep.n, 10 + c) for c in range(ncols)], axis=1)
+    scale = float(g["A_fro"])
+    e1 = np.linalg.norm(rep.apply(W) - g["Ahat_W"]) / (scale * np.sqrt(ncols))
+    e2 = np.linalg.norm(rep.apply_adjoint(W) - g["Ahat_tW"]) / (scale * np.sqrt(ncols))
+    return max(e1, e2)
+
+
+@pytest.mark.parametrize("name", ["c1s_A2", "log1k_A2", "rand500_A2", "c1_A2", "c2_A2"])
+def test_compress_A2_matches_reference(name):
+    tess, op, _ = gpu_problem(name)
+    _, _, k, p, mid, seed = build_case(name)
+    rep, report = P.compress(op, tess, k, mid, p=p, stream=P.RandomStream(seed), compute_error=False)
+    g = golden(name)
+    assert ahat_error_vs_golden(rep, g) <= TOL
+    mv = np.array([[report.matvecs.get(ph, {"A": 0})["A"], report.matvecs.get(ph, {"Astar": 0})["Astar"]]
+                   for ph in ("I", "II", "III")])
+    assert np.array_equal(mv, g["matvecs"])
+    assert report.storage_entries == int(g["storage_entries"])
+
+
+@pytest.mark.parametrize("name", ["c1s_A2", "log1k_A2", "c2_A2"])
+def test_compress_A2_dense_frobenius_vs_oracle(name):
+    """Full ||A_hat_gpu - A_hat_oracle||_F / ||A||_F on the same inputs, and the
+    approximation error within 1.05x of the oracle's."""
+    tess, op, A = gpu_problem(name)
+    bx, oop, k, p, mid, seed = build_case(name)
+    rep, _ = P.compress(op, tess, k, mid, p=p, stream=P.RandomStream(seed), compute_error=False)
+    orep, _ = O.compress(oop, bx, k, mid, p=p, stream=O.Stream(seed), compute_error=False)
+    Ad = oop.matrix
+    D_gpu, D_ref = rep.to_dense(), orep.to_dense()
+    nA = np.linalg.norm(Ad)
+    assert np.linalg.norm(D_gpu - D_ref) / nA <= TOL
+    err_gpu = np.linalg.norm(Ad - D_gpu) / nA
+    err_ref = np.linalg.norm(Ad - D_ref) / nA
+    assert err_gpu <= 1.05 * err_ref + 1e-15
+
+
+def test_relative_error_estimate_close_to_reference():
+    tess, op, _ = gpu_problem("c1s_A2")
+    rep, report = P.compress(op, tess, 10, "A2", p=5, stream=P.RandomStream(7), compute_error=True)
+    g = golden("c1s_A2")
+    assert report.relative_error == pytest.approx(float(g["rel_error"]), rel=1e-3, abs=1e-14)

@@ -1,0 +1,132 @@
+"""GPU parity of the individual CUDA kernels (through the C ABI) against the
+CPU oracle / numpy on the same seeded inputs."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle as O
+import paper_2501_05528_b200 as P
+from paper_2501_05528_b200 import _lib
+from paper_2501_05528_b200.bases import draw_test_blocks, tagged_sketch
+from paper_2501_05528_b200.linalg import device_normals
+from paper_2501_05528_b200.tessellation import device_tess
+from cases import golden
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def test_rng_streams_bitwise():
+    g = golden("rng")
+    specs, want, at = [], [], 0
+    for t in range(7):
+        spec = g[f"spec{t}"]
+        seed, r, c = int(spec[0]), int(spec[1]), int(spec[2])
+        key = tuple(int(v) for v in spec[3:] if v >= 0)
+        specs.append((P.RandomStream(seed, key), r, c, at, c, None))
+        want.append(g[f"normals{t}"].ravel())
+        at += r * c
+    out = torch.full((at,), np.nan, dtype=torch.float64, device=DEV)
+    device_normals(specs, out)
+    assert np.array_equal(out.cpu().numpy(), np.concatenate(want))
+
+
+def test_rng_long_stream_with_rowmap():
+    rows, cols = 3000, 777
+    st = P.RandomStream(7, (0, 0))
+    perm = np.random.default_rng(0).permutation(rows).astype(np.int32)
+    rowmap = torch.from_numpy(perm).to(DEV)
+    out = torch.empty((rows, cols), dtype=torch.float64, device=DEV)
+    device_normals([(st, rows, cols, 0, cols, rowmap)], out)
+    want = st.normal(rows, cols)
+    got = out.cpu().numpy()[perm]
+    mism = np.flatnonzero(got.ravel() != want.ravel())
+    assert len(mism) <= 5, len(mism)
+    assert np.allclose(got, want, rtol=4e-15, atol=0)
+
+
+def test_rng_many_small_streams():
+    b, m, gc = 300, 64, 30
+    t = P.build_tessellation(P.grid_points(b * m, 1), b) if False else None
+    specs = [(P.RandomStream(7).child(0).child(0, i), m, gc, i * m * gc, gc, None) for i in range(b)]
+    out = torch.empty(b * m * gc, dtype=torch.float64, device=DEV)
+    device_normals(specs, out)
+    got = out.cpu().numpy().reshape(b, m, gc)
+    for i in (0, 1, 17, 299):
+        assert np.array_equal(got[i], P.RandomStream(7).child(0).child(0, i).normal(m, gc))
+
+
+def _dense_apply_case(kind):
+    coords = O.cell_centres(24, 2)
+    n = len(coords)
+    if kind == "dense":
+        A = np.random.default_rng(1).standard_normal((n, n))
+        return coords, P.DenseOperator(A), A
+    diag = 3.25
+    op = P.KernelOperator(coords, kind, diag)
+    A = O.kernel_block(coords, np.arange(n), np.arange(n), kind, diag)
+    return coords, op, A
+
+
+@pytest.mark.parametrize("kind", ["dense", "log", "inv"])
+@pytest.mark.parametrize("w", [1, 37, 200])
+def test_apply_matches_numpy(kind, w):
+    coords, op, A = _dense_apply_case(kind)
+    X = np.random.default_rng(2).standard_normal((A.shape[0], w))
+    got = op.apply(X)
+    want = A @ X
+    assert np.linalg.norm(got - want) <= 1e-13 * np.linalg.norm(A) * np.linalg.norm(X)
+    got_t = op.apply_adjoint(X)
+    assert np.linalg.norm(got_t - A.T @ X) <= 1e-13 * np.linalg.norm(A) * np.linalg.norm(X)
+
+
+def test_fast_log_accuracy():
+    # kernel entries through the apply kernel with unit vectors
+    coords = np.random.default_rng(5).uniform(size=(300, 2))
+    op = P.KernelOperator(coords, "log", 0.0)
+    A = O.kernel_block(coords, np.arange(300), np.arange(300), "log", 0.0)
+    got = op.apply(np.eye(300))
+    err = np.abs(got - A)
+    assert err.max() <= 4e-16 * max(1.0, np.abs(A).max()) * 8
+
+
+@pytest.mark.parametrize("case", ["c1s", "log1k", "rand500"])
+def test_tagged_sketch_matches_oracle(case):
+    if case == "c1s":
+        from cases import c1_problem
+        bx, A = c1_problem(512, 8)
+        tess = P.build_tessellation(P.grid_points(512, 1), 8)
+        op, oop, gc = P.DenseOperator(A), O.Dense(A), 15
+    elif case == "log1k":
+        from cases import log_problem
+        bx, coords, oop = log_problem(32, 16)
+        tess = P.build_tessellation(P.grid_points(32, 2), 16)
+        op, gc = P.KernelOperator(coords, "log", oop.diag), 15
+    else:
+        from cases import rand500_problem
+        bx, coords, oop = rand500_problem()
+        tess = P.build_tessellation(P.PointCloud(coords, 2), 16)
+        op, gc = P.KernelOperator(coords, "log", 3.0), 12
+    dt = device_tess(tess, torch.device(DEV))
+    st = P.RandomStream(7).child(0)
+    plan = P.plan_tagging(tess, 0, "gaussian", P.RandomStream(7).child(1))
+    G = draw_test_blocks(dt, st, 0, gc)
+    H = draw_test_blocks(dt, st, 1, gc)
+    T_dev = torch.from_numpy(plan.matrix.entries).to(DEV)
+    Y, Z = tagged_sketch(op, dt, T_dev, plan.matrix.entries, G, H, gc)
+    oplan = O.TagPlan(plan.matrix.entries, plan.Z, plan.rho_base, 1)
+    _, bundle = O.bases_tagging(oop, bx, gc - 5 if gc > 5 else 1, 5, oplan, O.Stream(7).child(0), gc=gc)
+    Yh, Zh = dt.from_perm_rows(Y), dt.from_perm_rows(Z)
+    scale = np.linalg.norm(bundle.y)
+    assert np.linalg.norm(Yh - bundle.y) <= 1e-13 * scale
+    assert np.linalg.norm(Zh - bundle.z) <= 1e-13 * np.linalg.norm(bundle.z)
+
+
+@pytest.mark.parametrize("m,n,k", [(64, 20, 10), (256, 60, 48), (33, 33, 33), (100, 7, 7)])
+def test_col_basis_matches_numpy(m, n, k):
+    B = np.random.default_rng(m + n).standard_normal((m, n))
+    got = P.col_basis(B, k)
+    want = O.leading_q(B, k)
+    assert np.abs(got - want).max() <= 1e-12

@@ -1,0 +1,122 @@
+"""CPU-only tests: host planning, geometry, the C-ABI export table and the
+host build of the RNG decode (no compute calls need a GPU here)."""
+
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2501_05528_b200 as P
+from paper_2501_05528_b200 import _lib
+from cases import golden
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "ublr_b200.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[\w\*]+\s+\**(ublr_\w+)\s*\(", src, flags=re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = _lib.load()
+    names = header_functions()
+    assert len(names) >= 10
+    for name in names:
+        assert hasattr(lib, name), name
+        assert name in _lib.SIGNATURES, f"{name} missing from _lib.SIGNATURES"
+    assert lib.ublr_version() == 1
+
+
+def test_struct_layouts():
+    assert C.sizeof(_lib.OpDesc) == 64
+    assert C.sizeof(_lib.RngStreamDesc) == 56
+
+
+@pytest.mark.parametrize("name", ["grid2d", "grid1d", "rand2d", "grid3d"])
+def test_tessellation_matches_reference(name):
+    g = golden("geometry")
+    pts = P.PointCloud(g[f"{name}_coords"], g[f"{name}_coords"].shape[1])
+    t = P.build_tessellation(pts, int(g[f"{name}_b"]))
+    assert np.array_equal(np.concatenate(t.blocks), g[f"{name}_perm"])
+    assert np.array_equal(t.block_sizes, g[f"{name}_sizes"])
+    assert np.array_equal(np.concatenate([np.array(x) for x in t.neighbor_lists]), g[f"{name}_nbrflat"])
+    assert np.array_equal(P.color_boxes(t).colors, g[f"{name}_colours"])
+
+
+def test_tagging_plan_bitwise():
+    g = golden("plans")
+    t = P.build_tessellation(P.grid_points(64, 2), 64)
+    plan = P.plan_tagging(t, 0, "gaussian", P.RandomStream(7).child(1))
+    assert np.array_equal(plan.matrix.entries, g["c2_T"])
+    assert np.array_equal(plan.Z, g["c2_Z"])
+    assert np.allclose(plan.rho_base, g["c2_rho"], rtol=1e-10, equal_nan=True)
+    t16 = P.build_tessellation(P.grid_points(32, 2), 16)
+    plan = P.plan_tagging(t16, 0, "gaussian", P.RandomStream(7).child(1),
+                          extra_check=lambda T: P.b2_denominators_ok(T, t16))
+    assert np.array_equal(plan.Z, g["b2s_Z"])
+
+
+def test_pair_vectors_match_oracle():
+    import oracle as O
+    from paper_2501_05528_b200.tagging import pair_vectors
+    t = P.build_tessellation(P.grid_points(32, 2), 16)
+    T = P.RandomStream(3).normal(16, 10)
+    Z, den = pair_vectors(T, t)
+    bx = O.partition(O.cell_centres(32, 2), 16)
+    lim = 1e-10 * max(1.0, np.linalg.norm(T))
+    p = 0
+    for i in range(16):
+        for j in bx.nbrs[i]:
+            z, d = O.pair_vector(T, bx.nbrs[i], j, lim)
+            assert np.array_equal(z, Z[p]) and d == pytest.approx(den[p], rel=1e-14)
+            p += 1
+
+
+@pytest.fixture(scope="module")
+def rng_host():
+    path = os.path.join(ROOT, "tests", "native", "librng_host.so")
+    if not os.path.exists(path):
+        pytest.skip("tests/native/librng_host.so not built")
+    lib = C.CDLL(path)
+    lib.host_philox_words.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, C.c_void_p]
+    lib.host_normals.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, C.c_void_p]
+    lib.host_normals.restype = C.c_int64
+    return lib
+
+
+def test_philox_words_match_numpy(rng_host):
+    for seed, key in ((7, (0, 0, 3)), (1, ()), (123456789, (2,))):
+        st = P.RandomStream(seed, key)
+        k0, k1 = st.philox_key()
+        bg = np.random.Philox(np.random.SeedSequence(seed, spawn_key=key))
+        want = bg.random_raw(1001)
+        got = np.zeros(1001, dtype=np.uint64)
+        rng_host.host_philox_words(k0, k1, 1001, got.ctypes.data)
+        assert np.array_equal(got, want)
+
+
+def test_ziggurat_decode_matches_numpy(rng_host):
+    g = golden("rng")
+    for t in range(7):
+        spec = g[f"spec{t}"]
+        seed, r, c = int(spec[0]), int(spec[1]), int(spec[2])
+        key = tuple(int(v) for v in spec[3:] if v >= 0)
+        k0, k1 = P.RandomStream(seed, key).philox_key()
+        out = np.zeros(r * c)
+        rng_host.host_normals(k0, k1, r * c, out.ctypes.data)
+        assert np.array_equal(out.reshape(r, c), g[f"normals{t}"])
+    # a long stream exercises the wedge and tail branches many times
+    st = P.RandomStream(11, (5,))
+    k0, k1 = st.philox_key()
+    n = 2_000_000
+    out = np.zeros(n)
+    used = rng_host.host_normals(k0, k1, n, out.ctypes.data)
+    want = st.normal(1, n).ravel()
+    mism = np.flatnonzero(out != want)
+    # tail samples use log1p/exp; allow at most a handful of 1-ulp differences
+    assert len(mism) <= 5 and np.all(np.abs(out[mism] - want[mism]) <= 4e-15 * np.abs(want[mism]))
+    assert n < used < 1.03 * n
