@@ -44,7 +44,7 @@ enum { UBLR_OP_DENSE = 0, UBLR_OP_LOG = 1, UBLR_OP_INV = 2 };
 
 /* Operator descriptor: the black-box A of ref/operators.py:24-35, as the
  * GPU sees it. DENSE: A (original order, row-major, lda), gathered through
- * perm; transpose != 0 means A^T. LOG: A(x,y) = -log|x-y|; INV: 1/|x-y|;
+ * perm (NULL = identity); transpose != 0 means A^T. LOG: A(x,y) = -log|x-y|; INV: 1/|x-y|;
  * the diagonal (same original index) takes `diag`. coords are permuted,
  * structure-of-arrays: coords[a*n + p]. */
 typedef struct {
@@ -134,6 +134,17 @@ int ublr_nearfield_colour(const ublr_op_t* op, const int32_t* off, const int32_t
                           int n_colours, int m_max, const int32_t* pair_i, const int32_t* nidx, int n_pairs,
                           const int64_t* b_off, double* B, void* workspace, int64_t workspace_bytes,
                           void* stream);
+
+/* K12 — A_hat X (adjoint = 0) or A_hat^T X (adjoint = 1) for the compressed
+ * representation (ref/reconstruction.py:93-119): blockwise U C V^T X + B X.
+ * tpair[q] for q in the CSR row of j gives the pair index of (nidx[q], j).
+ * work: ublr_blr_apply_workspace_bytes(K, w). */
+int64_t ublr_blr_apply_workspace_bytes(int64_t K, int w);
+int ublr_blr_apply(const double* U, const double* V, int64_t ld_uv, const double* core, int64_t K,
+                   const double* B, const int64_t* b_off, const int32_t* off, const int32_t* roff,
+                   const int32_t* nptr, const int32_t* nidx, const int32_t* tpair, int b,
+                   const double* X, int64_t ld_x, int w, int adjoint, double* out, int64_t ld_o,
+                   double* work, void* stream);
 
 #ifdef __cplusplus
 }

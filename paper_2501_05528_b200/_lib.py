@@ -50,6 +50,8 @@ SIGNATURES = {
     "ublr_block_qr": (INT, [P, I64, INT, P, INT, INT, P, P, INT, INT, P, I64, P, INT]),
     "ublr_coupling": (INT, [C.POINTER(OpDesc), P, P, INT, INT, P, P, I64, P, I64, P, INT]),
     "ublr_nearfield_workspace_bytes": (I64, [INT, INT, INT]),
+    "ublr_blr_apply_workspace_bytes": (I64, [I64, INT]),
+    "ublr_blr_apply": (INT, [P, P, I64, P, I64, P, P, P, P, P, P, P, INT, P, I64, INT, INT, P, I64, P, P]),
     "ublr_nearfield_colour": (INT, [C.POINTER(OpDesc), P, P, INT, INT, P, P, I64, P, I64, P, P, P, INT, INT,
                                     P, P, INT, P, P, P, I64, P]),
 }
@@ -92,7 +94,8 @@ def check(rc: int, what: str = ""):
 
 # kernels each C-ABI entry point launches (for bench.py's `gpu_launches`)
 LAUNCHES = {"ublr_rng_normals": 7, "ublr_sketch_tagged": 1, "ublr_sketch_tagged_pair": 1, "ublr_apply": 1,
-            "ublr_block_qr": 1, "ublr_coupling": 1, "ublr_nearfield_colour": 2}
+            "ublr_block_qr": 1, "ublr_coupling": 1, "ublr_nearfield_colour": 2,
+            "ublr_blr_apply": 3}
 launch_count = 0
 _events = None  # name -> list of (start, end) CUDA events when instrumentation is on
 

@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(CP_THREADS) k_nf_B(ublr_op_t op, const int32_t
     int p_row = ri0 + r0 + tid;
     bool ok = r0 + tid < mi;
     if (KIND == UBLR_OP_DENSE) {
-      rowo[tid] = ok ? op.perm[p_row] : 0;
+      rowo[tid] = ok ? (op.perm ? op.perm[p_row] : p_row) : 0;
     } else {
       rowo[tid] = ok ? p_row : -1;
       for (int a = 0; a < 3; ++a) rowc[a][tid] = (ok && a < op.dim) ? op.coords[(int64_t)a * op.n + p_row] : 0.0;

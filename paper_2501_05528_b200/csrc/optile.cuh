@@ -25,7 +25,7 @@ __device__ __forceinline__ RowPoint load_row_point(const ublr_op_t& op, int p, b
   r.x0 = r.x1 = r.x2 = 0.0;
   if (!valid) return r;
   if (op.kind == UBLR_OP_DENSE) {
-    r.orig = op.perm[p];
+    r.orig = op.perm ? op.perm[p] : p;
   } else {
     r.x0 = op.coords[p];
     if (op.dim > 1) r.x1 = op.coords[op.n + p];
@@ -38,7 +38,7 @@ __device__ __forceinline__ RowPoint load_row_point(const ublr_op_t& op, int p, b
 template <int KIND>
 __device__ __forceinline__ double op_entry(const ublr_op_t& op, const RowPoint& row, int q, const LogTables* lt) {
   if (KIND == UBLR_OP_DENSE) {
-    int oq = op.perm[q];
+    int oq = op.perm ? op.perm[q] : q;
     return op.transpose ? op.A[(int64_t)oq * op.lda + row.orig] : op.A[(int64_t)row.orig * op.lda + oq];
   } else {
     if (q == row.p) return op.diag;
@@ -70,7 +70,7 @@ inline int check_op(const ublr_op_t* op) {
   if (!op) { set_error("null operator"); return UBLR_ERR_VALUE; }
   if (op->n <= 0) { set_error("operator has no rows"); return UBLR_ERR_VALUE; }
   if (op->kind == UBLR_OP_DENSE) {
-    if (!op->A || !op->perm || op->lda < op->n) { set_error("dense operator needs A, perm and lda >= n"); return UBLR_ERR_VALUE; }
+    if (!op->A || op->lda < op->n) { set_error("dense operator needs A and lda >= n (perm NULL = identity)"); return UBLR_ERR_VALUE; }
   } else if (op->kind == UBLR_OP_LOG || op->kind == UBLR_OP_INV) {
     if (!op->coords || op->dim < 1 || op->dim > 3) { set_error("kernel operator needs coords with 1 <= dim <= 3"); return UBLR_ERR_VALUE; }
   } else {

@@ -126,37 +126,23 @@ class UniformBLR:
 
 
 def blr_apply(rep: UniformBLR, Xd, adjoint=False):
-    """Blockwise U C V^T X + B X (ref/reconstruction.py:93-119).
-
-    Measurement path (error estimation, not timed by the reference): uses
-    batched torch products over the uniform-block layout."""
+    """Blockwise U C V^T X + B X, or the adjoint (ref/reconstruction.py:93-119),
+    through the C-ABI kernel `ublr_blr_apply` (ragged blocks supported)."""
     torch = _torch()
     dt = rep.dt
     n, w = Xd.shape
-    k = rep.rank
-    b = dt.b
-    if not (dt.sizes == dt.sizes[0]).all():
-        raise NotImplementedError("blr_apply measurement path needs uniform blocks")
-    m = int(dt.sizes[0])
-    ki = int(min(k, m))
-    L, R = (rep.V, rep.U) if not adjoint else (rep.U, rep.V)
-    Lb = L[:, :ki].reshape(b, m, ki)
-    Rb = R[:, :ki].reshape(b, m, ki)
-    Xb = Xd.reshape(b, m, w)
-    VtX = torch.bmm(Lb.transpose(1, 2), Xb).reshape(b * ki, w)
-    C = rep.core_d if not adjoint else rep.core_d.T
-    CV = (C @ VtX).reshape(b, ki, w)
-    out = torch.bmm(Rb, CV).reshape(n, w)
-    Bf = rep.B_d
-    pi = torch.as_tensor(dt.pair_i_h, device=Xd.device).long()
-    pj = torch.as_tensor(dt.nidx_h, device=Xd.device).long()
-    Bb = Bf.reshape(-1, m, m)
-    if not adjoint:
-        contrib = torch.bmm(Bb, Xb[pj])
-        out.view(b, m, w).index_add_(0, pi, contrib)
-    else:
-        contrib = torch.bmm(Bb.transpose(1, 2), Xb[pi])
-        out.view(b, m, w).index_add_(0, pj, contrib)
+    Xd = Xd.contiguous()
+    K = rep.total_rank
+    roff_h, roff = dt.roff(rep.rank)
+    out = torch.empty((n, w), dtype=torch.float64, device=Xd.device)
+    lib = _lib.load()
+    work = torch.empty(int(lib.ublr_blr_apply_workspace_bytes(K, w)) // 8 + 1, dtype=torch.float64,
+                       device=Xd.device)
+    core = rep.core_d if K > 0 else work
+    _lib.call("ublr_blr_apply", _lib.ptr(rep.U), _lib.ptr(rep.V), rep.U.stride(0), _lib.ptr(core), K,
+              _lib.ptr(rep.B_d), _lib.ptr(dt.b_off), _lib.ptr(dt.off), _lib.ptr(roff), _lib.ptr(dt.nptr),
+              _lib.ptr(dt.nidx), _lib.ptr(dt.tpair), dt.b, _lib.ptr(Xd), w, w, 1 if adjoint else 0,
+              _lib.ptr(out), w, _lib.ptr(work), _lib.stream_handle())
     return out
 
 

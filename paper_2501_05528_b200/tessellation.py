@@ -213,6 +213,9 @@ class DeviceTess:
         self.nidx_h = np.concatenate([np.asarray(x, dtype=np.int32) for x in tess.neighbor_lists])
         self.pair_i_h = np.repeat(np.arange(b, dtype=np.int32), nlen)
         self.n_pairs = int(len(self.nidx_h))
+        pos = {(int(i), int(j)): q for q, (i, j) in enumerate(zip(self.pair_i_h, self.nidx_h))}
+        # tpair[q]: index of the transposed pair (nidx[q], pair_i[q])
+        self.tpair_h = np.array([pos[(int(j), int(i))] for i, j in zip(self.pair_i_h, self.nidx_h)], dtype=np.int32)
         bsz = sizes[self.pair_i_h] * sizes[self.nidx_h]
         self.b_off_h = np.concatenate(([0], np.cumsum(bsz))).astype(np.int64)
         col = color_boxes(tess)
@@ -232,6 +235,7 @@ class DeviceTess:
         self.nptr = t(self.nptr_h)
         self.nidx = t(self.nidx_h)
         self.pair_i = t(self.pair_i_h)
+        self.tpair = t(self.tpair_h)
         self.b_off = t(self.b_off_h)
         self.colours = t(self.colours_h)
         self.cptr = t(self.cptr_h)

@@ -78,8 +78,15 @@ def test_compress_A2_dense_frobenius_vs_oracle(name):
     assert err_gpu <= 1.05 * err_ref + 1e-15
 
 
-def test_relative_error_estimate_close_to_reference():
-    tess, op, _ = gpu_problem("c1s_A2")
-    rep, report = P.compress(op, tess, 10, "A2", p=5, stream=P.RandomStream(7), compute_error=True)
-    g = golden("c1s_A2")
-    assert report.relative_error == pytest.approx(float(g["rel_error"]), rel=1e-3, abs=1e-14)
+@pytest.mark.parametrize("name", ["log1k_A2", "c1s_A2"])
+def test_relative_error_estimate_close_to_reference(name):
+    """The reference's 20-step power-method estimate, same start vectors."""
+    tess, op, _ = gpu_problem(name)
+    _, _, k, p, mid, seed = build_case(name)
+    rep, report = P.compress(op, tess, k, mid, p=p, stream=P.RandomStream(seed), compute_error=True)
+    g = golden(name)
+    ref = float(g["rel_error"])
+    if ref < 1e-11:   # exact-rank case: both estimates sit at rounding level
+        assert report.relative_error < 1e-11
+    else:
+        assert report.relative_error == pytest.approx(ref, rel=1e-4)
