@@ -146,6 +146,33 @@ int ublr_blr_apply(const double* U, const double* V, int64_t ld_uv, const double
                    const double* X, int64_t ld_x, int w, int adjoint, double* out, int64_t ld_o,
                    double* work, void* stream);
 
+/* Batched dense fp64 building blocks (no cuBLAS / cuSOLVER), used by the
+ * block-nullification null space (ref/linalg.py:72-94 at ref/bases.py:102-110)
+ * and the type-B solves (ref/reconstruction.py:252-421). Row-major;
+ * op(A) = A or A^T (ta); amap/bmap (nullable) remap STORAGE rows per batch
+ * entry (stride sAm / sBm), so gathered operands such as Omega[nbr(i)] are
+ * read in place; cmap remaps C's rows (scatter). C = alpha op(A) op(B) + beta C. */
+int ublr_gemm_batched(int ta, int tb, int M, int N, int K, double alpha, const double* A, int64_t lda, int64_t sA,
+                      const int32_t* amap, int64_t sAm, const double* B, int64_t ldb, int64_t sB,
+                      const int32_t* bmap, int64_t sBm, double beta, double* C, int64_t ldc, int64_t sC,
+                      const int32_t* cmap, int64_t sCm, int batch, void* stream);
+/* Panel step of a blocked upper Cholesky A = R^T R: factor the nb x nb
+ * diagonal block at (j0, j0) of each A_b into R_b and write R11^-1
+ * (batch x nb x nb) to Rinv. status != 0 if a block is not positive definite. */
+int ublr_potrf_diag(double* A, int64_t lda, int64_t sA, int j0, int nb, double* R, int64_t ldr, int64_t sR,
+                    double* Rinv, int* status, int batch, void* stream);
+/* Panel step of a blocked no-pivot LU of (W + diag(D)) where D_jj = sign(w_jj)
+ * is chosen when column j becomes the pivot (Householder reconstruction sign
+ * rule): writes L11\U11 into LU, L11^-1 / U11^-1 (batch x nb x nb) and D. */
+int ublr_lu_sign_diag(double* W, int64_t ldw, int64_t sW, int j0, int nb, double* LU, int64_t ldlu, int64_t sLU,
+                      double* Linv, double* Uinv, double* D, int64_t sD, int* status, int batch, void* stream);
+/* out_b[r][c] (or [c][r] with transpose) = src_b[map_b[r] * ld + col0 + c]. */
+int ublr_gather(const double* src, int64_t ld, int64_t s_src, const int32_t* map, int64_t s_map, int rows, int cols,
+                int col0, int transpose, double* out, int64_t ldo, int64_t s_out, int batch, void* stream);
+/* X_b[r][c] *= d_b[r]. */
+int ublr_scale_rows(double* X, int64_t ldx, int64_t s_x, const double* d, int64_t s_d, int rows, int cols,
+                    int batch, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

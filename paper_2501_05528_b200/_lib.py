@@ -51,6 +51,12 @@ SIGNATURES = {
     "ublr_coupling": (INT, [C.POINTER(OpDesc), P, P, INT, INT, P, P, I64, P, I64, P, INT]),
     "ublr_nearfield_workspace_bytes": (I64, [INT, INT, INT]),
     "ublr_blr_apply_workspace_bytes": (I64, [I64, INT]),
+    "ublr_gemm_batched": (INT, [INT, INT, INT, INT, INT, C.c_double, P, I64, I64, P, I64, P, I64, I64, P, I64,
+                                C.c_double, P, I64, I64, P, I64, INT, P]),
+    "ublr_potrf_diag": (INT, [P, I64, I64, INT, INT, P, I64, I64, P, P, INT, P]),
+    "ublr_lu_sign_diag": (INT, [P, I64, I64, INT, INT, P, I64, I64, P, P, P, I64, P, INT, P]),
+    "ublr_gather": (INT, [P, I64, I64, P, I64, INT, INT, INT, INT, P, I64, I64, INT, P]),
+    "ublr_scale_rows": (INT, [P, I64, I64, P, I64, INT, INT, INT, P]),
     "ublr_blr_apply": (INT, [P, P, I64, P, I64, P, P, P, P, P, P, P, INT, P, I64, INT, INT, P, I64, P, P]),
     "ublr_nearfield_colour": (INT, [C.POINTER(OpDesc), P, P, INT, INT, P, P, I64, P, I64, P, P, P, INT, INT,
                                     P, P, INT, P, P, P, I64, P]),
@@ -95,7 +101,8 @@ def check(rc: int, what: str = ""):
 # kernels each C-ABI entry point launches (for bench.py's `gpu_launches`)
 LAUNCHES = {"ublr_rng_normals": 7, "ublr_sketch_tagged": 1, "ublr_sketch_tagged_pair": 1, "ublr_apply": 1,
             "ublr_block_qr": 1, "ublr_coupling": 1, "ublr_nearfield_colour": 2,
-            "ublr_blr_apply": 3}
+            "ublr_blr_apply": 3, "ublr_gemm_batched": 1, "ublr_potrf_diag": 1, "ublr_lu_sign_diag": 1,
+            "ublr_gather": 1, "ublr_scale_rows": 1}
 launch_count = 0
 _events = None  # name -> list of (start, end) CUDA events when instrumentation is on
 

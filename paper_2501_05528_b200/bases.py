@@ -204,3 +204,183 @@ def tagging_bases(op, tess: Tessellation, k: int, p: int, plan, stream: RandomSt
     bases = BlockBases(dt, U, V, k, "tag", (s, s))
     bundle = SketchBundle("tag", dt, s, Y, Z, G=G, H=H, tagging=plan.matrix, group_cols=gc)
     return bases, bundle
+
+
+# ---------------------------------------------------------------------------
+# Block nullification (ref/bases.py:68-123)
+# ---------------------------------------------------------------------------
+
+def block_nullification_width(tess: Tessellation, r: int) -> int:
+    """ref/bases.py:68-75."""
+    widest = max(tess.neighbor_row_count(i) for i in range(tess.b))
+    return max(r + widest, 3 ** tess.dim * r)
+
+
+def nullspace_samples(dt, Om, ld_om, col_om, Ysrc, ld_y, s, r, k, S_out, chunk_bytes=12 << 30):
+    """S_i = Y_i P_k^(i) for every block, P_k^(i) the first k of the r trailing
+    null-space columns that null_basis(Omega[nbr(i)], r) returns
+    (ref/bases.py:102-110, ref/linalg.py:72-94), without a Householder QR:
+
+      G = B B^T = R^T R (blocked Cholesky), Qt_top = B[:, :n]^T R^-1,
+      LU of D - Qt_top with D_jj = sign(pivot) (Householder reconstruction:
+      reproduces LAPACK's dlarfg reflectors, tau in [1, 2]),
+      M = L^-T U^-T Qt_E^T,  P_k = [M - Qt_top D M ; E_bot - B[:, n:]^T R^-1 D M]
+
+    where B = Omega[nbr(i)] (n x s), Qt = B^T R^-1 and E selects columns
+    s-r .. s-r+k-1 (DESIGN.md §bn null space). Blocks with equal
+    neighbourhood size n are batched; Omega rows are gathered in place."""
+    import torch
+
+    from . import dense as D
+
+    dev = dt.device
+    om0 = D.addr(Om, col_om)      # Omega side: column offset inside the fused buffer
+    sizes = dt.sizes
+    nbr_n = np.array([int(sizes[dt.nidx_h[dt.nptr_h[i]:dt.nptr_h[i + 1]]].sum()) for i in range(dt.b)])
+    keys = sorted(set(zip(nbr_n.tolist(), sizes.tolist())))
+    for n, m in keys:
+        n, m = int(n), int(m)
+        if s - r < n:
+            raise ValueError("block-nullification width too small for a neighbourhood")
+        members = np.flatnonzero((nbr_n == n) & (sizes == m))
+        per_block = 5 * n * n * 8 + (s + 3 * n) * k * 8
+        ch = max(1, min(len(members), int(chunk_bytes // per_block), 65535))
+        eb = np.zeros((s - n, k))
+        eb[np.arange(s - r - n, s - r - n + k), np.arange(k)] = 1.0
+        Ebot = torch.from_numpy(eb).to(dev)
+        for c0 in range(0, len(members), ch):
+            blk = members[c0:c0 + ch]
+            nb_ = len(blk)
+            maps = np.stack([np.concatenate([np.arange(dt.off_h[j], dt.off_h[j + 1])
+                                             for j in dt.nidx_h[dt.nptr_h[i]:dt.nptr_h[i + 1]]]) for i in blk])
+            amap = torch.from_numpy(maps.astype(np.int32)).to(dev)
+            rows = np.stack([np.arange(dt.off_h[i], dt.off_h[i + 1]) for i in blk]).astype(np.int32)
+            rmap = torch.from_numpy(rows).to(dev)
+            f64 = dict(dtype=torch.float64, device=dev)
+            G = torch.empty((nb_, n, n), **f64)
+            R = torch.zeros((nb_, n, n), **f64)
+            Qt = torch.empty((nb_, n, n), **f64)
+            LU = torch.zeros((nb_, n, n), **f64)
+            Dg = torch.zeros((nb_, n), **f64)
+            nn = n * n
+            # G = B B^T  (B = Omega[nbr], gathered in place)
+            D.gemm(0, 1, n, n, s, 1.0, om0, ld_om, 0, om0, ld_om, 0, 0.0, D.addr(G), n, nn, nb_,
+                   amap=D.addr(amap), sAm=n, bmap=D.addr(amap), sBm=n)
+            fC = D.cholesky_upper(G, R)
+            # Qt_top = B[:, :n]^T R^-1
+            _lib.call("ublr_gather", om0, ld_om, 0, D.addr(amap), n, n, n, 0, 1, D.addr(Qt), n, nn, nb_,
+                      _lib.stream_handle())
+            tmp = torch.empty((nb_, n, D.NB), **f64)
+            D.trsm_right_upper(Qt, R, fC, tmp)
+            Qtop = Qt.clone()
+            neg = torch.full((n,), -1.0, **f64)
+            _lib.call("ublr_scale_rows", D.addr(Qt), n, nn, D.addr(neg), 0, n, n, nb_, _lib.stream_handle())
+            fL = D.lu_sign(Qt, LU, Dg)          # LU of D - Qt_top
+            # M = L^-T U^-T R^-T B[:, E]
+            Mm = torch.empty((nb_, n, k), **f64)
+            _lib.call("ublr_gather", om0, ld_om, 0, D.addr(amap), n, n, k, s - r, 0, D.addr(Mm), k, n * k, nb_,
+                      _lib.stream_handle())
+            tk = torch.empty((nb_, D.NB, k), **f64)
+            D.trsm_left(R, Mm, fC, fC.inv, upper=True, trans=True, tmp=tk)
+            D.trsm_left(LU, Mm, fL, fL.inv2, upper=True, trans=True, tmp=tk)
+            D.trsm_left(LU, Mm, fL, fL.inv, upper=False, trans=True, tmp=tk)
+            # P = [M - Qt_top (D M) ; E_bot - B[:, n:]^T R^-1 (D M)]
+            P = torch.empty((nb_, s, k), **f64)
+            P[:, :n].copy_(Mm)
+            P[:, n:].copy_(Ebot)
+            DM = Mm
+            _lib.call("ublr_scale_rows", D.addr(DM), k, n * k, D.addr(Dg), n, n, k, nb_, _lib.stream_handle())
+            D.gemm(0, 0, n, k, n, -1.0, D.addr(Qtop), n, nn, D.addr(DM), k, n * k, 1.0, D.addr(P), k, s * k, nb_)
+            D.trsm_left(R, DM, fC, fC.inv, upper=True, trans=False, tmp=tk)
+            D.gemm(1, 0, s - n, k, n, -1.0, om0 + 8 * n, ld_om, 0, D.addr(DM), k, n * k, 1.0, D.addr(P, n * k), k,
+                   s * k, nb_, amap=D.addr(amap), sAm=n)
+            # S_i = Y_i P  (rows of block i scattered into S_out)
+            D.gemm(0, 0, m, k, s, 1.0, D.addr(Ysrc), ld_y, 0, D.addr(P), k, s * k, 0.0, D.addr(S_out), k, 0, nb_,
+                   amap=D.addr(rmap), sAm=m, cmap=D.addr(rmap), sCm=m)
+            D.check_status(fC, "Cholesky of Omega[nbr] Omega[nbr]^T")
+            D.check_status(fL, "sign-selected LU")
+
+
+def block_nullification_bases(op, tess: Tessellation, k: int, p: int, stream: RandomStream):
+    """ref/bases.py:86-123 on the GPU. Returns (BlockBases, SketchBundle)."""
+    torch = _torch()
+    _lib.require_device()
+    dt = device_tess(tess, torch.device("cuda"))
+    r = k + p
+    s = block_nullification_width(tess, r)
+    n = dt.n
+    # Omega | Psi side by side (permuted rows); one numpy stream each, rows in global order
+    OP = torch.empty((n, 2 * s), dtype=torch.float64, device=dt.device)
+    device_normals([(stream.child(0), n, s, 0, 2 * s, dt.inv), (stream.child(1), n, s, s, 2 * s, dt.inv)], OP)
+    _bill(op, s, s)
+    inner = unwrap(op)
+    YZ = torch.empty((n, 2 * s), dtype=torch.float64, device=dt.device)
+    st = _lib.stream_handle()
+    if hasattr(inner, "device_op"):
+        if getattr(inner, "symmetric", False):
+            _lib.call("ublr_apply", inner.device_op(dt.perm), _lib.ptr(OP), 2 * s, 2 * s, _lib.ptr(YZ), 2 * s, st)
+        else:
+            _lib.call("ublr_apply", inner.device_op(dt.perm), _lib.ptr(OP), 2 * s, s, _lib.ptr(YZ), 2 * s, st)
+            _lib.call("ublr_apply", inner.device_op(dt.perm, adjoint=True), _lib.ptr(OP) + 8 * s, 2 * s, s,
+                      _lib.ptr(YZ) + 8 * s, 2 * s, st)
+    else:
+        Yh = inner.apply(dt.from_perm_rows(OP[:, :s]))
+        Zh = inner.apply_adjoint(dt.from_perm_rows(OP[:, s:]))
+        YZ[:, :s] = dt.to_perm_rows(Yh)
+        YZ[:, s:] = dt.to_perm_rows(Zh)
+    kq = max(1, min(k, dt.m_max))
+    U = torch.zeros((n, max(k, 1)), dtype=torch.float64, device=dt.device)
+    V = torch.zeros_like(U)
+    Sbuf = torch.zeros((n, kq), dtype=torch.float64, device=dt.device)
+    col0 = torch.zeros(dt.b, dtype=torch.int32, device=dt.device)
+    for side, dst in ((0, U), (1, V)):
+        if k < dt.m_max:
+            nullspace_samples(dt, OP, 2 * s, side * s, YZ[:, side * s:], 2 * s, s, r, kq, Sbuf)
+        _lib.call("ublr_block_qr", _lib.ptr(Sbuf), kq, 1, None, 0, 0, _lib.ptr(col0), _lib.ptr(dt.off), dt.b, kq,
+                  _lib.ptr(dst), dst.stride(0), st, dt.m_max)
+    bases = BlockBases(dt, U, V, k, "bn", (s, s))
+    bundle = SketchBundle("bn", dt, s, YZ[:, :s], YZ[:, s:], omega_d=OP[:, :s], psi_d=OP[:, s:])
+    return bases, bundle
+
+
+def naive_bases(op, tess: Tessellation, k: int, p: int, stream: RandomStream):
+    """Blocked randSVD baseline (ref/bases.py:213-260): b zeroed Gaussian
+    probes of r columns each, batched into one operator application per side."""
+    torch = _torch()
+    _lib.require_device()
+    dt = device_tess(tess, torch.device("cuda"))
+    r = k + p
+    n, b = dt.n, dt.b
+    w = b * r
+    f64 = dict(dtype=torch.float64, device=dt.device)
+    OM = torch.empty((n, w), **f64)
+    PS = torch.empty((n, w), **f64)
+    device_normals([(stream.child(0, i), n, r, i * r, w, dt.inv) for i in range(b)], OM)
+    device_normals([(stream.child(1, i), n, r, i * r, w, dt.inv) for i in range(b)], PS)
+    # zero the neighbourhood rows of each probe (ref/bases.py:237-239)
+    for i in range(b):
+        rows = torch.from_numpy(np.concatenate([np.arange(dt.off_h[j], dt.off_h[j + 1])
+                                                for j in dt.nidx_h[dt.nptr_h[i]:dt.nptr_h[i + 1]]])).to(dt.device)
+        OM[rows, i * r:(i + 1) * r] = 0.0
+        PS[rows, i * r:(i + 1) * r] = 0.0
+    _bill(op, w, w)
+    inner = unwrap(op)
+    st = _lib.stream_handle()
+    Y = torch.empty((n, w), **f64)
+    Z = torch.empty((n, w), **f64)
+    if hasattr(inner, "device_op"):
+        _lib.call("ublr_apply", inner.device_op(dt.perm), _lib.ptr(OM), w, w, _lib.ptr(Y), w, st)
+        _lib.call("ublr_apply", inner.device_op(dt.perm, adjoint=True), _lib.ptr(PS), w, w, _lib.ptr(Z), w, st)
+    else:
+        Y = dt.to_perm_rows(inner.apply(dt.from_perm_rows(OM)))
+        Z = dt.to_perm_rows(inner.apply_adjoint(dt.from_perm_rows(PS)))
+    kq = max(1, min(k, dt.m_max))
+    U = torch.zeros((n, max(k, 1)), **f64)
+    V = torch.zeros_like(U)
+    col0 = torch.arange(0, w, r, dtype=torch.int32, device=dt.device)
+    for src, dst in ((Y, U), (Z, V)):
+        _lib.call("ublr_block_qr", _lib.ptr(src), w, 1, None, 0, 0, _lib.ptr(col0), _lib.ptr(dt.off), b, kq,
+                  _lib.ptr(dst), dst.stride(0), st, dt.m_max)
+    bases = BlockBases(dt, U, V, k, "naive", (w, w))
+    bundle = SketchBundle("naive", dt, w, Y, Z, omega_d=OM, psi_d=PS, block_cols=r)
+    return bases, bundle

@@ -1,0 +1,356 @@
+// Batched dense fp64 building blocks for the block-nullification and type-B
+// solves (no cuBLAS/cuSOLVER on the hot path):
+//
+// * ublr_gemm_batched: C_b = alpha op(A_b) op(B_b) + beta C_b, row-major,
+//   optional storage-row gather maps (so Omega[nbr(i)] is read in place, no
+//   stacked copy), fp64 DMMA m8n8k4, 128x128 / 64x64 CTA tiles.
+// * ublr_potrf_diag: Cholesky (upper, A = R^T R) of an nb x nb diagonal block
+//   per batch entry in shared memory, plus R^-1 — the panel step of a
+//   right-looking blocked Cholesky driven from the host (dense.py).
+// * ublr_lu_sign_diag: LU without pivoting of an nb x nb diagonal block with
+//   the Householder-reconstruction sign choice (Ballard et al.): before each
+//   pivot j, D_jj = -sign(w_jj) is added to the diagonal, so |pivot| >= 1.
+//   Applied to D - Q1_top this reproduces LAPACK's dlarfg reflectors
+//   (tau_j = pivot_j * D_jj in [1, 2]); see DESIGN.md §bn null space.
+//   Also returns L^-1 and U^-1 of the block.
+#include "common.cuh"
+
+namespace ublr {
+namespace {
+
+constexpr int GT = 256;
+constexpr int GBK = 16;
+
+template <int BM, int BN, bool TA, bool TB>
+__global__ void __launch_bounds__(GT) k_gemm(int M, int N, int K, double alpha, const double* __restrict__ A,
+                                             int64_t lda, int64_t sA, const int32_t* __restrict__ amap,
+                                             int64_t sAm, const double* __restrict__ B, int64_t ldb, int64_t sB,
+                                             const int32_t* __restrict__ bmap, int64_t sBm, double beta,
+                                             double* __restrict__ C, int64_t ldc, int64_t sC,
+                                             const int32_t* __restrict__ cmap, int64_t sCm) {
+  constexpr int SA = BM + 4;
+  constexpr int SB = BN + 4;
+  constexpr int WM = BM / 2, WN = BN / 4;
+  constexpr int MI = WM / 8, NJ = WN / 8;
+  extern __shared__ double dsm[];
+  double (*As)[GBK][SA] = reinterpret_cast<double (*)[GBK][SA]>(dsm);
+  double (*Bs)[GBK][SB] = reinterpret_cast<double (*)[GBK][SB]>(dsm + 2 * GBK * SA);
+  const int bz = blockIdx.z;
+  A += bz * sA;
+  B += bz * sB;
+  C += bz * sC;
+  if (amap) amap += bz * sAm;
+  if (bmap) bmap += bz * sBm;
+  if (cmap) cmap += bz * sCm;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wr = warp >> 2, wc = warp & 3;
+
+  double acc[MI][NJ][2];
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  auto stage = [&](int buf, int k0) {
+    for (int e = tid; e < BM * GBK; e += GT) {
+      int i, kk;
+      if (!TA) { kk = e % GBK; i = e / GBK; } else { i = e % BM; kk = e / BM; }
+      int gi = m0 + i, gk = k0 + kk;
+      bool ok = gi < M && gk < K;
+      const double* src = A;
+      if (ok) {
+        if (!TA) { int64_t pr = amap ? amap[gi] : gi; src = A + pr * lda + gk; }
+        else { int64_t pr = amap ? amap[gk] : gk; src = A + pr * lda + gi; }
+      }
+      cp_async8(&As[buf][kk][i], src, ok);
+    }
+    for (int e = tid; e < BN * GBK; e += GT) {
+      int j, kk;
+      if (!TB) { j = e % BN; kk = e / BN; } else { kk = e % GBK; j = e / GBK; }
+      int gj = n0 + j, gk = k0 + kk;
+      bool ok = gj < N && gk < K;
+      const double* src = B;
+      if (ok) {
+        if (!TB) { int64_t pr = bmap ? bmap[gk] : gk; src = B + pr * ldb + gj; }
+        else { int64_t pr = bmap ? bmap[gj] : gj; src = B + pr * ldb + gk; }
+      }
+      cp_async8(&Bs[buf][kk][j], src, ok);
+    }
+    cp_async_commit();
+  };
+
+  const int nk = (K + GBK - 1) / GBK;
+  if (nk > 0) stage(0, 0);
+  for (int ks = 0; ks < nk; ++ks) {
+    int buf = ks & 1;
+    cp_async_wait<0>();
+    __syncthreads();
+    if (ks + 1 < nk) stage(buf ^ 1, (ks + 1) * GBK);
+#pragma unroll
+    for (int k4 = 0; k4 < GBK; k4 += 4) {
+      double a[MI], bb[NJ];
+#pragma unroll
+      for (int i = 0; i < MI; ++i) a[i] = As[buf][k4 + t][wr * WM + i * 8 + g];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) bb[j] = Bs[buf][k4 + t][wc * WN + j * 8 + g];
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) mma8x8x4(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < MI; ++i) {
+    int r = m0 + wr * WM + i * 8 + g;
+    if (r >= M) continue;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        int c = n0 + wc * WN + j * 8 + 2 * t + h;
+        if (c >= N) continue;
+        double v = alpha * acc[i][j][h];
+        double* dst = C + (int64_t)(cmap ? cmap[r] : r) * ldc + c;
+        *dst = (beta == 0.0) ? v : fma(beta, *dst, v);
+      }
+    }
+  }
+}
+
+template <int BM, int BN>
+int launch_gemm(int ta, int tb, int M, int N, int K, double alpha, const double* A, int64_t lda, int64_t sA,
+                const int32_t* amap, int64_t sAm, const double* B, int64_t ldb, int64_t sB, const int32_t* bmap,
+                int64_t sBm, double beta, double* C, int64_t ldc, int64_t sC, const int32_t* cmap, int64_t sCm,
+                int batch, cudaStream_t st) {
+  dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, batch);
+  size_t sm = (size_t)2 * GBK * ((BM + 4) + (BN + 4)) * sizeof(double);
+#define UBLR_G(TA, TB)                                                                                      \
+  {                                                                                                         \
+    UBLR_CUDA(cudaFuncSetAttribute(k_gemm<BM, BN, TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
+    k_gemm<BM, BN, TA, TB><<<grid, GT, sm, st>>>(M, N, K, alpha, A, lda, sA, amap, sAm, B, ldb, sB, bmap, sBm, \
+                                                 beta, C, ldc, sC, cmap, sCm);                             \
+  }
+  if (!ta && !tb) UBLR_G(false, false)
+  else if (!ta && tb) UBLR_G(false, true)
+  else if (ta && !tb) UBLR_G(true, false)
+  else UBLR_G(true, true)
+#undef UBLR_G
+  UBLR_LAUNCH_CHECK();
+  return UBLR_OK;
+}
+
+// ------------------------------------------------------------ small blocks
+constexpr int FT = 256;
+
+// in-place inverse of an upper-triangular nb x nb matrix in shared memory
+// (column-oriented back substitution; X = U^-1 written to `inv` with ld nb)
+__device__ void tri_inv_upper(const double* U, int ldu, double* inv, int nb) {
+  // solve U X = I column by column; thread c owns column c
+  for (int c = threadIdx.x; c < nb; c += blockDim.x) {
+    for (int r = nb - 1; r >= 0; --r) {
+      double s = (r == c) ? 1.0 : 0.0;
+      for (int q = r + 1; q <= c; ++q) s -= U[r * ldu + q] * inv[q * nb + c];
+      inv[r * nb + c] = (r <= c) ? s / U[r * ldu + r] : 0.0;
+    }
+  }
+}
+
+// unit lower-triangular inverse
+__device__ void tri_inv_unit_lower(const double* L, int ldl, double* inv, int nb) {
+  for (int c = threadIdx.x; c < nb; c += blockDim.x) {
+    for (int r = 0; r < nb; ++r) {
+      double s = (r == c) ? 1.0 : 0.0;
+      for (int q = c; q < r; ++q) s -= L[r * ldl + q] * inv[q * nb + c];
+      inv[r * nb + c] = (r >= c) ? s : 0.0;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(FT) k_potrf_diag(double* A, int64_t lda, int64_t sA, int j0, int nb,
+                                                   double* R, int64_t ldr, int64_t sR, double* Rinv,
+                                                   int* status) {
+  extern __shared__ double sm[];
+  double* S = sm;               // nb x (nb+1)
+  double* I = sm + nb * (nb + 1);
+  const int ld = nb + 1;
+  const int bz = blockIdx.x;
+  double* Ab = A + bz * sA + (int64_t)j0 * lda + j0;
+  for (int e = threadIdx.x; e < nb * nb; e += FT) S[(e / nb) * ld + e % nb] = Ab[(int64_t)(e / nb) * lda + e % nb];
+  __syncthreads();
+  // upper Cholesky, row-oriented right-looking: S = R^T R
+  for (int j = 0; j < nb; ++j) {
+    if (threadIdx.x == 0) {
+      double d = S[j * ld + j];
+      if (!(d > 0.0)) { atomicExch(status, 1); d = 1.0; }
+      S[j * ld + j] = sqrt(d);
+    }
+    __syncthreads();
+    double piv = S[j * ld + j];
+    for (int c = j + 1 + threadIdx.x; c < nb; c += FT) S[j * ld + c] /= piv;
+    __syncthreads();
+    for (int e = threadIdx.x; e < (nb - j - 1) * (nb - j - 1); e += FT) {
+      int r = j + 1 + e / (nb - j - 1), c = j + 1 + e % (nb - j - 1);
+      if (c >= r) S[r * ld + c] -= S[j * ld + r] * S[j * ld + c];
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < nb * nb; e += FT) {
+    int r = e / nb, c = e % nb;
+    if (r > c) S[r * ld + c] = 0.0;
+  }
+  __syncthreads();
+  tri_inv_upper(S, ld, I, nb);
+  __syncthreads();
+  double* Rb = R + bz * sR + (int64_t)j0 * ldr + j0;
+  double* Ib = Rinv + (int64_t)bz * nb * nb;
+  for (int e = threadIdx.x; e < nb * nb; e += FT) {
+    int r = e / nb, c = e % nb;
+    Rb[(int64_t)r * ldr + c] = S[r * ld + c];
+    Ib[e] = I[e];
+  }
+}
+
+__global__ void __launch_bounds__(FT) k_lu_sign_diag(double* W, int64_t ldw, int64_t sW, int j0, int nb,
+                                                     double* LU, int64_t ldlu, int64_t sLU, double* Linv,
+                                                     double* Uinv, double* D, int64_t sD, int* status) {
+  extern __shared__ double sm[];
+  double* S = sm;
+  double* I = sm + nb * (nb + 1);
+  const int ld = nb + 1;
+  const int bz = blockIdx.x;
+  double* Wb = W + bz * sW + (int64_t)j0 * ldw + j0;
+  for (int e = threadIdx.x; e < nb * nb; e += FT) S[(e / nb) * ld + e % nb] = Wb[(int64_t)(e / nb) * ldw + e % nb];
+  __syncthreads();
+  for (int j = 0; j < nb; ++j) {
+    if (threadIdx.x == 0) {
+      // working matrix W = -Q (eliminated so far); D_jj = -sign(q_jj) = sign(w_jj)
+      // makes the pivot w + D_jj of magnitude |w| + 1
+      double w = S[j * ld + j];
+      double d = (w > 0.0) ? 1.0 : -1.0;
+      S[j * ld + j] = w + d;
+      D[bz * sD + j0 + j] = d;
+    }
+    __syncthreads();
+    double piv = S[j * ld + j];
+    if (piv == 0.0) atomicExch(status, 1);
+    for (int r = j + 1 + threadIdx.x; r < nb; r += FT) S[r * ld + j] /= piv;
+    __syncthreads();
+    for (int e = threadIdx.x; e < (nb - j - 1) * (nb - j - 1); e += FT) {
+      int r = j + 1 + e / (nb - j - 1), c = j + 1 + e % (nb - j - 1);
+      S[r * ld + c] -= S[r * ld + j] * S[j * ld + c];
+    }
+    __syncthreads();
+  }
+  double* LUb = LU + bz * sLU + (int64_t)j0 * ldlu + j0;
+  for (int e = threadIdx.x; e < nb * nb; e += FT) LUb[(int64_t)(e / nb) * ldlu + e % nb] = S[(e / nb) * ld + e % nb];
+  tri_inv_unit_lower(S, ld, I, nb);
+  __syncthreads();
+  double* Lb = Linv + (int64_t)bz * nb * nb;
+  for (int e = threadIdx.x; e < nb * nb; e += FT) Lb[e] = I[e];
+  __syncthreads();
+  tri_inv_upper(S, ld, I, nb);
+  __syncthreads();
+  double* Ub = Uinv + (int64_t)bz * nb * nb;
+  for (int e = threadIdx.x; e < nb * nb; e += FT) Ub[e] = I[e];
+}
+
+// out[b][r][c] = src[b*s_src + map[b*s_map + r] * ld + col0 + c]   (transpose: out[b][c][r])
+__global__ void k_gather(const double* __restrict__ src, int64_t ld, int64_t s_src, const int32_t* __restrict__ map,
+                         int64_t s_map, int rows, int cols, int col0, int transpose, double* __restrict__ out,
+                         int64_t ldo, int64_t s_out) {
+  const int bz = blockIdx.y;
+  const int64_t tot = (int64_t)rows * cols;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    int r, c;
+    if (!transpose) { r = (int)(e / cols); c = (int)(e % cols); } else { c = (int)(e / rows); r = (int)(e % rows); }
+    int64_t pr = map ? map[bz * s_map + r] : r;
+    double v = src[bz * s_src + pr * ld + col0 + c];
+    if (!transpose) out[bz * s_out + (int64_t)r * ldo + c] = v;
+    else out[bz * s_out + (int64_t)c * ldo + r] = v;
+  }
+}
+
+// X[b][r][c] *= d[b*s_d + r]
+__global__ void k_scale_rows(double* __restrict__ X, int64_t ldx, int64_t s_x, const double* __restrict__ d,
+                             int64_t s_d, int rows, int cols) {
+  const int bz = blockIdx.y;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)rows * cols;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int r = (int)(e / cols), c = (int)(e % cols);
+    X[bz * s_x + (int64_t)r * ldx + c] *= d[bz * s_d + r];
+  }
+}
+
+}  // namespace
+}  // namespace ublr
+
+using namespace ublr;
+
+extern "C" int ublr_gather(const double* src, int64_t ld, int64_t s_src, const int32_t* map, int64_t s_map, int rows,
+                           int cols, int col0, int transpose, double* out, int64_t ldo, int64_t s_out, int batch,
+                           void* stream) {
+  UBLR_REQUIRE(src && out && rows >= 0 && cols >= 0 && batch >= 0 && batch <= 65535, UBLR_ERR_VALUE,
+               "ublr_gather: bad arguments");
+  if (!rows || !cols || !batch) return UBLR_OK;
+  int64_t tot = (int64_t)rows * cols;
+  dim3 grid((unsigned)((tot + 255) / 256 < 4096 ? (tot + 255) / 256 : 4096), batch);
+  k_gather<<<grid, 256, 0, (cudaStream_t)stream>>>(src, ld, s_src, map, s_map, rows, cols, col0, transpose, out, ldo,
+                                                   s_out);
+  UBLR_LAUNCH_CHECK();
+  return UBLR_OK;
+}
+
+extern "C" int ublr_scale_rows(double* X, int64_t ldx, int64_t s_x, const double* d, int64_t s_d, int rows, int cols,
+                               int batch, void* stream) {
+  UBLR_REQUIRE(X && d && rows >= 0 && cols >= 0 && batch >= 0 && batch <= 65535, UBLR_ERR_VALUE,
+               "ublr_scale_rows: bad arguments");
+  if (!rows || !cols || !batch) return UBLR_OK;
+  int64_t tot = (int64_t)rows * cols;
+  dim3 grid((unsigned)((tot + 255) / 256 < 4096 ? (tot + 255) / 256 : 4096), batch);
+  k_scale_rows<<<grid, 256, 0, (cudaStream_t)stream>>>(X, ldx, s_x, d, s_d, rows, cols);
+  UBLR_LAUNCH_CHECK();
+  return UBLR_OK;
+}
+
+extern "C" int ublr_gemm_batched(int ta, int tb, int M, int N, int K, double alpha, const double* A, int64_t lda,
+                                 int64_t sA, const int32_t* amap, int64_t sAm, const double* B, int64_t ldb,
+                                 int64_t sB, const int32_t* bmap, int64_t sBm, double beta, double* C, int64_t ldc,
+                                 int64_t sC, const int32_t* cmap, int64_t sCm, int batch, void* stream) {
+  UBLR_REQUIRE(M >= 0 && N >= 0 && K >= 0 && batch >= 0 && A && B && C, UBLR_ERR_VALUE, "ublr_gemm_batched: bad arguments");
+  UBLR_REQUIRE(batch <= 65535, UBLR_ERR_VALUE, "ublr_gemm_batched: batch <= 65535");
+  if (M == 0 || N == 0 || batch == 0) return UBLR_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t tiles128 = (int64_t)((M + 127) / 128) * ((N + 127) / 128) * batch;
+  if (M >= 96 && N >= 96 && tiles128 >= 148)
+    return launch_gemm<128, 128>(ta, tb, M, N, K, alpha, A, lda, sA, amap, sAm, B, ldb, sB, bmap, sBm, beta, C, ldc,
+                                 sC, cmap, sCm, batch, st);
+  return launch_gemm<64, 64>(ta, tb, M, N, K, alpha, A, lda, sA, amap, sAm, B, ldb, sB, bmap, sBm, beta, C, ldc, sC,
+                             cmap, sCm, batch, st);
+}
+
+extern "C" int ublr_potrf_diag(double* A, int64_t lda, int64_t sA, int j0, int nb, double* R, int64_t ldr,
+                               int64_t sR, double* Rinv, int* status, int batch, void* stream) {
+  UBLR_REQUIRE(A && R && Rinv && status && nb >= 1 && nb <= 96 && batch >= 1, UBLR_ERR_VALUE,
+               "ublr_potrf_diag: bad arguments");
+  size_t sm = (size_t)(nb * (nb + 1) + nb * nb) * sizeof(double);
+  cudaStream_t st = (cudaStream_t)stream;
+  UBLR_CUDA(cudaFuncSetAttribute(k_potrf_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  k_potrf_diag<<<batch, FT, sm, st>>>(A, lda, sA, j0, nb, R, ldr, sR, Rinv, status);
+  UBLR_LAUNCH_CHECK();
+  return UBLR_OK;
+}
+
+extern "C" int ublr_lu_sign_diag(double* W, int64_t ldw, int64_t sW, int j0, int nb, double* LU, int64_t ldlu,
+                                 int64_t sLU, double* Linv, double* Uinv, double* D, int64_t sD, int* status,
+                                 int batch, void* stream) {
+  UBLR_REQUIRE(W && LU && Linv && Uinv && D && status && nb >= 1 && nb <= 96 && batch >= 1, UBLR_ERR_VALUE,
+               "ublr_lu_sign_diag: bad arguments");
+  size_t sm = (size_t)(nb * (nb + 1) + nb * nb) * sizeof(double);
+  cudaStream_t st = (cudaStream_t)stream;
+  UBLR_CUDA(cudaFuncSetAttribute(k_lu_sign_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  k_lu_sign_diag<<<batch, FT, sm, st>>>(W, ldw, sW, j0, nb, LU, ldlu, sLU, Linv, Uinv, D, sD, status);
+  UBLR_LAUNCH_CHECK();
+  return UBLR_OK;
+}

@@ -1,0 +1,150 @@
+"""Host drivers of the blocked batched dense kernels (csrc/dense.cu).
+
+Right-looking blocked algorithms over batches of equal-size matrices; every
+flop runs in the sm_100a kernels (GEMM with DMMA, nb x nb panel
+factorisations in shared memory). All matrices are row-major CUDA float64
+tensors of shape (batch, rows, cols) unless stated.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+
+NB = 64
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def addr(t, offset_elems=0) -> int:
+    return int(t.data_ptr()) + 8 * int(offset_elems)
+
+
+def gemm(ta, tb, M, N, K, alpha, A, lda, sA, B, ldb, sB, beta, C, ldc, sC, batch,
+         amap=0, sAm=0, bmap=0, sBm=0, cmap=0, sCm=0):
+    """Pointer-level batched GEMM: A, B, C (and the optional row maps) are
+    addresses (ints)."""
+    _lib.call("ublr_gemm_batched", int(ta), int(tb), int(M), int(N), int(K), float(alpha), A, int(lda), int(sA),
+              amap or None, int(sAm), B, int(ldb), int(sB), bmap or None, int(sBm), float(beta), C, int(ldc), int(sC),
+              cmap or None, int(sCm), int(batch), _lib.stream_handle())
+
+
+class Factors:
+    """Diagonal-block inverses kept for the blocked triangular solves."""
+
+    def __init__(self, n, nb, batch, device):
+        torch = _torch()
+        self.n, self.nb, self.batch = n, nb, batch
+        self.blocks = [(j0, min(nb, n - j0)) for j0 in range(0, n, nb)]
+        self.inv = torch.zeros((len(self.blocks), batch, nb, nb), dtype=torch.float64, device=device)
+        self.inv2 = None  # second set (U^-1 for LU)
+
+
+def cholesky_upper(G, R, nb=NB):
+    """G_b = R_b^T R_b (G overwritten as workspace, R zero-initialised by the
+    caller). Returns Factors with R_jj^-1. Raises LinAlgError if not SPD."""
+    torch = _torch()
+    batch, n, _ = G.shape
+    f = Factors(n, nb, batch, G.device)
+    status = torch.zeros(1, dtype=torch.int32, device=G.device)
+    nn = n * n
+    for bi, (j0, jb) in enumerate(f.blocks):
+        _lib.call("ublr_potrf_diag", addr(G), n, nn, j0, jb, addr(R), n, nn, addr(f.inv[bi]), addr(status), batch,
+                  _lib.stream_handle())
+        if j0 + jb < n:
+            n2 = n - j0 - jb
+            # R12 = R11^-T G12
+            gemm(1, 0, jb, n2, jb, 1.0, addr(f.inv[bi]), jb, jb * jb, addr(G, j0 * n + j0 + jb), n, nn,
+                 0.0, addr(R, j0 * n + j0 + jb), n, nn, batch)
+            # G22 -= R12^T R12
+            gemm(1, 0, n2, n2, jb, -1.0, addr(R, j0 * n + j0 + jb), n, nn, addr(R, j0 * n + j0 + jb), n, nn,
+                 1.0, addr(G, (j0 + jb) * n + j0 + jb), n, nn, batch)
+    f.status = status
+    return f
+
+
+def lu_sign(W, LU, D, nb=NB):
+    """No-pivot LU of W + diag(D) with D_jj = sign(w_jj) picked at pivot time
+    (W overwritten). LU holds unit-L (strict lower) and U. Returns Factors
+    with L_jj^-1 (inv) and U_jj^-1 (inv2)."""
+    torch = _torch()
+    batch, n, _ = W.shape
+    f = Factors(n, nb, batch, W.device)
+    f.inv2 = torch.zeros_like(f.inv)
+    status = torch.zeros(1, dtype=torch.int32, device=W.device)
+    nn = n * n
+    for bi, (j0, jb) in enumerate(f.blocks):
+        _lib.call("ublr_lu_sign_diag", addr(W), n, nn, j0, jb, addr(LU), n, nn, addr(f.inv[bi]), addr(f.inv2[bi]),
+                  addr(D), n, addr(status), batch, _lib.stream_handle())
+        if j0 + jb < n:
+            n2 = n - j0 - jb
+            # U12 = L11^-1 W12
+            gemm(0, 0, jb, n2, jb, 1.0, addr(f.inv[bi]), jb, jb * jb, addr(W, j0 * n + j0 + jb), n, nn,
+                 0.0, addr(LU, j0 * n + j0 + jb), n, nn, batch)
+            # L21 = W21 U11^-1
+            gemm(0, 0, n2, jb, jb, 1.0, addr(W, (j0 + jb) * n + j0), n, nn, addr(f.inv2[bi]), jb, jb * jb,
+                 0.0, addr(LU, (j0 + jb) * n + j0), n, nn, batch)
+            # W22 -= L21 U12
+            gemm(0, 0, n2, n2, jb, -1.0, addr(LU, (j0 + jb) * n + j0), n, nn, addr(LU, j0 * n + j0 + jb), n, nn,
+                 1.0, addr(W, (j0 + jb) * n + j0 + jb), n, nn, batch)
+    f.status = status
+    return f
+
+
+def trsm_right_upper(X, R, f: Factors, tmp):
+    """X_b <- X_b R_b^-1 in place (X: batch x rows x n, R upper n x n).
+    tmp: (batch, rows, nb) scratch."""
+    batch, rows, n = X.shape
+    nn = n * n
+    sx = rows * n
+    st = tmp.shape[1] * tmp.shape[2]
+    for bi, (j0, jb) in enumerate(f.blocks):
+        if j0 > 0:  # X[:, j] -= Z[:, :j0] R[:j0, j]
+            gemm(0, 0, rows, jb, j0, -1.0, addr(X), n, sx, addr(R, j0), n, nn, 1.0, addr(X, j0), n, sx, batch)
+        _lib.call("ublr_gather", addr(X, j0), n, sx, None, 0, rows, jb, 0, 0, addr(tmp), tmp.shape[2], st, batch,
+                  _lib.stream_handle())
+        gemm(0, 0, rows, jb, jb, 1.0, addr(tmp), tmp.shape[2], st, addr(f.inv[bi]), jb, jb * jb,
+             0.0, addr(X, j0), n, sx, batch)
+
+
+def trsm_left(T, X, f: Factors, inv_set, upper: bool, trans: bool, tmp):
+    """X_b <- op(T_b)^-1 X_b in place, op = transpose if `trans`.
+    T: batch x n x n (only the triangle selected by `upper` is read; the
+    diagonal blocks come from the stored inverses `inv_set` of T's own
+    diagonal blocks). X: batch x n x w. tmp: batch x nb x w."""
+    batch, n, w = X.shape
+    nn = n * n
+    sx = n * w
+    stt = tmp.shape[1] * tmp.shape[2]
+    eff_lower = (not upper) != trans  # lower-triangular after op
+    order = list(enumerate(f.blocks))
+    if not eff_lower:
+        order = order[::-1]
+    for bi, (j0, jb) in order:
+        if eff_lower and j0 > 0:
+            # X_j -= op(T)[j, :j0] X[:j0]; op(T)[j, :j0] = T[j, :j0] or T[:j0, j]^T
+            if not trans:
+                gemm(0, 0, jb, w, j0, -1.0, addr(T, j0 * n), n, nn, addr(X), w, sx, 1.0, addr(X, j0 * w), w, sx, batch)
+            else:
+                gemm(1, 0, jb, w, j0, -1.0, addr(T, j0), n, nn, addr(X), w, sx, 1.0, addr(X, j0 * w), w, sx, batch)
+        elif not eff_lower and j0 + jb < n:
+            rest = n - j0 - jb
+            if not trans:
+                gemm(0, 0, jb, w, rest, -1.0, addr(T, j0 * n + j0 + jb), n, nn, addr(X, (j0 + jb) * w), w, sx,
+                     1.0, addr(X, j0 * w), w, sx, batch)
+            else:
+                gemm(1, 0, jb, w, rest, -1.0, addr(T, (j0 + jb) * n + j0), n, nn, addr(X, (j0 + jb) * w), w, sx,
+                     1.0, addr(X, j0 * w), w, sx, batch)
+        _lib.call("ublr_gather", addr(X, j0 * w), w, sx, None, 0, jb, w, 0, 0, addr(tmp), w, stt, batch,
+                  _lib.stream_handle())
+        gemm(1 if trans else 0, 0, jb, w, jb, 1.0, addr(inv_set[bi]), jb, jb * jb, addr(tmp), w, stt,
+             0.0, addr(X, j0 * w), w, sx, batch)
+
+
+def check_status(f: Factors, what: str):
+    if int(f.status.item()) != 0:
+        raise np.linalg.LinAlgError(f"{what}: factorisation broke down (matrix not positive definite / singular)")

@@ -14,7 +14,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .bases import BlockBases, tagging_bases
+from .bases import BlockBases, block_nullification_bases, naive_bases, tagging_bases
 from .linalg import RandomStream, device_normals
 from .operators import CountingOperator, DifferenceOperator, LinearOperatorHandle, counting_wrapper, unwrap
 from .tagging import DegenerateTagsError, plan_tagging
@@ -328,8 +328,10 @@ def compress_type_a(op, tess, k, p=10, method="tag", stream=None, distribution="
             plan = plan_tagging(tess, extra_cols, distribution, stream.child(1), optimize=optimize,
                                 max_redraws=max_tag_redraws)
             bases, _ = tagging_bases(cop, tess, k, p, plan, stream.child(0), extra_samples=extra_samples)
-        elif method in ("bn", "naive"):
-            raise NotImplementedError(f"step-I method {method!r} lands with the next kernels")
+        elif method == "bn":
+            bases, _ = block_nullification_bases(cop, tess, k, p, stream.child(0))
+        elif method == "naive":
+            bases, _ = naive_bases(cop, tess, k, p, stream.child(0))
         else:
             raise ValueError(f"unknown step-I method {method!r}")
     with _PhaseTimer(times, "II"), cop.ledger.phase("II"):

@@ -130,3 +130,79 @@ def test_col_basis_matches_numpy(m, n, k):
     got = P.col_basis(B, k)
     want = O.leading_q(B, k)
     assert np.abs(got - want).max() <= 1e-12
+
+
+# ---------------------------------------------------------------- dense toolkit
+from paper_2501_05528_b200 import dense as Dn  # noqa: E402
+
+
+@pytest.mark.parametrize("n", [64, 150, 300])
+def test_blocked_cholesky_and_trsm(n):
+    rng = np.random.default_rng(n)
+    batch = 3
+    Bm = rng.standard_normal((batch, n, n + 20))
+    Gh = Bm @ Bm.transpose(0, 2, 1)
+    G = torch.from_numpy(Gh.copy()).cuda()
+    R = torch.zeros_like(G)
+    f = Dn.cholesky_upper(G, R)
+    Dn.check_status(f, "chol")
+    Rh = R.cpu().numpy()
+    for b in range(batch):
+        want = np.linalg.cholesky(Gh[b]).T
+        assert np.abs(Rh[b] - want).max() <= 1e-10 * np.abs(want).max()
+    X = torch.from_numpy(rng.standard_normal((batch, 37, n))).cuda()
+    Xh = X.cpu().numpy()
+    Dn.trsm_right_upper(X, R, f, torch.empty((batch, 37, Dn.NB), dtype=torch.float64, device="cuda"))
+    for b in range(batch):
+        assert np.abs(X.cpu().numpy()[b] @ Rh[b] - Xh[b]).max() <= 1e-11 * np.abs(Xh[b]).max()
+    for upper, trans in ((True, True), (True, False)):
+        Y = torch.from_numpy(rng.standard_normal((batch, n, 5))).cuda()
+        Yh = Y.cpu().numpy()
+        Dn.trsm_left(R, Y, f, f.inv, upper=upper, trans=trans,
+                     tmp=torch.empty((batch, Dn.NB, 5), dtype=torch.float64, device="cuda"))
+        for b in range(batch):
+            T = Rh[b].T if trans else Rh[b]
+            assert np.abs(T @ Y.cpu().numpy()[b] - Yh[b]).max() <= 1e-10 * np.abs(Yh[b]).max()
+
+
+def test_lu_sign_reconstructs_householder():
+    """LU of D - Qt_top with the sign rule gives LAPACK's tau in [1, 2]."""
+    rng = np.random.default_rng(3)
+    n, s = 130, 150
+    B = rng.standard_normal((n, s))
+    Qt = np.linalg.qr(B.T)[0]            # some thin Q (signs arbitrary)
+    W = torch.from_numpy((-Qt[:n])[None].copy()).cuda()
+    LU = torch.zeros_like(W)
+    Dg = torch.zeros((1, n), dtype=torch.float64, device="cuda")
+    f = Dn.lu_sign(W, LU, Dg)
+    Dn.check_status(f, "lu")
+    LUh, d = LU.cpu().numpy()[0], Dg.cpu().numpy()[0]
+    L = np.tril(LUh, -1) + np.eye(n)
+    U = np.triu(LUh)
+    assert np.abs(L @ U - (np.diag(d) - Qt[:n])).max() <= 1e-12
+    tau = np.diag(U) * d
+    assert tau.min() >= 1.0 - 1e-12 and tau.max() <= 2.0 + 1e-12
+
+
+def test_nullspace_samples_match_reference_null_basis():
+    from paper_2501_05528_b200.bases import nullspace_samples
+    pts = P.grid_points(32, 2)
+    tess = P.build_tessellation(pts, 16)
+    dt = device_tess(tess, torch.device(DEV))
+    k, p = 8, 4
+    r = k + p
+    s = P.block_nullification_width(tess, r)
+    rng = np.random.default_rng(11)
+    Om = rng.standard_normal((dt.n, s))          # original row order
+    Yh = rng.standard_normal((dt.n, s))
+    OP = dt.to_perm_rows(Om)
+    Yd = dt.to_perm_rows(Yh)
+    S = torch.zeros((dt.n, k), dtype=torch.float64, device=DEV)
+    nullspace_samples(dt, OP, s, 0, Yd, s, s, r, k, S)
+    Sh = dt.from_perm_rows(S)
+    for i in range(tess.b):
+        nbr = tess.neighbor_indices(i)
+        Pk = O.null_tail(Om[nbr], r)[:, :k]
+        want = Yh[tess.blocks[i]] @ Pk
+        got = Sh[tess.blocks[i]]
+        assert np.abs(got - want).max() <= 1e-11 * np.abs(want).max(), i
