@@ -173,6 +173,16 @@ int ublr_gather(const double* src, int64_t ld, int64_t s_src, const int32_t* map
 int ublr_scale_rows(double* X, int64_t ldx, int64_t s_x, const double* d, int64_t s_d, int rows, int cols,
                     int batch, void* stream);
 
+/* Type B (ref/reconstruction.py:326-376): per near pair p = (pair_i[p], .)
+ * comb_p[r, q] = sum_c w_p[c] Y[off_i + r, c*gc + q] (w_p = z_p / denominator_p),
+ * out is n_pairs x m_max x gc. */
+int ublr_tag_combine_pairs(const double* Y, int64_t ld_y, int gc, int ell, const double* w, const int32_t* pair_i,
+                           const int32_t* off, int n_pairs, int m_max, double* out, void* stream);
+/* Explicit tagged test matrix Omega[r, c*gc + q] = T[block(r), c] G[r, q]
+ * (ref/bases.py:126-137), permuted rows. */
+int ublr_assemble_tagged(const double* T, int ell, const double* G, int64_t ld_g, int gc, const int32_t* off, int b,
+                         double* out, int64_t ld_o, int64_t n, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -355,8 +355,47 @@ def compress_type_a(op, tess, k, p=10, method="tag", stream=None, distribution="
     return rep, report
 
 
-def compress_type_b(*args, **kwargs):
-    raise NotImplementedError("type-B reconstruction lands with the next kernels")
+def compress_type_b(op, tess, k, p=10, method="bn", stream=None, distribution="gaussian", optimize=False,
+                    max_tag_redraws=5, compute_error=True, error_iterations=20, max_width=None):
+    """ref/reconstruction.py:586-677 on the GPU: bases, near field from the
+    reused sketches (phase III), then the core by least squares (phase II)."""
+    from .tagging import b2_denominators_ok
+    from .typeb import gaussian_pinv_discrepancy, pinv_core, tagging_pinv_discrepancy
+
+    stream = stream or RandomStream(0)
+    if method not in ("bn", "tag"):
+        raise ValueError("type B supports methods 'bn' and 'tag'")
+    _lib.require_device()
+    cop = counting_wrapper(op)
+    times, plan = {}, None
+    with _PhaseTimer(times, "I"), cop.ledger.phase("I"):
+        if method == "bn":
+            bases, bundle = block_nullification_bases(cop, tess, k, p, stream.child(0))
+        else:
+            plan = plan_tagging(tess, 0, distribution, stream.child(1), optimize=optimize,
+                                max_redraws=max_tag_redraws, extra_check=lambda T: b2_denominators_ok(T, tess))
+            bases, bundle = tagging_bases(cop, tess, k, p, plan, stream.child(0),
+                                          group_cols=tess.max_block_size + p)
+    with _PhaseTimer(times, "III"), cop.ledger.phase("III"):
+        if method == "bn":
+            B = gaussian_pinv_discrepancy(bundle, bases)
+        else:
+            B = tagging_pinv_discrepancy(bundle, bases)
+    with _PhaseTimer(times, "II"), cop.ledger.phase("II"):
+        core, _ = pinv_core(cop, bundle, bases, B, p, stream.child(2), max_width=max_width)
+    rep = UniformBLR(tess, k, bases.U, bases.V, core, B, bases.dt, {"method": METHOD_IDS[("B", method)]})
+    rel = relative_error(op, rep, error_iterations, stream.child(9)) if compute_error else None
+    aspect, ell = None, None
+    if plan is not None:
+        ell = plan.matrix.n_cols
+        aspect = {"base": _ratio_summary(plan.rho_base), "draws": plan.attempts}
+    report = CompressionReport(
+        method=METHOD_IDS[("B", method)],
+        config=_base_config(tess, k, p, stream, ell=ell, distribution=distribution if method == "tag" else None,
+                            extra_cols=None, optimize=optimize),
+        matvecs=cop.ledger.to_dict(), times_s=times, relative_error=rel,
+        storage_entries=rep.storage_entries, aspect_ratios=aspect)
+    return rep, report
 
 
 def compress(op, tess, k, method_id: str = "A2", **kwargs):

@@ -49,8 +49,8 @@ def ahat_error_vs_golden(rep, g, ncols=3):
 
 
 @pytest.mark.parametrize("name", ["c1s_A2", "log1k_A2", "rand500_A2", "c1_A2", "c2_A2",
-                                  "log1k_A1", "rand500_A1", "log1k_A3"])
-def test_compress_typeA_matches_reference(name):
+                                  "log1k_A1", "rand500_A1", "log1k_A3", "log1k_B1", "log1k_B2"])
+def test_compress_matches_reference(name):
     tess, op, _ = gpu_problem(name)
     _, _, k, p, mid, seed = build_case(name)
     rep, report = P.compress(op, tess, k, mid, p=p, stream=P.RandomStream(seed), compute_error=False)
@@ -62,8 +62,9 @@ def test_compress_typeA_matches_reference(name):
     assert report.storage_entries == int(g["storage_entries"])
 
 
-@pytest.mark.parametrize("name", ["c1s_A2", "log1k_A2", "c2_A2", "log1k_A1", "log1k_A3"])
-def test_compress_typeA_dense_frobenius_vs_oracle(name):
+@pytest.mark.parametrize("name", ["c1s_A2", "log1k_A2", "c2_A2", "log1k_A1", "log1k_A3", "log1k_B1",
+                                  "log1k_B2"])
+def test_compress_dense_frobenius_vs_oracle(name):
     """Full ||A_hat_gpu - A_hat_oracle||_F / ||A||_F on the same inputs, and the
     approximation error within 1.05x of the oracle's."""
     tess, op, A = gpu_problem(name)
