@@ -13,6 +13,7 @@
 //   variant pushes [G | H] through one pass over A (Z = A^T Psi = A Psi).
 #include "common.cuh"
 #include "optile.cuh"
+#include "gemm_core.cuh"
 
 namespace ublr {
 namespace {
@@ -103,6 +104,103 @@ __global__ void __launch_bounds__(AP_THREADS) k_apply(ublr_op_t op, const double
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
       int c = col0 + wc * WN + j * 8 + 2 * t;
+      if (c < w) out[(int64_t)r * ldo + c] = acc[i][j][0];
+      if (c + 1 < w) out[(int64_t)r * ldo + c + 1] = acc[i][j][1];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ apply v2
+// Producers for the shared DMMA main loop (gemm_core.cuh).
+template <int KIND, class Cfg>
+struct GenAProducer {
+  const ublr_op_t& op;
+  const LogTables* lt;
+  int row0, n;
+  RowPoint rp;
+  int grow, gk0;
+  __device__ GenAProducer(const ublr_op_t& op_, const LogTables* lt_, int row0_)
+      : op(op_), lt(lt_), row0(row0_), n((int)op_.n) {
+    grow = threadIdx.x % Cfg::BM;
+    gk0 = threadIdx.x / Cfg::BM;
+    rp = load_row_point(op, row0 + grow, row0 + grow < n);
+  }
+  __device__ __forceinline__ void stage(double* As, int ks) {
+    constexpr int KL = Cfg::NT / Cfg::BM;  // kk lanes
+    const int k0 = ks * Cfg::BK;
+#pragma unroll
+    for (int e = 0; e < Cfg::BK / KL; ++e) {
+      int kk = gk0 + e * KL;
+      int q = k0 + kk;
+      double v = 0.0;
+      if (rp.p >= 0 && q < n) v = op_entry<KIND>(op, rp, q, lt);
+      As[kk * Cfg::SA + grow] = v;
+    }
+  }
+};
+
+// B tile from a row-major matrix X (K rows x N cols, ld), rows k, cols n0..
+template <class Cfg>
+struct RowMajorBProducer {
+  const double* X;
+  int64_t ld;
+  int K, N, n0;
+  bool vec2;
+  __device__ __forceinline__ void stage(double* Bs, int ks) {
+    const int k0 = ks * Cfg::BK;
+    if (vec2) {
+      constexpr int HALF = Cfg::BN / 2;
+      for (int e = threadIdx.x; e < Cfg::BK * HALF; e += Cfg::NT) {
+        int kk = e / HALF, c = (e - kk * HALF) * 2;
+        int q = k0 + kk, col = n0 + c;
+        bool ok = q < K && col + 1 < N;
+        if (ok) {
+          cp_async16(&Bs[kk * Cfg::SB + c], X + (int64_t)q * ld + col, true);
+        } else {
+          cp_async8(&Bs[kk * Cfg::SB + c], (q < K && col < N) ? (const void*)(X + (int64_t)q * ld + col) : (const void*)X,
+                    q < K && col < N);
+          cp_async8(&Bs[kk * Cfg::SB + c + 1], X, false);
+        }
+      }
+    } else {
+      for (int e = threadIdx.x; e < Cfg::BK * Cfg::BN; e += Cfg::NT) {
+        int kk = e / Cfg::BN, c = e - kk * Cfg::BN;
+        int q = k0 + kk, col = n0 + c;
+        bool ok = q < K && col < N;
+        cp_async8(&Bs[kk * Cfg::SB + c], ok ? (const void*)(X + (int64_t)q * ld + col) : (const void*)X, ok);
+      }
+    }
+  }
+};
+
+template <int KIND, class Cfg>
+__global__ void __launch_bounds__(Cfg::NT) k_apply2(ublr_op_t op, const double* __restrict__ X, int64_t ldx, int w,
+                                                    double* __restrict__ out, int64_t ldo, int vec2) {
+  __shared__ LogTables lt;
+  extern __shared__ double dsm[];
+  if (KIND == UBLR_OP_LOG) init_log_tables(&lt);
+  const int n = (int)op.n;
+  const int row0 = blockIdx.y * Cfg::BM;
+  const int col0 = blockIdx.x * Cfg::BN;
+  GenAProducer<KIND, Cfg> ap(op, &lt, row0);
+  RowMajorBProducer<Cfg> bp{X, ldx, n, w, col0, vec2 != 0};
+  double acc[Cfg::MI][Cfg::NJ][2];
+#pragma unroll
+  for (int i = 0; i < Cfg::MI; ++i)
+#pragma unroll
+    for (int j = 0; j < Cfg::NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  __syncthreads();
+  dmma_mainloop<Cfg>(ap, bp, (n + Cfg::BK - 1) / Cfg::BK, dsm, acc);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wr = warp / Cfg::WNW, wc = warp % Cfg::WNW;
+#pragma unroll
+  for (int i = 0; i < Cfg::MI; ++i) {
+    int r = row0 + wr * Cfg::WM + i * 8 + g;
+    if (r >= n) continue;
+#pragma unroll
+    for (int j = 0; j < Cfg::NJ; ++j) {
+      int c = col0 + wc * Cfg::WN + j * 8 + 2 * t;
       if (c < w) out[(int64_t)r * ldo + c] = acc[i][j][0];
       if (c + 1 < w) out[(int64_t)r * ldo + c + 1] = acc[i][j][1];
     }
@@ -262,20 +360,23 @@ extern "C" int ublr_apply(const ublr_op_t* op, const double* X, int64_t ld_x, in
   cudaStream_t st = (cudaStream_t)stream;
   dim3 grid;
   grid.y = (unsigned)((op->n + AP_BM - 1) / AP_BM);
-#define UBLR_AP_LAUNCH(BN)                                                                                 \
-  UBLR_DISPATCH_KIND(op->kind, KIND, {                                                                    \
-    size_t sm = (size_t)2 * AP_BK * ((AP_BM + 4) + ((BN) + 4)) * sizeof(double);                         \
-    UBLR_CUDA(cudaFuncSetAttribute(k_apply<KIND, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
-    k_apply<KIND, BN><<<grid, AP_THREADS, sm, st>>>(*op, X, ld_x, w, out, ld_o);                           \
+  using CfgW = TileCfg<128, 128, 32, 4, 4, 2>;
+  using CfgN = TileCfg<128, 64, 32, 4, 4, 2>;
+  int vec2 = ((ld_x % 2) == 0 && (((uintptr_t)X) % 16) == 0) ? 1 : 0;
+#define UBLR_AP2(CFG)                                                                                         \
+  UBLR_DISPATCH_KIND(op->kind, KIND, {                                                                      \
+    size_t sm = CFG::smem_bytes();                                                                          \
+    UBLR_CUDA(cudaFuncSetAttribute(k_apply2<KIND, CFG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
+    k_apply2<KIND, CFG><<<grid, CFG::NT, sm, st>>>(*op, X, ld_x, w, out, ld_o, vec2);                         \
   })
   if (w <= 64) {
     grid.x = (unsigned)((w + 63) / 64);
-    UBLR_AP_LAUNCH(64);
+    UBLR_AP2(CfgN);
   } else {
     grid.x = (unsigned)((w + 127) / 128);
-    UBLR_AP_LAUNCH(128);
+    UBLR_AP2(CfgW);
   }
-#undef UBLR_AP_LAUNCH
+#undef UBLR_AP2
   UBLR_LAUNCH_CHECK();
   return UBLR_OK;
 }
