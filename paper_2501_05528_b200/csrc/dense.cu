@@ -14,6 +14,7 @@
 //   (tau_j = pivot_j * D_jj in [1, 2]); see DESIGN.md §bn null space.
 //   Also returns L^-1 and U^-1 of the block.
 #include "common.cuh"
+#include "gemm_core.cuh"
 
 namespace ublr {
 namespace {
@@ -21,20 +22,15 @@ namespace {
 constexpr int GT = 256;
 constexpr int GBK = 16;
 
-template <int BM, int BN, bool TA, bool TB>
-__global__ void __launch_bounds__(GT) k_gemm(int M, int N, int K, double alpha, const double* __restrict__ A,
-                                             int64_t lda, int64_t sA, const int32_t* __restrict__ amap,
-                                             int64_t sAm, const double* __restrict__ B, int64_t ldb, int64_t sB,
-                                             const int32_t* __restrict__ bmap, int64_t sBm, double beta,
-                                             double* __restrict__ C, int64_t ldc, int64_t sC,
-                                             const int32_t* __restrict__ cmap, int64_t sCm) {
-  constexpr int SA = BM + 4;
-  constexpr int SB = BN + 4;
-  constexpr int WM = BM / 2, WN = BN / 4;
-  constexpr int MI = WM / 8, NJ = WN / 8;
+template <class Cfg, bool TA, bool TB>
+__global__ void __launch_bounds__(Cfg::NT) k_gemm2(int M, int N, int K, double alpha, const double* __restrict__ A,
+                                                   int64_t lda, int64_t sA, const int32_t* __restrict__ amap,
+                                                   int64_t sAm, const double* __restrict__ B, int64_t ldb, int64_t sB,
+                                                   const int32_t* __restrict__ bmap, int64_t sBm, double beta,
+                                                   double* __restrict__ C, int64_t ldc, int64_t sC,
+                                                   const int32_t* __restrict__ cmap, int64_t sCm, int vecA, int vecB) {
+  static_assert(Cfg::A_KM == TA && Cfg::B_KM == !TB, "tile orientation must follow the operand storage");
   extern __shared__ double dsm[];
-  double (*As)[GBK][SA] = reinterpret_cast<double (*)[GBK][SA]>(dsm);
-  double (*Bs)[GBK][SB] = reinterpret_cast<double (*)[GBK][SB]>(dsm + 2 * GBK * SA);
   const int bz = blockIdx.z;
   A += bz * sA;
   B += bz * sB;
@@ -42,101 +38,84 @@ __global__ void __launch_bounds__(GT) k_gemm(int M, int N, int K, double alpha, 
   if (amap) amap += bz * sAm;
   if (bmap) bmap += bz * sBm;
   if (cmap) cmap += bz * sCm;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int m0 = blockIdx.y * Cfg::BM, n0 = blockIdx.x * Cfg::BN;
+  struct AP {
+    const double* A; int64_t lda; const int32_t* amap; int M, K, m0; bool vec;
+    __device__ __forceinline__ void stage(double* As, int ks) {
+      const int k0 = ks * Cfg::BK;
+      if (TA) {
+        if (amap) tile_copy<Cfg::NT>(As, Cfg::SA, A, lda, Cfg::BK, Cfg::BM, k0, m0, K, M, MappedRows{amap}, vec);
+        else tile_copy<Cfg::NT>(As, Cfg::SA, A, lda, Cfg::BK, Cfg::BM, k0, m0, K, M, IdentityRows{}, vec);
+      } else {
+        if (amap) tile_copy<Cfg::NT>(As, Cfg::SA, A, lda, Cfg::BM, Cfg::BK, m0, k0, M, K, MappedRows{amap}, vec);
+        else tile_copy<Cfg::NT>(As, Cfg::SA, A, lda, Cfg::BM, Cfg::BK, m0, k0, M, K, IdentityRows{}, vec);
+      }
+    }
+  } ap{A, lda, amap, M, K, m0, vecA != 0};
+  struct BP {
+    const double* B; int64_t ldb; const int32_t* bmap; int N, K, n0; bool vec;
+    __device__ __forceinline__ void stage(double* Bs, int ks) {
+      const int k0 = ks * Cfg::BK;
+      if (!TB) {
+        if (bmap) tile_copy<Cfg::NT>(Bs, Cfg::SB, B, ldb, Cfg::BK, Cfg::BN, k0, n0, K, N, MappedRows{bmap}, vec);
+        else tile_copy<Cfg::NT>(Bs, Cfg::SB, B, ldb, Cfg::BK, Cfg::BN, k0, n0, K, N, IdentityRows{}, vec);
+      } else {
+        if (bmap) tile_copy<Cfg::NT>(Bs, Cfg::SB, B, ldb, Cfg::BN, Cfg::BK, n0, k0, N, K, MappedRows{bmap}, vec);
+        else tile_copy<Cfg::NT>(Bs, Cfg::SB, B, ldb, Cfg::BN, Cfg::BK, n0, k0, N, K, IdentityRows{}, vec);
+      }
+    }
+  } bp{B, ldb, bmap, N, K, n0, vecB != 0};
+  double acc[Cfg::MI][Cfg::NJ][2];
+#pragma unroll
+  for (int i = 0; i < Cfg::MI; ++i)
+#pragma unroll
+    for (int j = 0; j < Cfg::NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  dmma_mainloop<Cfg>(ap, bp, (K + Cfg::BK - 1) / Cfg::BK, dsm, acc);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int wr = warp >> 2, wc = warp & 3;
-
-  double acc[MI][NJ][2];
+  const int wr = warp / Cfg::WNW, wc = warp % Cfg::WNW;
 #pragma unroll
-  for (int i = 0; i < MI; ++i)
-#pragma unroll
-    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-  auto stage = [&](int buf, int k0) {
-    for (int e = tid; e < BM * GBK; e += GT) {
-      int i, kk;
-      if (!TA) { kk = e % GBK; i = e / GBK; } else { i = e % BM; kk = e / BM; }
-      int gi = m0 + i, gk = k0 + kk;
-      bool ok = gi < M && gk < K;
-      const double* src = A;
-      if (ok) {
-        if (!TA) { int64_t pr = amap ? amap[gi] : gi; src = A + pr * lda + gk; }
-        else { int64_t pr = amap ? amap[gk] : gk; src = A + pr * lda + gi; }
-      }
-      cp_async8(&As[buf][kk][i], src, ok);
-    }
-    for (int e = tid; e < BN * GBK; e += GT) {
-      int j, kk;
-      if (!TB) { j = e % BN; kk = e / BN; } else { kk = e % GBK; j = e / GBK; }
-      int gj = n0 + j, gk = k0 + kk;
-      bool ok = gj < N && gk < K;
-      const double* src = B;
-      if (ok) {
-        if (!TB) { int64_t pr = bmap ? bmap[gk] : gk; src = B + pr * ldb + gj; }
-        else { int64_t pr = bmap ? bmap[gj] : gj; src = B + pr * ldb + gk; }
-      }
-      cp_async8(&Bs[buf][kk][j], src, ok);
-    }
-    cp_async_commit();
-  };
-
-  const int nk = (K + GBK - 1) / GBK;
-  if (nk > 0) stage(0, 0);
-  for (int ks = 0; ks < nk; ++ks) {
-    int buf = ks & 1;
-    cp_async_wait<0>();
-    __syncthreads();
-    if (ks + 1 < nk) stage(buf ^ 1, (ks + 1) * GBK);
-#pragma unroll
-    for (int k4 = 0; k4 < GBK; k4 += 4) {
-      double a[MI], bb[NJ];
-#pragma unroll
-      for (int i = 0; i < MI; ++i) a[i] = As[buf][k4 + t][wr * WM + i * 8 + g];
-#pragma unroll
-      for (int j = 0; j < NJ; ++j) bb[j] = Bs[buf][k4 + t][wc * WN + j * 8 + g];
-#pragma unroll
-      for (int i = 0; i < MI; ++i)
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) mma8x8x4(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < MI; ++i) {
-    int r = m0 + wr * WM + i * 8 + g;
+  for (int i = 0; i < Cfg::MI; ++i) {
+    int r = m0 + wr * Cfg::WM + i * 8 + g;
     if (r >= M) continue;
+    double* crow = C + (int64_t)(cmap ? cmap[r] : r) * ldc;
 #pragma unroll
-    for (int j = 0; j < NJ; ++j) {
+    for (int j = 0; j < Cfg::NJ; ++j) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        int c = n0 + wc * WN + j * 8 + 2 * t + h;
+        int c = n0 + wc * Cfg::WN + j * 8 + 2 * t + h;
         if (c >= N) continue;
         double v = alpha * acc[i][j][h];
-        double* dst = C + (int64_t)(cmap ? cmap[r] : r) * ldc + c;
-        *dst = (beta == 0.0) ? v : fma(beta, *dst, v);
+        crow[c] = (beta == 0.0) ? v : fma(beta, crow[c], v);
       }
     }
   }
 }
 
-template <int BM, int BN>
-int launch_gemm(int ta, int tb, int M, int N, int K, double alpha, const double* A, int64_t lda, int64_t sA,
-                const int32_t* amap, int64_t sAm, const double* B, int64_t ldb, int64_t sB, const int32_t* bmap,
-                int64_t sBm, double beta, double* C, int64_t ldc, int64_t sC, const int32_t* cmap, int64_t sCm,
-                int batch, cudaStream_t st) {
+template <int BM, int BN, int WMW, int WNW, int STAGES>
+int launch_gemm2(int ta, int tb, int M, int N, int K, double alpha, const double* A, int64_t lda, int64_t sA,
+                 const int32_t* amap, int64_t sAm, const double* B, int64_t ldb, int64_t sB, const int32_t* bmap,
+                 int64_t sBm, double beta, double* C, int64_t ldc, int64_t sC, const int32_t* cmap, int64_t sCm,
+                 int batch, cudaStream_t st) {
   dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, batch);
-  size_t sm = (size_t)2 * GBK * ((BM + 4) + (BN + 4)) * sizeof(double);
-#define UBLR_G(TA, TB)                                                                                      \
-  {                                                                                                         \
-    UBLR_CUDA(cudaFuncSetAttribute(k_gemm<BM, BN, TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
-    k_gemm<BM, BN, TA, TB><<<grid, GT, sm, st>>>(M, N, K, alpha, A, lda, sA, amap, sAm, B, ldb, sB, bmap, sBm, \
-                                                 beta, C, ldc, sC, cmap, sCm);                             \
+  auto aligned = [](const void* p, int64_t ld, int64_t stride) {
+    return (((uintptr_t)p) % 16 == 0) && (ld % 2 == 0) && (stride % 2 == 0);
+  };
+  int vecA = aligned(A, lda, sA) ? 1 : 0;
+  int vecB = aligned(B, ldb, sB) ? 1 : 0;
+#define UBLR_G2(TA, TB)                                                                                       \
+  {                                                                                                           \
+    using Cfg = TileCfg<BM, BN, 32, WMW, WNW, STAGES, TA, !TB>;                                               \
+    size_t sm = Cfg::smem_bytes();                                                                            \
+    UBLR_CUDA(cudaFuncSetAttribute(k_gemm2<Cfg, TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
+    k_gemm2<Cfg, TA, TB><<<grid, Cfg::NT, sm, st>>>(M, N, K, alpha, A, lda, sA, amap, sAm, B, ldb, sB, bmap, sBm,  \
+                                                    beta, C, ldc, sC, cmap, sCm, vecA, vecB);                 \
   }
-  if (!ta && !tb) UBLR_G(false, false)
-  else if (!ta && tb) UBLR_G(false, true)
-  else if (ta && !tb) UBLR_G(true, false)
-  else UBLR_G(true, true)
-#undef UBLR_G
+  if (!ta && !tb) UBLR_G2(false, false)
+  else if (!ta && tb) UBLR_G2(false, true)
+  else if (ta && !tb) UBLR_G2(true, false)
+  else UBLR_G2(true, true)
+#undef UBLR_G2
   UBLR_LAUNCH_CHECK();
   return UBLR_OK;
 }
@@ -324,10 +303,10 @@ extern "C" int ublr_gemm_batched(int ta, int tb, int M, int N, int K, double alp
   cudaStream_t st = (cudaStream_t)stream;
   int64_t tiles128 = (int64_t)((M + 127) / 128) * ((N + 127) / 128) * batch;
   if (M >= 96 && N >= 96 && tiles128 >= 148)
-    return launch_gemm<128, 128>(ta, tb, M, N, K, alpha, A, lda, sA, amap, sAm, B, ldb, sB, bmap, sBm, beta, C, ldc,
-                                 sC, cmap, sCm, batch, st);
-  return launch_gemm<64, 64>(ta, tb, M, N, K, alpha, A, lda, sA, amap, sAm, B, ldb, sB, bmap, sBm, beta, C, ldc, sC,
-                             cmap, sCm, batch, st);
+    return launch_gemm2<128, 128, 4, 4, 2>(ta, tb, M, N, K, alpha, A, lda, sA, amap, sAm, B, ldb, sB, bmap, sBm, beta,
+                                           C, ldc, sC, cmap, sCm, batch, st);
+  return launch_gemm2<64, 64, 2, 4, 2>(ta, tb, M, N, K, alpha, A, lda, sA, amap, sAm, B, ldb, sB, bmap, sBm, beta, C,
+                                       ldc, sC, cmap, sCm, batch, st);
 }
 
 extern "C" int ublr_potrf_diag(double* A, int64_t lda, int64_t sA, int j0, int nb, double* R, int64_t ldr,

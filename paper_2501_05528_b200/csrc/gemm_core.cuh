@@ -1,36 +1,45 @@
 // Shared fp64 DMMA main loop for the operator-apply and batched GEMM kernels.
 //
 // CTA tile BM x BN, k-step BK, WMW x WNW warps, each warp owning a
-// (BM/WMW) x (BN/WNW) tile of m8n8k4 accumulators. Operand tiles live in
-// shared memory k-major (As[k][m], Bs[k][n]) with a +4 double pad, so the
-// fragment loads (lane (g, t) reads As[k0+t][m0+g]) are conflict-free.
-// A STAGES-deep ring of shared buffers lets the producers (cp.async for
-// stored operands, in-register generation for operator tiles) fill stage
-// ks+STAGES-1 while the tensor pipe consumes stage ks; the fragments of the
-// next k4 slice are loaded before the current slice's DMMAs issue.
+// (BM/WMW) x (BN/WNW) tile of m8n8k4 accumulators. Each operand tile is kept
+// in shared memory in the orientation its global source is contiguous in
+// (so cp.async can move 16-byte chunks):
+//   A k-major As[k][m] (stride BM+4)  or m-major As[m][k] (stride BK+4),
+//   B k-major Bs[k][n] (stride BN+4)  or n-major Bs[n][k] (stride BK+4).
+// With those +4 pads the fragment loads (lane (g, t) reads A[m0+g][k0+t],
+// B[k0+t][n0+g]) are bank-conflict-free in both orientations.
+// A STAGES-deep ring lets the producers (cp.async for stored operands,
+// in-register generation for operator tiles) fill stage ks+STAGES-1 while
+// the tensor pipe consumes stage ks; the fragments of the next k4 slice are
+// loaded before the current slice's DMMAs issue.
 #pragma once
 #include "common.cuh"
 
 namespace ublr {
 
-template <int BM_, int BN_, int BK_, int WMW_, int WNW_, int STAGES_>
+template <int BM_, int BN_, int BK_, int WMW_, int WNW_, int STAGES_, bool A_KM_ = true, bool B_KM_ = true>
 struct TileCfg {
   static constexpr int BM = BM_, BN = BN_, BK = BK_, WMW = WMW_, WNW = WNW_, STAGES = STAGES_;
+  static constexpr bool A_KM = A_KM_, B_KM = B_KM_;
   static constexpr int NT = WMW * WNW * 32;
-  static constexpr int SA = BM + 4;
-  static constexpr int SB = BN + 4;
+  static constexpr int SA = A_KM ? BM + 4 : BK + 4;  // row stride of the A tile in smem
+  static constexpr int SB = B_KM ? BN + 4 : BK + 4;
   static constexpr int WM = BM / WMW;
   static constexpr int WN = BN / WNW;
   static constexpr int MI = WM / 8;
   static constexpr int NJ = WN / 8;
-  static constexpr int A_STAGE = BK * SA;  // doubles
-  static constexpr int B_STAGE = BK * SB;
+  static constexpr int A_STAGE = A_KM ? BK * SA : BM * SA;  // doubles
+  static constexpr int B_STAGE = B_KM ? BK * SB : BN * SB;
   static constexpr size_t smem_bytes() { return (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double); }
+  // smem index of A(m, k) / B(k, n) inside one stage
+  __device__ static __forceinline__ int ai(int m, int k) { return A_KM ? k * SA + m : m * SA + k; }
+  __device__ static __forceinline__ int bi(int k, int n) { return B_KM ? k * SB + n : n * SB + k; }
 };
 
 // acc += A_tile * B_tile over nk k-steps. Producers fill one stage:
-//   ap.stage(double* As /*[BK][SA]*/, int ks);  bp.stage(double* Bs /*[BK][SB]*/, int ks)
-// and may issue cp.async; one commit group per stage is made here.
+//   ap.stage(double* As, int ks);  bp.stage(double* Bs, int ks)
+// (indexing through Cfg::ai / Cfg::bi) and may issue cp.async; one commit
+// group per stage is made here.
 template <class Cfg, class AP, class BP>
 __device__ __forceinline__ void dmma_mainloop(AP& ap, BP& bp, int nk, double* smem,
                                               double (&acc)[Cfg::MI][Cfg::NJ][2]) {
@@ -67,18 +76,18 @@ __device__ __forceinline__ void dmma_mainloop(AP& ap, BP& bp, int nk, double* sm
     const double* Bs = Bs0 + (ks % STAGES) * Cfg::B_STAGE;
     double a[2][Cfg::MI], b[2][Cfg::NJ];
 #pragma unroll
-    for (int i = 0; i < Cfg::MI; ++i) a[0][i] = As[t * Cfg::SA + am0 + i * 8];
+    for (int i = 0; i < Cfg::MI; ++i) a[0][i] = As[Cfg::ai(am0 + i * 8, t)];
 #pragma unroll
-    for (int j = 0; j < Cfg::NJ; ++j) b[0][j] = Bs[t * Cfg::SB + bn0 + j * 8];
+    for (int j = 0; j < Cfg::NJ; ++j) b[0][j] = Bs[Cfg::bi(t, bn0 + j * 8)];
 #pragma unroll
     for (int k4 = 0; k4 < BK / 4; ++k4) {
       const int cur = k4 & 1;
       if (k4 + 1 < BK / 4) {
         const int kr = (k4 + 1) * 4 + t;
 #pragma unroll
-        for (int i = 0; i < Cfg::MI; ++i) a[cur ^ 1][i] = As[kr * Cfg::SA + am0 + i * 8];
+        for (int i = 0; i < Cfg::MI; ++i) a[cur ^ 1][i] = As[Cfg::ai(am0 + i * 8, kr)];
 #pragma unroll
-        for (int j = 0; j < Cfg::NJ; ++j) b[cur ^ 1][j] = Bs[kr * Cfg::SB + bn0 + j * 8];
+        for (int j = 0; j < Cfg::NJ; ++j) b[cur ^ 1][j] = Bs[Cfg::bi(kr, bn0 + j * 8)];
       }
 #pragma unroll
       for (int i = 0; i < Cfg::MI; ++i)
@@ -88,5 +97,44 @@ __device__ __forceinline__ void dmma_mainloop(AP& ap, BP& bp, int nk, double* sm
   }
   cp_async_wait<0>();
 }
+
+// Copy a (rows x cols) tile of a row-major global matrix, contiguous along
+// cols, into shared memory at dst[r * sstride + c] (r < rows, c < cols),
+// zero-filling outside (rlim, clim). Row r's global row is rowmap(r).
+// 16-byte cp.async when `vec2` (even ld / offsets, 16B-aligned base).
+template <int NT, class RowMap>
+__device__ __forceinline__ void tile_copy(double* dst, int sstride, const double* src, int64_t ld, int rows, int cols,
+                                          int r0, int c0, int rlim, int clim, RowMap rowmap, bool vec2) {
+  if (vec2) {
+    const int half = cols >> 1;
+    for (int e = threadIdx.x; e < rows * half; e += NT) {
+      int r = e / half, c = (e - r * half) * 2;
+      int gr = r0 + r, gc = c0 + c;
+      double* d = dst + r * sstride + c;
+      if (gr < rlim && gc + 1 < clim) {
+        cp_async16(d, src + (int64_t)rowmap(gr) * ld + gc, true);
+      } else {
+        bool ok = gr < rlim && gc < clim;
+        cp_async8(d, ok ? (const void*)(src + (int64_t)rowmap(gr) * ld + gc) : (const void*)src, ok);
+        cp_async8(d + 1, src, false);
+      }
+    }
+  } else {
+    for (int e = threadIdx.x; e < rows * cols; e += NT) {
+      int r = e / cols, c = e - r * cols;
+      int gr = r0 + r, gc = c0 + c;
+      bool ok = gr < rlim && gc < clim;
+      cp_async8(dst + r * sstride + c, ok ? (const void*)(src + (int64_t)rowmap(gr) * ld + gc) : (const void*)src, ok);
+    }
+  }
+}
+
+struct IdentityRows {
+  __device__ __forceinline__ int operator()(int r) const { return r; }
+};
+struct MappedRows {
+  const int32_t* map;
+  __device__ __forceinline__ int operator()(int r) const { return map[r]; }
+};
 
 }  // namespace ublr

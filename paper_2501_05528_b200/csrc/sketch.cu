@@ -134,7 +134,7 @@ struct GenAProducer {
       int q = k0 + kk;
       double v = 0.0;
       if (rp.p >= 0 && q < n) v = op_entry<KIND>(op, rp, q, lt);
-      As[kk * Cfg::SA + grow] = v;
+      As[Cfg::ai(grow, kk)] = v;
     }
   }
 };
@@ -147,29 +147,7 @@ struct RowMajorBProducer {
   int K, N, n0;
   bool vec2;
   __device__ __forceinline__ void stage(double* Bs, int ks) {
-    const int k0 = ks * Cfg::BK;
-    if (vec2) {
-      constexpr int HALF = Cfg::BN / 2;
-      for (int e = threadIdx.x; e < Cfg::BK * HALF; e += Cfg::NT) {
-        int kk = e / HALF, c = (e - kk * HALF) * 2;
-        int q = k0 + kk, col = n0 + c;
-        bool ok = q < K && col + 1 < N;
-        if (ok) {
-          cp_async16(&Bs[kk * Cfg::SB + c], X + (int64_t)q * ld + col, true);
-        } else {
-          cp_async8(&Bs[kk * Cfg::SB + c], (q < K && col < N) ? (const void*)(X + (int64_t)q * ld + col) : (const void*)X,
-                    q < K && col < N);
-          cp_async8(&Bs[kk * Cfg::SB + c + 1], X, false);
-        }
-      }
-    } else {
-      for (int e = threadIdx.x; e < Cfg::BK * Cfg::BN; e += Cfg::NT) {
-        int kk = e / Cfg::BN, c = e - kk * Cfg::BN;
-        int q = k0 + kk, col = n0 + c;
-        bool ok = q < K && col < N;
-        cp_async8(&Bs[kk * Cfg::SB + c], ok ? (const void*)(X + (int64_t)q * ld + col) : (const void*)X, ok);
-      }
-    }
+    tile_copy<Cfg::NT>(Bs, Cfg::SB, X, ld, Cfg::BK, Cfg::BN, ks * Cfg::BK, n0, K, N, IdentityRows{}, vec2);
   }
 };
 
@@ -346,6 +324,163 @@ __global__ void __launch_bounds__(TS_THREADS) k_sketch_tagged(ublr_op_t op, cons
   }
 }
 
+// ------------------------------------------------------- tagged sketch v2
+// CTA = 64 consecutive permuted rows x BN test-block columns, 16 warps
+// (4 x 4; warp tile 16 x BN/4). k-steps run block by block (step table from
+// the host: block j, first column, end column); at the last step of block j
+// each thread folds its W = A_{rows, J_j} X_j fragment into the ell tag
+// groups held in registers: acc[c] += T[j, c] * W. Row tiles of 64 keep the
+// test-block panel reuse at 64 rows per load (L2 traffic ~2 TB/s at peak).
+template <int KIND, int L, class Cfg>
+__global__ void __launch_bounds__(Cfg::NT) k_sketch_tagged2(ublr_op_t op, const int4* __restrict__ steps, int nsteps,
+                                                            const double* __restrict__ T, int ell,
+                                                            const double* __restrict__ G,
+                                                            const double* __restrict__ H, int64_t ldx, int gc,
+                                                            double* __restrict__ Y, double* __restrict__ Z,
+                                                            int64_t ldy, int vec2) {
+  constexpr int BK = Cfg::BK, STAGES = Cfg::STAGES;
+  __shared__ LogTables lt;
+  extern __shared__ double dsm[];
+  if (KIND == UBLR_OP_LOG) init_log_tables(&lt);
+  const int n = (int)op.n;
+  const int ncols = (H ? 2 : 1) * gc;
+  const int row0 = blockIdx.y * Cfg::BM;
+  const int col0 = blockIdx.x * Cfg::BN;
+  GenAProducer<KIND, Cfg> ap(op, &lt, row0);
+  // A producer works on absolute column indices q0 .. q0+BK masked by qend
+  struct AStep {
+    GenAProducer<KIND, Cfg>* g;
+    const int4* steps;
+    __device__ __forceinline__ void stage(double* As, int ks) {
+      int4 s = steps[ks];
+      constexpr int KL = Cfg::NT / Cfg::BM;
+#pragma unroll
+      for (int e = 0; e < BK / KL; ++e) {
+        int kk = g->gk0 + e * KL;
+        int q = s.y + kk;
+        double v = 0.0;
+        if (g->rp.p >= 0 && q < s.z) v = op_entry<KIND>(g->op, g->rp, q, g->lt);
+        As[Cfg::ai(g->grow, kk)] = v;
+      }
+    }
+  } as{&ap, steps};
+  struct BStep {
+    const double* G; const double* H; int64_t ldx; int gc, ncols, col0; bool vec2; const int4* steps;
+    __device__ __forceinline__ void stage(double* Bs, int ks) {
+      int4 s = steps[ks];
+      // columns [col0, col0+BN) of [G | H]; the G/H split is at gc
+      if (col0 + Cfg::BN <= gc || !H) {
+        tile_copy<Cfg::NT>(Bs, Cfg::SB, G, ldx, BK, Cfg::BN, s.y, col0, s.z, gc, IdentityRows{}, vec2 && !(gc & 1));
+      } else if (col0 >= gc) {
+        tile_copy<Cfg::NT>(Bs, Cfg::SB, H, ldx, BK, Cfg::BN, s.y, col0 - gc, s.z, gc, IdentityRows{}, vec2 && !(gc & 1));
+      } else {
+        for (int e = threadIdx.x; e < BK * Cfg::BN; e += Cfg::NT) {
+          int kk = e / Cfg::BN, c = e - kk * Cfg::BN;
+          int q = s.y + kk, col = col0 + c;
+          bool ok = q < s.z && col < ncols;
+          const double* src = G;
+          if (ok) src = (col < gc) ? (G + (int64_t)q * ldx + col) : (H + (int64_t)q * ldx + (col - gc));
+          cp_async8(&Bs[kk * Cfg::SB + c], src, ok);
+        }
+      }
+    }
+  } bs{G, H, ldx, gc, ncols, col0, vec2 != 0, steps};
+
+  double acc[L][Cfg::MI][Cfg::NJ][2];
+  double w[Cfg::MI][Cfg::NJ][2];
+#pragma unroll
+  for (int c = 0; c < L; ++c)
+#pragma unroll
+    for (int i = 0; i < Cfg::MI; ++i)
+#pragma unroll
+      for (int j = 0; j < Cfg::NJ; ++j) acc[c][i][j][0] = acc[c][i][j][1] = 0.0;
+#pragma unroll
+  for (int i = 0; i < Cfg::MI; ++i)
+#pragma unroll
+    for (int j = 0; j < Cfg::NJ; ++j) w[i][j][0] = w[i][j][1] = 0.0;
+  __syncthreads();
+
+  double* As0 = dsm;
+  double* Bs0 = dsm + STAGES * Cfg::A_STAGE;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wr = warp / Cfg::WNW, wc = warp % Cfg::WNW;
+  const int am0 = wr * Cfg::WM + g;
+  const int bn0 = wc * Cfg::WN + g;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nsteps) {
+      as.stage(As0 + s * Cfg::A_STAGE, s);
+      bs.stage(Bs0 + s * Cfg::B_STAGE, s);
+    }
+    cp_async_commit();
+  }
+  for (int ks = 0; ks < nsteps; ++ks) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      int nx = ks + STAGES - 1;
+      if (nx < nsteps) {
+        as.stage(As0 + (nx % STAGES) * Cfg::A_STAGE, nx);
+        bs.stage(Bs0 + (nx % STAGES) * Cfg::B_STAGE, nx);
+      }
+      cp_async_commit();
+    }
+    const double* As = As0 + (ks % STAGES) * Cfg::A_STAGE;
+    const double* Bs = Bs0 + (ks % STAGES) * Cfg::B_STAGE;
+#pragma unroll
+    for (int k4 = 0; k4 < BK / 4; ++k4) {
+      const int kr = k4 * 4 + t;
+      double a[Cfg::MI], b[Cfg::NJ];
+#pragma unroll
+      for (int i = 0; i < Cfg::MI; ++i) a[i] = As[Cfg::ai(am0 + i * 8, kr)];
+#pragma unroll
+      for (int j = 0; j < Cfg::NJ; ++j) b[j] = Bs[Cfg::bi(kr, bn0 + j * 8)];
+#pragma unroll
+      for (int i = 0; i < Cfg::MI; ++i)
+#pragma unroll
+        for (int j = 0; j < Cfg::NJ; ++j) mma8x8x4(w[i][j][0], w[i][j][1], a[i], b[j]);
+    }
+    int4 st = steps[ks];
+    if (st.w) {  // last step of block st.x: fold W into the tag groups
+      const double* Tj = T + (int64_t)st.x * ell;
+#pragma unroll
+      for (int c = 0; c < L; ++c) {
+        double tc = (c < ell) ? __ldg(&Tj[c]) : 0.0;
+#pragma unroll
+        for (int i = 0; i < Cfg::MI; ++i)
+#pragma unroll
+          for (int j = 0; j < Cfg::NJ; ++j) {
+            acc[c][i][j][0] = fma(tc, w[i][j][0], acc[c][i][j][0]);
+            acc[c][i][j][1] = fma(tc, w[i][j][1], acc[c][i][j][1]);
+          }
+      }
+#pragma unroll
+      for (int i = 0; i < Cfg::MI; ++i)
+#pragma unroll
+        for (int j = 0; j < Cfg::NJ; ++j) w[i][j][0] = w[i][j][1] = 0.0;
+    }
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int i = 0; i < Cfg::MI; ++i) {
+    int row = row0 + wr * Cfg::WM + i * 8 + g;
+    if (row >= n) continue;
+#pragma unroll
+    for (int j = 0; j < Cfg::NJ; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        int col = col0 + wc * Cfg::WN + j * 8 + 2 * t + h;
+        if (col >= ncols) continue;
+        double* dst = (col < gc) ? Y : Z;
+        int q = (col < gc) ? col : col - gc;
+#pragma unroll
+        for (int c = 0; c < L; ++c)
+          if (c < ell) dst[(int64_t)row * ldy + c * gc + q] = acc[c][i][j][h];
+      }
+  }
+}
+
 }  // namespace
 }  // namespace ublr
 
@@ -385,28 +520,55 @@ namespace {
 int sketch_common(const ublr_op_t* op, const int32_t* off, int b, const double* T,
                   int ell, const double* G, const double* H, int64_t ld_x, int gc, double* Y, double* Z,
                   int64_t ld_y, cudaStream_t st) {
-  int ncols = (H ? 2 : 1) * gc;
+  const int ncols = (H ? 2 : 1) * gc;
+  // step table (block, first column, end column, last-step flag) from the host copy of off
+  std::string hoff((size_t)4 * (b + 1), '\0');
+  UBLR_CUDA(cudaMemcpyAsync(&hoff[0], off, 4 * (b + 1), cudaMemcpyDeviceToHost, st));
+  UBLR_CUDA(cudaStreamSynchronize(st));
+  const int32_t* ho = (const int32_t*)hoff.data();
+  std::string hsteps;
+  int nsteps = 0;
+  for (int j = 0; j < b; ++j)
+    for (int q = ho[j]; q < ho[j + 1]; q += 32) {
+      int4 s4 = make_int4(j, q, ho[j + 1], q + 32 >= ho[j + 1] ? 1 : 0);
+      hsteps.append((const char*)&s4, sizeof(int4));
+      ++nsteps;
+    }
+  int4* dsteps = nullptr;
+  UBLR_CUDA(cudaMallocAsync((void**)&dsteps, sizeof(int4) * (size_t)nsteps, st));
+  UBLR_CUDA(cudaMemcpyAsync(dsteps, hsteps.data(), sizeof(int4) * (size_t)nsteps, cudaMemcpyHostToDevice, st));
+  int vec2 = ((ld_x % 2) == 0 && ((uintptr_t)G) % 16 == 0 && (!H || ((uintptr_t)H) % 16 == 0)) ? 1 : 0;
   dim3 grid;
-  grid.y = (unsigned)((op->n + TS_BM - 1) / TS_BM);
-#define UBLR_TS_LAUNCH(L, BN)                                                                              \
-  {                                                                                                        \
-    grid.x = (unsigned)((ncols + (BN) - 1) / (BN));                                                       \
-    UBLR_DISPATCH_KIND(op->kind, KIND, {                                                                  \
-      size_t sm = (size_t)2 * TS_BK * ((TS_BM + 4) + ((BN) + 4)) * sizeof(double);                       \
-      UBLR_CUDA(cudaFuncSetAttribute(k_sketch_tagged<KIND, L, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                     (int)sm));                                                          \
-      k_sketch_tagged<KIND, L, BN><<<grid, TS_THREADS, sm, st>>>(*op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y); \
-    })                                                                                                     \
+  grid.y = (unsigned)((op->n + 63) / 64);
+  int rc = UBLR_OK;
+#define UBLR_TS2(L, BMv, BNv, WMWv, WNWv)                                                                     \
+  {                                                                                                          \
+    using Cfg = TileCfg<BMv, BNv, 32, WMWv, WNWv, 2>;                                                        \
+    grid.x = (unsigned)((ncols + (BNv) - 1) / (BNv));                                                        \
+    grid.y = (unsigned)((op->n + (BMv) - 1) / (BMv));                                                        \
+    UBLR_DISPATCH_KIND(op->kind, KIND, {                                                                     \
+      size_t sm = Cfg::smem_bytes();                                                                         \
+      UBLR_CUDA(cudaFuncSetAttribute(k_sketch_tagged2<KIND, L, Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                     (int)sm));                                                             \
+      k_sketch_tagged2<KIND, L, Cfg><<<grid, Cfg::NT, sm, st>>>(*op, dsteps, nsteps, T, ell, G, H, ld_x, gc, Y, Z, \
+                                                                ld_y, vec2);                                 \
+    })                                                                                                       \
   }
-  if (ell <= 4) UBLR_TS_LAUNCH(4, 128)
-  else if (ell <= 10) UBLR_TS_LAUNCH(10, 64)
-  else if (ell <= 28) UBLR_TS_LAUNCH(28, 64)
+  if (ell <= 4) UBLR_TS2(4, 64, 64, 4, 4)
+  else if (ell <= 10) UBLR_TS2(10, 64, 32, 4, 4)
+  else if (ell <= 28) UBLR_TS2(28, 32, 32, 4, 4)
   else {
     set_error("tagged sketch supports ell <= 28 (d <= 3 without extra columns)");
-    return UBLR_ERR_VALUE;
+    rc = UBLR_ERR_VALUE;
   }
-#undef UBLR_TS_LAUNCH
-  UBLR_LAUNCH_CHECK();
+#undef UBLR_TS2
+  cudaError_t e = cudaGetLastError();
+  UBLR_CUDA(cudaFreeAsync(dsteps, st));
+  if (rc) return rc;
+  if (e != cudaSuccess) {
+    set_error(std::string("CUDA error: ") + cudaGetErrorString(e));
+    return UBLR_ERR_CUDA;
+  }
   return UBLR_OK;
 }
 }  // namespace
