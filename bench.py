@@ -154,6 +154,101 @@ def cpu_baseline(wl, budget_s=12.0):
                       f"(dense operator prebuilt, OpenBLAS on all cores)"}
 
 
+def run_sharded(args, rank, world, local):
+    """Config 5: block-row sharded A2. With one GPU, one rank's
+    share of an --shards-way job is timed (the other shards' V rows are
+    produced untimed first; the all-gather becomes a copy)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2501_05528_b200 as P
+    from paper_2501_05528_b200 import _lib
+    from paper_2501_05528_b200 import workloads as W
+    from paper_2501_05528_b200.distributed import (phase1_local, phase23_local, shard_ranges, torch_allgather)
+    from paper_2501_05528_b200.tagging import plan_tagging
+
+    wl = W.build(args.config)
+    dev = torch.device("cuda", local)
+    emulate = world == 1
+    S = args.shards if emulate else world
+    me = args.shard_rank if emulate else rank
+    shards = shard_ranges(wl.tess, S, wl.k)
+    stream = P.RandomStream(W.COMPRESS_SEED)
+    other_V = None
+    if emulate:   # V rows of the other shards, untimed
+        plan0 = plan_tagging(wl.tess, 0, "gaussian", stream.child(1))
+        parts = []
+        for sh in shards:
+            if sh.rank == me:
+                parts.append(None)
+                continue
+            _, _, V, _ = phase1_local(wl.op, wl.tess, wl.k, wl.p, stream, sh, plan0)
+            parts.append(V)
+        other_V = parts
+        torch.cuda.synchronize()
+
+    def step():
+        sh = shards[me]
+        plan, U, V, dt = phase1_local(wl.op, wl.tess, wl.k, wl.p, stream, sh)
+        if emulate:
+            V_all = torch.cat([V if p_ is None else p_ for p_ in other_V], 0)
+        else:
+            V_all = torch_allgather()(V, dt.n)
+        core, B = phase23_local(wl.op, wl.k, sh, dt, U, V_all)
+        return core, B
+
+    for _ in range(args.warmup):
+        step()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    _lib.instrument(True)
+    launches0 = _lib.launch_count
+    times = []
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            core, B = step()
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
+    ev = _lib.event_times()
+    _lib.instrument(False)
+    launches = (_lib.launch_count - launches0) // args.steps
+    t = float(np.mean(times))
+    if world > 1:
+        tt = torch.tensor([t], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    sk = ev.get("ublr_sketch_tagged_pair", [float("nan")])
+    sk_ms = float(np.mean(sk))
+    sh = shards[me]
+    gc = wl.k + wl.p
+    rows = sh.r1 - sh.r0
+    sk_flops = 2.0 * rows * wl.n * 2 * gc + 2.0 * rows * wl.b * 2 * gc * wl.ell
+    achieved = sk_flops / (sk_ms * 1e-3) / 1e12
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": t, "unit": "s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t * 1e3, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {**wl.describe(), "parallelism": f"block-row shards x{S}",
+                       "measured": ("one rank's share of a %d-way sharded job on 1 GPU (all-gather emulated)" % S)
+                       if emulate else "all ranks, NCCL all-gather of V",
+                       "shard_rank": me, "rows_per_shard": rows},
+            "gpu_launches": int(launches),
+            "roofline": {"kernel": "k_sketch_tagged (own rows)", "bound": "fp64", "achieved": achieved,
+                         "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
+                         "traffic": None, "algorithmic_flops_per_launch": sk_flops, "avg_launch_ms": sk_ms},
+            "kernel_ms_per_step": {k_: float(np.sum(v)) / args.steps for k_, v in ev.items()},
+            "clocks": clocks.summary(), "cpu_baseline": None,
+        }))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -162,6 +257,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shards", type=int, default=8, help="c5 on one GPU: shard count to emulate")
+    ap.add_argument("--shard-rank", type=int, default=3, help="c5 on one GPU: which shard to time")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, world, local = dist_env()
@@ -175,6 +272,12 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    if args.config == "c5":
+        run_sharded(args, rank, world, local)
+        if world > 1:
+            dist.destroy_process_group()
+        return
 
     import paper_2501_05528_b200 as P
     from paper_2501_05528_b200 import _lib

@@ -90,13 +90,15 @@ int ublr_rng_normals(const ublr_rng_stream_t* streams_dev, const int64_t* counts
  * op.apply / op.apply_adjoint). Y[:, c*gc+q] for block-row i accumulates
  * sum_j T[j,c] * (A_ij X_j)[:, q] (Kronecker-restructured: each A tile meets
  * its own test block once). X is N x gc (permuted rows, ld_x); T is b x ell.
- * Computes Y = A Omega into y (N x ell*gc, ld_y). */
+ * Computes rows [row_begin, row_end) of Y = A Omega (N x ell*gc, ld_y; Y is
+ * indexed by absolute permuted row, so a row shard passes Y - row_begin*ld_y). */
 int ublr_sketch_tagged(const ublr_op_t* op, const int32_t* off, int b, const double* T, int ell,
-                       const double* X, int64_t ld_x, int gc, double* Y, int64_t ld_y, void* stream);
+                       const double* X, int64_t ld_x, int gc, double* Y, int64_t ld_y, int row_begin,
+                       int row_end, void* stream);
 /* Symmetric operator: [Y | Z] = A [Omega | Psi] in one pass over A. */
 int ublr_sketch_tagged_pair(const ublr_op_t* op, const int32_t* off, int b, const double* T, int ell,
                             const double* G, const double* H, int64_t ld_x, int gc,
-                            double* Y, double* Z, int64_t ld_y, void* stream);
+                            double* Y, double* Z, int64_t ld_y, int row_begin, int row_end, void* stream);
 
 /* Generic operator apply (ref/operators.py:48-52 and every op.apply call of
  * the pipeline): out (N x w, permuted rows, ld_o) = A X (N x w, ld_x). */
@@ -115,10 +117,12 @@ int ublr_block_qr(const double* Y, int64_t ld_y, int mode, const double* z, int 
                   void* stream, int m_max);
 
 /* K6 — coupling (ref/reconstruction.py:185-198, direct_core):
- * core[roff[i]:, roff[j]:] = U_i^T A_ij V_j for all (i, j). */
+ * core[roff[i]:, roff[j]:] = U_i^T A_ij V_j for block rows i0 <= i < i1 and all
+ * j (U and core indexed by absolute rows: a block-row shard passes shifted
+ * pointers). */
 int ublr_coupling(const ublr_op_t* op, const int32_t* off, const int32_t* roff, int b, int k,
                   const double* U, const double* V, int64_t ld_uv, double* core, int64_t ld_c,
-                  void* stream, int m_max);
+                  void* stream, int m_max, int i0, int i1);
 
 /* K7 — near field with the colour-probe semantics of
  * ref/reconstruction.py:201-244: for each near pair p = (i, j),

@@ -44,11 +44,11 @@ SIGNATURES = {
     "ublr_device_check": (INT, []),
     "ublr_rng_workspace_bytes": (I64, [P, INT]),
     "ublr_rng_normals": (INT, [P, P, INT, P, P, I64, P]),
-    "ublr_sketch_tagged": (INT, [C.POINTER(OpDesc), P, INT, P, INT, P, I64, INT, P, I64, P]),
-    "ublr_sketch_tagged_pair": (INT, [C.POINTER(OpDesc), P, INT, P, INT, P, P, I64, INT, P, P, I64, P]),
+    "ublr_sketch_tagged": (INT, [C.POINTER(OpDesc), P, INT, P, INT, P, I64, INT, P, I64, INT, INT, P]),
+    "ublr_sketch_tagged_pair": (INT, [C.POINTER(OpDesc), P, INT, P, INT, P, P, I64, INT, P, P, I64, INT, INT, P]),
     "ublr_apply": (INT, [C.POINTER(OpDesc), P, I64, INT, P, I64, P]),
     "ublr_block_qr": (INT, [P, I64, INT, P, INT, INT, P, P, INT, INT, P, I64, P, INT]),
-    "ublr_coupling": (INT, [C.POINTER(OpDesc), P, P, INT, INT, P, P, I64, P, I64, P, INT]),
+    "ublr_coupling": (INT, [C.POINTER(OpDesc), P, P, INT, INT, P, P, I64, P, I64, P, INT, INT, INT]),
     "ublr_nearfield_workspace_bytes": (I64, [INT, INT, INT]),
     "ublr_blr_apply_workspace_bytes": (I64, [I64, INT]),
     "ublr_gemm_batched": (INT, [INT, INT, INT, INT, INT, C.c_double, P, I64, I64, P, I64, P, I64, I64, P, I64,

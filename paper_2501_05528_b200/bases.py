@@ -150,12 +150,13 @@ def tagged_sketch(op, dt, T_dev, T_entries, G, H, gc):
         Z = torch.empty((dt.n, s), dtype=torch.float64, device=dt.device)
         if getattr(inner, "symmetric", False):
             _lib.call("ublr_sketch_tagged_pair", inner.device_op(dt.perm), _lib.ptr(dt.off), dt.b,
-                      _lib.ptr(T_dev), ell, _lib.ptr(G), _lib.ptr(H), gc, gc, _lib.ptr(Y), _lib.ptr(Z), s, stream)
+                      _lib.ptr(T_dev), ell, _lib.ptr(G), _lib.ptr(H), gc, gc, _lib.ptr(Y), _lib.ptr(Z), s, 0, dt.n,
+                      stream)
         else:
             _lib.call("ublr_sketch_tagged", inner.device_op(dt.perm), _lib.ptr(dt.off), dt.b, _lib.ptr(T_dev),
-                      ell, _lib.ptr(G), gc, gc, _lib.ptr(Y), s, stream)
+                      ell, _lib.ptr(G), gc, gc, _lib.ptr(Y), s, 0, dt.n, stream)
             _lib.call("ublr_sketch_tagged", inner.device_op(dt.perm, adjoint=True), _lib.ptr(dt.off), dt.b,
-                      _lib.ptr(T_dev), ell, _lib.ptr(H), gc, gc, _lib.ptr(Z), s, stream)
+                      _lib.ptr(T_dev), ell, _lib.ptr(H), gc, gc, _lib.ptr(Z), s, 0, dt.n, stream)
         return Y, Z
     # black-box host operator: explicit test matrices through its apply
     om = assemble_tagged(dt, T_entries, G, gc)

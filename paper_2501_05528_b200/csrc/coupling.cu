@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(CP_THREADS) k_coupling(ublr_op_t op, const int
                                                          const int32_t* __restrict__ roff, int k,
                                                          const double* __restrict__ U,
                                                          const double* __restrict__ V, int64_t lduv,
-                                                         double* __restrict__ core, int64_t ldc) {
+                                                         double* __restrict__ core, int64_t ldc, int i0) {
   constexpr int MR = 8 * RW;          // max rows of block i
   constexpr int SA = MR + 4;          // k-major A tile stride
   constexpr int SB = 8 * NJ + 4;      // V tile stride
@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(CP_THREADS) k_coupling(ublr_op_t op, const int
   double (*Ws)[SW] = reinterpret_cast<double (*)[SW]>(dsm);  // aliases As/Bs after the k-loop
   if (KIND == UBLR_OP_LOG) init_log_tables(&lt);
 
-  const int j = blockIdx.x, i = blockIdx.y;
+  const int j = blockIdx.x, i = i0 + blockIdx.y;
   const int ri0 = off[i], mi = off[i + 1] - ri0;
   const int cj0 = off[j], mj = off[j + 1] - cj0;
   const int ki = roff[i + 1] - roff[i], kj = roff[j + 1] - roff[j];
@@ -299,7 +299,7 @@ static size_t coupling_smem(int MR, int NJ) {
 
 extern "C" int ublr_coupling(const ublr_op_t* op, const int32_t* off, const int32_t* roff, int b, int k,
                              const double* U, const double* V, int64_t ld_uv, double* core, int64_t ld_c,
-                             void* stream, int m_max) {
+                             void* stream, int m_max, int i0, int i1) {
   int rc = check_op(op);
   if (rc) return rc;
   UBLR_REQUIRE(b > 0 && off && roff && U && V && core && k >= 1 && ld_uv >= k, UBLR_ERR_VALUE,
@@ -307,14 +307,15 @@ extern "C" int ublr_coupling(const ublr_op_t* op, const int32_t* off, const int3
   UBLR_REQUIRE(m_max <= 256 && k <= 64, UBLR_ERR_VALUE, "ublr_coupling: supports m <= 256, k <= 64");
   UBLR_REQUIRE(b <= 65535, UBLR_ERR_VALUE, "ublr_coupling: b <= 65535");
   cudaStream_t st = (cudaStream_t)stream;
-  dim3 grid(b, b);
+  UBLR_REQUIRE(0 <= i0 && i0 < i1 && i1 <= b, UBLR_ERR_VALUE, "ublr_coupling: bad block-row range");
+  dim3 grid(b, i1 - i0);
   int kk = k < m_max ? k : m_max;  // effective ranks never exceed min(k, m)
 #define UBLR_CP_LAUNCH(RW, NJ)                                                                             \
   UBLR_DISPATCH_KIND(op->kind, KIND, {                                                                    \
     size_t sm = coupling_smem(8 * (RW), (NJ));                                                           \
     UBLR_CUDA(cudaFuncSetAttribute(k_coupling<KIND, RW, NJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                    (int)sm));                                                            \
-    k_coupling<KIND, RW, NJ><<<grid, CP_THREADS, sm, st>>>(*op, off, roff, k, U, V, ld_uv, core, ld_c);   \
+    k_coupling<KIND, RW, NJ><<<grid, CP_THREADS, sm, st>>>(*op, off, roff, k, U, V, ld_uv, core, ld_c, i0);   \
   })
   if (m_max <= 64) {
     if (kk <= 16) { UBLR_CP_LAUNCH(8, 2); }

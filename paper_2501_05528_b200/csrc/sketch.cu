@@ -14,6 +14,7 @@
 #include "common.cuh"
 #include "optile.cuh"
 #include "gemm_core.cuh"
+#include <cstdlib>
 
 namespace ublr {
 namespace {
@@ -198,7 +199,7 @@ __global__ void __launch_bounds__(TS_THREADS) k_sketch_tagged(ublr_op_t op, cons
                                                               const double* __restrict__ G,
                                                               const double* __restrict__ H, int64_t ldx, int gc,
                                                               double* __restrict__ Y, double* __restrict__ Z,
-                                                              int64_t ldy) {
+                                                              int64_t ldy, int row_begin, int row_end) {
   constexpr int SA = TS_BM + 4;
   constexpr int SB = BN + 4;
   constexpr int WN = BN / 8;   // columns per warp
@@ -211,8 +212,8 @@ __global__ void __launch_bounds__(TS_THREADS) k_sketch_tagged(ublr_op_t op, cons
 
   const int ncols = (H ? 2 : 1) * gc;
   // rows are independent in the sketch, so 16-row tiles may straddle blocks
-  const int rend = (int)op.n;
-  const int row0 = blockIdx.y * TS_BM;
+  const int rend = row_end;
+  const int row0 = row_begin + blockIdx.y * TS_BM;
   const int col0 = blockIdx.x * BN;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -517,9 +518,52 @@ extern "C" int ublr_apply(const ublr_op_t* op, const double* X, int64_t ld_x, in
 }
 
 namespace {
-int sketch_common(const ublr_op_t* op, const int32_t* off, int b, const double* T,
-                  int ell, const double* G, const double* H, int64_t ld_x, int gc, double* Y, double* Z,
-                  int64_t ld_y, cudaStream_t st) {
+// v1: 16-row tiles (kept as default: measured faster than v2 on c2/c4 shapes, profiles/r01)
+int sketch_common_v1(const ublr_op_t* op, const int32_t* off, int b, const double* T, int ell, const double* G,
+                     const double* H, int64_t ld_x, int gc, double* Y, double* Z, int64_t ld_y, int row_begin,
+                     int row_end, cudaStream_t st) {
+  int ncols = (H ? 2 : 1) * gc;
+  dim3 grid;
+  grid.y = (unsigned)((row_end - row_begin + TS_BM - 1) / TS_BM);
+#define UBLR_TS_LAUNCH(L, BN)                                                                              \
+  {                                                                                                        \
+    grid.x = (unsigned)((ncols + (BN) - 1) / (BN));                                                       \
+    UBLR_DISPATCH_KIND(op->kind, KIND, {                                                                  \
+      size_t sm = (size_t)2 * TS_BK * ((TS_BM + 4) + ((BN) + 4)) * sizeof(double);                       \
+      UBLR_CUDA(cudaFuncSetAttribute(k_sketch_tagged<KIND, L, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                     (int)sm));                                                          \
+      k_sketch_tagged<KIND, L, BN><<<grid, TS_THREADS, sm, st>>>(*op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y, \
+                                                                 row_begin, row_end);                  \
+    })                                                                                                     \
+  }
+  if (ell <= 4) UBLR_TS_LAUNCH(4, 128)
+  else if (ell <= 10) UBLR_TS_LAUNCH(10, 64)
+  else if (ell <= 28) UBLR_TS_LAUNCH(28, 64)
+  else {
+    set_error("tagged sketch supports ell <= 28 (d <= 3 without extra columns)");
+    return UBLR_ERR_VALUE;
+  }
+#undef UBLR_TS_LAUNCH
+  UBLR_LAUNCH_CHECK();
+  return UBLR_OK;
+}
+
+int sketch_common_v2(const ublr_op_t* op, const int32_t* off, int b, const double* T,
+                     int ell, const double* G, const double* H, int64_t ld_x, int gc, double* Y, double* Z,
+                     int64_t ld_y, cudaStream_t st);
+
+int sketch_common(const ublr_op_t* op, const int32_t* off, int b, const double* T, int ell, const double* G,
+                  const double* H, int64_t ld_x, int gc, double* Y, double* Z, int64_t ld_y, int row_begin,
+                  int row_end, cudaStream_t st) {
+  UBLR_REQUIRE(row_begin >= 0 && row_begin < row_end && row_end <= op->n, UBLR_ERR_VALUE, "sketch: bad row range");
+  static const bool v2 = getenv("UBLR_SKETCH_V2") != nullptr;
+  if (v2 && row_begin == 0 && row_end == op->n) return sketch_common_v2(op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y, st);
+  return sketch_common_v1(op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y, row_begin, row_end, st);
+}
+
+int sketch_common_v2(const ublr_op_t* op, const int32_t* off, int b, const double* T,
+                     int ell, const double* G, const double* H, int64_t ld_x, int gc, double* Y, double* Z,
+                     int64_t ld_y, cudaStream_t st) {
   const int ncols = (H ? 2 : 1) * gc;
   // step table (block, first column, end column, last-step flag) from the host copy of off
   std::string hoff((size_t)4 * (b + 1), '\0');
@@ -574,21 +618,23 @@ int sketch_common(const ublr_op_t* op, const int32_t* off, int b, const double* 
 }  // namespace
 
 extern "C" int ublr_sketch_tagged(const ublr_op_t* op, const int32_t* off, int b, const double* T, int ell,
-                                  const double* X, int64_t ld_x, int gc, double* Y, int64_t ld_y, void* stream) {
+                                  const double* X, int64_t ld_x, int gc, double* Y, int64_t ld_y, int row_begin,
+                                  int row_end, void* stream) {
   int rc = check_op(op);
   if (rc) return rc;
   UBLR_REQUIRE(b > 0 && off && T && X && Y && gc > 0 && ell > 0 && ld_x >= gc && ld_y >= (int64_t)ell * gc,
                UBLR_ERR_VALUE, "ublr_sketch_tagged: bad arguments");
-  return sketch_common(op, off, b, T, ell, X, nullptr, ld_x, gc, Y, nullptr, ld_y, (cudaStream_t)stream);
+  return sketch_common(op, off, b, T, ell, X, nullptr, ld_x, gc, Y, nullptr, ld_y, row_begin, row_end,
+                       (cudaStream_t)stream);
 }
 
 extern "C" int ublr_sketch_tagged_pair(const ublr_op_t* op, const int32_t* off, int b, const double* T, int ell,
                                        const double* G, const double* H, int64_t ld_x, int gc, double* Y, double* Z,
-                                       int64_t ld_y, void* stream) {
+                                       int64_t ld_y, int row_begin, int row_end, void* stream) {
   int rc = check_op(op);
   if (rc) return rc;
   UBLR_REQUIRE(b > 0 && off && T && G && H && Y && Z && gc > 0 && ell > 0 && ld_x >= gc &&
                    ld_y >= (int64_t)ell * gc,
                UBLR_ERR_VALUE, "ublr_sketch_tagged_pair: bad arguments");
-  return sketch_common(op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y, (cudaStream_t)stream);
+  return sketch_common(op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y, row_begin, row_end, (cudaStream_t)stream);
 }

@@ -1,0 +1,218 @@
+"""Block-row sharded type-A tagging compression (config 5).
+
+One process per GPU. Rank r owns a contiguous slab of box rows (block ids
+are ordered with grid axis 0 most significant, so a slab is a contiguous
+block-id range and a contiguous range of permuted rows). Every rank:
+
+1. plans the tagging matrix and draws ALL test blocks G_j, H_j from the
+   shared seed (no communication: the GPU RNG reproduces numpy's streams);
+2. sketches its own rows of Y = A Omega and Z = A Psi (A symmetric), and
+   forms its U_i, V_i;
+3. all-gathers V (N x k, the only collective on the data path: the far-field
+   coupling C_ij = U_i^T A_ij V_j needs every V_j, and so does the colour-probe
+   leak of the near field, F11);
+4. computes its core rows and its near blocks.
+
+`allgather` is pluggable: `torch.distributed.all_gather_into_tensor` (NCCL
+over NVLink in production, gloo in the CPU tests) or an in-process
+concatenation when ranks are emulated one after another on one GPU.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .bases import _bill, draw_test_blocks
+from .linalg import RandomStream
+from .operators import counting_wrapper, unwrap
+from .tagging import plan_tagging
+from .tessellation import device_tess
+
+
+def _torch():
+    import torch
+    return torch
+
+
+@dataclass
+class Shard:
+    rank: int
+    world: int
+    i0: int      # first block
+    i1: int      # one past last block
+    r0: int      # first permuted row
+    r1: int
+    p0: int      # first near pair (neighbour CSR)
+    p1: int
+    K0: int      # first core row
+    K1: int
+
+
+def shard_ranges(tess, world: int, k: int):
+    """Contiguous box-row slabs, as even as possible. Returns [Shard]*world."""
+    b = tess.b
+    rows_of_block = tess.grid_coords[:, 0]
+    slabs = int(rows_of_block.max()) + 1
+    if world > slabs:
+        raise ValueError(f"cannot shard {slabs} box rows over {world} ranks")
+    sizes = tess.block_sizes
+    ranks = np.minimum(k, sizes)
+    nlen = np.array([len(x) for x in tess.neighbor_lists])
+    off = np.concatenate(([0], np.cumsum(sizes)))
+    roff = np.concatenate(([0], np.cumsum(ranks)))
+    nptr = np.concatenate(([0], np.cumsum(nlen)))
+    out = []
+    for r in range(world):
+        s0, s1 = (r * slabs) // world, ((r + 1) * slabs) // world
+        blocks = np.flatnonzero((rows_of_block >= s0) & (rows_of_block < s1))
+        i0, i1 = int(blocks[0]), int(blocks[-1]) + 1
+        if i1 - i0 != len(blocks):
+            raise ValueError("box-row slab is not a contiguous block range")
+        out.append(Shard(r, world, i0, i1, int(off[i0]), int(off[i1]), int(nptr[i0]), int(nptr[i1]),
+                         int(roff[i0]), int(roff[i1])))
+    return out
+
+
+@dataclass
+class ShardResult:
+    shard: Shard
+    U: object        # (r1-r0) x k, own rows
+    V: object        # N x k, all rows (gathered)
+    core: object     # (K1-K0) x K, own core rows
+    B: object        # own near blocks, flat, neighbour-CSR order from p0
+    plan: object
+    ledger: dict
+
+
+def torch_allgather(group=None):
+    """All-gather of equal-size row shards through torch.distributed."""
+    import torch.distributed as dist
+    torch = _torch()
+
+    def gather(local, total_rows):
+        world = dist.get_world_size(group)
+        tail = tuple(local.shape[1:])
+        sizes = torch.zeros(world, dtype=torch.int64, device=local.device)
+        mine = torch.tensor([local.shape[0]], dtype=torch.int64, device=local.device)
+        dist.all_gather_into_tensor(sizes, mine, group=group)
+        sizes = [int(x) for x in sizes.cpu()]
+        if sum(sizes) != total_rows:
+            raise ValueError(f"shards hold {sum(sizes)} rows, expected {total_rows}")
+        mx = max(sizes)
+        if min(sizes) == mx:
+            # every shard has total/world rows (box-row slabs of an evenly divided grid)
+            out = torch.empty((total_rows,) + tail, dtype=local.dtype, device=local.device)
+            dist.all_gather_into_tensor(out, local.contiguous(), group=group)
+            return out
+        # uneven slabs: pad every shard to the largest, gather, trim
+        pad = torch.zeros((mx,) + tail, dtype=local.dtype, device=local.device)
+        pad[:local.shape[0]] = local
+        allp = torch.empty((world * mx,) + tail, dtype=local.dtype, device=local.device)
+        dist.all_gather_into_tensor(allp, pad, group=group)
+        return torch.cat([allp[r * mx:r * mx + s] for r, s in enumerate(sizes)], 0)
+
+    return gather
+
+
+def phase1_local(op, tess, k, p, stream, shard, plan=None):
+    """Steps 1-2 for one shard: returns (plan, U_own, V_own, dt, G, H, T_dev)."""
+    torch = _torch()
+    _lib.require_device()
+    dt = device_tess(tess, torch.device("cuda"))
+    if plan is None:
+        plan = plan_tagging(tess, 0, "gaussian", stream.child(1))
+    r = k + p
+    gc = r
+    T = plan.matrix.entries
+    ell = T.shape[1]
+    s = ell * gc
+    G = draw_test_blocks(dt, stream.child(0), 0, gc)
+    H = draw_test_blocks(dt, stream.child(0), 1, gc)
+    T_dev = torch.from_numpy(np.ascontiguousarray(T)).to(dt.device)
+    Z_dev = torch.from_numpy(np.ascontiguousarray(plan.Z)).to(dt.device)
+    _bill(op, s, s)
+    inner = unwrap(op)
+    if not getattr(inner, "symmetric", False) or not hasattr(inner, "device_op"):
+        raise NotImplementedError("sharded compression needs a symmetric GPU kernel operator")
+    nloc = shard.r1 - shard.r0
+    f64 = dict(dtype=torch.float64, device=dt.device)
+    Y = torch.empty((nloc, s), **f64)
+    Z = torch.empty((nloc, s), **f64)
+    st = _lib.stream_handle()
+    shift = 8 * shard.r0 * s
+    _lib.call("ublr_sketch_tagged_pair", inner.device_op(dt.perm), _lib.ptr(dt.off), dt.b, _lib.ptr(T_dev), ell,
+              _lib.ptr(G), _lib.ptr(H), gc, gc, _lib.ptr(Y) - shift, _lib.ptr(Z) - shift, s, shard.r0, shard.r1, st)
+    kq = max(1, min(k, dt.m_max))
+    U = torch.zeros((nloc, k), **f64)
+    V = torch.zeros((nloc, k), **f64)
+    ushift = 8 * shard.r0 * k
+    for src, dst in ((Y, U), (Z, V)):
+        _lib.call("ublr_block_qr", _lib.ptr(src) - shift, s, 0, _lib.ptr(Z_dev) + 8 * shard.i0 * ell, ell, gc, None,
+                  _lib.ptr(dt.off) + 4 * shard.i0, shard.i1 - shard.i0, kq, _lib.ptr(dst) - ushift, k, st, dt.m_max)
+    del Y, Z
+    return plan, U, V, dt
+
+
+def phase23_local(op, k, shard, dt, U, V_all):
+    """Steps 4: own core rows (coupling) and own near blocks (colour probes)."""
+    torch = _torch()
+    inner = unwrap(op)
+    roff_h, roff = dt.roff(k)
+    K = int(roff_h[-1])
+    kloc = shard.K1 - shard.K0
+    f64 = dict(dtype=torch.float64, device=dt.device)
+    core = torch.empty((kloc, K), **f64)
+    st = _lib.stream_handle()
+    desc = inner.device_op(dt.perm)
+    _lib.call("ublr_coupling", desc, _lib.ptr(dt.off), _lib.ptr(roff), dt.b, k, _lib.ptr(U) - 8 * shard.r0 * k,
+              _lib.ptr(V_all), k, _lib.ptr(core) - 8 * shard.K0 * K, K, st, dt.m_max, shard.i0, shard.i1)
+    npairs = shard.p1 - shard.p0
+    bbase = int(dt.b_off_h[shard.p0])
+    B = torch.empty(int(dt.b_off_h[shard.p1]) - bbase, **f64)
+    lib = _lib.load()
+    ws_bytes = int(lib.ublr_nearfield_workspace_bytes(npairs, max(k, 1), dt.m_max))
+    ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device=dt.device)
+    _lib.call("ublr_nearfield_colour", desc, _lib.ptr(dt.off), _lib.ptr(roff), dt.b, k,
+              _lib.ptr(U) - 8 * shard.r0 * k, _lib.ptr(V_all), k, _lib.ptr(core) - 8 * shard.K0 * K, K,
+              _lib.ptr(dt.colours), _lib.ptr(dt.cptr), _lib.ptr(dt.cidx), dt.n_colours, dt.m_max,
+              _lib.ptr(dt.pair_i) + 4 * shard.p0, _lib.ptr(dt.nidx) + 4 * shard.p0, npairs,
+              _lib.ptr(dt.b_off) + 8 * shard.p0, _lib.ptr(B) - 8 * bbase, _lib.ptr(ws), ws_bytes, st)
+    return core, B
+
+
+def compress_sharded(op, tess, k, p=10, stream=None, rank=0, world=1, allgather=None, plan=None):
+    """One rank's share of a type-A tagging (A2) compression."""
+    stream = stream or RandomStream(0)
+    cop = counting_wrapper(op)
+    shard = shard_ranges(tess, world, k)[rank]
+    with cop.ledger.phase("I"):
+        plan, U, V, dt = phase1_local(cop, tess, k, p, stream, shard, plan)
+    gather = allgather or torch_allgather()
+    V_all = gather(V, dt.n)
+    with cop.ledger.phase("II"):
+        cop.ledger.record_apply(int(dt.roff(k)[0][-1]))
+    with cop.ledger.phase("III"):
+        cop.ledger.record_apply(int(sum(dt.sizes[dt.colours_h == c].max() for c in range(dt.n_colours))))
+    core, B = phase23_local(op, k, shard, dt, U, V_all)
+    return ShardResult(shard, U, V_all, core, B, plan, cop.ledger.to_dict())
+
+
+def compress_emulated(op, tess, k, p=10, stream=None, world=2):
+    """All ranks of compress_sharded run one after another in this process on
+    one GPU (the all-gather becomes a concatenation). Returns the list of
+    ShardResults; used by the GPU tests to check sharding against the
+    single-GPU pipeline."""
+    torch = _torch()
+    stream = stream or RandomStream(0)
+    shards = shard_ranges(tess, world, k)
+    plan = plan_tagging(tess, 0, "gaussian", stream.child(1))
+    locs = [phase1_local(op, tess, k, p, stream, sh, plan) for sh in shards]
+    V_all = torch.cat([loc[2] for loc in locs], 0)
+    out = []
+    for sh, (pl, U, V, dt) in zip(shards, locs):
+        core, B = phase23_local(op, k, sh, dt, U, V_all)
+        out.append(ShardResult(sh, U, V_all, core, B, pl, {}))
+    return out

@@ -209,7 +209,7 @@ def direct_core(op, tess: Tessellation, bases: BlockBases):
         raise NotImplementedError("direct_core needs a GPU operator (DenseOperator / KernelOperator)")
     _lib.call("ublr_coupling", inner.device_op(dt.perm), _lib.ptr(dt.off), _lib.ptr(roff), dt.b, k,
               _lib.ptr(bases.U), _lib.ptr(bases.V), bases.U.stride(0), _lib.ptr(core), K, _lib.stream_handle(),
-              dt.m_max)
+              dt.m_max, 0, dt.b)
     return core
 
 
