@@ -68,15 +68,26 @@ def device_normals(specs, out):
     specs = list(specs)
     if not specs:
         return out
-    rec = np.zeros(len(specs), dtype=_lib.RNG_STREAM_DTYPE)
-    counts = np.zeros(len(specs), dtype=np.int64)
-    keep = []
-    for s, (stream, rows, cols, off, ld, rowmap) in enumerate(specs):
-        k0, k1 = stream.philox_key()
-        rec[s] = (k0, k1, rows * cols, max(cols, 1), ld, off, _lib.ptr(rowmap))
-        counts[s] = rows * cols
-        if rowmap is not None:
-            keep.append(rowmap)
+    from .seedseq import philox_keys
+
+    ns = len(specs)
+    rec = np.zeros(ns, dtype=_lib.RNG_STREAM_DTYPE)
+    by_seed = {}
+    for s, sp in enumerate(specs):
+        by_seed.setdefault(sp[0].seed, []).append(s)
+    for seed, idx in by_seed.items():   # vectorised SeedSequence (bit-identical to numpy's)
+        kk = philox_keys(seed, [specs[s][0].key for s in idx])
+        rec["key0"][idx] = kk[:, 0]
+        rec["key1"][idx] = kk[:, 1]
+    rows = np.array([sp[1] for sp in specs], dtype=np.int64)
+    cols = np.array([sp[2] for sp in specs], dtype=np.int64)
+    counts = rows * cols
+    rec["count"] = counts
+    rec["cols"] = np.maximum(cols, 1)
+    rec["ld"] = [sp[4] for sp in specs]
+    rec["out_offset"] = [sp[3] for sp in specs]
+    rec["rowmap"] = [_lib.ptr(sp[5]) for sp in specs]
+    keep = [sp[5] for sp in specs if sp[5] is not None]
     lib = _lib.load()
     ws_bytes = int(lib.ublr_rng_workspace_bytes(counts.ctypes.data, len(specs)))
     ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device=out.device)

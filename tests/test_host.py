@@ -120,3 +120,14 @@ def test_ziggurat_decode_matches_numpy(rng_host):
     # tail samples use log1p/exp; allow at most a handful of 1-ulp differences
     assert len(mism) <= 5 and np.all(np.abs(out[mism] - want[mism]) <= 4e-15 * np.abs(want[mism]))
     assert n < used < 1.03 * n
+
+
+def test_vectorised_seedsequence_matches_numpy():
+    from paper_2501_05528_b200.seedseq import philox_keys
+    keys = [(0, 0, i) for i in range(200)] + [(0, 1, i) for i in range(200)]
+    odd = [(), (0,), (2,), (9, 0), (1, 17, 3), (0, 0, 2 ** 33 + 5), (1, 2 ** 40)]
+    for seed in (7, 0, 1, 123456789, 2 ** 40 + 3):
+        for ks in (keys, odd, keys[:1]):
+            got = philox_keys(seed, ks)
+            want = np.array([np.random.SeedSequence(seed, spawn_key=k).generate_state(2, np.uint64) for k in ks])
+            assert np.array_equal(got, want)
