@@ -15,6 +15,7 @@
 // pair, then B_p = sum_j' A_ij' - U_i S_p with A generated on the fly.
 #include "common.cuh"
 #include "optile.cuh"
+#include "gemm_core.cuh"
 
 namespace ublr {
 namespace {
@@ -125,6 +126,133 @@ __global__ void __launch_bounds__(CP_THREADS) k_coupling(ublr_op_t op, const int
     double s = 0.0;
     for (int r = 0; r < mi; ++r) s = fma(__ldg(&Ui[(int64_t)r * lduv + a]), Ws[r][c], s);
     core[(int64_t)(roff[i] + a) * ldc + roff[j] + c] = s;
+  }
+}
+
+// ------------------------------------------------------------- coupling v2
+// C_ij = U_i^T (A_ij V_j) per CTA (i, j) on the shared DMMA main loop:
+// phase 1 W = A_ij V_j (m_i x k_j, A_ij generated per 32-column k-step,
+// V_j rows by cp.async), phase 2 C = U_i^T W with W staged in shared memory
+// (k-major) and the 8x8 output tiles of C spread over the warps.
+struct OffsetRows {
+  int base;
+  __device__ __forceinline__ int operator()(int r) const { return base + r; }
+};
+
+template <int KIND, class Cfg>
+struct CouplingAProducer {
+  const ublr_op_t& op;
+  const LogTables* lt;
+  int cj0, mj;
+  RowPoint rp;
+  int grow, gk0;
+  __device__ CouplingAProducer(const ublr_op_t& op_, const LogTables* lt_, int ri0, int mi, int cj0_, int mj_)
+      : op(op_), lt(lt_), cj0(cj0_), mj(mj_) {
+    grow = threadIdx.x % Cfg::BM;
+    gk0 = threadIdx.x / Cfg::BM;
+    rp = load_row_point(op, ri0 + grow, grow < mi);
+  }
+  __device__ __forceinline__ void stage(double* As, int ks) { stage_part(As, ks, 0, 1); }
+  __device__ __forceinline__ void stage_part(double* As, int ks, int part, int nparts) {
+    constexpr int KL = Cfg::NT / Cfg::BM;
+    constexpr int E = Cfg::BK / KL;
+    const int e0 = (part * E) / nparts, e1 = ((part + 1) * E) / nparts;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if (e < e0 || e >= e1) continue;
+      int kk = gk0 + e * KL;
+      int q = ks * Cfg::BK + kk;
+      double v = 0.0;
+      if (rp.p >= 0 && q < mj) v = op_entry<KIND>(op, rp, cj0 + q, lt);
+      As[Cfg::ai(grow, kk)] = v;
+    }
+  }
+};
+
+template <class Cfg>
+struct CouplingBProducer {
+  const double* V;
+  int64_t ld;
+  int cj0, mj, kj;
+  bool vec2;
+  __device__ __forceinline__ void stage(double* Bs, int ks) {
+    tile_copy<Cfg::NT>(Bs, Cfg::SB, V, ld, Cfg::BK, Cfg::BN, ks * Cfg::BK, 0, mj, kj, OffsetRows{cj0}, vec2);
+  }
+};
+
+template <int KIND, class Cfg>
+__global__ void __launch_bounds__(Cfg::NT) k_coupling2(ublr_op_t op, const int32_t* __restrict__ off,
+                                                       const int32_t* __restrict__ roff, const double* __restrict__ U,
+                                                       const double* __restrict__ V, int64_t lduv,
+                                                       double* __restrict__ core, int64_t ldc, int i0, int vec2) {
+  static_assert(Cfg::WNW == 1, "each warp owns whole rows of W");
+  constexpr int BN = Cfg::BN;
+  constexpr int NJ2 = BN / 8;
+  constexpr int SW = BN + 4;
+  __shared__ LogTables lt;
+  extern __shared__ double dsm[];
+  if (KIND == UBLR_OP_LOG) init_log_tables(&lt);
+  const int j = blockIdx.x, i = i0 + blockIdx.y;
+  const int ri0 = off[i], mi = off[i + 1] - ri0;
+  const int cj0 = off[j], mj = off[j + 1] - cj0;
+  const int ki = roff[i + 1] - roff[i], kj = roff[j + 1] - roff[j];
+  CouplingAProducer<KIND, Cfg> ap(op, &lt, ri0, mi, cj0, mj);
+  CouplingBProducer<Cfg> bp{V, lduv, cj0, mj, kj, vec2 != 0};
+  double acc[Cfg::MI][Cfg::NJ][2];
+#pragma unroll
+  for (int a = 0; a < Cfg::MI; ++a)
+#pragma unroll
+    for (int c = 0; c < Cfg::NJ; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
+  __syncthreads();
+  dmma_mainloop<Cfg>(ap, bp, (mj + Cfg::BK - 1) / Cfg::BK, dsm, acc);
+  __syncthreads();
+  // W -> shared, k-major (row r of W = k index of C = U^T W)
+  double* Ws = dsm;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int a = 0; a < Cfg::MI; ++a)
+#pragma unroll
+    for (int c = 0; c < Cfg::NJ; ++c) {
+      int r = warp * Cfg::WM + a * 8 + g;
+      Ws[r * SW + c * 8 + 2 * t] = acc[a][c][0];
+      Ws[r * SW + c * 8 + 2 * t + 1] = acc[a][c][1];
+    }
+  __syncthreads();
+  // C = U_i^T W : (ki x kj) in 8x8 tiles, tile ids spread over the warps
+  constexpr int NW = Cfg::NT / 32;
+  const int mt = (ki + 7) / 8, nt = (kj + 7) / 8;
+  const double* Ui = U + (int64_t)ri0 * lduv;
+  constexpr int MAXT = (8 * NJ2 + NW - 1) / NW;  // tiles per warp when ki, kj <= BN
+  double c2[MAXT][2];
+#pragma unroll
+  for (int q = 0; q < MAXT; ++q) c2[q][0] = c2[q][1] = 0.0;
+  for (int r0 = 0; r0 < mi; r0 += 4) {
+    const int r = r0 + t;
+    const bool rok = r < mi;
+#pragma unroll
+    for (int q = 0; q < MAXT; ++q) {
+      int tile = warp + q * NW;
+      if (tile >= mt * nt) break;
+      int ta = tile / nt, tc = tile - (tile / nt) * nt;
+      int acol = ta * 8 + g;
+      double av = (rok && acol < ki) ? __ldg(&Ui[(int64_t)r * lduv + acol]) : 0.0;
+      double bv = rok ? Ws[r * SW + tc * 8 + g] : 0.0;
+      mma8x8x4(c2[q][0], c2[q][1], av, bv);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < MAXT; ++q) {
+    int tile = warp + q * NW;
+    if (tile >= mt * nt) break;
+    int ta = tile / nt, tc = tile - (tile / nt) * nt;
+    int a = ta * 8 + g;
+    int c = tc * 8 + 2 * t;
+    if (a < ki) {
+      double* dst = core + (int64_t)(roff[i] + a) * ldc + roff[j];
+      if (c < kj) dst[c] = c2[q][0];
+      if (c + 1 < kj) dst[c + 1] = c2[q][1];
+    }
   }
 }
 
@@ -310,23 +438,28 @@ extern "C" int ublr_coupling(const ublr_op_t* op, const int32_t* off, const int3
   UBLR_REQUIRE(0 <= i0 && i0 < i1 && i1 <= b, UBLR_ERR_VALUE, "ublr_coupling: bad block-row range");
   dim3 grid(b, i1 - i0);
   int kk = k < m_max ? k : m_max;  // effective ranks never exceed min(k, m)
-#define UBLR_CP_LAUNCH(RW, NJ)                                                                             \
-  UBLR_DISPATCH_KIND(op->kind, KIND, {                                                                    \
-    size_t sm = coupling_smem(8 * (RW), (NJ));                                                           \
-    UBLR_CUDA(cudaFuncSetAttribute(k_coupling<KIND, RW, NJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                   (int)sm));                                                            \
-    k_coupling<KIND, RW, NJ><<<grid, CP_THREADS, sm, st>>>(*op, off, roff, k, U, V, ld_uv, core, ld_c, i0);   \
+  int vec2 = ((ld_uv % 2) == 0 && ((uintptr_t)V) % 16 == 0) ? 1 : 0;
+#define UBLR_CP2(BM, BN)                                                                                     \
+  UBLR_DISPATCH_KIND(op->kind, KIND, {                                                                      \
+    using Cfg = TileCfg<BM, BN, 32, 8, 1, 2>;                                                               \
+    size_t sm = Cfg::smem_bytes();                                                                          \
+    size_t sw = (size_t)(BM) * ((BN) + 4) * sizeof(double);                                                 \
+    if (sw > sm) sm = sw;                                                                                   \
+    UBLR_CUDA(cudaFuncSetAttribute(k_coupling2<KIND, Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
+    k_coupling2<KIND, Cfg><<<grid, Cfg::NT, sm, st>>>(*op, off, roff, U, V, ld_uv, core, ld_c, i0, vec2);     \
   })
   if (m_max <= 64) {
-    if (kk <= 16) { UBLR_CP_LAUNCH(8, 2); }
-    else if (kk <= 32) { UBLR_CP_LAUNCH(8, 4); }
-    else { UBLR_CP_LAUNCH(8, 8); }
+    if (kk <= 16) { UBLR_CP2(64, 16); }
+    else if (kk <= 24) { UBLR_CP2(64, 24); }
+    else if (kk <= 48) { UBLR_CP2(64, 48); }
+    else { UBLR_CP2(64, 64); }
   } else {
-    if (kk <= 16) { UBLR_CP_LAUNCH(32, 2); }
-    else if (kk <= 32) { UBLR_CP_LAUNCH(32, 4); }
-    else { UBLR_CP_LAUNCH(32, 8); }
+    if (kk <= 16) { UBLR_CP2(256, 16); }
+    else if (kk <= 24) { UBLR_CP2(256, 24); }
+    else if (kk <= 48) { UBLR_CP2(256, 48); }
+    else { UBLR_CP2(256, 64); }
   }
-#undef UBLR_CP_LAUNCH
+#undef UBLR_CP2
   UBLR_LAUNCH_CHECK();
   return UBLR_OK;
 }

@@ -70,7 +70,8 @@ __global__ void __launch_bounds__(Cfg::NT) k_gemm2(int M, int N, int K, double a
   for (int i = 0; i < Cfg::MI; ++i)
 #pragma unroll
     for (int j = 0; j < Cfg::NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  dmma_mainloop<Cfg>(ap, bp, (K + Cfg::BK - 1) / Cfg::BK, dsm, acc);
+  WholeStage<decltype(ap)> apw{ap};
+  dmma_mainloop<Cfg>(apw, bp, (K + Cfg::BK - 1) / Cfg::BK, dsm, acc);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int wr = warp / Cfg::WNW, wc = warp % Cfg::WNW;

@@ -63,15 +63,9 @@ __device__ __forceinline__ void dmma_mainloop(AP& ap, BP& bp, int nk, double* sm
   for (int ks = 0; ks < nk; ++ks) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
-    {
-      int nx = ks + STAGES - 1;
-      int slot = nx % STAGES;
-      if (nx < nk) {
-        ap.stage(As0 + slot * Cfg::A_STAGE, nx);
-        bp.stage(Bs0 + slot * Cfg::B_STAGE, nx);
-      }
-      cp_async_commit();
-    }
+    const int nx = ks + STAGES - 1;
+    double* As_nx = As0 + (nx % STAGES) * Cfg::A_STAGE;
+    if (nx < nk) bp.stage(Bs0 + (nx % STAGES) * Cfg::B_STAGE, nx);
     const double* As = As0 + (ks % STAGES) * Cfg::A_STAGE;
     const double* Bs = Bs0 + (ks % STAGES) * Cfg::B_STAGE;
     double a[2][Cfg::MI], b[2][Cfg::NJ];
@@ -89,14 +83,28 @@ __device__ __forceinline__ void dmma_mainloop(AP& ap, BP& bp, int nk, double* sm
 #pragma unroll
         for (int j = 0; j < Cfg::NJ; ++j) b[cur ^ 1][j] = Bs[Cfg::bi(kr, bn0 + j * 8)];
       }
+      // the A producer's work for the next stage is spread over the k4 slices,
+      // so operator-tile evaluation interleaves with this slice's DMMAs
+      if (nx < nk) ap.stage_part(As_nx, nx, k4, BK / 4);
 #pragma unroll
       for (int i = 0; i < Cfg::MI; ++i)
 #pragma unroll
         for (int j = 0; j < Cfg::NJ; ++j) mma8x8x4(acc[i][j][0], acc[i][j][1], a[cur][i], b[cur][j]);
     }
+    cp_async_commit();
   }
   cp_async_wait<0>();
 }
+
+// Adapter giving a whole-stage producer the stage_part interface (work done at part 0).
+template <class P>
+struct WholeStage {
+  P& p;
+  __device__ __forceinline__ void stage(double* s, int ks) { p.stage(s, ks); }
+  __device__ __forceinline__ void stage_part(double* s, int ks, int part, int) {
+    if (part == 0) p.stage(s, ks);
+  }
+};
 
 // Copy a (rows x cols) tile of a row-major global matrix, contiguous along
 // cols, into shared memory at dst[r * sstride + c] (r < rows, c < cols),

@@ -126,11 +126,16 @@ struct GenAProducer {
     gk0 = threadIdx.x / Cfg::BM;
     rp = load_row_point(op, row0 + grow, row0 + grow < n);
   }
-  __device__ __forceinline__ void stage(double* As, int ks) {
+  __device__ __forceinline__ void stage(double* As, int ks) { stage_part(As, ks, 0, 1); }
+  // entries [part*E/nparts, (part+1)*E/nparts) of this thread's E = BK/KL entries
+  __device__ __forceinline__ void stage_part(double* As, int ks, int part, int nparts) {
     constexpr int KL = Cfg::NT / Cfg::BM;  // kk lanes
+    constexpr int E = Cfg::BK / KL;
     const int k0 = ks * Cfg::BK;
+    const int e0 = (part * E) / nparts, e1 = ((part + 1) * E) / nparts;
 #pragma unroll
-    for (int e = 0; e < Cfg::BK / KL; ++e) {
+    for (int e = 0; e < E; ++e) {
+      if (e < e0 || e >= e1) continue;
       int kk = gk0 + e * KL;
       int q = k0 + kk;
       double v = 0.0;

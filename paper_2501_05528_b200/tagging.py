@@ -163,12 +163,14 @@ def _evaluate(T: TaggingMatrix, tess: Tessellation, attempts: int) -> TaggingPla
         raise DegenerateTagsError(f"block {i}: null-vector residual {res[i]:.3e} exceeds {limit:.3e}")
     b = tess.b
     P = np.abs(E @ Z.T)                     # P[j, i] = |<t_j, z^(i)>|
-    near = np.zeros((b, b), dtype=bool)
-    for i, nb in enumerate(tess.neighbor_lists):
-        near[nb, i] = True
-    far_any = (~near).any(axis=0)
-    hi = np.where(near, -np.inf, P).max(axis=0)
-    lo = np.where(near, np.inf, P).min(axis=0)
+    nl = np.array([len(nb) for nb in tess.neighbor_lists])
+    rows_near = np.concatenate([np.asarray(nb, dtype=np.int64) for nb in tess.neighbor_lists])
+    cols_near = np.repeat(np.arange(b), nl)
+    far_any = nl < b
+    P[rows_near, cols_near] = np.inf        # exclude the near field from the min ...
+    lo = P.min(axis=0)
+    P[rows_near, cols_near] = -np.inf       # ... and from the max
+    hi = P.max(axis=0)
     rho = np.full(b, np.nan)
     with np.errstate(divide="ignore", invalid="ignore"):
         r = np.where(hi == 0.0, 1.0, np.where(lo == 0.0, np.inf, hi / lo))

@@ -59,5 +59,21 @@ def bench_sketch():
 
 if __name__ == "__main__":
     torch.cuda.set_device(0)
-    for what in (sys.argv[1:] or ["apply", "gemm", "sketch"]):
+    for what in (sys.argv[1:] or ["apply", "gemm", "sketch", "coupling"]):
         globals()["bench_" + what]()
+
+
+def bench_coupling():
+    from paper_2501_05528_b200.bases import BlockBases
+    from paper_2501_05528_b200.reconstruction import direct_core
+    for per, b, k, kind in ((256, 256, 48, "inv"), (256, 256, 40, "log"), (64, 64, 20, "log")):
+        pts = P.grid_points(per, 2)
+        tess = P.build_tessellation(pts, b)
+        dt = device_tess(tess, torch.device("cuda"))
+        op = P.KernelOperator(pts, kind, 1.0)
+        U = torch.randn(dt.n, k, dtype=torch.float64, device="cuda")
+        bs = BlockBases(dt, U, U.clone(), k, "tag", (0, 0))
+        t = timeit(lambda: direct_core(op, tess, bs), reps=2)
+        n = dt.n
+        fl = 2.0 * n * n * k + 2.0 * n * (b * k) * k
+        print(f"coupling {kind} N={n} b={b} k={k}: {t*1e3:.2f} ms {fl/t/1e12:.2f} TFLOP/s ({fl/t/1e12/37.13:.1%})")
