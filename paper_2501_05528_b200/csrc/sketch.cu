@@ -14,6 +14,7 @@
 #include "common.cuh"
 #include "optile.cuh"
 #include "gemm_core.cuh"
+#include "tmem.cuh"
 #include <cstdlib>
 
 namespace ublr {
@@ -487,6 +488,232 @@ __global__ void __launch_bounds__(Cfg::NT) k_sketch_tagged2(ublr_op_t op, const 
   }
 }
 
+// ------------------------------------------------------- tagged sketch v3
+// CTA = BM (32) permuted rows x BN (128 or 64) test-block columns, 8 warps
+// (2 x 4; warp tile 16 x BN/4). The ell tag-group accumulators of the CTA
+// (BM x BN x ell doubles: 320 KB for 32 x 128 x 10) do not fit in the
+// register file, so the first TG groups live in TMEM (tcgen05.st/ld, 256 KB
+// per SM) and the rest in registers. Every A tile is generated once per
+// (row tile, column tile) — once per row tile when 2gc <= BN — and every
+// test-block panel is reused by BM rows.
+template <int KIND, int L, class Cfg>
+__global__ void __launch_bounds__(Cfg::NT, 1) k_sketch_tagged3(ublr_op_t op, const int32_t* __restrict__ off, int b,
+                                                               const double* __restrict__ T, int ell,
+                                                               const double* __restrict__ G,
+                                                               const double* __restrict__ H, int64_t ldx, int gc,
+                                                               double* __restrict__ Y, double* __restrict__ Z,
+                                                               int64_t ldy, int row_begin, int row_end, int vec2) {
+  constexpr int BK = Cfg::BK, STAGES = Cfg::STAGES;
+  constexpr int WD = Cfg::MI * Cfg::NJ * 2;            // W doubles per thread
+  constexpr int TCAP = (256 / 2) / WD;                 // groups per thread that fit in 256 TMEM columns
+  constexpr int TG = (L < TCAP) ? L : TCAP;            // groups kept in TMEM
+  constexpr int RG = L - TG;                           // groups kept in registers
+  static_assert(WD % 8 == 0, "W per thread must be a multiple of 8 doubles");
+  static_assert(Cfg::NT == 256, "two warps share each TMEM lane quarter");
+  __shared__ LogTables lt;
+  __shared__ uint32_t tbase_slot;
+  extern __shared__ double dsm[];
+  if (KIND == UBLR_OP_LOG) init_log_tables(&lt);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  if (warp == 0) tmem::alloc(&tbase_slot, 512);
+  tmem::fence_before();
+  __syncthreads();
+  tmem::fence_after();
+  const uint32_t tbase = tbase_slot;
+  const int colbase = (warp >> 2) * 256;             // warps w and w+4 split the quarter's columns
+
+  const int ncols = (H ? 2 : 1) * gc;
+  const int row0 = row_begin + blockIdx.y * Cfg::BM;
+  const int col0 = blockIdx.x * Cfg::BN;
+  // A producer (absolute columns q0.. masked by qend), interleavable
+  struct AP {
+    const ublr_op_t& op; const LogTables* lt; RowPoint rp; int grow, gk0;
+    int q0n, qendn;   // columns of the stage being produced
+    __device__ __forceinline__ void stage_part(double* As, int, int part, int nparts) {
+      constexpr int KL = Cfg::NT / Cfg::BM;
+      constexpr int E = BK / KL;
+      const int e0 = (part * E) / nparts, e1 = ((part + 1) * E) / nparts;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        if (e < e0 || e >= e1) continue;
+        int kk = gk0 + e * KL;
+        int q = q0n + kk;
+        double v = 0.0;
+        if (rp.p >= 0 && q < qendn) v = op_entry<KIND>(op, rp, q, lt);
+        As[Cfg::ai(grow, kk)] = v;
+      }
+    }
+  } ap{op, &lt, load_row_point(op, row0 + (int)(threadIdx.x % Cfg::BM), row0 + (int)(threadIdx.x % Cfg::BM) < row_end),
+       (int)(threadIdx.x % Cfg::BM), (int)(threadIdx.x / Cfg::BM), 0, 0};
+  auto b_stage = [&](double* Bs, int q0, int qend) {
+    if (col0 + Cfg::BN <= gc || !H) {
+      tile_copy<Cfg::NT>(Bs, Cfg::SB, G, ldx, BK, Cfg::BN, q0, col0, qend, gc, IdentityRows{}, vec2 != 0);
+    } else if (col0 >= gc) {
+      tile_copy<Cfg::NT>(Bs, Cfg::SB, H, ldx, BK, Cfg::BN, q0, col0 - gc, qend, gc, IdentityRows{}, vec2 != 0);
+    } else {
+      for (int e = threadIdx.x; e < BK * Cfg::BN; e += Cfg::NT) {
+        int kk = e / Cfg::BN, c = e - kk * Cfg::BN;
+        int q = q0 + kk, col = col0 + c;
+        bool ok = q < qend && col < ncols;
+        const double* src = G;
+        if (ok) src = (col < gc) ? (G + (int64_t)q * ldx + col) : (H + (int64_t)q * ldx + (col - gc));
+        cp_async8(&Bs[kk * Cfg::SB + c], src, ok);
+      }
+    }
+  };
+
+  double w[Cfg::MI][Cfg::NJ][2];
+  double racc[RG > 0 ? RG : 1][Cfg::MI][Cfg::NJ][2];
+#pragma unroll
+  for (int i = 0; i < Cfg::MI; ++i)
+#pragma unroll
+    for (int j = 0; j < Cfg::NJ; ++j) {
+      w[i][j][0] = w[i][j][1] = 0.0;
+#pragma unroll
+      for (int c = 0; c < (RG > 0 ? RG : 1); ++c) racc[c][i][j][0] = racc[c][i][j][1] = 0.0;
+    }
+  {  // zero the TMEM groups
+    double z[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) z[q] = 0.0;
+#pragma unroll
+    for (int c = 0; c < TG; ++c)
+#pragma unroll
+      for (int h = 0; h < WD / 8; ++h) tmem::st8(tmem::addr(tbase, warp, colbase + (c * WD + h * 8) * 2), z);
+    tmem::wait_st();
+  }
+  __syncthreads();
+
+  double* As0 = dsm;
+  double* Bs0 = dsm + STAGES * Cfg::A_STAGE;
+  const int wr = warp / Cfg::WNW, wc = warp % Cfg::WNW;
+  const int am0 = wr * Cfg::WM + g;
+  const int bn0 = wc * Cfg::WN + g;
+  // stage 0
+  int j = 0, q0 = off[0], qend = off[1];
+  ap.q0n = q0; ap.qendn = qend;
+  ap.stage_part(As0, 0, 0, 1);
+  b_stage(Bs0, q0, qend);
+  cp_async_commit();
+  int slot = 0;
+  for (;;) {
+    // coordinates of the next stage
+    int nq0 = q0 + BK, nj = j, nqend = qend;
+    if (nq0 >= qend) {
+      nj = j + 1;
+      if (nj < b) { nq0 = off[nj]; nqend = off[nj + 1]; }
+    }
+    const bool more = nj < b;
+    cp_async_wait<0>();
+    __syncthreads();
+    double* As_nx = As0 + (slot ^ 1) * Cfg::A_STAGE;
+    if (more) b_stage(Bs0 + (slot ^ 1) * Cfg::B_STAGE, nq0, nqend);
+    ap.q0n = nq0; ap.qendn = nqend;
+    const double* As = As0 + slot * Cfg::A_STAGE;
+    const double* Bs = Bs0 + slot * Cfg::B_STAGE;
+#pragma unroll
+    for (int k4 = 0; k4 < BK / 4; ++k4) {
+      const int kr = k4 * 4 + t;
+      double a[Cfg::MI], bb[Cfg::NJ];
+#pragma unroll
+      for (int i = 0; i < Cfg::MI; ++i) a[i] = As[Cfg::ai(am0 + i * 8, kr)];
+#pragma unroll
+      for (int jj = 0; jj < Cfg::NJ; ++jj) bb[jj] = Bs[Cfg::bi(kr, bn0 + jj * 8)];
+      if (more) ap.stage_part(As_nx, 0, k4, BK / 4);
+#pragma unroll
+      for (int i = 0; i < Cfg::MI; ++i)
+#pragma unroll
+        for (int jj = 0; jj < Cfg::NJ; ++jj) mma8x8x4(w[i][jj][0], w[i][jj][1], a[i], bb[jj]);
+    }
+    cp_async_commit();
+    if (nj != j) {
+      // block j complete: acc_c += T[j, c] * W  (TMEM groups, then register groups)
+      const double* Tj = T + (int64_t)j * ell;
+      double wf[WD];
+#pragma unroll
+      for (int i = 0; i < Cfg::MI; ++i)
+#pragma unroll
+        for (int jj = 0; jj < Cfg::NJ; ++jj) {
+          wf[(i * Cfg::NJ + jj) * 2] = w[i][jj][0];
+          wf[(i * Cfg::NJ + jj) * 2 + 1] = w[i][jj][1];
+          w[i][jj][0] = w[i][jj][1] = 0.0;
+        }
+#pragma unroll
+      for (int c = 0; c < TG; ++c) {
+        const double tc = (c < ell) ? __ldg(&Tj[c]) : 0.0;
+#pragma unroll
+        for (int h = 0; h < WD / 8; ++h) {
+          double v[8];
+          const uint32_t ta = tmem::addr(tbase, warp, colbase + (c * WD + h * 8) * 2);
+          tmem::ld8(ta, v);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) v[q] = fma(tc, wf[h * 8 + q], v[q]);
+          tmem::st8(ta, v);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < RG; ++c) {
+        const double tc = (TG + c < ell) ? __ldg(&Tj[TG + c]) : 0.0;
+#pragma unroll
+        for (int i = 0; i < Cfg::MI; ++i)
+#pragma unroll
+          for (int jj = 0; jj < Cfg::NJ; ++jj) {
+            racc[c][i][jj][0] = fma(tc, wf[(i * Cfg::NJ + jj) * 2], racc[c][i][jj][0]);
+            racc[c][i][jj][1] = fma(tc, wf[(i * Cfg::NJ + jj) * 2 + 1], racc[c][i][jj][1]);
+          }
+      }
+      tmem::wait_st();
+    }
+    if (!more) break;
+    j = nj; q0 = nq0; qend = nqend;
+    slot ^= 1;
+  }
+  cp_async_wait<0>();
+  // epilogue
+#pragma unroll
+  for (int c = 0; c < L; ++c) {
+    if (c >= ell) break;
+    double accv[WD];
+    if (c < TG) {
+#pragma unroll
+      for (int h = 0; h < WD / 8; ++h) {
+        double v[8];
+        tmem::ld8(tmem::addr(tbase, warp, colbase + (c * WD + h * 8) * 2), v);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) accv[h * 8 + q] = v[q];
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < Cfg::MI; ++i)
+#pragma unroll
+        for (int jj = 0; jj < Cfg::NJ; ++jj) {
+          accv[(i * Cfg::NJ + jj) * 2] = racc[(c - TG) < 0 ? 0 : (c - TG)][i][jj][0];
+          accv[(i * Cfg::NJ + jj) * 2 + 1] = racc[(c - TG) < 0 ? 0 : (c - TG)][i][jj][1];
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < Cfg::MI; ++i) {
+      int row = row0 + wr * Cfg::WM + i * 8 + g;
+      if (row >= row_end) continue;
+#pragma unroll
+      for (int jj = 0; jj < Cfg::NJ; ++jj)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          int col = col0 + wc * Cfg::WN + jj * 8 + 2 * t + h;
+          if (col >= ncols) continue;
+          double* dst = (col < gc) ? Y : Z;
+          int q = (col < gc) ? col : col - gc;
+          dst[(int64_t)row * ldy + c * gc + q] = accv[(i * Cfg::NJ + jj) * 2 + h];
+        }
+    }
+  }
+  tmem::fence_before();
+  __syncthreads();
+  tmem::fence_after();
+  if (warp == 0) tmem::dealloc(tbase, 512);
+}
+
 }  // namespace
 }  // namespace ublr
 
@@ -557,12 +784,43 @@ int sketch_common_v2(const ublr_op_t* op, const int32_t* off, int b, const doubl
                      int ell, const double* G, const double* H, int64_t ld_x, int gc, double* Y, double* Z,
                      int64_t ld_y, cudaStream_t st);
 
+int sketch_common_v3(const ublr_op_t* op, const int32_t* off, int b, const double* T, int ell, const double* G,
+                     const double* H, int64_t ld_x, int gc, double* Y, double* Z, int64_t ld_y, int row_begin,
+                     int row_end, cudaStream_t st) {
+  const int ncols = (H ? 2 : 1) * gc;
+  int vec2 = ((ld_x % 2) == 0 && ((uintptr_t)G) % 16 == 0 && (!H || ((uintptr_t)H) % 16 == 0)) ? 1 : 0;
+  dim3 grid;
+#define UBLR_TS3(L, BNv)                                                                                        \
+  {                                                                                                             \
+    using Cfg = TileCfg<32, BNv, 32, 2, 4, 2>;                                                                  \
+    grid.x = (unsigned)((ncols + (BNv) - 1) / (BNv));                                                           \
+    grid.y = (unsigned)((row_end - row_begin + 31) / 32);                                                       \
+    UBLR_DISPATCH_KIND(op->kind, KIND, {                                                                        \
+      size_t sm = Cfg::smem_bytes();                                                                            \
+      UBLR_CUDA(cudaFuncSetAttribute(k_sketch_tagged3<KIND, L, Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                     (int)sm));                                                                \
+      k_sketch_tagged3<KIND, L, Cfg><<<grid, Cfg::NT, sm, st>>>(*op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y,   \
+                                                                row_begin, row_end, vec2);                     \
+    })                                                                                                          \
+  }
+  if (ncols <= 64) {
+    if (ell <= 4) UBLR_TS3(4, 64) else UBLR_TS3(10, 64)
+  } else {
+    if (ell <= 4) UBLR_TS3(4, 128) else UBLR_TS3(10, 128)
+  }
+#undef UBLR_TS3
+  UBLR_LAUNCH_CHECK();
+  return UBLR_OK;
+}
+
 int sketch_common(const ublr_op_t* op, const int32_t* off, int b, const double* T, int ell, const double* G,
                   const double* H, int64_t ld_x, int gc, double* Y, double* Z, int64_t ld_y, int row_begin,
                   int row_end, cudaStream_t st) {
   UBLR_REQUIRE(row_begin >= 0 && row_begin < row_end && row_end <= op->n, UBLR_ERR_VALUE, "sketch: bad row range");
-  static const bool v2 = getenv("UBLR_SKETCH_V2") != nullptr;
-  if (v2 && row_begin == 0 && row_end == op->n) return sketch_common_v2(op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y, st);
+  static const char* ver = getenv("UBLR_SKETCH_VERSION");
+  const int v = ver ? atoi(ver) : 3;
+  if (v == 2 && row_begin == 0 && row_end == op->n) return sketch_common_v2(op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y, st);
+  if (v == 3 && ell <= 10) return sketch_common_v3(op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y, row_begin, row_end, st);
   return sketch_common_v1(op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y, row_begin, row_end, st);
 }
 

@@ -57,12 +57,6 @@ def bench_sketch():
         fl = 2 * (2.0 * n * n * gc + 2.0 * n * b * gc * 10)
         print(f"sketch {kind} N={n} b={b} gc={gc}: {t*1e3:.2f} ms {fl/t/1e12:.2f} TFLOP/s ({fl/t/1e12/37.13:.1%})")
 
-if __name__ == "__main__":
-    torch.cuda.set_device(0)
-    for what in (sys.argv[1:] or ["apply", "gemm", "sketch", "coupling"]):
-        globals()["bench_" + what]()
-
-
 def bench_coupling():
     from paper_2501_05528_b200.bases import BlockBases
     from paper_2501_05528_b200.reconstruction import direct_core
@@ -77,3 +71,10 @@ def bench_coupling():
         n = dt.n
         fl = 2.0 * n * n * k + 2.0 * n * (b * k) * k
         print(f"coupling {kind} N={n} b={b} k={k}: {t*1e3:.2f} ms {fl/t/1e12:.2f} TFLOP/s ({fl/t/1e12/37.13:.1%})")
+
+
+if __name__ == "__main__":
+    torch.cuda.set_device(0)
+    for what in (sys.argv[1:] or ["apply", "gemm", "sketch", "coupling"]):
+        globals()["bench_" + what]()
+
