@@ -505,11 +505,14 @@ __global__ void __launch_bounds__(Cfg::NT, 1) k_sketch_tagged3(ublr_op_t op, con
                                                                int64_t ldy, int row_begin, int row_end, int vec2) {
   constexpr int BK = Cfg::BK, STAGES = Cfg::STAGES;
   constexpr int WD = Cfg::MI * Cfg::NJ * 2;            // W doubles per thread
-  constexpr int TCAP = (256 / 2) / WD;                 // groups per thread that fit in 256 TMEM columns
+  constexpr int NWARP = Cfg::NT / 32;
+  constexpr int WCOLS = 512 / (NWARP / 4);             // TMEM columns per warp (warps sharing a lane quarter split 512)
+  constexpr int WDP = (WD + 7) / 8 * 8;                // TMEM stride per group (whole x16 chunks)
+  constexpr int TCAP = (WCOLS / 2) / WDP;              // groups per thread that fit
   constexpr int TG = (L < TCAP) ? L : TCAP;            // groups kept in TMEM
   constexpr int RG = L - TG;                           // groups kept in registers
-  static_assert(WD % 8 == 0, "W per thread must be a multiple of 8 doubles");
-  static_assert(Cfg::NT == 256, "two warps share each TMEM lane quarter");
+  static_assert(NWARP % 4 == 0, "lane quarters are shared evenly");
+  static_assert(TG * WDP * 2 <= WCOLS, "TMEM groups overflow the warp's columns");
   __shared__ LogTables lt;
   __shared__ uint32_t tbase_slot;
   extern __shared__ double dsm[];
@@ -521,7 +524,7 @@ __global__ void __launch_bounds__(Cfg::NT, 1) k_sketch_tagged3(ublr_op_t op, con
   __syncthreads();
   tmem::fence_after();
   const uint32_t tbase = tbase_slot;
-  const int colbase = (warp >> 2) * 256;             // warps w and w+4 split the quarter's columns
+  const int colbase = (warp >> 2) * WCOLS;           // warps sharing a lane quarter split its columns
 
   const int ncols = (H ? 2 : 1) * gc;
   const int row0 = row_begin + blockIdx.y * Cfg::BM;
@@ -580,7 +583,7 @@ __global__ void __launch_bounds__(Cfg::NT, 1) k_sketch_tagged3(ublr_op_t op, con
 #pragma unroll
     for (int c = 0; c < TG; ++c)
 #pragma unroll
-      for (int h = 0; h < WD / 8; ++h) tmem::st8(tmem::addr(tbase, warp, colbase + (c * WD + h * 8) * 2), z);
+      for (int h = 0; h < WDP / 8; ++h) tmem::st8(tmem::addr(tbase, warp, colbase + (c * WDP + h * 8) * 2), z);
     tmem::wait_st();
   }
   __syncthreads();
@@ -630,7 +633,9 @@ __global__ void __launch_bounds__(Cfg::NT, 1) k_sketch_tagged3(ublr_op_t op, con
     if (nj != j) {
       // block j complete: acc_c += T[j, c] * W  (TMEM groups, then register groups)
       const double* Tj = T + (int64_t)j * ell;
-      double wf[WD];
+      double wf[WDP];
+#pragma unroll
+      for (int q = WD; q < WDP; ++q) wf[q] = 0.0;
 #pragma unroll
       for (int i = 0; i < Cfg::MI; ++i)
 #pragma unroll
@@ -643,9 +648,9 @@ __global__ void __launch_bounds__(Cfg::NT, 1) k_sketch_tagged3(ublr_op_t op, con
       for (int c = 0; c < TG; ++c) {
         const double tc = (c < ell) ? __ldg(&Tj[c]) : 0.0;
 #pragma unroll
-        for (int h = 0; h < WD / 8; ++h) {
+        for (int h = 0; h < WDP / 8; ++h) {
           double v[8];
-          const uint32_t ta = tmem::addr(tbase, warp, colbase + (c * WD + h * 8) * 2);
+          const uint32_t ta = tmem::addr(tbase, warp, colbase + (c * WDP + h * 8) * 2);
           tmem::ld8(ta, v);
 #pragma unroll
           for (int q = 0; q < 8; ++q) v[q] = fma(tc, wf[h * 8 + q], v[q]);
@@ -674,12 +679,12 @@ __global__ void __launch_bounds__(Cfg::NT, 1) k_sketch_tagged3(ublr_op_t op, con
 #pragma unroll
   for (int c = 0; c < L; ++c) {
     if (c >= ell) break;
-    double accv[WD];
+    double accv[WDP];
     if (c < TG) {
 #pragma unroll
-      for (int h = 0; h < WD / 8; ++h) {
+      for (int h = 0; h < WDP / 8; ++h) {
         double v[8];
-        tmem::ld8(tmem::addr(tbase, warp, colbase + (c * WD + h * 8) * 2), v);
+        tmem::ld8(tmem::addr(tbase, warp, colbase + (c * WDP + h * 8) * 2), v);
 #pragma unroll
         for (int q = 0; q < 8; ++q) accv[h * 8 + q] = v[q];
       }
@@ -792,7 +797,7 @@ int sketch_common_v3(const ublr_op_t* op, const int32_t* off, int b, const doubl
   dim3 grid;
 #define UBLR_TS3(L, BNv)                                                                                        \
   {                                                                                                             \
-    using Cfg = TileCfg<32, BNv, 32, 2, 4, 2>;                                                                  \
+    using Cfg = TileCfg<32, BNv, 32, 2, 8, 2>;                                                                  \
     grid.x = (unsigned)((ncols + (BNv) - 1) / (BNv));                                                           \
     grid.y = (unsigned)((row_end - row_begin + 31) / 32);                                                       \
     UBLR_DISPATCH_KIND(op->kind, KIND, {                                                                        \
