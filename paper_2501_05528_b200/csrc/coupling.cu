@@ -156,7 +156,8 @@ struct CouplingAProducer {
   __device__ __forceinline__ void stage_part(double* As, int ks, int part, int nparts) {
     constexpr int KL = Cfg::NT / Cfg::BM;
     constexpr int E = Cfg::BK / KL;
-    const int e0 = (part * E) / nparts, e1 = ((part + 1) * E) / nparts;
+    int e0, e1;
+    chunk_range<E, 2>(part, nparts, e0, e1);
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       if (e < e0 || e >= e1) continue;
@@ -222,7 +223,15 @@ __global__ void __launch_bounds__(Cfg::NT) k_coupling2(ublr_op_t op, const int32
   // C = U_i^T W : (ki x kj) in 8x8 tiles, tile ids spread over the warps
   constexpr int NW = Cfg::NT / 32;
   const int mt = (ki + 7) / 8, nt = (kj + 7) / 8;
+  // U_i -> shared (behind W), so phase 2 reads both operands from shared memory
+  constexpr int SU = BN + 1;
+  double* Us = dsm + Cfg::BM * SW;
   const double* Ui = U + (int64_t)ri0 * lduv;
+  for (int e = threadIdx.x; e < mi * ki; e += Cfg::NT) {
+    int r = e / ki, a = e - r * ki;
+    Us[r * SU + a] = Ui[(int64_t)r * lduv + a];
+  }
+  __syncthreads();
   constexpr int MAXT = (8 * NJ2 + NW - 1) / NW;  // tiles per warp when ki, kj <= BN
   double c2[MAXT][2];
 #pragma unroll
@@ -236,7 +245,7 @@ __global__ void __launch_bounds__(Cfg::NT) k_coupling2(ublr_op_t op, const int32
       if (tile >= mt * nt) break;
       int ta = tile / nt, tc = tile - (tile / nt) * nt;
       int acol = ta * 8 + g;
-      double av = (rok && acol < ki) ? __ldg(&Ui[(int64_t)r * lduv + acol]) : 0.0;
+      double av = (rok && acol < ki) ? Us[r * SU + acol] : 0.0;
       double bv = rok ? Ws[r * SW + tc * 8 + g] : 0.0;
       mma8x8x4(c2[q][0], c2[q][1], av, bv);
     }
@@ -443,7 +452,7 @@ extern "C" int ublr_coupling(const ublr_op_t* op, const int32_t* off, const int3
   UBLR_DISPATCH_KIND(op->kind, KIND, {                                                                      \
     using Cfg = TileCfg<BM, BN, 32, 8, 1, 2>;                                                               \
     size_t sm = Cfg::smem_bytes();                                                                          \
-    size_t sw = (size_t)(BM) * ((BN) + 4) * sizeof(double);                                                 \
+    size_t sw = (size_t)(BM) * ((BN) + 4 + (BN) + 1) * sizeof(double);  /* W and U_i after the main loop */  \
     if (sw > sm) sm = sw;                                                                                   \
     UBLR_CUDA(cudaFuncSetAttribute(k_coupling2<KIND, Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
     k_coupling2<KIND, Cfg><<<grid, Cfg::NT, sm, st>>>(*op, off, roff, U, V, ld_uv, core, ld_c, i0, vec2);     \

@@ -96,6 +96,21 @@ __device__ __forceinline__ void dmma_mainloop(AP& ap, BP& bp, int nk, double* sm
   cp_async_wait<0>();
 }
 
+// Entries [e0, e1) of a producer's E per-thread entries handled in `part` of
+// `nparts`, grouped CHUNK at a time (independent evaluations in flight
+// together) and issued at the last slice of each chunk's window.
+template <int E, int CHUNK>
+__device__ __forceinline__ void chunk_range(int part, int nparts, int& e0, int& e1) {
+  if (nparts <= 1) { e0 = 0; e1 = E; return; }
+  const int csz = (E + nparts - 1) / nparts > CHUNK ? (E + nparts - 1) / nparts : CHUNK;  // entries per chunk
+  const int nch = (E + csz - 1) / csz;
+  const int per = nparts / nch;                      // slices per chunk window (>= 1)
+  const int ch = part / per;
+  if (part % per != per - 1 || ch >= nch) { e0 = e1 = 0; return; }
+  e0 = ch * csz;
+  e1 = (ch + 1) * csz < E ? (ch + 1) * csz : E;
+}
+
 // Adapter giving a whole-stage producer the stage_part interface (work done at part 0).
 template <class P>
 struct WholeStage {

@@ -133,7 +133,8 @@ struct GenAProducer {
     constexpr int KL = Cfg::NT / Cfg::BM;  // kk lanes
     constexpr int E = Cfg::BK / KL;
     const int k0 = ks * Cfg::BK;
-    const int e0 = (part * E) / nparts, e1 = ((part + 1) * E) / nparts;
+    int e0, e1;
+    chunk_range<E, 2>(part, nparts, e0, e1);
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       if (e < e0 || e >= e1) continue;
@@ -536,7 +537,8 @@ __global__ void __launch_bounds__(Cfg::NT, 1) k_sketch_tagged3(ublr_op_t op, con
     __device__ __forceinline__ void stage_part(double* As, int, int part, int nparts) {
       constexpr int KL = Cfg::NT / Cfg::BM;
       constexpr int E = BK / KL;
-      const int e0 = (part * E) / nparts, e1 = ((part + 1) * E) / nparts;
+      int e0, e1;
+      chunk_range<E, 2>(part, nparts, e0, e1);
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         if (e < e0 || e >= e1) continue;
