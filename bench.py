@@ -336,10 +336,9 @@ def main():
             h2d = wl.points.coords.nbytes
         rep, report = P.compress(op, wl.tess, wl.k, wl.method, p=wl.p, stream=P.RandomStream(W.COMPRESS_SEED),
                                  compute_error=False)
-        U, V, C, B = (rep.U.cpu(), rep.V.cpu(), rep.core_d.cpu(), rep.B_d.cpu())  # D2H of the result
-        torch.cuda.synchronize()
+        host = rep.to_host()                                      # D2H of the result (pinned)
         e2e_times.append(time.perf_counter() - t0)
-        d2h = sum(x.numel() * 8 for x in (U, V, C, B))
+        d2h = sum(x.nbytes for x in host.values())
     e2e = float(np.median(e2e_times))
     if world > 1:
         t = torch.tensor([e2e], device=dev)

@@ -146,11 +146,17 @@ struct CouplingAProducer {
   int cj0, mj;
   RowPoint rp;
   int grow, gk0;
-  __device__ CouplingAProducer(const ublr_op_t& op_, const LogTables* lt_, int ri0, int mi, int cj0_, int mj_)
+  ColRing<Cfg::BK> ring;
+  __device__ CouplingAProducer(const ublr_op_t& op_, const LogTables* lt_, int ri0, int mi, int cj0_, int mj_,
+                               double* ringbuf)
       : op(op_), lt(lt_), cj0(cj0_), mj(mj_) {
     grow = threadIdx.x % Cfg::BM;
     gk0 = threadIdx.x / Cfg::BM;
     rp = load_row_point(op, ri0 + grow, grow < mi);
+    ring.buf = ringbuf;
+  }
+  __device__ __forceinline__ void prefetch(int ks) {
+    if (KIND != UBLR_OP_DENSE) ring.prefetch(op, ks, cj0 + ks * Cfg::BK, cj0 + mj, Cfg::NT);
   }
   __device__ __forceinline__ void stage(double* As, int ks) { stage_part(As, ks, 0, 1); }
   __device__ __forceinline__ void stage_part(double* As, int ks, int part, int nparts) {
@@ -164,7 +170,10 @@ struct CouplingAProducer {
       int kk = gk0 + e * KL;
       int q = ks * Cfg::BK + kk;
       double v = 0.0;
-      if (rp.p >= 0 && q < mj) v = op_entry<KIND>(op, rp, cj0 + q, lt);
+      if (rp.p >= 0 && q < mj) {
+        if (KIND == UBLR_OP_DENSE) v = op_entry<KIND>(op, rp, cj0 + q, lt);
+        else v = kernel_entry<KIND>(op, rp, cj0 + q, ring.at(ks, 0, kk), ring.at(ks, 1, kk), ring.at(ks, 2, kk), lt);
+      }
       As[Cfg::ai(grow, kk)] = v;
     }
   }
@@ -191,13 +200,14 @@ __global__ void __launch_bounds__(Cfg::NT) k_coupling2(ublr_op_t op, const int32
   constexpr int NJ2 = BN / 8;
   constexpr int SW = BN + 4;
   __shared__ LogTables lt;
+  __shared__ double ringbuf[9 * Cfg::BK];
   extern __shared__ double dsm[];
   if (KIND == UBLR_OP_LOG) init_log_tables(&lt);
   const int j = blockIdx.x, i = i0 + blockIdx.y;
   const int ri0 = off[i], mi = off[i + 1] - ri0;
   const int cj0 = off[j], mj = off[j + 1] - cj0;
   const int ki = roff[i + 1] - roff[i], kj = roff[j + 1] - roff[j];
-  CouplingAProducer<KIND, Cfg> ap(op, &lt, ri0, mi, cj0, mj);
+  CouplingAProducer<KIND, Cfg> ap(op, &lt, ri0, mi, cj0, mj, ringbuf);
   CouplingBProducer<Cfg> bp{V, lduv, cj0, mj, kj, vec2 != 0};
   double acc[Cfg::MI][Cfg::NJ][2];
 #pragma unroll

@@ -52,6 +52,13 @@ __device__ __forceinline__ void dmma_mainloop(AP& ap, BP& bp, int nk, double* sm
   const int am0 = wr * Cfg::WM + g;
   const int bn0 = wc * Cfg::WN + g;
 
+  // producers may stage per-k-step side data (column coordinates) one step ahead
+#pragma unroll
+  for (int s = 0; s < STAGES; ++s)
+    if (s < nk) ap.prefetch(s);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < nk) {
@@ -66,6 +73,7 @@ __device__ __forceinline__ void dmma_mainloop(AP& ap, BP& bp, int nk, double* sm
     const int nx = ks + STAGES - 1;
     double* As_nx = As0 + (nx % STAGES) * Cfg::A_STAGE;
     if (nx < nk) bp.stage(Bs0 + (nx % STAGES) * Cfg::B_STAGE, nx);
+    if (nx + 1 < nk) ap.prefetch(nx + 1);
     const double* As = As0 + (ks % STAGES) * Cfg::A_STAGE;
     const double* Bs = Bs0 + (ks % STAGES) * Cfg::B_STAGE;
     double a[2][Cfg::MI], b[2][Cfg::NJ];
@@ -119,6 +127,7 @@ struct WholeStage {
   __device__ __forceinline__ void stage_part(double* s, int ks, int part, int) {
     if (part == 0) p.stage(s, ks);
   }
+  __device__ __forceinline__ void prefetch(int) {}
 };
 
 // Copy a (rows x cols) tile of a row-major global matrix, contiguous along

@@ -57,6 +57,45 @@ __device__ __forceinline__ double op_entry(const ublr_op_t& op, const RowPoint& 
   }
 }
 
+// Entry from explicit column coordinates (kernel operators): the column
+// point's coordinates come from a shared-memory ring filled ahead of time
+// (ColRing), so tile generation does not wait on global loads.
+template <int KIND>
+__device__ __forceinline__ double kernel_entry(const ublr_op_t& op, const RowPoint& row, int q, double c0, double c1,
+                                               double c2, const LogTables* lt) {
+  if (q == row.p) return op.diag;
+  double d = row.x0 - c0;
+  double r2 = d * d;
+  if (op.dim > 1) {
+    d = row.x1 - c1;
+    r2 = fma(d, d, r2);
+  }
+  if (op.dim > 2) {
+    d = row.x2 - c2;
+    r2 = fma(d, d, r2);
+  }
+  if (KIND == UBLR_OP_LOG) return -0.5 * fast_log(r2, lt);
+  return rsqrt(r2);
+}
+
+// Three-slot shared-memory ring of column coordinates (3 dims x BK per slot)
+// for the k-steps of an operator-tile producer; slot = stage % 3.
+template <int BK>
+struct ColRing {
+  double* buf;  // 9 * BK doubles
+  __device__ __forceinline__ void prefetch(const ublr_op_t& op, int stage, int q0, int qend, int nthreads) {
+    const int slot = stage % 3;
+    for (int e = threadIdx.x; e < op.dim * BK; e += nthreads) {
+      int a = e / BK, kk = e - a * BK;
+      int q = q0 + kk;
+      bool ok = q < qend;
+      cp_async8(&buf[(slot * 3 + a) * BK + kk], ok ? (const void*)(op.coords + (int64_t)a * op.n + q) : (const void*)op.coords,
+                ok);
+    }
+  }
+  __device__ __forceinline__ double at(int stage, int a, int kk) const { return buf[((stage % 3) * 3 + a) * BK + kk]; }
+};
+
 // Runtime -> compile-time dispatch on the operator kind.
 #define UBLR_DISPATCH_KIND(kind, KIND_NAME, ...)                       \
   switch (kind) {                                                      \

@@ -121,11 +121,16 @@ struct GenAProducer {
   int row0, n;
   RowPoint rp;
   int grow, gk0;
-  __device__ GenAProducer(const ublr_op_t& op_, const LogTables* lt_, int row0_)
+  ColRing<Cfg::BK> ring;
+  __device__ GenAProducer(const ublr_op_t& op_, const LogTables* lt_, int row0_, double* ringbuf)
       : op(op_), lt(lt_), row0(row0_), n((int)op_.n) {
     grow = threadIdx.x % Cfg::BM;
     gk0 = threadIdx.x / Cfg::BM;
     rp = load_row_point(op, row0 + grow, row0 + grow < n);
+    ring.buf = ringbuf;
+  }
+  __device__ __forceinline__ void prefetch(int ks) {
+    if (KIND != UBLR_OP_DENSE) ring.prefetch(op, ks, ks * Cfg::BK, n, Cfg::NT);
   }
   __device__ __forceinline__ void stage(double* As, int ks) { stage_part(As, ks, 0, 1); }
   // entries [part*E/nparts, (part+1)*E/nparts) of this thread's E = BK/KL entries
@@ -141,7 +146,10 @@ struct GenAProducer {
       int kk = gk0 + e * KL;
       int q = k0 + kk;
       double v = 0.0;
-      if (rp.p >= 0 && q < n) v = op_entry<KIND>(op, rp, q, lt);
+      if (rp.p >= 0 && q < n) {
+        if (KIND == UBLR_OP_DENSE) v = op_entry<KIND>(op, rp, q, lt);
+        else v = kernel_entry<KIND>(op, rp, q, ring.at(ks, 0, kk), ring.at(ks, 1, kk), ring.at(ks, 2, kk), lt);
+      }
       As[Cfg::ai(grow, kk)] = v;
     }
   }
@@ -163,12 +171,13 @@ template <int KIND, class Cfg>
 __global__ void __launch_bounds__(Cfg::NT) k_apply2(ublr_op_t op, const double* __restrict__ X, int64_t ldx, int w,
                                                     double* __restrict__ out, int64_t ldo, int vec2) {
   __shared__ LogTables lt;
+  __shared__ double ringbuf[9 * Cfg::BK];
   extern __shared__ double dsm[];
   if (KIND == UBLR_OP_LOG) init_log_tables(&lt);
   const int n = (int)op.n;
   const int row0 = blockIdx.y * Cfg::BM;
   const int col0 = blockIdx.x * Cfg::BN;
-  GenAProducer<KIND, Cfg> ap(op, &lt, row0);
+  GenAProducer<KIND, Cfg> ap(op, &lt, row0, ringbuf);
   RowMajorBProducer<Cfg> bp{X, ldx, n, w, col0, vec2 != 0};
   double acc[Cfg::MI][Cfg::NJ][2];
 #pragma unroll
@@ -332,163 +341,6 @@ __global__ void __launch_bounds__(TS_THREADS) k_sketch_tagged(ublr_op_t op, cons
   }
 }
 
-// ------------------------------------------------------- tagged sketch v2
-// CTA = 64 consecutive permuted rows x BN test-block columns, 16 warps
-// (4 x 4; warp tile 16 x BN/4). k-steps run block by block (step table from
-// the host: block j, first column, end column); at the last step of block j
-// each thread folds its W = A_{rows, J_j} X_j fragment into the ell tag
-// groups held in registers: acc[c] += T[j, c] * W. Row tiles of 64 keep the
-// test-block panel reuse at 64 rows per load (L2 traffic ~2 TB/s at peak).
-template <int KIND, int L, class Cfg>
-__global__ void __launch_bounds__(Cfg::NT) k_sketch_tagged2(ublr_op_t op, const int4* __restrict__ steps, int nsteps,
-                                                            const double* __restrict__ T, int ell,
-                                                            const double* __restrict__ G,
-                                                            const double* __restrict__ H, int64_t ldx, int gc,
-                                                            double* __restrict__ Y, double* __restrict__ Z,
-                                                            int64_t ldy, int vec2) {
-  constexpr int BK = Cfg::BK, STAGES = Cfg::STAGES;
-  __shared__ LogTables lt;
-  extern __shared__ double dsm[];
-  if (KIND == UBLR_OP_LOG) init_log_tables(&lt);
-  const int n = (int)op.n;
-  const int ncols = (H ? 2 : 1) * gc;
-  const int row0 = blockIdx.y * Cfg::BM;
-  const int col0 = blockIdx.x * Cfg::BN;
-  GenAProducer<KIND, Cfg> ap(op, &lt, row0);
-  // A producer works on absolute column indices q0 .. q0+BK masked by qend
-  struct AStep {
-    GenAProducer<KIND, Cfg>* g;
-    const int4* steps;
-    __device__ __forceinline__ void stage(double* As, int ks) {
-      int4 s = steps[ks];
-      constexpr int KL = Cfg::NT / Cfg::BM;
-#pragma unroll
-      for (int e = 0; e < BK / KL; ++e) {
-        int kk = g->gk0 + e * KL;
-        int q = s.y + kk;
-        double v = 0.0;
-        if (g->rp.p >= 0 && q < s.z) v = op_entry<KIND>(g->op, g->rp, q, g->lt);
-        As[Cfg::ai(g->grow, kk)] = v;
-      }
-    }
-  } as{&ap, steps};
-  struct BStep {
-    const double* G; const double* H; int64_t ldx; int gc, ncols, col0; bool vec2; const int4* steps;
-    __device__ __forceinline__ void stage(double* Bs, int ks) {
-      int4 s = steps[ks];
-      // columns [col0, col0+BN) of [G | H]; the G/H split is at gc
-      if (col0 + Cfg::BN <= gc || !H) {
-        tile_copy<Cfg::NT>(Bs, Cfg::SB, G, ldx, BK, Cfg::BN, s.y, col0, s.z, gc, IdentityRows{}, vec2 && !(gc & 1));
-      } else if (col0 >= gc) {
-        tile_copy<Cfg::NT>(Bs, Cfg::SB, H, ldx, BK, Cfg::BN, s.y, col0 - gc, s.z, gc, IdentityRows{}, vec2 && !(gc & 1));
-      } else {
-        for (int e = threadIdx.x; e < BK * Cfg::BN; e += Cfg::NT) {
-          int kk = e / Cfg::BN, c = e - kk * Cfg::BN;
-          int q = s.y + kk, col = col0 + c;
-          bool ok = q < s.z && col < ncols;
-          const double* src = G;
-          if (ok) src = (col < gc) ? (G + (int64_t)q * ldx + col) : (H + (int64_t)q * ldx + (col - gc));
-          cp_async8(&Bs[kk * Cfg::SB + c], src, ok);
-        }
-      }
-    }
-  } bs{G, H, ldx, gc, ncols, col0, vec2 != 0, steps};
-
-  double acc[L][Cfg::MI][Cfg::NJ][2];
-  double w[Cfg::MI][Cfg::NJ][2];
-#pragma unroll
-  for (int c = 0; c < L; ++c)
-#pragma unroll
-    for (int i = 0; i < Cfg::MI; ++i)
-#pragma unroll
-      for (int j = 0; j < Cfg::NJ; ++j) acc[c][i][j][0] = acc[c][i][j][1] = 0.0;
-#pragma unroll
-  for (int i = 0; i < Cfg::MI; ++i)
-#pragma unroll
-    for (int j = 0; j < Cfg::NJ; ++j) w[i][j][0] = w[i][j][1] = 0.0;
-  __syncthreads();
-
-  double* As0 = dsm;
-  double* Bs0 = dsm + STAGES * Cfg::A_STAGE;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane >> 2, t = lane & 3;
-  const int wr = warp / Cfg::WNW, wc = warp % Cfg::WNW;
-  const int am0 = wr * Cfg::WM + g;
-  const int bn0 = wc * Cfg::WN + g;
-#pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nsteps) {
-      as.stage(As0 + s * Cfg::A_STAGE, s);
-      bs.stage(Bs0 + s * Cfg::B_STAGE, s);
-    }
-    cp_async_commit();
-  }
-  for (int ks = 0; ks < nsteps; ++ks) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    {
-      int nx = ks + STAGES - 1;
-      if (nx < nsteps) {
-        as.stage(As0 + (nx % STAGES) * Cfg::A_STAGE, nx);
-        bs.stage(Bs0 + (nx % STAGES) * Cfg::B_STAGE, nx);
-      }
-      cp_async_commit();
-    }
-    const double* As = As0 + (ks % STAGES) * Cfg::A_STAGE;
-    const double* Bs = Bs0 + (ks % STAGES) * Cfg::B_STAGE;
-#pragma unroll
-    for (int k4 = 0; k4 < BK / 4; ++k4) {
-      const int kr = k4 * 4 + t;
-      double a[Cfg::MI], b[Cfg::NJ];
-#pragma unroll
-      for (int i = 0; i < Cfg::MI; ++i) a[i] = As[Cfg::ai(am0 + i * 8, kr)];
-#pragma unroll
-      for (int j = 0; j < Cfg::NJ; ++j) b[j] = Bs[Cfg::bi(kr, bn0 + j * 8)];
-#pragma unroll
-      for (int i = 0; i < Cfg::MI; ++i)
-#pragma unroll
-        for (int j = 0; j < Cfg::NJ; ++j) mma8x8x4(w[i][j][0], w[i][j][1], a[i], b[j]);
-    }
-    int4 st = steps[ks];
-    if (st.w) {  // last step of block st.x: fold W into the tag groups
-      const double* Tj = T + (int64_t)st.x * ell;
-#pragma unroll
-      for (int c = 0; c < L; ++c) {
-        double tc = (c < ell) ? __ldg(&Tj[c]) : 0.0;
-#pragma unroll
-        for (int i = 0; i < Cfg::MI; ++i)
-#pragma unroll
-          for (int j = 0; j < Cfg::NJ; ++j) {
-            acc[c][i][j][0] = fma(tc, w[i][j][0], acc[c][i][j][0]);
-            acc[c][i][j][1] = fma(tc, w[i][j][1], acc[c][i][j][1]);
-          }
-      }
-#pragma unroll
-      for (int i = 0; i < Cfg::MI; ++i)
-#pragma unroll
-        for (int j = 0; j < Cfg::NJ; ++j) w[i][j][0] = w[i][j][1] = 0.0;
-    }
-  }
-  cp_async_wait<0>();
-#pragma unroll
-  for (int i = 0; i < Cfg::MI; ++i) {
-    int row = row0 + wr * Cfg::WM + i * 8 + g;
-    if (row >= n) continue;
-#pragma unroll
-    for (int j = 0; j < Cfg::NJ; ++j)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        int col = col0 + wc * Cfg::WN + j * 8 + 2 * t + h;
-        if (col >= ncols) continue;
-        double* dst = (col < gc) ? Y : Z;
-        int q = (col < gc) ? col : col - gc;
-#pragma unroll
-        for (int c = 0; c < L; ++c)
-          if (c < ell) dst[(int64_t)row * ldy + c * gc + q] = acc[c][i][j][h];
-      }
-  }
-}
-
 // ------------------------------------------------------- tagged sketch v3
 // CTA = BM (32) permuted rows x BN (128 or 64) test-block columns, 8 warps
 // (2 x 4; warp tile 16 x BN/4). The ell tag-group accumulators of the CTA
@@ -531,9 +383,12 @@ __global__ void __launch_bounds__(Cfg::NT, 1) k_sketch_tagged3(ublr_op_t op, con
   const int row0 = row_begin + blockIdx.y * Cfg::BM;
   const int col0 = blockIdx.x * Cfg::BN;
   // A producer (absolute columns q0.. masked by qend), interleavable
+  __shared__ double ringbuf[9 * BK];
   struct AP {
     const ublr_op_t& op; const LogTables* lt; RowPoint rp; int grow, gk0;
     int q0n, qendn;   // columns of the stage being produced
+    int sidx;         // its stage index (ring slot)
+    ColRing<BK> ring;
     __device__ __forceinline__ void stage_part(double* As, int, int part, int nparts) {
       constexpr int KL = Cfg::NT / Cfg::BM;
       constexpr int E = BK / KL;
@@ -545,12 +400,15 @@ __global__ void __launch_bounds__(Cfg::NT, 1) k_sketch_tagged3(ublr_op_t op, con
         int kk = gk0 + e * KL;
         int q = q0n + kk;
         double v = 0.0;
-        if (rp.p >= 0 && q < qendn) v = op_entry<KIND>(op, rp, q, lt);
+        if (rp.p >= 0 && q < qendn) {
+          if (KIND == UBLR_OP_DENSE) v = op_entry<KIND>(op, rp, q, lt);
+          else v = kernel_entry<KIND>(op, rp, q, ring.at(sidx, 0, kk), ring.at(sidx, 1, kk), ring.at(sidx, 2, kk), lt);
+        }
         As[Cfg::ai(grow, kk)] = v;
       }
     }
   } ap{op, &lt, load_row_point(op, row0 + (int)(threadIdx.x % Cfg::BM), row0 + (int)(threadIdx.x % Cfg::BM) < row_end),
-       (int)(threadIdx.x % Cfg::BM), (int)(threadIdx.x / Cfg::BM), 0, 0};
+       (int)(threadIdx.x % Cfg::BM), (int)(threadIdx.x / Cfg::BM), 0, 0, 0, ColRing<BK>{ringbuf}};
   auto b_stage = [&](double* Bs, int q0, int qend) {
     if (col0 + Cfg::BN <= gc || !H) {
       tile_copy<Cfg::NT>(Bs, Cfg::SB, G, ldx, BK, Cfg::BN, q0, col0, qend, gc, IdentityRows{}, vec2 != 0);
@@ -595,26 +453,41 @@ __global__ void __launch_bounds__(Cfg::NT, 1) k_sketch_tagged3(ublr_op_t op, con
   const int wr = warp / Cfg::WNW, wc = warp % Cfg::WNW;
   const int am0 = wr * Cfg::WM + g;
   const int bn0 = wc * Cfg::WN + g;
-  // stage 0
+  // stage coordinates: (block, first column, end column); advance() walks k-steps block by block
+  auto advance = [&](int& jj, int& qq0, int& qqe) {
+    qq0 += BK;
+    if (qq0 >= qqe) {
+      ++jj;
+      if (jj < b) { qq0 = off[jj]; qqe = off[jj + 1]; }
+    }
+  };
   int j = 0, q0 = off[0], qend = off[1];
-  ap.q0n = q0; ap.qendn = qend;
+  int j1 = j, q01 = q0, qe1 = qend;
+  advance(j1, q01, qe1);
+  if (KIND != UBLR_OP_DENSE) {
+    ap.ring.prefetch(op, 0, q0, qend, Cfg::NT);
+    if (j1 < b) ap.ring.prefetch(op, 1, q01, qe1, Cfg::NT);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  ap.q0n = q0; ap.qendn = qend; ap.sidx = 0;
   ap.stage_part(As0, 0, 0, 1);
   b_stage(Bs0, q0, qend);
   cp_async_commit();
-  int slot = 0;
+  int slot = 0, sidx = 0;
   for (;;) {
-    // coordinates of the next stage
-    int nq0 = q0 + BK, nj = j, nqend = qend;
-    if (nq0 >= qend) {
-      nj = j + 1;
-      if (nj < b) { nq0 = off[nj]; nqend = off[nj + 1]; }
-    }
+    // next stage (j1, q01, qe1) and the one after (j2, q02, qe2)
+    int nj = j1, nq0 = q01, nqend = qe1;
+    int j2 = nj, q02 = nq0, qe2 = nqend;
+    if (nj < b) advance(j2, q02, qe2);
     const bool more = nj < b;
     cp_async_wait<0>();
     __syncthreads();
     double* As_nx = As0 + (slot ^ 1) * Cfg::A_STAGE;
     if (more) b_stage(Bs0 + (slot ^ 1) * Cfg::B_STAGE, nq0, nqend);
-    ap.q0n = nq0; ap.qendn = nqend;
+    if (KIND != UBLR_OP_DENSE && more && j2 < b) ap.ring.prefetch(op, sidx + 2, q02, qe2, Cfg::NT);
+    ap.q0n = nq0; ap.qendn = nqend; ap.sidx = sidx + 1;
     const double* As = As0 + slot * Cfg::A_STAGE;
     const double* Bs = Bs0 + slot * Cfg::B_STAGE;
 #pragma unroll
@@ -674,7 +547,9 @@ __global__ void __launch_bounds__(Cfg::NT, 1) k_sketch_tagged3(ublr_op_t op, con
     }
     if (!more) break;
     j = nj; q0 = nq0; qend = nqend;
+    j1 = j2; q01 = q02; qe1 = qe2;
     slot ^= 1;
+    ++sidx;
   }
   cp_async_wait<0>();
   // epilogue
@@ -787,10 +662,6 @@ int sketch_common_v1(const ublr_op_t* op, const int32_t* off, int b, const doubl
   return UBLR_OK;
 }
 
-int sketch_common_v2(const ublr_op_t* op, const int32_t* off, int b, const double* T,
-                     int ell, const double* G, const double* H, int64_t ld_x, int gc, double* Y, double* Z,
-                     int64_t ld_y, cudaStream_t st);
-
 int sketch_common_v3(const ublr_op_t* op, const int32_t* off, int b, const double* T, int ell, const double* G,
                      const double* H, int64_t ld_x, int gc, double* Y, double* Z, int64_t ld_y, int row_begin,
                      int row_end, cudaStream_t st) {
@@ -826,65 +697,10 @@ int sketch_common(const ublr_op_t* op, const int32_t* off, int b, const double* 
   UBLR_REQUIRE(row_begin >= 0 && row_begin < row_end && row_end <= op->n, UBLR_ERR_VALUE, "sketch: bad row range");
   static const char* ver = getenv("UBLR_SKETCH_VERSION");
   const int v = ver ? atoi(ver) : 3;
-  if (v == 2 && row_begin == 0 && row_end == op->n) return sketch_common_v2(op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y, st);
   if (v == 3 && ell <= 10) return sketch_common_v3(op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y, row_begin, row_end, st);
   return sketch_common_v1(op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y, row_begin, row_end, st);
 }
 
-int sketch_common_v2(const ublr_op_t* op, const int32_t* off, int b, const double* T,
-                     int ell, const double* G, const double* H, int64_t ld_x, int gc, double* Y, double* Z,
-                     int64_t ld_y, cudaStream_t st) {
-  const int ncols = (H ? 2 : 1) * gc;
-  // step table (block, first column, end column, last-step flag) from the host copy of off
-  std::string hoff((size_t)4 * (b + 1), '\0');
-  UBLR_CUDA(cudaMemcpyAsync(&hoff[0], off, 4 * (b + 1), cudaMemcpyDeviceToHost, st));
-  UBLR_CUDA(cudaStreamSynchronize(st));
-  const int32_t* ho = (const int32_t*)hoff.data();
-  std::string hsteps;
-  int nsteps = 0;
-  for (int j = 0; j < b; ++j)
-    for (int q = ho[j]; q < ho[j + 1]; q += 32) {
-      int4 s4 = make_int4(j, q, ho[j + 1], q + 32 >= ho[j + 1] ? 1 : 0);
-      hsteps.append((const char*)&s4, sizeof(int4));
-      ++nsteps;
-    }
-  int4* dsteps = nullptr;
-  UBLR_CUDA(cudaMallocAsync((void**)&dsteps, sizeof(int4) * (size_t)nsteps, st));
-  UBLR_CUDA(cudaMemcpyAsync(dsteps, hsteps.data(), sizeof(int4) * (size_t)nsteps, cudaMemcpyHostToDevice, st));
-  int vec2 = ((ld_x % 2) == 0 && ((uintptr_t)G) % 16 == 0 && (!H || ((uintptr_t)H) % 16 == 0)) ? 1 : 0;
-  dim3 grid;
-  grid.y = (unsigned)((op->n + 63) / 64);
-  int rc = UBLR_OK;
-#define UBLR_TS2(L, BMv, BNv, WMWv, WNWv)                                                                     \
-  {                                                                                                          \
-    using Cfg = TileCfg<BMv, BNv, 32, WMWv, WNWv, 2>;                                                        \
-    grid.x = (unsigned)((ncols + (BNv) - 1) / (BNv));                                                        \
-    grid.y = (unsigned)((op->n + (BMv) - 1) / (BMv));                                                        \
-    UBLR_DISPATCH_KIND(op->kind, KIND, {                                                                     \
-      size_t sm = Cfg::smem_bytes();                                                                         \
-      UBLR_CUDA(cudaFuncSetAttribute(k_sketch_tagged2<KIND, L, Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                     (int)sm));                                                             \
-      k_sketch_tagged2<KIND, L, Cfg><<<grid, Cfg::NT, sm, st>>>(*op, dsteps, nsteps, T, ell, G, H, ld_x, gc, Y, Z, \
-                                                                ld_y, vec2);                                 \
-    })                                                                                                       \
-  }
-  if (ell <= 4) UBLR_TS2(4, 64, 64, 4, 4)
-  else if (ell <= 10) UBLR_TS2(10, 64, 32, 4, 4)
-  else if (ell <= 28) UBLR_TS2(28, 32, 32, 4, 4)
-  else {
-    set_error("tagged sketch supports ell <= 28 (d <= 3 without extra columns)");
-    rc = UBLR_ERR_VALUE;
-  }
-#undef UBLR_TS2
-  cudaError_t e = cudaGetLastError();
-  UBLR_CUDA(cudaFreeAsync(dsteps, st));
-  if (rc) return rc;
-  if (e != cudaSuccess) {
-    set_error(std::string("CUDA error: ") + cudaGetErrorString(e));
-    return UBLR_ERR_CUDA;
-  }
-  return UBLR_OK;
-}
 }  // namespace
 
 extern "C" int ublr_sketch_tagged(const ublr_op_t* op, const int32_t* off, int b, const double* T, int ell,

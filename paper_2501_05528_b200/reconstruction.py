@@ -98,6 +98,19 @@ class UniformBLR:
             self._host["B"] = out
         return self._host["B"]
 
+    def to_host(self) -> dict:
+        """Copy U, V, core and the near blocks to pinned host memory in one
+        asynchronous pass (one stream sync); returns numpy arrays in the
+        device layout (permuted rows)."""
+        torch = _torch()
+        out = {}
+        for name, t in (("U", self.U), ("V", self.V), ("core", self.core_d), ("B", self.B_d)):
+            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            h.copy_(t, non_blocking=True)
+            out[name] = h
+        torch.cuda.current_stream().synchronize()
+        return {k: v.numpy() for k, v in out.items()}
+
     @property
     def storage_entries(self) -> int:
         return int(2 * sum(self.dt.sizes * self.effective_ranks) + self.total_rank ** 2 + self.dt.b_off_h[-1])
