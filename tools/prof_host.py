@@ -1,0 +1,19 @@
+"""cProfile of one c2 compression (host-side overhead hunt)."""
+import cProfile, io, os, pstats, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2501_05528_b200 as P
+from paper_2501_05528_b200 import workloads as W
+wl = W.build(sys.argv[1] if len(sys.argv) > 1 else "c2")
+for _ in range(3):
+    P.compress(wl.op, wl.tess, wl.k, wl.method, p=wl.p, stream=P.RandomStream(7), compute_error=False)
+torch.cuda.synchronize()
+pr = cProfile.Profile()
+pr.enable()
+for _ in range(20):
+    P.compress(wl.op, wl.tess, wl.k, wl.method, p=wl.p, stream=P.RandomStream(7), compute_error=False)
+torch.cuda.synchronize()
+pr.disable()
+s = io.StringIO()
+pstats.Stats(pr, stream=s).sort_stats("cumulative").print_stats(35)
+print(s.getvalue()[:6000])
