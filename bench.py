@@ -154,6 +154,36 @@ def cpu_baseline(wl, budget_s=12.0):
                       f"(dense operator prebuilt, OpenBLAS on all cores)"}
 
 
+KERNEL_OF = {"ublr_sketch_tagged_pair": "k_sketch_tagged3 (Kronecker-restructured tagged sketch, TMEM tag groups)",
+             "ublr_sketch_tagged": "k_sketch_tagged3 (Kronecker-restructured tagged sketch, TMEM tag groups)",
+             "ublr_apply": "k_apply2 (operator apply, A generated on the fly)",
+             "ublr_gemm_batched": "k_gemm2 (batched DMMA GEMM)",
+             "ublr_coupling": "k_coupling2 (C_ij = U_i^T A_ij V_j)"}
+
+
+def roofline_of(ev, work, config):
+    """Dominant C-ABI kernel by device time among those with an algorithmic
+    flop count; achieved = flops / CUDA-event time of that kernel."""
+    cands = [(float(np.sum(ev[k])), k) for k in ev if work.get(k, 0.0) > 0]
+    if not cands:
+        return None
+    t_ms, name = max(cands)
+    achieved = work[name] / (t_ms * 1e-3) / 1e12
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", f"traffic_{config}.json")
+    if os.path.exists(tfile):
+        tj = json.load(open(tfile))
+        if tj.get("entry") == name:
+            traffic = tj.get("dram_bytes_per_launch")
+    n_launch = len(ev[name])
+    return {"kernel": KERNEL_OF.get(name, name), "entry": name, "bound": "fp64", "achieved": achieved,
+            "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+            "peak_source": "measured DMMA m8n8k4 burst (profiles/fp64_peak_r01.txt); MEASURED_PEAKS.json has no "
+                           "fp64 entry",
+            "algorithmic_flops_per_launch": work[name] / n_launch, "avg_launch_ms": t_ms / n_launch,
+            "launches_timed": n_launch}
+
+
 def run_sharded(args, rank, world, local):
     """Config 5: block-row sharded A2. With one GPU, one rank's
     share of an --shards-way job is timed (the other shards' V rows are
@@ -224,13 +254,9 @@ def run_sharded(args, rank, world, local):
         tt = torch.tensor([t], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t = float(tt.item())
-    sk = ev.get("ublr_sketch_tagged_pair", [float("nan")])
-    sk_ms = float(np.mean(sk))
+    roof = roofline_of(ev, _lib.work, args.config)
     sh = shards[me]
-    gc = wl.k + wl.p
     rows = sh.r1 - sh.r0
-    sk_flops = 2.0 * rows * wl.n * 2 * gc + 2.0 * rows * wl.b * 2 * gc * wl.ell
-    achieved = sk_flops / (sk_ms * 1e-3) / 1e12
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": t, "unit": "s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -241,9 +267,7 @@ def run_sharded(args, rank, world, local):
                        if emulate else "all ranks, NCCL all-gather of V",
                        "shard_rank": me, "rows_per_shard": rows},
             "gpu_launches": int(launches),
-            "roofline": {"kernel": "k_sketch_tagged (own rows)", "bound": "fp64", "achieved": achieved,
-                         "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
-                         "traffic": None, "algorithmic_flops_per_launch": sk_flops, "avg_launch_ms": sk_ms},
+            "roofline": roof,
             "kernel_ms_per_step": {k_: float(np.sum(v)) / args.steps for k_, v in ev.items()},
             "clocks": clocks.summary(), "cpu_baseline": None,
         }))
@@ -349,15 +373,7 @@ def main():
         e2e = float(t.item())
 
     # --- roofline of the dominant kernel -------------------------------------
-    sk_name = "ublr_sketch_tagged_pair" if "ublr_sketch_tagged_pair" in ev else "ublr_sketch_tagged"
-    sk_ms = float(np.mean(ev.get(sk_name, [float("nan")])))
-    per_step_calls = max(1, len(ev.get(sk_name, [])) // args.steps)
-    sk_flops = flops.get("sketch", float("nan")) / per_step_calls
-    achieved = sk_flops / (sk_ms * 1e-3) / 1e12
-    traffic = None
-    tfile = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
-    if os.path.exists(tfile):
-        traffic = json.load(open(tfile)).get("dram_bytes_per_launch")
+    roof = roofline_of(ev, _lib.work, args.config)
     kernel_ms = {k: float(np.sum(v)) / args.steps for k, v in ev.items()}
 
     if rank == 0:
@@ -370,12 +386,7 @@ def main():
                        "l2": "flushed between timed steps (256 MB write)"},
             "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(launches),
-            "roofline": {"kernel": "k_sketch_tagged (Kronecker-restructured tagged sketch)", "bound": "fp64",
-                         "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                         "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
-                         "peak_source": "measured DMMA m8n8k4 (profiles/fp64_peak_r01.txt); MEASURED_PEAKS.json "
-                                        "has no fp64 entry",
-                         "algorithmic_flops_per_launch": sk_flops, "avg_launch_ms": sk_ms},
+            "roofline": roof,
             "kernel_ms_per_step": kernel_ms,
             "phase_s": report.times_s,
             "clocks": clocks.summary(),

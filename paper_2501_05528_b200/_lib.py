@@ -109,10 +109,21 @@ launch_count = 0
 _events = None  # name -> list of (start, end) CUDA events when instrumentation is on
 
 
+work = {}  # name -> algorithmic flops issued while instrumenting
+
+
+def add_work(name: str, flops: float):
+    """Algorithmic flop count of a launch (bench.py roofline numerator)."""
+    if _events is not None:
+        work[name] = work.get(name, 0.0) + float(flops)
+
+
 def instrument(enable: bool = True):
     """Record CUDA events around every C-ABI launch (bench.py roofline)."""
     global _events
     _events = {} if enable else None
+    if enable:
+        work.clear()
 
 
 def event_times():
@@ -122,11 +133,36 @@ def event_times():
     return {k: [a.elapsed_time(b) for a, b in v] for k, v in (_events or {}).items()}
 
 
+def _work_of(name, args):
+    """Algorithmic fp64 flops of the hot entry points, from their arguments."""
+    try:
+        if name == "ublr_apply":
+            n = args[0].n
+            return 2.0 * n * n * int(args[3])
+        if name in ("ublr_sketch_tagged", "ublr_sketch_tagged_pair"):
+            pair = name.endswith("pair")
+            n, b, ell = args[0].n, int(args[2]), int(args[4])
+            gc = int(args[8] if pair else args[7])
+            r0, r1 = (int(args[12]), int(args[13])) if pair else (int(args[10]), int(args[11]))
+            cols = (2 if pair else 1) * gc
+            return 2.0 * (r1 - r0) * n * cols + 2.0 * (r1 - r0) * b * cols * ell
+        if name == "ublr_gemm_batched":
+            return 2.0 * int(args[2]) * int(args[3]) * int(args[4]) * int(args[22])
+        if name == "ublr_coupling":
+            n, b, k, m = args[0].n, int(args[3]), int(args[4]), int(args[11])
+            rows = (int(args[13]) - int(args[12])) * m
+            return 2.0 * rows * n * k + 2.0 * rows * (b * k) * k
+    except Exception:  # pragma: no cover - accounting only
+        return 0.0
+    return 0.0
+
+
 def call(name: str, *args):
     """Call a status-returning C-ABI function and raise on failure."""
     global launch_count
     launch_count += LAUNCHES.get(name, 0)
     if _events is not None:
+        add_work(name, _work_of(name, args))
         import torch
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()

@@ -138,6 +138,22 @@ def draw_test_blocks(dt, stream: RandomStream, side: int, cols: int):
     return device_normals(specs, out)
 
 
+def draw_test_pair(dt, stream: RandomStream, cols: int):
+    """(G, H) with G_i = gaussian(m_i, cols, stream.child(0, i)) and
+    H_i = ...child(1, i) (ref/bases.py:163-168), drawn in ONE launch set into
+    a (2, N, cols) buffer."""
+    from .linalg import device_normals_keys
+
+    torch = _torch()
+    GH = torch.empty((2, dt.n, cols), dtype=torch.float64, device=dt.device)
+    b = dt.b
+    keys = [stream.key + (side, i) for side in (0, 1) for i in range(b)]
+    rows = np.concatenate([dt.sizes, dt.sizes])
+    offs = np.concatenate([dt.off_h[:-1].astype(np.int64) * cols, dt.n * cols + dt.off_h[:-1].astype(np.int64) * cols])
+    device_normals_keys(stream.seed, keys, rows, cols, offs, cols, None, GH)
+    return GH[0], GH[1]
+
+
 def tagged_sketch(op, dt, T_dev, T_entries, G, H, gc):
     """Y = A Omega, Z = A^* Psi for the tagged test matrices; returns (Y, Z)."""
     torch = _torch()
@@ -195,8 +211,7 @@ def tagging_bases(op, tess: Tessellation, k: int, p: int, plan, stream: RandomSt
     s = ell * gc
     if k > dt.m_max and k > 0:
         pass  # every block takes the identity basis (ref/bases.py:80-82)
-    G = draw_test_blocks(dt, stream, 0, gc)
-    H = draw_test_blocks(dt, stream, 1, gc)
+    G, H = draw_test_pair(dt, stream, gc)
     T_dev = torch.from_numpy(np.ascontiguousarray(T_entries)).to(dt.device)
     Z_dev = torch.from_numpy(np.ascontiguousarray(plan.Z)).to(dt.device)
     _bill(op, s, s)

@@ -25,7 +25,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .bases import _bill, draw_test_blocks
+from .bases import _bill, draw_test_pair
 from .linalg import RandomStream
 from .operators import counting_wrapper, unwrap
 from .tagging import plan_tagging
@@ -129,8 +129,7 @@ def phase1_local(op, tess, k, p, stream, shard, plan=None):
     T = plan.matrix.entries
     ell = T.shape[1]
     s = ell * gc
-    G = draw_test_blocks(dt, stream.child(0), 0, gc)
-    H = draw_test_blocks(dt, stream.child(0), 1, gc)
+    G, H = draw_test_pair(dt, stream.child(0), gc)
     T_dev = torch.from_numpy(np.ascontiguousarray(T)).to(dt.device)
     Z_dev = torch.from_numpy(np.ascontiguousarray(plan.Z)).to(dt.device)
     _bill(op, s, s)

@@ -99,6 +99,34 @@ def device_normals(specs, out):
     return out
 
 
+def device_normals_keys(seed, keys, rows, cols, offsets, ld, rowmap, out):
+    """Vectorised form of device_normals for many streams of one seed:
+    stream s is RandomStream(seed, keys[s]) with rows[s] x cols normals at
+    out.flat[offsets[s] + r * ld + c] (rowmap shared by all streams or None)."""
+    import torch
+
+    from .seedseq import philox_keys
+
+    _lib.require_device()
+    ns = len(keys)
+    rec = np.zeros(ns, dtype=_lib.RNG_STREAM_DTYPE)
+    kk = philox_keys(seed, keys)
+    rec["key0"], rec["key1"] = kk[:, 0], kk[:, 1]
+    counts = np.asarray(rows, dtype=np.int64) * int(cols)
+    rec["count"] = counts
+    rec["cols"] = max(int(cols), 1)
+    rec["ld"] = int(ld)
+    rec["out_offset"] = np.asarray(offsets, dtype=np.int64)
+    rec["rowmap"] = _lib.ptr(rowmap)
+    lib = _lib.load()
+    ws_bytes = int(lib.ublr_rng_workspace_bytes(counts.ctypes.data, ns))
+    ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device=out.device)
+    rec_d = torch.from_numpy(rec.view(np.uint8)).to(out.device, non_blocking=False)
+    _lib.call("ublr_rng_normals", _lib.ptr(rec_d), counts.ctypes.data, ns, _lib.ptr(out), _lib.ptr(ws), ws_bytes,
+              _lib.stream_handle())
+    return out
+
+
 def col_basis(B, k: int) -> np.ndarray:
     """ref/linalg.py:55-69 on the GPU (Householder QR kernel K4)."""
     import torch

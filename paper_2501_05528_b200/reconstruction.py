@@ -301,8 +301,9 @@ def _ratio_summary(values: np.ndarray) -> dict:
     fin = values[np.isfinite(values)]
     if fin.size == 0:
         return {"count": 0}
-    return {"count": int(fin.size), "min": float(fin.min()), "q1": float(np.quantile(fin, 0.25)),
-            "median": float(np.median(fin)), "q3": float(np.quantile(fin, 0.75)), "max": float(fin.max())}
+    q1, med, q3 = np.quantile(fin, (0.25, 0.5, 0.75))
+    return {"count": int(fin.size), "min": float(fin.min()), "q1": float(q1),
+            "median": float(med), "q3": float(q3), "max": float(fin.max())}
 
 
 def _base_config(tess, k, p, stream, **extra) -> dict:
