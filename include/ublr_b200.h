@@ -173,6 +173,9 @@ int ublr_lu_sign_diag(double* W, int64_t ldw, int64_t sW, int j0, int nb, double
 /* out_b[r][c] (or [c][r] with transpose) = src_b[map_b[r] * ld + col0 + c]. */
 int ublr_gather(const double* src, int64_t ld, int64_t s_src, const int32_t* map, int64_t s_map, int rows, int cols,
                 int col0, int transpose, double* out, int64_t ldo, int64_t s_out, int batch, void* stream);
+/* Gram assembly from shared neighbour-pair products: block (a, b) of G_c is
+ * P[pid] or P[-pid-1]^T, pid = map[c][a][b] (nb x nb blocks of m x m). */
+int ublr_assemble_gram(const double* P, const int32_t* map, int nb, int m, double* G, int batch, void* stream);
 /* X_b[r][c] *= d_b[r]. */
 int ublr_scale_rows(double* X, int64_t ldx, int64_t s_x, const double* d, int64_t s_d, int rows, int cols,
                     int batch, void* stream);

@@ -57,6 +57,7 @@ SIGNATURES = {
     "ublr_lu_sign_diag": (INT, [P, I64, I64, INT, INT, P, I64, I64, P, P, P, I64, P, INT, P]),
     "ublr_gather": (INT, [P, I64, I64, P, I64, INT, INT, INT, INT, P, I64, I64, INT, P]),
     "ublr_scale_rows": (INT, [P, I64, I64, P, I64, INT, INT, INT, P]),
+    "ublr_assemble_gram": (INT, [P, P, INT, INT, P, INT, P]),
     "ublr_tag_combine_pairs": (INT, [P, I64, INT, INT, P, P, P, INT, INT, P, P]),
     "ublr_assemble_tagged": (INT, [P, INT, P, I64, INT, P, INT, P, I64, I64, P]),
     "ublr_blr_apply": (INT, [P, P, I64, P, I64, P, P, P, P, P, P, P, INT, P, I64, INT, INT, P, I64, P, P]),

@@ -254,6 +254,23 @@ def nullspace_samples(dt, Om, ld_om, col_om, Ysrc, ld_y, s, r, k, S_out, chunk_b
     sizes = dt.sizes
     nbr_n = np.array([int(sizes[dt.nidx_h[dt.nptr_h[i]:dt.nptr_h[i + 1]]].sum()) for i in range(dt.b)])
     keys = sorted(set(zip(nbr_n.tolist(), sizes.tolist())))
+    shared = None
+    if (sizes == sizes[0]).all():
+        # Omega_j Omega_j'^T once per pair of blocks that share a neighbourhood
+        # (13 per block on a 2-D grid instead of 81 per neighbourhood Gram)
+        m0 = int(sizes[0])
+        pairs = sorted({(min(a, c), max(a, c)) for i in range(dt.b)
+                        for a in dt.nidx_h[dt.nptr_h[i]:dt.nptr_h[i + 1]].tolist()
+                        for c in dt.nidx_h[dt.nptr_h[i]:dt.nptr_h[i + 1]].tolist()})
+        if len(pairs) <= 65535:
+            pid = {pq: t for t, pq in enumerate(pairs)}
+            pa = np.array(pairs, dtype=np.int64)
+            amap_p = torch.from_numpy((dt.off_h[pa[:, 0]][:, None] + np.arange(m0)[None, :]).astype(np.int32)).to(dev)
+            bmap_p = torch.from_numpy((dt.off_h[pa[:, 1]][:, None] + np.arange(m0)[None, :]).astype(np.int32)).to(dev)
+            P_all = torch.empty((len(pairs), m0, m0), dtype=torch.float64, device=dev)
+            D.gemm(0, 1, m0, m0, s, 1.0, om0, ld_om, 0, om0, ld_om, 0, 0.0, D.addr(P_all), m0, m0 * m0, len(pairs),
+                   amap=D.addr(amap_p), sAm=m0, bmap=D.addr(bmap_p), sBm=m0)
+            shared = (P_all, pid)
     for n, m in keys:
         n, m = int(n), int(m)
         if s - r < n:
@@ -279,9 +296,24 @@ def nullspace_samples(dt, Om, ld_om, col_om, Ysrc, ld_y, s, r, k, S_out, chunk_b
             LU = torch.zeros((nb_, n, n), **f64)
             Dg = torch.zeros((nb_, n), **f64)
             nn = n * n
-            # G = B B^T  (B = Omega[nbr], gathered in place)
-            D.gemm(0, 1, n, n, s, 1.0, om0, ld_om, 0, om0, ld_om, 0, 0.0, D.addr(G), n, nn, nb_,
-                   amap=D.addr(amap), sAm=n, bmap=D.addr(amap), sBm=n)
+            # G = B B^T  (B = Omega[nbr]): from the shared neighbour-pair products
+            # when blocks are uniform, else gathered in place
+            if shared is not None:
+                P_all, pid = shared
+                nbl = n // m
+                gm = np.empty((nb_, nbl, nbl), dtype=np.int32)
+                for c, i in enumerate(blk):
+                    L = dt.nidx_h[dt.nptr_h[i]:dt.nptr_h[i + 1]]
+                    for a in range(nbl):
+                        for bq in range(nbl):
+                            ja, jb = int(L[a]), int(L[bq])
+                            gm[c, a, bq] = pid[(ja, jb)] if ja <= jb else -pid[(jb, ja)] - 1
+                gmap = torch.from_numpy(gm).to(dev)
+                _lib.call("ublr_assemble_gram", D.addr(P_all), D.addr(gmap), nbl, m, D.addr(G), nb_,
+                          _lib.stream_handle())
+            else:
+                D.gemm(0, 1, n, n, s, 1.0, om0, ld_om, 0, om0, ld_om, 0, 0.0, D.addr(G), n, nn, nb_,
+                       amap=D.addr(amap), sAm=n, bmap=D.addr(amap), sBm=n)
             fC = D.cholesky_upper(G, R)
             # Qt_top = B[:, :n]^T R^-1
             _lib.call("ublr_gather", om0, ld_om, 0, D.addr(amap), n, n, n, 0, 1, D.addr(Qt), n, nn, nb_,

@@ -334,3 +334,38 @@ extern "C" int ublr_lu_sign_diag(double* W, int64_t ldw, int64_t sW, int j0, int
   UBLR_LAUNCH_CHECK();
   return UBLR_OK;
 }
+
+// ------------------------------------------------------------ Gram assembly
+// G_c (n x n, n = nb * m) for chunk entry c from shared block products:
+// block (a, b) of G_c is P[pid] (m x m) if pid = map[c][a][b] >= 0, or the
+// transpose of P[-pid - 1] otherwise (Omega_j Omega_j'^T is computed once per
+// neighbouring pair and reused by every neighbourhood containing both).
+namespace ublr {
+namespace {
+__global__ void k_assemble_gram(const double* __restrict__ P, const int32_t* __restrict__ map, int nb, int m,
+                                double* __restrict__ G) {
+  const int c = blockIdx.y;
+  const int n = nb * m;
+  const int64_t tot = (int64_t)n * n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    int r = (int)(e / n), q = (int)(e % n);
+    int a = r / m, b = q / m, rr = r - a * m, qq = q - b * m;
+    int pid = map[((int64_t)c * nb + a) * nb + b];
+    double v = (pid >= 0) ? P[(int64_t)pid * m * m + (int64_t)rr * m + qq]
+                          : P[(int64_t)(-pid - 1) * m * m + (int64_t)qq * m + rr];
+    G[(int64_t)c * tot + e] = v;
+  }
+}
+}  // namespace
+}  // namespace ublr
+
+extern "C" int ublr_assemble_gram(const double* P, const int32_t* map, int nb, int m, double* G, int batch,
+                                  void* stream) {
+  UBLR_REQUIRE(P && map && G && nb > 0 && m > 0 && batch > 0 && batch <= 65535, UBLR_ERR_VALUE,
+               "ublr_assemble_gram: bad arguments");
+  int64_t tot = (int64_t)nb * m * nb * m;
+  dim3 grid((unsigned)((tot + 255) / 256 < 2048 ? (tot + 255) / 256 : 2048), batch);
+  k_assemble_gram<<<grid, 256, 0, (cudaStream_t)stream>>>(P, map, nb, m, G);
+  UBLR_LAUNCH_CHECK();
+  return UBLR_OK;
+}

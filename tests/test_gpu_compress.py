@@ -92,3 +92,47 @@ def test_relative_error_estimate_close_to_reference(name):
         assert report.relative_error < 1e-11
     else:
         assert report.relative_error == pytest.approx(ref, rel=1e-4)
+
+
+def _uniform_synthetic(d, b, m, k, seed):
+    """tests/conftest.py:20-31 of the reference: exact-rank synthetic on a grid."""
+    per_axis = round(b ** (1.0 / d))
+    pts_axis = per_axis * round(m ** (1.0 / d))
+    coords = O.cell_centres(pts_axis, d)
+    bx = O.partition(coords, b)
+    U, V, core, near = O.synthetic_factors(bx, k, O.Stream(seed).child(17))
+    A = O.synthetic_dense(bx, U, V, core, near)
+    tess = P.build_tessellation(P.PointCloud(coords, d), b)
+    return bx, tess, A
+
+
+@pytest.mark.parametrize("mid", ["A2", "A3", "B2"])
+def test_three_dimensional_geometry(mid):
+    """27-neighbour neighbourhoods, 28-column tagging (ref tests/test_reconstruction.py:441-447)."""
+    bx, tess, A = _uniform_synthetic(3, 64, 8, 3, 1)
+    assert max(len(n) for n in tess.neighbor_lists) == 27
+    rep, report = P.compress(P.DenseOperator(A), tess, 3, mid, stream=P.RandomStream(2), compute_error=True)
+    assert report.relative_error <= 1e-7
+    orep, _ = O.compress(O.Dense(A), bx, 3, mid, p=10, stream=O.Stream(2), compute_error=False)
+    assert np.linalg.norm(rep.to_dense() - orep.to_dense()) / np.linalg.norm(A) <= 1e-10
+
+
+@pytest.mark.parametrize("mid", ["A1", "A2", "A3", "B1", "B2"])
+def test_rank_at_least_block_size_uses_identity_bases(mid):
+    """k >= m_i: the reference keeps the identity basis (ref/bases.py:78-83)."""
+    bx, tess, A = _uniform_synthetic(1, 8, 16, 4, 3)
+    k = 16
+    rep, _ = P.compress(P.DenseOperator(A), tess, k, mid, p=4, stream=P.RandomStream(4), compute_error=False)
+    orep, _ = O.compress(O.Dense(A), bx, k, mid, p=4, stream=O.Stream(4), compute_error=False)
+    assert np.array_equal(rep.effective_ranks, orep.ranks)
+    assert np.linalg.norm(rep.to_dense() - orep.to_dense()) / np.linalg.norm(A) <= 1e-10
+
+
+@pytest.mark.parametrize("mid", ["A1", "A2", "A3", "B1", "B2"])
+def test_exact_rank_recovery_all_methods(mid):
+    """Acceptance criterion 1 of the reference (tests/test_acceptance.py:44-72)."""
+    for d, b, m, k in ((1, 8, 16, 2), (1, 8, 40, 5), (2, 16, 16, 2), (2, 81, 16, 5)):
+        bx, tess, A = _uniform_synthetic(d, b, m, k, 100 + b)
+        _, report = P.compress(P.DenseOperator(A), tess, k, mid, p=10, stream=P.RandomStream(55),
+                               error_iterations=20)
+        assert report.relative_error <= 1e-7, (d, b, m, k, report.relative_error)
