@@ -186,8 +186,10 @@ def block_bases_from_tagged(dt, Y, Z, Z_dev, ell, gc, k):
     """U_i, V_i = leading Q of the z^(i)-combined samples (K4)."""
     torch = _torch()
     s = ell * gc
-    U = torch.zeros((dt.n, k), dtype=torch.float64, device=dt.device)
-    V = torch.zeros((dt.n, k), dtype=torch.float64, device=dt.device)
+    # every column is written unless some block has fewer than k points
+    alloc = torch.empty if k < int(dt.sizes.min()) else torch.zeros
+    U = alloc((dt.n, k), dtype=torch.float64, device=dt.device)
+    V = alloc((dt.n, k), dtype=torch.float64, device=dt.device)
     stream = _lib.stream_handle()
     kq = max(1, min(k, dt.m_max))
     for src, dst in ((Y, U), (Z, V)):

@@ -175,8 +175,8 @@ __global__ void __launch_bounds__(Cfg::NT) k_apply2(ublr_op_t op, const double* 
   extern __shared__ double dsm[];
   if (KIND == UBLR_OP_LOG) init_log_tables(&lt);
   const int n = (int)op.n;
-  const int row0 = blockIdx.y * Cfg::BM;
-  const int col0 = blockIdx.x * Cfg::BN;
+  const int row0 = blockIdx.x * Cfg::BM;
+  const int col0 = blockIdx.y * Cfg::BN;
   GenAProducer<KIND, Cfg> ap(op, &lt, row0, ringbuf);
   RowMajorBProducer<Cfg> bp{X, ldx, n, w, col0, vec2 != 0};
   double acc[Cfg::MI][Cfg::NJ][2];
@@ -380,8 +380,8 @@ __global__ void __launch_bounds__(Cfg::NT, 1) k_sketch_tagged3(ublr_op_t op, con
   const int colbase = (warp >> 2) * WCOLS;           // warps sharing a lane quarter split its columns
 
   const int ncols = (H ? 2 : 1) * gc;
-  const int row0 = row_begin + blockIdx.y * Cfg::BM;
-  const int col0 = blockIdx.x * Cfg::BN;
+  const int row0 = row_begin + blockIdx.x * Cfg::BM;
+  const int col0 = blockIdx.y * Cfg::BN;
   // A producer (absolute columns q0.. masked by qend), interleavable
   __shared__ double ringbuf[9 * BK];
   struct AP {
@@ -609,7 +609,7 @@ extern "C" int ublr_apply(const ublr_op_t* op, const double* X, int64_t ld_x, in
   if (w == 0) return UBLR_OK;
   cudaStream_t st = (cudaStream_t)stream;
   dim3 grid;
-  grid.y = (unsigned)((op->n + AP_BM - 1) / AP_BM);
+  grid.x = (unsigned)((op->n + 127) / 128);  // row tiles fastest: CTAs in flight share one X column slab in L2
   using CfgW = TileCfg<128, 128, 32, 4, 4, 2>;
   using CfgN = TileCfg<128, 64, 32, 4, 4, 2>;
   int vec2 = ((ld_x % 2) == 0 && (((uintptr_t)X) % 16) == 0) ? 1 : 0;
@@ -620,10 +620,10 @@ extern "C" int ublr_apply(const ublr_op_t* op, const double* X, int64_t ld_x, in
     k_apply2<KIND, CFG><<<grid, CFG::NT, sm, st>>>(*op, X, ld_x, w, out, ld_o, vec2);                         \
   })
   if (w <= 64) {
-    grid.x = (unsigned)((w + 63) / 64);
+    grid.y = (unsigned)((w + 63) / 64);
     UBLR_AP2(CfgN);
   } else {
-    grid.x = (unsigned)((w + 127) / 128);
+    grid.y = (unsigned)((w + 127) / 128);
     UBLR_AP2(CfgW);
   }
 #undef UBLR_AP2
@@ -671,8 +671,8 @@ int sketch_common_v3(const ublr_op_t* op, const int32_t* off, int b, const doubl
 #define UBLR_TS3(L, BNv)                                                                                        \
   {                                                                                                             \
     using Cfg = TileCfg<32, BNv, 32, 2, 8, 2>;                                                                  \
-    grid.x = (unsigned)((ncols + (BNv) - 1) / (BNv));                                                           \
-    grid.y = (unsigned)((row_end - row_begin + 31) / 32);                                                       \
+    grid.y = (unsigned)((ncols + (BNv) - 1) / (BNv));                                                           \
+    grid.x = (unsigned)((row_end - row_begin + 31) / 32);                                                       \
     UBLR_DISPATCH_KIND(op->kind, KIND, {                                                                        \
       size_t sm = Cfg::smem_bytes();                                                                            \
       UBLR_CUDA(cudaFuncSetAttribute(k_sketch_tagged3<KIND, L, Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
