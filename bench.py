@@ -156,7 +156,7 @@ def cpu_baseline(wl, budget_s=12.0):
 
 KERNEL_OF = {"ublr_sketch_tagged_pair": "k_sketch_tagged3 (Kronecker-restructured tagged sketch, TMEM tag groups)",
              "ublr_sketch_tagged": "k_sketch_tagged3 (Kronecker-restructured tagged sketch, TMEM tag groups)",
-             "ublr_apply": "k_apply2 (operator apply, A generated on the fly)",
+             "ublr_apply": "k_apply3 (operator apply, warp-specialised: A generated by producer warps, DMMA consumers)",
              "ublr_gemm_batched": "k_gemm2 (batched DMMA GEMM)",
              "ublr_coupling": "k_coupling2 (C_ij = U_i^T A_ij V_j)"}
 

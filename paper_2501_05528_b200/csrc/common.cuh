@@ -50,6 +50,17 @@ __device__ __forceinline__ void mma8x8x4(double& d0, double& d1, double a, doubl
                : "d"(a), "d"(b));
 }
 
+// D(16x8) += A(16x8) B(8x8), fp64 (DMMA, 8x fewer instructions than m8n8k4
+// for the same work). Lane (g, t): a0 = A[g][t], a1 = A[g+8][t],
+// a2 = A[g][t+4], a3 = A[g+8][t+4]; b0 = B[t][g], b1 = B[t+4][g];
+// d0, d1 = D[g][2t, 2t+1]; d2, d3 = D[g+8][2t, 2t+1].
+__device__ __forceinline__ void mma16x8x8(double& d0, double& d1, double& d2, double& d3, double a0, double a1,
+                                          double a2, double a3, double b0, double b1) {
+  asm volatile("mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+               : "+d"(d0), "+d"(d1), "+d"(d2), "+d"(d3)
+               : "d"(a0), "d"(a1), "d"(a2), "d"(a3), "d"(b0), "d"(b1));
+}
+
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
   unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   int n = pred ? 8 : 0;
@@ -89,7 +100,8 @@ __device__ __forceinline__ double fast_log(double x, const LogTables* tb) {
   int e = (int)((bits >> 52) & 0x7ff) - 1023;
   int j = (int)((bits >> 45) & 0x7f);
   double f = __longlong_as_double((bits & 0x000fffffffffffffLL) | 0x3ff0000000000000LL);
-  double c = 1.0 + (j + 0.5) * (1.0 / 128.0);
+  // c = 1 + (j + 0.5) / 128 = 1 + (2j + 1) 2^-8, built from bits (no FP64 op)
+  double c = __longlong_as_double(0x3ff0000000000000LL | ((long long)(2 * j + 1) << 44));
   double t = (f - c) * tb->invc[j];
   // log(1+t) = t - t^2/2 + t^3/3 - ... (8 terms)
   double p = -1.0 / 8.0;

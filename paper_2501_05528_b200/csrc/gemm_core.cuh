@@ -15,6 +15,10 @@
 #pragma once
 #include "common.cuh"
 
+#ifndef UBLR_MMA_K8
+#define UBLR_MMA_K8 0
+#endif
+
 namespace ublr {
 
 template <int BM_, int BN_, int BK_, int WMW_, int WNW_, int STAGES_, bool A_KM_ = true, bool B_KM_ = true>
@@ -76,6 +80,36 @@ __device__ __forceinline__ void dmma_mainloop(AP& ap, BP& bp, int nk, double* sm
     if (nx + 1 < nk) ap.prefetch(nx + 1);
     const double* As = As0 + (ks % STAGES) * Cfg::A_STAGE;
     const double* Bs = Bs0 + (ks % STAGES) * Cfg::B_STAGE;
+    if constexpr (UBLR_MMA_K8 && Cfg::MI % 2 == 0) {
+    // m16n8k8: 8-row groups (2i, 2i+1) of acc form one 16-row MMA tile
+    constexpr int MI2 = Cfg::MI / 2;
+    // single-buffered fragments (the double-buffered form spills at 128
+    // registers); ptxas hoists the next slice's loads over these MMAs
+#pragma unroll
+    for (int k8 = 0; k8 < BK / 8; ++k8) {
+      const int k0 = k8 * 8;
+      double a[MI2][4], b[Cfg::NJ][2];
+#pragma unroll
+      for (int i = 0; i < MI2; ++i) {
+        a[i][0] = As[Cfg::ai(am0 + i * 16, k0 + t)];
+        a[i][1] = As[Cfg::ai(am0 + i * 16 + 8, k0 + t)];
+        a[i][2] = As[Cfg::ai(am0 + i * 16, k0 + t + 4)];
+        a[i][3] = As[Cfg::ai(am0 + i * 16 + 8, k0 + t + 4)];
+      }
+#pragma unroll
+      for (int j = 0; j < Cfg::NJ; ++j) {
+        b[j][0] = Bs[Cfg::bi(k0 + t, bn0 + j * 8)];
+        b[j][1] = Bs[Cfg::bi(k0 + t + 4, bn0 + j * 8)];
+      }
+      if (nx < nk) ap.stage_part(As_nx, nx, k8, BK / 8);
+#pragma unroll
+      for (int i = 0; i < MI2; ++i)
+#pragma unroll
+        for (int j = 0; j < Cfg::NJ; ++j)
+          mma16x8x8(acc[2 * i][j][0], acc[2 * i][j][1], acc[2 * i + 1][j][0], acc[2 * i + 1][j][1], a[i][0], a[i][1],
+                    a[i][2], a[i][3], b[j][0], b[j][1]);
+    }
+    } else {
     double a[2][Cfg::MI], b[2][Cfg::NJ];
 #pragma unroll
     for (int i = 0; i < Cfg::MI; ++i) a[0][i] = As[Cfg::ai(am0 + i * 8, t)];
@@ -98,6 +132,7 @@ __device__ __forceinline__ void dmma_mainloop(AP& ap, BP& bp, int nk, double* sm
       for (int i = 0; i < Cfg::MI; ++i)
 #pragma unroll
         for (int j = 0; j < Cfg::NJ; ++j) mma8x8x4(acc[i][j][0], acc[i][j][1], a[cur][i], b[cur][j]);
+    }
     }
     cp_async_commit();
   }

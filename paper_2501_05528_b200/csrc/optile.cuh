@@ -78,6 +78,27 @@ __device__ __forceinline__ double kernel_entry(const ublr_op_t& op, const RowPoi
   return rsqrt(r2);
 }
 
+// Branch-free form for a compile-time dimension: out-of-range rows/columns
+// are left to the caller (their X rows are zero / their outputs are not
+// stored), the diagonal is a select. Same operation order as kernel_entry,
+// so the two give identical bits.
+template <int KIND, int DIM>
+__device__ __forceinline__ double kernel_entry_dim(const RowPoint& row, int q, double c0, double c1, double c2,
+                                                   double diag, const LogTables* lt) {
+  double d = row.x0 - c0;
+  double r2 = d * d;
+  if (DIM > 1) {
+    d = row.x1 - c1;
+    r2 = fma(d, d, r2);
+  }
+  if (DIM > 2) {
+    d = row.x2 - c2;
+    r2 = fma(d, d, r2);
+  }
+  const double v = (KIND == UBLR_OP_LOG) ? -0.5 * fast_log(r2, lt) : rsqrt(r2);
+  return q == row.p ? diag : v;
+}
+
 // Three-slot shared-memory ring of column coordinates (3 dims x BK per slot)
 // for the k-steps of an operator-tile producer; slot = stage % 3.
 template <int BK>

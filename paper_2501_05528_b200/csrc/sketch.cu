@@ -15,6 +15,7 @@
 #include "optile.cuh"
 #include "gemm_core.cuh"
 #include "tmem.cuh"
+#include "ws.cuh"
 #include <cstdlib>
 
 namespace ublr {
@@ -200,6 +201,198 @@ __global__ void __launch_bounds__(Cfg::NT) k_apply2(ublr_op_t op, const double* 
       if (c + 1 < w) out[(int64_t)r * ldo + c + 1] = acc[i][j][1];
     }
   }
+}
+
+// ------------------------------------------------ apply, warp-specialised
+// Kernel operators (A generated on the fly). Producer warps own the A tile
+// (row p of the tile, a KPT-entry slice of each k-step, column points from a
+// shared-memory coordinate ring) and cp.async the X tile; 8 consumer warps
+// run DMMA on stages taken from a full/empty mbarrier ring, so no CTA-wide
+// barrier sits inside the k loop.
+//
+// Why this shape (profiles/r01, tools/apply_variants.py): DMMA and the FP64
+// ALU share one issue pipe. With the generation switched off the consumers
+// reach 96 % of the DMMA peak; the generation costs ~22 FP64 operations per
+// entry, so the tile is made wide (BN = 256: each generated entry feeds 256
+// output columns) and short (BM = 64), halving the generation work per flop
+// against a 128 x 128 tile. The accumulator tile (64 x 256 doubles) is what
+// the register file can hold next to the fragments.
+template <int BM_, int BN_, int BK_, int STAGES_, int WMW_, int WNW_, int NPROD_>
+struct Ap3Cfg {
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, STAGES = STAGES_, WMW = WMW_, WNW = WNW_;
+  static constexpr int NPROD = NPROD_, NCONS = 32 * WMW * WNW, NT = NPROD + NCONS;
+  static constexpr int PH = NPROD / BM;        // producer threads per A-tile row
+  static constexpr int KPT = BK / PH;          // k entries per producer thread per step
+  static constexpr int PB = KPT < 8 ? KPT : 8; // entries evaluated together (ILP against the shared pipe)
+  static constexpr int SA = BM + 4, SB = BN + 4;
+  static constexpr int A_STAGE = BK * SA, B_STAGE = BK * SB;
+  static constexpr int WM = BM / WMW, WN = BN / WNW, MI = WM / 8, NJ = WN / 8;
+  // setmaxnreg moves registers inside the CTA's own pool: the kernel starts
+  // at 65536 / NT (rounded down to 8) per thread; what the producers give
+  // back, the consumers take.
+  static constexpr int START_REGS = (65536 / NT) / 8 * 8;
+  static constexpr int CONS_REGS = NT == 384 ? 208 : 200;
+  static constexpr int PROD_REGS = (START_REGS * NPROD - NCONS * (CONS_REGS - START_REGS)) / NPROD / 8 * 8;
+  static_assert(NPROD % BM == 0 && BK % PH == 0 && KPT % PB == 0, "producer split");
+  static_assert(PROD_REGS >= 40, "producers need registers for the entry evaluation");
+  static_assert(NPROD * (START_REGS - PROD_REGS) >= NCONS * (CONS_REGS - START_REGS),
+                "consumers would wait forever for registers the producers never release");
+  static constexpr size_t smem_bytes() { return (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double); }
+};
+// Measured on B200 at c3/c4 sizes (log kernel, N = 65536, w = 4708 / 7590;
+// tools/apply_variants.py): 64x256 tile, BK 16, 4 stages, 8 producer warps
+// 78 / 80 % of the DMMA peak; 4 producer warps 77 / 79 %; 128x128 tile
+// 71 %; the synchronous k_apply2 (UBLR_APPLY_CFG=4) 60.5 %.
+using Ap3Wide = Ap3Cfg<64, 256, 16, 4, 2, 4, 256>;     // default
+using Ap3Square = Ap3Cfg<128, 128, 32, 3, 2, 4, 256>;  // UBLR_APPLY_CFG=5
+
+template <int KIND, int DIM, class C>
+__global__ void __launch_bounds__(C::NT, 1) k_apply3(ublr_op_t op, const double* __restrict__ X, int64_t ldx,
+                                                     int w, double* __restrict__ out, int64_t ldo, int vec2) {
+  constexpr int BM = C::BM, BN = C::BN, BK = C::BK, STAGES = C::STAGES, SA = C::SA, SB = C::SB;
+  constexpr int NPROD = C::NPROD, NCONS = C::NCONS, KPT = C::KPT, PB = C::PB;
+  constexpr int MI = C::MI, NJ = C::NJ;
+  __shared__ LogTables lt;
+  __shared__ double ringbuf[9 * BK];
+  __shared__ uint64_t full[STAGES], empty[STAGES];
+  extern __shared__ double dsm[];
+  double* As0 = dsm;
+  double* Bs0 = dsm + STAGES * C::A_STAGE;
+  const int n = (int)op.n;
+  const int row0 = blockIdx.x * BM, col0 = blockIdx.y * BN;
+  const int nk = (n + BK - 1) / BK;
+  ColRing<BK> ring{ringbuf};
+  if (KIND == UBLR_OP_LOG) init_log_tables(&lt);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      ws::mbar_init(&full[s], 2 * NPROD);  // NPROD cp.async arrivals (X tile) + NPROD generator arrivals
+      ws::mbar_init(&empty[s], NCONS);
+    }
+  }
+  __syncthreads();
+
+  if (threadIdx.x < NPROD) {
+    // ---------------- producers
+    ws::regs_dec<C::PROD_REGS>();
+    const int p = threadIdx.x % BM;            // A-tile row
+    const int kq0 = (threadIdx.x / BM) * KPT;  // first k entry of this thread
+    // rows past n generate junk that is never stored; columns past n are
+    // zeroed (their X rows are zero-filled too)
+    const RowPoint rp = load_row_point(op, min(row0 + p, n - 1), true);
+    const RowPoint rq = {row0 + p, rp.orig, rp.x0, rp.x1, rp.x2};
+    const double diag = op.diag;
+    ring.prefetch(op, 0, 0, n, NPROD);
+    cp_async_commit();
+    for (int ks = 0; ks < nk; ++ks) {
+      const int s = ks % STAGES;
+      const uint32_t u = (uint32_t)(ks / STAGES);
+      // this step's column points: own copies landed, then every producer's
+      if (ks == 0) cp_async_wait<0>();
+      else cp_async_wait<1>();
+      ws::named_sync(1, NPROD);
+      if (ks + 1 < nk) ring.prefetch(op, ks + 1, (ks + 1) * BK, n, NPROD);
+      cp_async_commit();
+      ws::mbar_wait(&empty[s], (u & 1) ^ 1);
+      tile_copy<NPROD>(Bs0 + s * C::B_STAGE, SB, X, ldx, BK, BN, ks * BK, col0, n, w, IdentityRows{}, vec2 != 0);
+      cp_async_commit();
+      ws::mbar_cp_async_arrive(&full[s]);
+      double* As = As0 + s * C::A_STAGE;
+      const int k0 = ks * BK;
+      const double* cr = ring.buf + (ks % 3) * 3 * BK;
+#pragma unroll
+      for (int kb = 0; kb < KPT; kb += PB) {
+        double v[PB];
+#pragma unroll
+        for (int e = 0; e < PB; ++e) {
+          const int kk = kq0 + kb + e;
+          const double a = kernel_entry_dim<KIND, DIM>(rq, k0 + kk, cr[kk], DIM > 1 ? cr[BK + kk] : 0.0,
+                                                       DIM > 2 ? cr[2 * BK + kk] : 0.0, diag, &lt);
+          v[e] = k0 + kk < n ? a : 0.0;  // zero-filled coordinates may sit on a row point
+        }
+#pragma unroll
+        for (int e = 0; e < PB; ++e) As[(kq0 + kb + e) * SA + p] = v[e];
+      }
+      ws::mbar_arrive(&full[s]);
+    }
+    cp_async_wait<0>();
+    return;
+  }
+
+  // ---------------- consumers
+  ws::regs_inc<C::CONS_REGS>();
+  const int ct = threadIdx.x - NPROD;
+  const int warp = ct >> 5, lane = ct & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wr = warp / C::WNW, wc = warp % C::WNW;
+  const int am0 = wr * C::WM + g, bn0 = wc * C::WN + g;
+  double acc[MI][NJ][2];
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int ks = 0; ks < nk; ++ks) {
+    const int s = ks % STAGES;
+    ws::mbar_wait(&full[s], (uint32_t)(ks / STAGES) & 1);
+    const double* As = As0 + s * C::A_STAGE;
+    const double* Bs = Bs0 + s * C::B_STAGE;
+    double a[2][MI], b[2][NJ];
+#pragma unroll
+    for (int i = 0; i < MI; ++i) a[0][i] = As[t * SA + am0 + i * 8];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) b[0][j] = Bs[t * SB + bn0 + j * 8];
+#pragma unroll
+    for (int k4 = 0; k4 < BK / 4; ++k4) {
+      const int cur = k4 & 1;
+      if (k4 + 1 < BK / 4) {
+        const int kr = (k4 + 1) * 4 + t;
+#pragma unroll
+        for (int i = 0; i < MI; ++i) a[cur ^ 1][i] = As[kr * SA + am0 + i * 8];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) b[cur ^ 1][j] = Bs[kr * SB + bn0 + j * 8];
+      }
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) mma8x8x4(acc[i][j][0], acc[i][j][1], a[cur][i], b[cur][j]);
+    }
+    ws::mbar_arrive(&empty[s]);
+  }
+  const bool pair = (ldo % 2) == 0 && (((uintptr_t)out) % 16) == 0;
+#pragma unroll
+  for (int i = 0; i < MI; ++i) {
+    const int r = row0 + wr * C::WM + i * 8 + g;
+    if (r >= n) continue;
+    double* orow = out + (int64_t)r * ldo;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int c = col0 + wc * C::WN + j * 8 + 2 * t;
+      if (pair && c + 1 < w) {
+        *reinterpret_cast<double2*>(orow + c) = make_double2(acc[i][j][0], acc[i][j][1]);
+      } else {
+        if (c < w) orow[c] = acc[i][j][0];
+        if (c + 1 < w) orow[c + 1] = acc[i][j][1];
+      }
+    }
+  }
+}
+
+template <class C>
+int launch_apply3(const ublr_op_t* op, const double* X, int64_t ld_x, int w, double* out, int64_t ld_o, int vec2,
+                  cudaStream_t st) {
+  dim3 grid((unsigned)((op->n + C::BM - 1) / C::BM), (unsigned)((w + C::BN - 1) / C::BN));
+  size_t sm = C::smem_bytes();
+#define UBLR_AP3(KIND, DIM)                                                                                       \
+  {                                                                                                               \
+    UBLR_CUDA(cudaFuncSetAttribute(k_apply3<KIND, DIM, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
+    k_apply3<KIND, DIM, C><<<grid, C::NT, sm, st>>>(*op, X, ld_x, w, out, ld_o, vec2);                           \
+  }
+  if (op->kind == UBLR_OP_LOG) {
+    if (op->dim == 1) UBLR_AP3(UBLR_OP_LOG, 1) else if (op->dim == 2) UBLR_AP3(UBLR_OP_LOG, 2) else UBLR_AP3(UBLR_OP_LOG, 3)
+  } else {
+    if (op->dim == 1) UBLR_AP3(UBLR_OP_INV, 1) else if (op->dim == 2) UBLR_AP3(UBLR_OP_INV, 2) else UBLR_AP3(UBLR_OP_INV, 3)
+  }
+#undef UBLR_AP3
+  return UBLR_OK;
 }
 
 // ---------------------------------------------------------- tagged sketch
@@ -609,22 +802,30 @@ extern "C" int ublr_apply(const ublr_op_t* op, const double* X, int64_t ld_x, in
   if (w == 0) return UBLR_OK;
   cudaStream_t st = (cudaStream_t)stream;
   dim3 grid;
-  grid.x = (unsigned)((op->n + 127) / 128);  // row tiles fastest: CTAs in flight share one X column slab in L2
   using CfgW = TileCfg<128, 128, 32, 4, 4, 2>;
   using CfgN = TileCfg<128, 64, 32, 4, 4, 2>;
+  static int variant = [] {
+    const char* e = getenv("UBLR_APPLY_CFG");
+    return e ? atoi(e) : 0;
+  }();
   int vec2 = ((ld_x % 2) == 0 && (((uintptr_t)X) % 16) == 0) ? 1 : 0;
+  // row tiles fastest (grid.x): CTAs in flight share one X column slab in L2
 #define UBLR_AP2(CFG)                                                                                         \
   UBLR_DISPATCH_KIND(op->kind, KIND, {                                                                      \
+    grid.x = (unsigned)((op->n + CFG::BM - 1) / CFG::BM);                                                   \
+    grid.y = (unsigned)((w + CFG::BN - 1) / CFG::BN);                                                       \
     size_t sm = CFG::smem_bytes();                                                                          \
     UBLR_CUDA(cudaFuncSetAttribute(k_apply2<KIND, CFG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
     k_apply2<KIND, CFG><<<grid, CFG::NT, sm, st>>>(*op, X, ld_x, w, out, ld_o, vec2);                         \
   })
-  if (w <= 64) {
-    grid.y = (unsigned)((w + 63) / 64);
+  if (w > 64 && op->kind != UBLR_OP_DENSE && (variant == 0 || variant == 5)) {
+    rc = variant == 5 ? launch_apply3<Ap3Square>(op, X, ld_x, w, out, ld_o, vec2, st)
+                      : launch_apply3<Ap3Wide>(op, X, ld_x, w, out, ld_o, vec2, st);
+    if (rc) return rc;
+  } else if (w <= 64) {
     UBLR_AP2(CfgN);
   } else {
-    grid.y = (unsigned)((w + 127) / 128);
-    UBLR_AP2(CfgW);
+    UBLR_AP2(CfgW);  // dense operator, or UBLR_APPLY_CFG=4 (the synchronous k_apply2)
   }
 #undef UBLR_AP2
   UBLR_LAUNCH_CHECK();
