@@ -78,6 +78,22 @@ const char* ublr_last_error(void);
 int ublr_version(void);
 int ublr_device_check(void);
 
+/* Philox keys of the reference's RandomStream(seed, key) (ref/linalg.py:30-35:
+ * np.random.Philox(SeedSequence(seed, spawn_key=key)), i.e.
+ * SeedSequence.generate_state(2, uint64)) for n spawn keys prefix + suffix_s.
+ * Host function. `run` = uint32 words of the seed (little-endian, >= 1 word),
+ * `prefix` the words shared by all keys, `suffix` n x nsuffix words;
+ * keys_out is n x 2 uint64. */
+int ublr_seedseq_keys(const uint32_t* run, int nrun, const uint32_t* prefix, int nprefix,
+                      const uint32_t* suffix, int nsuffix, int64_t n, uint64_t* keys_out);
+
+/* Null vectors for the tagging plan (ref/tagging.py:126-139, through
+ * ref/linalg.py:72-94): for each row set s (CSR ptr/idx into the b x ell
+ * tagging matrix T, fewer than ell rows), Z[s] = last column of the complete
+ * Householder Q of T[rows]^T and res[s] = ||T[rows] Z[s]||. Host function. */
+int ublr_null_vectors(const double* T, int ell, const int32_t* ptr, const int32_t* idx, int nsets, double* Z,
+                      double* res);
+
 /* K1 — ref/linalg.py:38-52 (`RandomStream.normal` / `gaussian`), called at
  * ref/bases.py:97-98, :163-168, :229-230 and ref/reconstruction.py:405.
  * Bit-compatible with numpy. `streams` is a DEVICE array. Workspace bytes

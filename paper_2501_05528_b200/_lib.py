@@ -42,6 +42,8 @@ SIGNATURES = {
     "ublr_last_error": (C.c_char_p, []),
     "ublr_version": (INT, []),
     "ublr_device_check": (INT, []),
+    "ublr_seedseq_keys": (INT, [P, INT, P, INT, P, INT, I64, P]),
+    "ublr_null_vectors": (INT, [P, INT, P, P, INT, P, P]),
     "ublr_rng_workspace_bytes": (I64, [P, INT]),
     "ublr_rng_normals": (INT, [P, P, INT, P, P, I64, P]),
     "ublr_sketch_tagged": (INT, [C.POINTER(OpDesc), P, INT, P, INT, P, I64, INT, P, I64, INT, INT, P]),
@@ -119,10 +121,17 @@ def add_work(name: str, flops: float):
         work[name] = work.get(name, 0.0) + float(flops)
 
 
-def instrument(enable: bool = True):
-    """Record CUDA events around every C-ABI launch (bench.py roofline)."""
-    global _events
+_only = None  # instrument only these entry points (None: all)
+
+
+def instrument(enable: bool = True, only=None):
+    """Record CUDA events around C-ABI launches (bench.py roofline): every
+    entry point, or just the names in `only` (two event records per launch
+    of host time, so the timed bench region instruments only the kernel it
+    reports)."""
+    global _events, _only
     _events = {} if enable else None
+    _only = set(only) if only else None
     if enable:
         work.clear()
 
@@ -162,7 +171,7 @@ def call(name: str, *args):
     """Call a status-returning C-ABI function and raise on failure."""
     global launch_count
     launch_count += LAUNCHES.get(name, 0)
-    if _events is not None:
+    if _events is not None and (_only is None or name in _only):
         add_work(name, _work_of(name, args))
         import torch
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -193,6 +202,15 @@ def require_device():
 def ptr(t) -> int:
     """Device pointer of a torch tensor (or 0 for None)."""
     return 0 if t is None else int(t.data_ptr())
+
+
+def h2d(a, device):
+    """Host array -> device tensor without blocking the host: staged through
+    torch's pinned-memory cache and copied with non_blocking=True (a pageable
+    copy would wait for all work queued before it)."""
+    import torch
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    return t.pin_memory().to(device, non_blocking=True)
 
 
 def stream_handle():

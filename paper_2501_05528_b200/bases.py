@@ -147,10 +147,10 @@ def draw_test_pair(dt, stream: RandomStream, cols: int):
     torch = _torch()
     GH = torch.empty((2, dt.n, cols), dtype=torch.float64, device=dt.device)
     b = dt.b
-    keys = [stream.key + (side, i) for side in (0, 1) for i in range(b)]
+    suffix = np.stack([np.repeat(np.arange(2), b), np.tile(np.arange(b), 2)], axis=1)  # (side, i)
     rows = np.concatenate([dt.sizes, dt.sizes])
     offs = np.concatenate([dt.off_h[:-1].astype(np.int64) * cols, dt.n * cols + dt.off_h[:-1].astype(np.int64) * cols])
-    device_normals_keys(stream.seed, keys, rows, cols, offs, cols, None, GH)
+    device_normals_keys(stream.seed, stream.key, rows, cols, offs, cols, None, GH, suffix=suffix)
     return GH[0], GH[1]
 
 
@@ -199,8 +199,15 @@ def block_bases_from_tagged(dt, Y, Z, Z_dev, ell, gc, k):
 
 
 def tagging_bases(op, tess: Tessellation, k: int, p: int, plan, stream: RandomStream,
-                  group_cols: int | None = None, extra_samples: bool = False):
-    """ref/bases.py:140-204 on the GPU. Returns (BlockBases, SketchBundle)."""
+                  group_cols: int | None = None, extra_samples: bool = False, first=None):
+    """ref/bases.py:140-204 on the GPU. Returns (BlockBases, SketchBundle).
+
+    `plan` is a TaggingPlan, or a zero-argument callable producing one (the
+    host redraw policy of ref/tagging.py:306-352) together with `first`, the
+    policy's first draw. The sketch depends only on the tagging matrix, not on
+    the null vectors, so with a callable the sketch of `first` is launched
+    before the host evaluates the plan and runs on the GPU meanwhile; if the
+    policy redraws, the sketch is recomputed for the accepted matrix."""
     torch = _torch()
     if extra_samples:
         raise NotImplementedError("extra_samples (ref/bases.py:177-182) is not on the B200 hot path (SURVEY F12)")
@@ -208,19 +215,26 @@ def tagging_bases(op, tess: Tessellation, k: int, p: int, plan, stream: RandomSt
     dt = device_tess(tess, torch.device("cuda"))
     r = k + p
     gc = r if group_cols is None else group_cols
-    T_entries = plan.matrix.entries
+    planner = plan if callable(plan) else None
+    matrix = first if planner is not None else plan.matrix
+    T_entries = matrix.entries
     ell = T_entries.shape[1]
     s = ell * gc
-    if k > dt.m_max and k > 0:
-        pass  # every block takes the identity basis (ref/bases.py:80-82)
     G, H = draw_test_pair(dt, stream, gc)
-    T_dev = torch.from_numpy(np.ascontiguousarray(T_entries)).to(dt.device)
-    Z_dev = torch.from_numpy(np.ascontiguousarray(plan.Z)).to(dt.device)
+    T_dev = _lib.h2d(T_entries, dt.device)
     _bill(op, s, s)
     Y, Z = tagged_sketch(op, dt, T_dev, T_entries, G, H, gc)
+    if planner is not None:
+        plan = planner()                     # host work, overlapping the sketch
+        if plan.matrix is not matrix:        # redrawn: sketch the accepted matrix
+            T_entries = plan.matrix.entries
+            T_dev = _lib.h2d(T_entries, dt.device)
+            Y, Z = tagged_sketch(op, dt, T_dev, T_entries, G, H, gc)
+    Z_dev = _lib.h2d(plan.Z, dt.device)
     U, V = block_bases_from_tagged(dt, Y, Z, Z_dev, ell, gc, k)
     bases = BlockBases(dt, U, V, k, "tag", (s, s))
     bundle = SketchBundle("tag", dt, s, Y, Z, G=G, H=H, tagging=plan.matrix, group_cols=gc)
+    bundle.plan = plan
     return bases, bundle
 
 

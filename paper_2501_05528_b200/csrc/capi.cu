@@ -1,5 +1,7 @@
 // C-ABI plumbing: error text, version, device check.
 #include "common.cuh"
+#include <cmath>
+#include <vector>
 
 namespace ublr {
 static thread_local std::string g_last_error;
@@ -19,5 +21,127 @@ extern "C" int ublr_device_check(void) {
   UBLR_CUDA(cudaGetDeviceProperties(&p, dev));
   UBLR_REQUIRE(p.major == 10 && p.minor == 0, UBLR_ERR_VALUE,
                std::string("ublr_b200 is built for sm_100a; found ") + p.name);
+  return UBLR_OK;
+}
+
+// numpy SeedSequence(seed, spawn_key = prefix + suffix_s).generate_state(2,
+// uint64) for n spawn keys at once (host code; numpy's published algorithm:
+// O'Neill's seed_seq hash mixing over a 4-word uint32 pool,
+// numpy/random/bit_generator.pyx). Restated from paper_2501_05528_b200/seedseq.py
+// (checked bit-for-bit against numpy in tests/test_host.py).
+namespace {
+constexpr uint32_t SS_INIT_A = 0x43b0d7e5u, SS_MULT_A = 0x931e8875u, SS_INIT_B = 0x8b51f9ddu,
+                   SS_MULT_B = 0x58f38dedu, SS_MIX_L = 0xca01f9ddu, SS_MIX_R = 0x4973f715u;
+}  // namespace
+
+extern "C" int ublr_seedseq_keys(const uint32_t* run, int nrun, const uint32_t* prefix, int nprefix,
+                                 const uint32_t* suffix, int nsuffix, int64_t n, uint64_t* keys_out) {
+  UBLR_REQUIRE(run && nrun >= 1 && nprefix >= 0 && nsuffix >= 0 && n >= 0 && keys_out &&
+                   (nprefix == 0 || prefix) && (nsuffix == 0 || suffix),
+               UBLR_ERR_VALUE, "ublr_seedseq_keys: bad arguments");
+  const int nspawn = nprefix + nsuffix;
+  const int nr = (nspawn > 0 && nrun < 4) ? 4 : nrun;  // run entropy padded to the pool size
+  const int L = nr + nspawn;
+  std::vector<uint32_t> ent((size_t)L);
+  for (int64_t s = 0; s < n; ++s) {
+    for (int i = 0; i < nr; ++i) ent[i] = i < nrun ? run[i] : 0u;
+    for (int i = 0; i < nprefix; ++i) ent[nr + i] = prefix[i];
+    for (int i = 0; i < nsuffix; ++i) ent[nr + nprefix + i] = suffix[s * nsuffix + i];
+    uint32_t hc = SS_INIT_A;
+    auto hashmix = [&hc](uint32_t v) {
+      v ^= hc;
+      hc *= SS_MULT_A;
+      v *= hc;
+      return v ^ (v >> 16);
+    };
+    auto mix = [](uint32_t x, uint32_t y) {
+      uint32_t r = SS_MIX_L * x - SS_MIX_R * y;
+      return r ^ (r >> 16);
+    };
+    uint32_t pool[4];
+    for (int i = 0; i < 4; ++i) pool[i] = hashmix(i < L ? ent[i] : 0u);
+    for (int a = 0; a < 4; ++a)
+      for (int d = 0; d < 4; ++d)
+        if (a != d) pool[d] = mix(pool[d], hashmix(pool[a]));
+    for (int a = 4; a < L; ++a)
+      for (int d = 0; d < 4; ++d) pool[d] = mix(pool[d], hashmix(ent[a]));
+    uint32_t hb = SS_INIT_B, st[4];
+    for (int i = 0; i < 4; ++i) {
+      uint32_t v = pool[i] ^ hb;
+      hb *= SS_MULT_B;
+      v *= hb;
+      st[i] = v ^ (v >> 16);
+    }
+    keys_out[2 * s] = (uint64_t)st[0] | ((uint64_t)st[1] << 32);
+    keys_out[2 * s + 1] = (uint64_t)st[2] | ((uint64_t)st[3] << 32);
+  }
+  return UBLR_OK;
+}
+
+// Null vectors of tagging-row subsets (host code; ref/tagging.py:126-139 via
+// ref/linalg.py:72-94: the last column of the complete Householder Q of
+// T[rows]^T). Per set: Householder QR of the ell x sz matrix A = T[rows]^T in
+// LAPACK's dgeqr2 convention (v_0 = 1, beta = -sign(alpha) ||x||,
+// tau = (beta - alpha) / beta), then q = H_0 H_1 ... H_{k-1} e_{ell-1}.
+// Equal to numpy's qr(mode="complete")[0][:, -1] up to rounding.
+extern "C" int ublr_null_vectors(const double* T, int ell, const int32_t* ptr, const int32_t* idx, int nsets,
+                                 double* Z, double* res) {
+  UBLR_REQUIRE(T && ell >= 1 && ptr && idx && nsets >= 0 && Z && res, UBLR_ERR_VALUE,
+               "ublr_null_vectors: bad arguments");
+  std::vector<double> A, tau;
+  for (int s = 0; s < nsets; ++s) {
+    const int r0 = ptr[s], sz = ptr[s + 1] - ptr[s];
+    UBLR_REQUIRE(sz >= 0 && sz < ell, UBLR_ERR_VALUE, "ublr_null_vectors: a set has >= ell rows (no null vector)");
+    A.assign((size_t)ell * sz, 0.0);  // column-major ell x sz: A[i + j*ell] = T[idx[r0+j], i]
+    for (int j = 0; j < sz; ++j)
+      for (int i = 0; i < ell; ++i) A[i + (size_t)j * ell] = T[(size_t)idx[r0 + j] * ell + i];
+    tau.assign(sz, 0.0);
+    for (int j = 0; j < sz; ++j) {
+      double* col = &A[(size_t)j * ell];
+      const double alpha = col[j];
+      double ss = 0.0, scale = 0.0;
+      for (int i = j + 1; i < ell; ++i) scale = fmax(scale, fabs(col[i]));
+      if (scale > 0.0) {
+        for (int i = j + 1; i < ell; ++i) ss += (col[i] / scale) * (col[i] / scale);
+      }
+      const double xnorm = scale * sqrt(ss);
+      if (xnorm == 0.0) {
+        tau[j] = 0.0;
+        continue;
+      }
+      const double beta = -copysign(hypot(alpha, xnorm), alpha);
+      tau[j] = (beta - alpha) / beta;
+      const double inv = 1.0 / (alpha - beta);
+      for (int i = j + 1; i < ell; ++i) col[i] *= inv;
+      col[j] = beta;
+      // apply H_j = I - tau v v^T (v = [1, col[j+1:]]) to the remaining columns
+      for (int c = j + 1; c < sz; ++c) {
+        double* a = &A[(size_t)c * ell];
+        double w = a[j];
+        for (int i = j + 1; i < ell; ++i) w += col[i] * a[i];
+        w *= tau[j];
+        a[j] -= w;
+        for (int i = j + 1; i < ell; ++i) a[i] -= w * col[i];
+      }
+    }
+    double* z = Z + (size_t)s * ell;
+    for (int i = 0; i < ell; ++i) z[i] = (i == ell - 1) ? 1.0 : 0.0;
+    for (int j = sz - 1; j >= 0; --j) {
+      const double* v = &A[(size_t)j * ell];
+      double w = z[j];
+      for (int i = j + 1; i < ell; ++i) w += v[i] * z[i];
+      w *= tau[j];
+      z[j] -= w;
+      for (int i = j + 1; i < ell; ++i) z[i] -= w * v[i];
+    }
+    double r2 = 0.0;
+    for (int j = 0; j < sz; ++j) {
+      const double* t = T + (size_t)idx[r0 + j] * ell;
+      double d = 0.0;
+      for (int i = 0; i < ell; ++i) d += t[i] * z[i];
+      r2 += d * d;
+    }
+    res[s] = sqrt(r2);
+  }
   return UBLR_OK;
 }

@@ -130,8 +130,8 @@ def phase1_local(op, tess, k, p, stream, shard, plan=None):
     ell = T.shape[1]
     s = ell * gc
     G, H = draw_test_pair(dt, stream.child(0), gc)
-    T_dev = torch.from_numpy(np.ascontiguousarray(T)).to(dt.device)
-    Z_dev = torch.from_numpy(np.ascontiguousarray(plan.Z)).to(dt.device)
+    T_dev = _lib.h2d(T, dt.device)
+    Z_dev = _lib.h2d(plan.Z, dt.device)
     _bill(op, s, s)
     inner = unwrap(op)
     if not getattr(inner, "symmetric", False) or not hasattr(inner, "device_op"):

@@ -91,7 +91,7 @@ def device_normals(specs, out):
     lib = _lib.load()
     ws_bytes = int(lib.ublr_rng_workspace_bytes(counts.ctypes.data, len(specs)))
     ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device=out.device)
-    rec_d = torch.from_numpy(rec.view(np.uint8)).to(out.device)
+    rec_d = _lib.h2d(rec.view(np.uint8), out.device)
     _lib.call("ublr_rng_normals", _lib.ptr(rec_d), counts.ctypes.data, len(specs), _lib.ptr(out),
               _lib.ptr(ws), ws_bytes, _lib.stream_handle())
     # keep host/device descriptors alive until the stream has consumed them
@@ -99,18 +99,22 @@ def device_normals(specs, out):
     return out
 
 
-def device_normals_keys(seed, keys, rows, cols, offsets, ld, rowmap, out):
+def device_normals_keys(seed, keys, rows, cols, offsets, ld, rowmap, out, suffix=None):
     """Vectorised form of device_normals for many streams of one seed:
     stream s is RandomStream(seed, keys[s]) with rows[s] x cols normals at
-    out.flat[offsets[s] + r * ld + c] (rowmap shared by all streams or None)."""
-    import torch
-
-    from .seedseq import philox_keys
+    out.flat[offsets[s] + r * ld + c] (rowmap shared by all streams or None).
+    With `suffix` ((n, ns) ints), `keys` is one prefix tuple and stream s is
+    RandomStream(seed, keys + tuple(suffix[s])); the keys are derived by the
+    C-ABI host function ublr_seedseq_keys."""
+    from .seedseq import philox_keys, philox_keys_suffixed
 
     _lib.require_device()
-    ns = len(keys)
+    if suffix is not None:
+        kk = philox_keys_suffixed(seed, keys, suffix)
+    else:
+        kk = philox_keys(seed, keys)
+    ns = kk.shape[0]
     rec = np.zeros(ns, dtype=_lib.RNG_STREAM_DTYPE)
-    kk = philox_keys(seed, keys)
     rec["key0"], rec["key1"] = kk[:, 0], kk[:, 1]
     counts = np.asarray(rows, dtype=np.int64) * int(cols)
     rec["count"] = counts
@@ -120,8 +124,9 @@ def device_normals_keys(seed, keys, rows, cols, offsets, ld, rowmap, out):
     rec["rowmap"] = _lib.ptr(rowmap)
     lib = _lib.load()
     ws_bytes = int(lib.ublr_rng_workspace_bytes(counts.ctypes.data, ns))
+    import torch
     ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device=out.device)
-    rec_d = torch.from_numpy(rec.view(np.uint8)).to(out.device, non_blocking=False)
+    rec_d = _lib.h2d(rec.view(np.uint8), out.device)
     _lib.call("ublr_rng_normals", _lib.ptr(rec_d), counts.ctypes.data, ns, _lib.ptr(out), _lib.ptr(ws), ws_bytes,
               _lib.stream_handle())
     return out

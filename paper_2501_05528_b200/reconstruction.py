@@ -9,6 +9,7 @@ signatures; their work runs in the CUDA kernels of `csrc/` through the C ABI.
 from __future__ import annotations
 
 import time
+from collections.abc import Mapping
 from dataclasses import dataclass
 
 import numpy as np
@@ -17,7 +18,7 @@ from . import _lib
 from .bases import BlockBases, block_nullification_bases, naive_bases, tagging_bases
 from .linalg import RandomStream, device_normals
 from .operators import CountingOperator, DifferenceOperator, LinearOperatorHandle, counting_wrapper, unwrap
-from .tagging import DegenerateTagsError, plan_tagging
+from .tagging import DegenerateTagsError, make_tagging_matrix, plan_tagging
 from .tessellation import BoxColoring, Tessellation, color_boxes, device_tess
 
 METHOD_IDS = {("A", "bn"): "A1", ("A", "tag"): "A2", ("A", "naive"): "A3", ("B", "bn"): "B1", ("B", "tag"): "B2"}
@@ -227,11 +228,17 @@ def direct_core(op, tess: Tessellation, bases: BlockBases):
 
 
 def _check_coloring(tess, colors):
-    colors = np.asarray(colors)
-    for i in range(tess.b):
-        nc = colors[tess.neighbor_lists[i]]
-        if len(set(nc.tolist())) != len(nc):
-            raise ValueError(f"invalid coloring: two same-color probes collide in the neighborhood of block {i}")
+    """ref/reconstruction.py:214-221: no two blocks of one neighbourhood share a colour."""
+    from .tagging import _neighbour_csr
+    colors = np.asarray(colors, dtype=np.int64)
+    ptr, idx = _neighbour_csr(tess)
+    seg = np.repeat(np.arange(tess.b, dtype=np.int64), np.diff(ptr))
+    key = seg * (int(colors.max(initial=0)) + 1) + colors[idx]
+    if np.unique(key).size != key.size:
+        for i in range(tess.b):
+            nc = colors[tess.neighbor_lists[i]]
+            if len(set(nc.tolist())) != len(nc):
+                raise ValueError(f"invalid coloring: two same-color probes collide in the neighborhood of block {i}")
 
 
 def structured_identity_discrepancy(op, tess: Tessellation, bases: BlockBases, core, coloring: BoxColoring):
@@ -297,13 +304,31 @@ class CompressionReport:
                 "aspect_ratios": self.aspect_ratios}
 
 
+def _quantiles(sorted_vals: np.ndarray, qs) -> list:
+    """np.quantile(..., method="linear") on sorted data, restated (same
+    virtual index and two-sided lerp as numpy, so the same bits) without
+    numpy's per-call overhead."""
+    n = sorted_vals.size
+    out = []
+    for q in qs:
+        v = n * q + (1.0 - q) - 1.0
+        lo = int(np.floor(v))
+        lo = min(max(lo, 0), n - 1)
+        hi = min(lo + 1, n - 1)
+        t = v - np.floor(v)
+        a, b = float(sorted_vals[lo]), float(sorted_vals[hi])
+        d = b - a
+        out.append(b - d * (1.0 - t) if t >= 0.5 else a + d * t)
+    return out
+
+
 def _ratio_summary(values: np.ndarray) -> dict:
-    fin = values[np.isfinite(values)]
+    fin = np.sort(values[np.isfinite(values)])
     if fin.size == 0:
         return {"count": 0}
-    q1, med, q3 = np.quantile(fin, (0.25, 0.5, 0.75))
-    return {"count": int(fin.size), "min": float(fin.min()), "q1": float(q1),
-            "median": float(med), "q3": float(q3), "max": float(fin.max())}
+    q1, med, q3 = _quantiles(fin, (0.25, 0.5, 0.75))
+    return {"count": int(fin.size), "min": float(fin[0]), "q1": float(q1),
+            "median": float(med), "q3": float(q3), "max": float(fin[-1])}
 
 
 def _base_config(tess, k, p, stream, **extra) -> dict:
@@ -313,20 +338,55 @@ def _base_config(tess, k, p, stream, **extra) -> dict:
     return cfg
 
 
-class _PhaseTimer:
-    """perf_counter around a phase with device synchronisation at the edges,
-    so times_s keeps the reference's per-phase meaning (ref/reconstruction.py:524-551)."""
+class PhaseTimes(Mapping):
+    """Per-phase seconds (ref/reconstruction.py:524-551 `times_s`), measured as
+    CUDA-event spans on the compression stream. Recording never blocks the
+    host; the events are resolved (one synchronisation) on first read."""
 
-    def __init__(self, times, name):
+    def __init__(self):
+        self._events = {}
+        self._values = None
+
+    def _record(self, name, e0, e1):
+        self._events[name] = (e0, e1)
+        self._values = None
+
+    def _resolve(self):
+        if self._values is None:
+            vals = {}
+            for name, (e0, e1) in self._events.items():
+                e1.synchronize()
+                vals[name] = e0.elapsed_time(e1) / 1e3
+            self._values = vals
+        return self._values
+
+    def __getitem__(self, key):
+        return self._resolve()[key]
+
+    def __iter__(self):
+        return iter(self._resolve())
+
+    def __len__(self):
+        return len(self._events)
+
+    def __repr__(self):
+        return repr(dict(self._resolve()))
+
+
+class _PhaseTimer:
+    """CUDA events around a phase on the current stream (no host sync)."""
+
+    def __init__(self, times: PhaseTimes, name):
         self.times, self.name = times, name
 
     def __enter__(self):
-        _torch().cuda.synchronize()
-        self.t0 = time.perf_counter()
+        self.e0 = _torch().cuda.Event(enable_timing=True)
+        self.e0.record()
 
     def __exit__(self, *exc):
-        _torch().cuda.synchronize()
-        self.times[self.name] = time.perf_counter() - self.t0
+        e1 = _torch().cuda.Event(enable_timing=True)
+        e1.record()
+        self.times._record(self.name, self.e0, e1)
 
 
 def compress_type_a(op, tess, k, p=10, method="tag", stream=None, distribution="gaussian", extra_cols=0,
@@ -336,12 +396,20 @@ def compress_type_a(op, tess, k, p=10, method="tag", stream=None, distribution="
     stream = stream or RandomStream(0)
     _lib.require_device()
     cop = counting_wrapper(op)
-    times, plan = {}, None
+    times, plan = PhaseTimes(), None
     with _PhaseTimer(times, "I"), cop.ledger.phase("I"):
         if method == "tag":
-            plan = plan_tagging(tess, extra_cols, distribution, stream.child(1), optimize=optimize,
-                                max_redraws=max_tag_redraws)
-            bases, _ = tagging_bases(cop, tess, k, p, plan, stream.child(0), extra_samples=extra_samples)
+            if optimize:
+                raise NotImplementedError("null-vector optimisation (ref/tagging.py:142-292) is outside the "
+                                          "B200 hot path")
+            # the sketch of the policy's first draw runs while the host evaluates the plan
+            first = make_tagging_matrix(tess.b, tess.dim, extra_cols, distribution, stream.child(1).child(0))
+            bases, bundle = tagging_bases(
+                cop, tess, k, p,
+                lambda: plan_tagging(tess, extra_cols, distribution, stream.child(1), max_redraws=max_tag_redraws,
+                                     first=first),
+                stream.child(0), extra_samples=extra_samples, first=first)
+            plan = bundle.plan
         elif method == "bn":
             bases, _ = block_nullification_bases(cop, tess, k, p, stream.child(0))
         elif method == "naive":
@@ -381,15 +449,21 @@ def compress_type_b(op, tess, k, p=10, method="bn", stream=None, distribution="g
         raise ValueError("type B supports methods 'bn' and 'tag'")
     _lib.require_device()
     cop = counting_wrapper(op)
-    times, plan = {}, None
+    times, plan = PhaseTimes(), None
     with _PhaseTimer(times, "I"), cop.ledger.phase("I"):
         if method == "bn":
             bases, bundle = block_nullification_bases(cop, tess, k, p, stream.child(0))
         else:
-            plan = plan_tagging(tess, 0, distribution, stream.child(1), optimize=optimize,
-                                max_redraws=max_tag_redraws, extra_check=lambda T: b2_denominators_ok(T, tess))
-            bases, bundle = tagging_bases(cop, tess, k, p, plan, stream.child(0),
-                                          group_cols=tess.max_block_size + p)
+            if optimize:
+                raise NotImplementedError("null-vector optimisation (ref/tagging.py:142-292) is outside the "
+                                          "B200 hot path")
+            first = make_tagging_matrix(tess.b, tess.dim, 0, distribution, stream.child(1).child(0))
+            bases, bundle = tagging_bases(
+                cop, tess, k, p,
+                lambda: plan_tagging(tess, 0, distribution, stream.child(1), max_redraws=max_tag_redraws,
+                                     extra_check=lambda T: b2_denominators_ok(T, tess), first=first),
+                stream.child(0), group_cols=tess.max_block_size + p, first=first)
+            plan = bundle.plan
     with _PhaseTimer(times, "III"), cop.ledger.phase("III"):
         if method == "bn":
             B = gaussian_pinv_discrepancy(bundle, bases)

@@ -105,3 +105,33 @@ def philox_keys(seed: int, keys) -> np.ndarray:
             res = k64[:, 0::2] | (k64[:, 1::2] << np.uint64(32))
             out[idxs] = res
     return out
+
+
+def _word_list(values) -> list:
+    out = []
+    for v in values:
+        out.extend(_words(int(v)))
+    return out
+
+
+def philox_keys_suffixed(seed: int, prefix, suffix) -> np.ndarray:
+    """(n, 2) uint64 Philox keys of RandomStream(seed, prefix + tuple(suffix[s]))
+    through the C-ABI host function (the per-compression key derivation of the
+    product path; philox_keys above is the numpy restatement it is checked
+    against). suffix: (n, ns) array of components < 2**32."""
+    from . import _lib
+
+    suffix = np.ascontiguousarray(suffix, dtype=np.int64)
+    if suffix.ndim != 2:
+        raise ValueError("suffix must be (n, ns)")
+    if suffix.size and (suffix.min() < 0 or suffix.max() >= 2 ** 32):
+        raise ValueError("suffix components must be uint32 words")
+    run = np.array(_words(int(seed)), dtype=np.uint32)
+    pre = np.array(_word_list(prefix), dtype=np.uint32)
+    suf = suffix.astype(np.uint32)
+    n = suf.shape[0]
+    out = np.zeros((n, 2), dtype=np.uint64)
+    _lib.check(_lib.load().ublr_seedseq_keys(run.ctypes.data, len(run), pre.ctypes.data if len(pre) else None,
+                                             len(pre), suf.ctypes.data if suf.size else None, suf.shape[1], n,
+                                             out.ctypes.data), "ublr_seedseq_keys")
+    return out

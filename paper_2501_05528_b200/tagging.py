@@ -13,6 +13,7 @@ phase I at b = 4096).
 from __future__ import annotations
 
 import warnings
+from collections.abc import Sequence
 from dataclasses import dataclass
 
 import numpy as np
@@ -55,6 +56,22 @@ class ProjectedTags:
     values: np.ndarray
 
 
+class NullVectors(Sequence):
+    """The per-block NullVector records of a plan, materialised on access
+    (the plan keeps the stacked (b, ell) array)."""
+
+    def __init__(self, Z, res):
+        self.Z, self.res = Z, res
+
+    def __len__(self):
+        return self.Z.shape[0]
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[j] for j in range(*i.indices(len(self)))]
+        return NullVector(block=int(i), vector=self.Z[i], residual=float(self.res[i]))
+
+
 @dataclass
 class TaggingPlan:
     matrix: TaggingMatrix
@@ -66,6 +83,8 @@ class TaggingPlan:
     @property
     def Z(self) -> np.ndarray:
         """(b, ell) stacked null vectors."""
+        if isinstance(self.null_vectors, NullVectors):
+            return self.null_vectors.Z
         return np.stack([nv.vector for nv in self.null_vectors])
 
 
@@ -94,12 +113,54 @@ def make_tagging_matrix(b, d, extra_cols=0, distribution="gaussian", stream=None
     return TaggingMatrix(entries, d, extra_cols, distribution, stream.seed)
 
 
-def batched_null_vectors(T: np.ndarray, rows_list: list, rtol: float = 1e-12):
+def _csr(rows_list):
+    ptr = np.zeros(len(rows_list) + 1, dtype=np.int32)
+    ptr[1:] = np.cumsum([len(r) for r in rows_list])
+    idx = np.concatenate([np.asarray(r, dtype=np.int32) for r in rows_list]) if rows_list else np.zeros(0, np.int32)
+    return ptr, np.ascontiguousarray(idx, dtype=np.int32)
+
+
+def _neighbour_csr(tess):
+    """CSR of the neighbour lists, cached on the tessellation."""
+    c = tess._device.get("nbr_csr")
+    if c is None:
+        c = _csr(tess.neighbor_lists)
+        tess._device["nbr_csr"] = c
+    return c
+
+
+def batched_null_vectors(T: np.ndarray, rows_list: list, rtol: float = 1e-12, csr=None):
     """Last column of the complete QR of T[rows]^T for every row set
-    (== null_basis(T[rows], 1)[:, 0], ref/linalg.py:72-94), grouped by size.
+    (== null_basis(T[rows], 1)[:, 0], ref/linalg.py:72-94), by the C-ABI host
+    function ublr_null_vectors (Householder in LAPACK's convention; equal to
+    numpy's qr(mode="complete") up to rounding, checked in tests/test_host.py).
 
     Returns (Z (n_sets, ell), residual ||T[rows] z|| (n_sets,), ok mask where
     the reference's residual test passes)."""
+    from . import _lib
+
+    T = np.ascontiguousarray(T, dtype=np.float64)
+    ell = T.shape[1]
+    ptr, idx = csr if csr is not None else _csr(rows_list)
+    n = len(ptr) - 1
+    if n and int(np.diff(ptr).max()) >= ell:
+        raise DegenerateTagsError("requested null space of dimension 1 does not exist")
+    Z = np.zeros((n, ell))
+    res = np.zeros(n)
+    _lib.check(_lib.load().ublr_null_vectors(T.ctypes.data, ell, ptr.ctypes.data, idx.ctypes.data, n,
+                                             Z.ctypes.data, res.ctypes.data), "ublr_null_vectors")
+    # ||T[rows]||_F per set (the reference's residual scale)
+    rn2 = np.einsum("ij,ij->i", T, T)
+    seg = np.add.reduceat(rn2[idx], ptr[:-1]) if idx.size else np.zeros(n)
+    seg[np.diff(ptr) == 0] = 0.0
+    scale = np.maximum(1.0, np.sqrt(seg))
+    ok = res <= rtol * scale
+    return Z, res, ok
+
+
+def batched_null_vectors_numpy(T: np.ndarray, rows_list: list, rtol: float = 1e-12):
+    """numpy form of batched_null_vectors (the reference's own QR); kept as
+    the cross-check for the C-ABI version."""
     ell = T.shape[1]
     n = len(rows_list)
     Z = np.zeros((n, ell))
@@ -153,7 +214,7 @@ def aspect_ratio(pt: ProjectedTags, tess: Tessellation, i: int | None = None) ->
 def _evaluate(T: TaggingMatrix, tess: Tessellation, attempts: int) -> TaggingPlan:
     """ref/tagging.py:355-379 for optimize=False, batched."""
     E = T.entries
-    Z, res, ok = batched_null_vectors(E, tess.neighbor_lists)
+    Z, res, ok = batched_null_vectors(E, tess.neighbor_lists, csr=_neighbour_csr(tess))
     if not ok.all():
         i = int(np.flatnonzero(~ok)[0])
         raise DegenerateTagsError(f"block {i}: requested null space does not exist")
@@ -162,9 +223,10 @@ def _evaluate(T: TaggingMatrix, tess: Tessellation, attempts: int) -> TaggingPla
         i = int(np.flatnonzero(res > limit)[0])
         raise DegenerateTagsError(f"block {i}: null-vector residual {res[i]:.3e} exceeds {limit:.3e}")
     b = tess.b
+    ptr, idx = _neighbour_csr(tess)
     P = np.abs(E @ Z.T)                     # P[j, i] = |<t_j, z^(i)>|
-    nl = np.array([len(nb) for nb in tess.neighbor_lists])
-    rows_near = np.concatenate([np.asarray(nb, dtype=np.int64) for nb in tess.neighbor_lists])
+    nl = np.diff(ptr)
+    rows_near = idx
     cols_near = np.repeat(np.arange(b), nl)
     far_any = nl < b
     P[rows_near, cols_near] = np.inf        # exclude the near field from the min ...
@@ -175,19 +237,24 @@ def _evaluate(T: TaggingMatrix, tess: Tessellation, attempts: int) -> TaggingPla
     with np.errstate(divide="ignore", invalid="ignore"):
         r = np.where(hi == 0.0, 1.0, np.where(lo == 0.0, np.inf, hi / lo))
     rho[far_any] = r[far_any]
-    nvs = [NullVector(block=i, vector=Z[i], residual=float(res[i])) for i in range(b)]
+    nvs = NullVectors(Z, res)
     return TaggingPlan(matrix=T, null_vectors=nvs, rho_base=rho, rho_optimized=None, attempts=attempts)
 
 
 def plan_tagging(tess, extra_cols=0, distribution="gaussian", stream=None, optimize=False,
-                 max_redraws=5, ratio_limit=1e6, extra_check=None) -> TaggingPlan:
-    """Redraw policy of ref/tagging.py:306-352."""
+                 max_redraws=5, ratio_limit=1e6, extra_check=None, first=None) -> TaggingPlan:
+    """Redraw policy of ref/tagging.py:306-352. `first` may carry the policy's
+    first draw (make_tagging_matrix(..., stream.child(0))) when the caller has
+    already made it."""
     if optimize:
         raise NotImplementedError("null-vector optimisation (ref/tagging.py:142-292) is outside the B200 hot path")
     stream = stream or RandomStream(0)
     last, plan = None, None
     for attempt in range(max_redraws + 1):
-        T = make_tagging_matrix(tess.b, tess.dim, extra_cols, distribution, stream.child(attempt))
+        if attempt == 0 and first is not None:
+            T = first
+        else:
+            T = make_tagging_matrix(tess.b, tess.dim, extra_cols, distribution, stream.child(attempt))
         if extra_check is not None and not extra_check(T):
             last = DegenerateTagsError("extra_check rejected the draw")
             continue
