@@ -186,6 +186,21 @@ int ublr_potrf_diag(double* A, int64_t lda, int64_t sA, int j0, int nb, double* 
  * rule): writes L11\U11 into LU, L11^-1 / U11^-1 (batch x nb x nb) and D. */
 int ublr_lu_sign_diag(double* W, int64_t ldw, int64_t sW, int j0, int nb, double* LU, int64_t ldlu, int64_t sLU,
                       double* Linv, double* Uinv, double* D, int64_t sD, int* status, int batch, void* stream);
+/* R-scaled variant for the block-nullification null space:
+ * the factored matrix is D R - B1^T = (D - Q_top) R with R upper triangular
+ * (n x n, batch stride sR). Row j of D R is added when j becomes the pivot
+ * row, and after the panel the rows' D R12 (columns j0+nb .. n) are added to
+ * W12 so that U12 = L11^-1 W12 follows. L is the L of (D - Q_top); U = U' R^-1.
+ * With R == NULL this is ublr_lu_sign_diag. */
+int ublr_lu_sign_diag_r(double* W, int64_t ldw, int64_t sW, int j0, int nb, double* LU, int64_t ldlu, int64_t sLU,
+                        double* Linv, double* Uinv, double* D, int64_t sD, int* status, const double* R, int64_t ldr,
+                        int64_t sR, int n, int batch, void* stream);
+/* C_b = alpha A_b^T A_b + beta C_b on the tiles that touch the upper triangle
+ * (A_b: K x M row-major; the strictly-lower tiles of C are left untouched,
+ * tiles crossing the diagonal are written whole). Symmetric rank-k update of
+ * the blocked Cholesky. */
+int ublr_syrk_upper_batched(int M, int K, double alpha, const double* A, int64_t lda, int64_t sA, double beta,
+                            double* C, int64_t ldc, int64_t sC, int batch, void* stream);
 /* out_b[r][c] (or [c][r] with transpose) = src_b[map_b[r] * ld + col0 + c]. */
 int ublr_gather(const double* src, int64_t ld, int64_t s_src, const int32_t* map, int64_t s_map, int rows, int cols,
                 int col0, int transpose, double* out, int64_t ldo, int64_t s_out, int batch, void* stream);

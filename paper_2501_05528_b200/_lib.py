@@ -57,6 +57,8 @@ SIGNATURES = {
                                 C.c_double, P, I64, I64, P, I64, INT, P]),
     "ublr_potrf_diag": (INT, [P, I64, I64, INT, INT, P, I64, I64, P, P, INT, P]),
     "ublr_lu_sign_diag": (INT, [P, I64, I64, INT, INT, P, I64, I64, P, P, P, I64, P, INT, P]),
+    "ublr_lu_sign_diag_r": (INT, [P, I64, I64, INT, INT, P, I64, I64, P, P, P, I64, P, P, I64, I64, INT, INT, P]),
+    "ublr_syrk_upper_batched": (INT, [INT, INT, C.c_double, P, I64, I64, C.c_double, P, I64, I64, INT, P]),
     "ublr_gather": (INT, [P, I64, I64, P, I64, INT, INT, INT, INT, P, I64, I64, INT, P]),
     "ublr_scale_rows": (INT, [P, I64, I64, P, I64, INT, INT, INT, P]),
     "ublr_assemble_gram": (INT, [P, P, INT, INT, P, INT, P]),
@@ -107,7 +109,7 @@ def check(rc: int, what: str = ""):
 LAUNCHES = {"ublr_rng_normals": 7, "ublr_sketch_tagged": 1, "ublr_sketch_tagged_pair": 1, "ublr_apply": 1,
             "ublr_block_qr": 1, "ublr_coupling": 1, "ublr_nearfield_colour": 2,
             "ublr_blr_apply": 3, "ublr_gemm_batched": 1, "ublr_potrf_diag": 1, "ublr_lu_sign_diag": 1,
-            "ublr_gather": 1, "ublr_scale_rows": 1, "ublr_tag_combine_pairs": 1, "ublr_assemble_tagged": 1}
+            "ublr_lu_sign_diag_r": 1, "ublr_syrk_upper_batched": 1, "ublr_gather": 1, "ublr_scale_rows": 1, "ublr_tag_combine_pairs": 1, "ublr_assemble_tagged": 1}
 launch_count = 0
 _events = None  # name -> list of (start, end) CUDA events when instrumentation is on
 
@@ -158,6 +160,8 @@ def _work_of(name, args):
             return 2.0 * (r1 - r0) * n * cols + 2.0 * (r1 - r0) * b * cols * ell
         if name == "ublr_gemm_batched":
             return 2.0 * int(args[2]) * int(args[3]) * int(args[4]) * int(args[22])
+        if name == "ublr_syrk_upper_batched":
+            return 1.0 * int(args[0]) * (int(args[0]) + 1) * int(args[1]) * int(args[10])
         if name == "ublr_coupling":
             n, b, k, m = args[0].n, int(args[3]), int(args[4]), int(args[11])
             rows = (int(args[13]) - int(args[12])) * m

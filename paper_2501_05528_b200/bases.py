@@ -253,10 +253,11 @@ def nullspace_samples(dt, Om, ld_om, col_om, Ysrc, ld_y, s, r, k, S_out, chunk_b
     null-space columns that null_basis(Omega[nbr(i)], r) returns
     (ref/bases.py:102-110, ref/linalg.py:72-94), without a Householder QR:
 
-      G = B B^T = R^T R (blocked Cholesky), Qt_top = B[:, :n]^T R^-1,
-      LU of D - Qt_top with D_jj = sign(pivot) (Householder reconstruction:
-      reproduces LAPACK's dlarfg reflectors, tau in [1, 2]),
-      M = L^-T U^-T Qt_E^T,  P_k = [M - Qt_top D M ; E_bot - B[:, n:]^T R^-1 D M]
+      G = B B^T = R^T R (blocked Cholesky),
+      LU of (D - Qt_top) R = D R - B[:, :n]^T with D_jj = sign(pivot)
+      (Householder reconstruction: reproduces LAPACK's dlarfg reflectors,
+      tau in [1, 2]; Qt = B^T R^-1 is never formed),
+      M = L^-T U'^-T B[:, E],  P_k = [M ; E_bot] - B^T R^-1 D M
 
     where B = Omega[nbr(i)] (n x s), Qt = B^T R^-1 and E selects columns
     s-r .. s-r+k-1 (DESIGN.md §bn null space). Blocks with equal
@@ -292,7 +293,7 @@ def nullspace_samples(dt, Om, ld_om, col_om, Ysrc, ld_y, s, r, k, S_out, chunk_b
         if s - r < n:
             raise ValueError("block-nullification width too small for a neighbourhood")
         members = np.flatnonzero((nbr_n == n) & (sizes == m))
-        per_block = 5 * n * n * 8 + (s + 3 * n) * k * 8
+        per_block = 3 * n * n * 8 + (s + 3 * n) * k * 8
         ch = max(1, min(len(members), int(chunk_bytes // per_block), 65535))
         eb = np.zeros((s - n, k))
         eb[np.arange(s - r - n, s - r - n + k), np.arange(k)] = 1.0
@@ -308,7 +309,6 @@ def nullspace_samples(dt, Om, ld_om, col_om, Ysrc, ld_y, s, r, k, S_out, chunk_b
             f64 = dict(dtype=torch.float64, device=dev)
             G = torch.empty((nb_, n, n), **f64)
             R = torch.zeros((nb_, n, n), **f64)
-            Qt = torch.empty((nb_, n, n), **f64)
             LU = torch.zeros((nb_, n, n), **f64)
             Dg = torch.zeros((nb_, n), **f64)
             nn = n * n
@@ -331,33 +331,29 @@ def nullspace_samples(dt, Om, ld_om, col_om, Ysrc, ld_y, s, r, k, S_out, chunk_b
                 D.gemm(0, 1, n, n, s, 1.0, om0, ld_om, 0, om0, ld_om, 0, 0.0, D.addr(G), n, nn, nb_,
                        amap=D.addr(amap), sAm=n, bmap=D.addr(amap), sBm=n)
             fC = D.cholesky_upper(G, R)
-            # Qt_top = B[:, :n]^T R^-1
-            _lib.call("ublr_gather", om0, ld_om, 0, D.addr(amap), n, n, n, 0, 1, D.addr(Qt), n, nn, nb_,
+            # LU of D R - B1^T = (D - Q_top) R  (B1 = B[:, :n]; G is free again)
+            W = G
+            _lib.call("ublr_gather", om0, ld_om, 0, D.addr(amap), n, n, n, 0, 1, D.addr(W), n, nn, nb_,
                       _lib.stream_handle())
-            tmp = torch.empty((nb_, n, D.NB), **f64)
-            D.trsm_right_upper(Qt, R, fC, tmp)
-            Qtop = Qt.clone()
             neg = torch.full((n,), -1.0, **f64)
-            _lib.call("ublr_scale_rows", D.addr(Qt), n, nn, D.addr(neg), 0, n, n, nb_, _lib.stream_handle())
-            fL = D.lu_sign(Qt, LU, Dg)          # LU of D - Qt_top
-            # M = L^-T U^-T R^-T B[:, E]
+            _lib.call("ublr_scale_rows", D.addr(W), n, nn, D.addr(neg), 0, n, n, nb_, _lib.stream_handle())
+            fL = D.lu_sign(W, LU, Dg, R=R)
+            # M = L^-T U^-T R^-T B[:, E] = L^-T U'^-T B[:, E]   (U' = U R)
             Mm = torch.empty((nb_, n, k), **f64)
             _lib.call("ublr_gather", om0, ld_om, 0, D.addr(amap), n, n, k, s - r, 0, D.addr(Mm), k, n * k, nb_,
                       _lib.stream_handle())
             tk = torch.empty((nb_, D.NB, k), **f64)
-            D.trsm_left(R, Mm, fC, fC.inv, upper=True, trans=True, tmp=tk)
             D.trsm_left(LU, Mm, fL, fL.inv2, upper=True, trans=True, tmp=tk)
             D.trsm_left(LU, Mm, fL, fL.inv, upper=False, trans=True, tmp=tk)
-            # P = [M - Qt_top (D M) ; E_bot - B[:, n:]^T R^-1 (D M)]
+            # P = [M ; E_bot] - B^T R^-1 (D M)
             P = torch.empty((nb_, s, k), **f64)
             P[:, :n].copy_(Mm)
             P[:, n:].copy_(Ebot)
             DM = Mm
             _lib.call("ublr_scale_rows", D.addr(DM), k, n * k, D.addr(Dg), n, n, k, nb_, _lib.stream_handle())
-            D.gemm(0, 0, n, k, n, -1.0, D.addr(Qtop), n, nn, D.addr(DM), k, n * k, 1.0, D.addr(P), k, s * k, nb_)
             D.trsm_left(R, DM, fC, fC.inv, upper=True, trans=False, tmp=tk)
-            D.gemm(1, 0, s - n, k, n, -1.0, om0 + 8 * n, ld_om, 0, D.addr(DM), k, n * k, 1.0, D.addr(P, n * k), k,
-                   s * k, nb_, amap=D.addr(amap), sAm=n)
+            D.gemm(1, 0, s, k, n, -1.0, om0, ld_om, 0, D.addr(DM), k, n * k, 1.0, D.addr(P), k, s * k, nb_,
+                   amap=D.addr(amap), sAm=n)
             # S_i = Y_i P  (rows of block i scattered into S_out)
             D.gemm(0, 0, m, k, s, 1.0, D.addr(Ysrc), ld_y, 0, D.addr(P), k, s * k, 0.0, D.addr(S_out), k, 0, nb_,
                    amap=D.addr(rmap), sAm=m, cmap=D.addr(rmap), sCm=m)

@@ -28,9 +28,12 @@ __global__ void __launch_bounds__(Cfg::NT) k_gemm2(int M, int N, int K, double a
                                                    int64_t sAm, const double* __restrict__ B, int64_t ldb, int64_t sB,
                                                    const int32_t* __restrict__ bmap, int64_t sBm, double beta,
                                                    double* __restrict__ C, int64_t ldc, int64_t sC,
-                                                   const int32_t* __restrict__ cmap, int64_t sCm, int vecA, int vecB) {
+                                                   const int32_t* __restrict__ cmap, int64_t sCm, int vecA, int vecB,
+                                                   int upper_only) {
   static_assert(Cfg::A_KM == TA && Cfg::B_KM == !TB, "tile orientation must follow the operand storage");
   extern __shared__ double dsm[];
+  // symmetric rank-k updates only need the tiles that touch the upper triangle
+  if (upper_only && (int)(blockIdx.x + 1) * Cfg::BN <= (int)blockIdx.y * Cfg::BM) return;
   const int bz = blockIdx.z;
   A += bz * sA;
   B += bz * sB;
@@ -97,7 +100,7 @@ template <int BM, int BN, int WMW, int WNW, int STAGES>
 int launch_gemm2(int ta, int tb, int M, int N, int K, double alpha, const double* A, int64_t lda, int64_t sA,
                  const int32_t* amap, int64_t sAm, const double* B, int64_t ldb, int64_t sB, const int32_t* bmap,
                  int64_t sBm, double beta, double* C, int64_t ldc, int64_t sC, const int32_t* cmap, int64_t sCm,
-                 int batch, cudaStream_t st) {
+                 int batch, cudaStream_t st, int upper_only = 0) {
   dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, batch);
   auto aligned = [](const void* p, int64_t ld, int64_t stride) {
     return (((uintptr_t)p) % 16 == 0) && (ld % 2 == 0) && (stride % 2 == 0);
@@ -110,7 +113,7 @@ int launch_gemm2(int ta, int tb, int M, int N, int K, double alpha, const double
     size_t sm = Cfg::smem_bytes();                                                                            \
     UBLR_CUDA(cudaFuncSetAttribute(k_gemm2<Cfg, TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
     k_gemm2<Cfg, TA, TB><<<grid, Cfg::NT, sm, st>>>(M, N, K, alpha, A, lda, sA, amap, sAm, B, ldb, sB, bmap, sBm,  \
-                                                    beta, C, ldc, sC, cmap, sCm, vecA, vecB);                 \
+                                                    beta, C, ldc, sC, cmap, sCm, vecA, vecB, upper_only);     \
   }
   if (!ta && !tb) UBLR_G2(false, false)
   else if (!ta && tb) UBLR_G2(false, true)
@@ -194,7 +197,8 @@ __global__ void __launch_bounds__(FT) k_potrf_diag(double* A, int64_t lda, int64
 
 __global__ void __launch_bounds__(FT) k_lu_sign_diag(double* W, int64_t ldw, int64_t sW, int j0, int nb,
                                                      double* LU, int64_t ldlu, int64_t sLU, double* Linv,
-                                                     double* Uinv, double* D, int64_t sD, int* status) {
+                                                     double* Uinv, double* D, int64_t sD, int* status,
+                                                     const double* __restrict__ R, int64_t ldr, int64_t sR, int n) {
   extern __shared__ double sm[];
   double* S = sm;
   double* I = sm + nb * (nb + 1);
@@ -203,14 +207,31 @@ __global__ void __launch_bounds__(FT) k_lu_sign_diag(double* W, int64_t ldw, int
   double* Wb = W + bz * sW + (int64_t)j0 * ldw + j0;
   for (int e = threadIdx.x; e < nb * nb; e += FT) S[(e / nb) * ld + e % nb] = Wb[(int64_t)(e / nb) * ldw + e % nb];
   __syncthreads();
+  const double* Rb = R ? R + bz * sR + (int64_t)j0 * ldr + j0 : nullptr;
+  __shared__ double dsh;
   for (int j = 0; j < nb; ++j) {
-    if (threadIdx.x == 0) {
-      // working matrix W = -Q (eliminated so far); D_jj = -sign(q_jj) = sign(w_jj)
-      // makes the pivot w + D_jj of magnitude |w| + 1
-      double w = S[j * ld + j];
-      double d = (w > 0.0) ? 1.0 : -1.0;
-      S[j * ld + j] = w + d;
-      D[bz * sD + j0 + j] = d;
+    if (!Rb) {
+      if (threadIdx.x == 0) {
+        // working matrix W = -Q (eliminated so far); D_jj = -sign(q_jj) = sign(w_jj)
+        // makes the pivot w + D_jj of magnitude |w| + 1
+        double w = S[j * ld + j];
+        double d = (w > 0.0) ? 1.0 : -1.0;
+        S[j * ld + j] = w + d;
+        D[bz * sD + j0 + j] = d;
+      }
+    } else {
+      // R-scaled form: the matrix is D R - B1^T = (D - Q_top) R; row j of D R
+      // enters when j becomes the pivot row (earlier multipliers never read it,
+      // R being upper triangular). Same sign rule: sign(w'_jj) = sign(w_jj).
+      if (threadIdx.x == 0) {
+        double w = S[j * ld + j];
+        double d = (w > 0.0) ? 1.0 : -1.0;
+        dsh = d;
+        D[bz * sD + j0 + j] = d;
+      }
+      __syncthreads();
+      const double d = dsh;
+      for (int c = j + threadIdx.x; c < nb; c += FT) S[j * ld + c] = fma(d, Rb[(int64_t)j * ldr + c], S[j * ld + c]);
     }
     __syncthreads();
     double piv = S[j * ld + j];
@@ -225,6 +246,17 @@ __global__ void __launch_bounds__(FT) k_lu_sign_diag(double* W, int64_t ldw, int
   }
   double* LUb = LU + bz * sLU + (int64_t)j0 * ldlu + j0;
   for (int e = threadIdx.x; e < nb * nb; e += FT) LUb[(int64_t)(e / nb) * ldlu + e % nb] = S[(e / nb) * ld + e % nb];
+  if (Rb) {
+    // the panel rows' D R to the right of the block, before U12 = L11^-1 W12
+    const int rest = n - j0 - nb;
+    double* Wb2 = Wb + nb;
+    const double* Rb2 = Rb + nb;
+    for (int r = 0; r < nb; ++r) {
+      const double d = D[bz * sD + j0 + r];
+      for (int c = threadIdx.x; c < rest; c += FT)
+        Wb2[(int64_t)r * ldw + c] = fma(d, Rb2[(int64_t)r * ldr + c], Wb2[(int64_t)r * ldw + c]);
+    }
+  }
   tri_inv_unit_lower(S, ld, I, nb);
   __syncthreads();
   double* Lb = Linv + (int64_t)bz * nb * nb;
@@ -310,6 +342,20 @@ extern "C" int ublr_gemm_batched(int ta, int tb, int M, int N, int K, double alp
                                        ldc, sC, cmap, sCm, batch, st);
 }
 
+extern "C" int ublr_syrk_upper_batched(int M, int K, double alpha, const double* A, int64_t lda, int64_t sA,
+                                       double beta, double* C, int64_t ldc, int64_t sC, int batch, void* stream) {
+  UBLR_REQUIRE(M >= 0 && K >= 0 && batch >= 0 && A && C, UBLR_ERR_VALUE, "ublr_syrk_upper_batched: bad arguments");
+  UBLR_REQUIRE(batch <= 65535, UBLR_ERR_VALUE, "ublr_syrk_upper_batched: batch <= 65535");
+  if (M == 0 || batch == 0) return UBLR_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t tiles128 = (int64_t)((M + 127) / 128) * ((M + 127) / 128) * batch / 2;
+  if (M >= 96 && tiles128 >= 148)
+    return launch_gemm2<128, 128, 4, 4, 2>(1, 0, M, M, K, alpha, A, lda, sA, nullptr, 0, A, lda, sA, nullptr, 0, beta,
+                                           C, ldc, sC, nullptr, 0, batch, st, 1);
+  return launch_gemm2<64, 64, 2, 4, 2>(1, 0, M, M, K, alpha, A, lda, sA, nullptr, 0, A, lda, sA, nullptr, 0, beta, C,
+                                       ldc, sC, nullptr, 0, batch, st, 1);
+}
+
 extern "C" int ublr_potrf_diag(double* A, int64_t lda, int64_t sA, int j0, int nb, double* R, int64_t ldr,
                                int64_t sR, double* Rinv, int* status, int batch, void* stream) {
   UBLR_REQUIRE(A && R && Rinv && status && nb >= 1 && nb <= 96 && batch >= 1, UBLR_ERR_VALUE,
@@ -325,12 +371,21 @@ extern "C" int ublr_potrf_diag(double* A, int64_t lda, int64_t sA, int j0, int n
 extern "C" int ublr_lu_sign_diag(double* W, int64_t ldw, int64_t sW, int j0, int nb, double* LU, int64_t ldlu,
                                  int64_t sLU, double* Linv, double* Uinv, double* D, int64_t sD, int* status,
                                  int batch, void* stream) {
+  return ublr_lu_sign_diag_r(W, ldw, sW, j0, nb, LU, ldlu, sLU, Linv, Uinv, D, sD, status, nullptr, 0, 0, 0, batch,
+                             stream);
+}
+
+extern "C" int ublr_lu_sign_diag_r(double* W, int64_t ldw, int64_t sW, int j0, int nb, double* LU, int64_t ldlu,
+                                   int64_t sLU, double* Linv, double* Uinv, double* D, int64_t sD, int* status,
+                                   const double* R, int64_t ldr, int64_t sR, int n, int batch, void* stream) {
   UBLR_REQUIRE(W && LU && Linv && Uinv && D && status && nb >= 1 && nb <= 96 && batch >= 1, UBLR_ERR_VALUE,
                "ublr_lu_sign_diag: bad arguments");
+  UBLR_REQUIRE(!R || n >= j0 + nb, UBLR_ERR_VALUE, "ublr_lu_sign_diag_r: n < j0 + nb");
   size_t sm = (size_t)(nb * (nb + 1) + nb * nb) * sizeof(double);
   cudaStream_t st = (cudaStream_t)stream;
   UBLR_CUDA(cudaFuncSetAttribute(k_lu_sign_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  k_lu_sign_diag<<<batch, FT, sm, st>>>(W, ldw, sW, j0, nb, LU, ldlu, sLU, Linv, Uinv, D, sD, status);
+  k_lu_sign_diag<<<batch, FT, sm, st>>>(W, ldw, sW, j0, nb, LU, ldlu, sLU, Linv, Uinv, D, sD, status, R, ldr, sR,
+                                         n);
   UBLR_LAUNCH_CHECK();
   return UBLR_OK;
 }

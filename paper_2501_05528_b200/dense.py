@@ -20,6 +20,12 @@ def _torch():
     return torch
 
 
+def _dense(*ts):
+    for t in ts:
+        if t is not None and not t.is_contiguous():
+            raise ValueError("dense kernels take contiguous row-major (batch, rows, cols) tensors")
+
+
 def addr(t, offset_elems=0) -> int:
     return int(t.data_ptr()) + 8 * int(offset_elems)
 
@@ -48,6 +54,7 @@ def cholesky_upper(G, R, nb=NB):
     """G_b = R_b^T R_b (G overwritten as workspace, R zero-initialised by the
     caller). Returns Factors with R_jj^-1. Raises LinAlgError if not SPD."""
     torch = _torch()
+    _dense(G, R)
     batch, n, _ = G.shape
     f = Factors(n, nb, batch, G.device)
     status = torch.zeros(1, dtype=torch.int32, device=G.device)
@@ -60,26 +67,37 @@ def cholesky_upper(G, R, nb=NB):
             # R12 = R11^-T G12
             gemm(1, 0, jb, n2, jb, 1.0, addr(f.inv[bi]), jb, jb * jb, addr(G, j0 * n + j0 + jb), n, nn,
                  0.0, addr(R, j0 * n + j0 + jb), n, nn, batch)
-            # G22 -= R12^T R12
-            gemm(1, 0, n2, n2, jb, -1.0, addr(R, j0 * n + j0 + jb), n, nn, addr(R, j0 * n + j0 + jb), n, nn,
-                 1.0, addr(G, (j0 + jb) * n + j0 + jb), n, nn, batch)
+            # G22 -= R12^T R12 (upper-triangle tiles only: the panel steps read
+            # nothing below the diagonal)
+            _lib.call("ublr_syrk_upper_batched", n2, jb, -1.0, addr(R, j0 * n + j0 + jb), n, nn, 1.0,
+                      addr(G, (j0 + jb) * n + j0 + jb), n, nn, batch, _lib.stream_handle())
     f.status = status
     return f
 
 
-def lu_sign(W, LU, D, nb=NB):
+def lu_sign(W, LU, D, nb=NB, R=None):
     """No-pivot LU of W + diag(D) with D_jj = sign(w_jj) picked at pivot time
     (W overwritten). LU holds unit-L (strict lower) and U. Returns Factors
-    with L_jj^-1 (inv) and U_jj^-1 (inv2)."""
+    with L_jj^-1 (inv) and U_jj^-1 (inv2).
+
+    With an upper-triangular R (batch x n x n) the factored matrix is
+    W + diag(D) R instead (row j of D R joins when j becomes the pivot row):
+    for W = -B1^T and R the Cholesky factor of B B^T this is (D - Q_top) R,
+    whose L is the L of D - Q_top (bn null space)."""
     torch = _torch()
+    _dense(W, LU, D, R)
     batch, n, _ = W.shape
     f = Factors(n, nb, batch, W.device)
     f.inv2 = torch.zeros_like(f.inv)
     status = torch.zeros(1, dtype=torch.int32, device=W.device)
     nn = n * n
     for bi, (j0, jb) in enumerate(f.blocks):
-        _lib.call("ublr_lu_sign_diag", addr(W), n, nn, j0, jb, addr(LU), n, nn, addr(f.inv[bi]), addr(f.inv2[bi]),
-                  addr(D), n, addr(status), batch, _lib.stream_handle())
+        if R is None:
+            _lib.call("ublr_lu_sign_diag", addr(W), n, nn, j0, jb, addr(LU), n, nn, addr(f.inv[bi]),
+                      addr(f.inv2[bi]), addr(D), n, addr(status), batch, _lib.stream_handle())
+        else:
+            _lib.call("ublr_lu_sign_diag_r", addr(W), n, nn, j0, jb, addr(LU), n, nn, addr(f.inv[bi]),
+                      addr(f.inv2[bi]), addr(D), n, addr(status), addr(R), n, nn, n, batch, _lib.stream_handle())
         if j0 + jb < n:
             n2 = n - j0 - jb
             # U12 = L11^-1 W12

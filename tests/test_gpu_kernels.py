@@ -184,6 +184,45 @@ def test_lu_sign_reconstructs_householder():
     assert tau.min() >= 1.0 - 1e-12 and tau.max() <= 2.0 + 1e-12
 
 
+def test_lu_sign_r_scaled_matches_unscaled_l():
+    """LU of D R - B1^T (R = chol(B B^T)) has the L and signs of LU(D - Q_top)
+    with Q_top = B1^T R^-1, and U' = U R (the bn null-space shortcut)."""
+    rng = np.random.default_rng(5)
+    n, s, batch = 200, 230, 3
+    Bs = rng.standard_normal((batch, n, s))
+    Rh = np.ascontiguousarray(np.stack([np.linalg.cholesky(b @ b.T).T for b in Bs]))
+    B1T = np.ascontiguousarray(np.stack([b[:, :n].T for b in Bs]))
+    W = torch.from_numpy(-B1T).cuda()
+    R = torch.from_numpy(Rh).cuda()
+    LU = torch.zeros_like(W)
+    Dg = torch.zeros((batch, n), dtype=torch.float64, device="cuda")
+    f = Dn.lu_sign(W, LU, Dg, R=R)
+    Dn.check_status(f, "lu")
+    W0 = torch.from_numpy(-np.ascontiguousarray(np.stack([np.linalg.solve(Rh[b].T, B1T[b].T).T
+                                                          for b in range(batch)]))).cuda()
+    LU0 = torch.zeros_like(W0)
+    D0 = torch.zeros_like(Dg)
+    Dn.check_status(Dn.lu_sign(W0, LU0, D0), "lu")
+    assert torch.equal(Dg, D0)
+    for b in range(batch):
+        A, A0 = LU[b].cpu().numpy(), LU0[b].cpu().numpy()
+        assert np.abs(np.tril(A, -1) - np.tril(A0, -1)).max() <= 1e-10
+        assert np.abs(np.triu(A) - np.triu(A0) @ Rh[b]).max() <= 1e-10 * np.abs(np.triu(A)).max()
+
+
+def test_syrk_upper_matches_gemm_on_upper_triangle():
+    rng = np.random.default_rng(6)
+    for M, K in ((300, 64), (77, 13)):
+        A = torch.from_numpy(rng.standard_normal((2, K, M))).cuda()
+        C = torch.from_numpy(rng.standard_normal((2, M, M))).cuda()
+        ref = C.cpu().numpy() - np.einsum("bki,bkj->bij", A.cpu().numpy(), A.cpu().numpy())
+        _lib.call("ublr_syrk_upper_batched", M, K, -1.0, A.data_ptr(), M, K * M, 1.0, C.data_ptr(), M, M * M, 2,
+                  _lib.stream_handle())
+        iu = np.triu_indices(M)
+        got = C.cpu().numpy()
+        assert np.abs(got[:, iu[0], iu[1]] - ref[:, iu[0], iu[1]]).max() <= 1e-11
+
+
 def test_nullspace_samples_match_reference_null_basis():
     from paper_2501_05528_b200.bases import nullspace_samples
     pts = P.grid_points(32, 2)
