@@ -68,16 +68,39 @@ __global__ void __launch_bounds__(Cfg::NT) k_gemm2(int M, int N, int K, double a
       }
     }
   } bp{B, ldb, bmap, N, K, n0, vecB != 0};
-  double acc[Cfg::MI][Cfg::NJ][2];
-#pragma unroll
-  for (int i = 0; i < Cfg::MI; ++i)
-#pragma unroll
-    for (int j = 0; j < Cfg::NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  WholeStage<decltype(ap)> apw{ap};
-  dmma_mainloop<Cfg>(apw, bp, (K + Cfg::BK - 1) / Cfg::BK, dsm, acc);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int wr = warp / Cfg::WNW, wc = warp % Cfg::WNW;
+  // alpha = +-1 with beta != 0 (the trailing updates C -= A B): start the
+  // accumulators from alpha*beta*C, loaded before the main loop so the C read
+  // overlaps the operand prologue; the epilogue is then store-only.
+  const bool preload = beta != 0.0 && (alpha == 1.0 || alpha == -1.0);
+  const double ab = alpha * beta;
+  // 16-byte C accesses when every fragment pair is aligned
+  const bool cvec = ((((uintptr_t)C) | ((uintptr_t)(ldc * 8))) & 15) == 0;
+  double acc[Cfg::MI][Cfg::NJ][2];
+#pragma unroll
+  for (int i = 0; i < Cfg::MI; ++i) {
+    int r = m0 + wr * Cfg::WM + i * 8 + g;
+    const double* crow = C + (int64_t)(r < M ? (cmap ? cmap[r] : r) : 0) * ldc;
+#pragma unroll
+    for (int j = 0; j < Cfg::NJ; ++j) {
+      acc[i][j][0] = acc[i][j][1] = 0.0;
+      int c = n0 + wc * Cfg::WN + j * 8 + 2 * t;
+      if (preload && r < M) {
+        if (cvec && c + 1 < N) {
+          double2 v = *reinterpret_cast<const double2*>(crow + c);
+          acc[i][j][0] = ab * v.x;
+          acc[i][j][1] = ab * v.y;
+        } else {
+          if (c < N) acc[i][j][0] = ab * crow[c];
+          if (c + 1 < N) acc[i][j][1] = ab * crow[c + 1];
+        }
+      }
+    }
+  }
+  WholeStage<decltype(ap)> apw{ap};
+  dmma_mainloop<Cfg>(apw, bp, (K + Cfg::BK - 1) / Cfg::BK, dsm, acc);
 #pragma unroll
   for (int i = 0; i < Cfg::MI; ++i) {
     int r = m0 + wr * Cfg::WM + i * 8 + g;
@@ -85,12 +108,21 @@ __global__ void __launch_bounds__(Cfg::NT) k_gemm2(int M, int N, int K, double a
     double* crow = C + (int64_t)(cmap ? cmap[r] : r) * ldc;
 #pragma unroll
     for (int j = 0; j < Cfg::NJ; ++j) {
+      int c = n0 + wc * Cfg::WN + j * 8 + 2 * t;
+      if (preload) {
+        if (cvec && c + 1 < N) {
+          *reinterpret_cast<double2*>(crow + c) = make_double2(alpha * acc[i][j][0], alpha * acc[i][j][1]);
+        } else {
+          if (c < N) crow[c] = alpha * acc[i][j][0];
+          if (c + 1 < N) crow[c + 1] = alpha * acc[i][j][1];
+        }
+        continue;
+      }
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        int c = n0 + wc * Cfg::WN + j * 8 + 2 * t + h;
-        if (c >= N) continue;
+        if (c + h >= N) continue;
         double v = alpha * acc[i][j][h];
-        crow[c] = (beta == 0.0) ? v : fma(beta, crow[c], v);
+        crow[c + h] = (beta == 0.0) ? v : fma(beta, crow[c + h], v);
       }
     }
   }

@@ -575,6 +575,9 @@ __global__ void __launch_bounds__(Cfg::NT, 1) k_sketch_tagged3(ublr_op_t op, con
   const int ncols = (H ? 2 : 1) * gc;
   const int row0 = row_begin + blockIdx.x * Cfg::BM;
   const int col0 = blockIdx.y * Cfg::BN;
+  // a G | H straddling column tile splits into two 16-byte-aligned copies
+  // when both parts start on even columns (smem +4 padding keeps rows 16B aligned)
+  const bool split_vec = vec2 != 0 && (gc % 2) == 0 && ((gc - col0) % 2) == 0;
   // A producer (absolute columns q0.. masked by qend), interleavable
   __shared__ double ringbuf[9 * BK];
   struct AP {
@@ -607,6 +610,11 @@ __global__ void __launch_bounds__(Cfg::NT, 1) k_sketch_tagged3(ublr_op_t op, con
       tile_copy<Cfg::NT>(Bs, Cfg::SB, G, ldx, BK, Cfg::BN, q0, col0, qend, gc, IdentityRows{}, vec2 != 0);
     } else if (col0 >= gc) {
       tile_copy<Cfg::NT>(Bs, Cfg::SB, H, ldx, BK, Cfg::BN, q0, col0 - gc, qend, gc, IdentityRows{}, vec2 != 0);
+    } else if (split_vec) {
+      // the tile straddles G | H: two strided copies (16-byte cp.async)
+      tile_copy<Cfg::NT>(Bs, Cfg::SB, G, ldx, BK, gc - col0, q0, col0, qend, gc, IdentityRows{}, true);
+      tile_copy<Cfg::NT>(Bs + (gc - col0), Cfg::SB, H, ldx, BK, Cfg::BN - (gc - col0), q0, 0, qend, gc,
+                         IdentityRows{}, true);
     } else {
       for (int e = threadIdx.x; e < BK * Cfg::BN; e += Cfg::NT) {
         int kk = e / Cfg::BN, c = e - kk * Cfg::BN;

@@ -15,5 +15,5 @@ for _ in range(20):
 torch.cuda.synchronize()
 pr.disable()
 s = io.StringIO()
-pstats.Stats(pr, stream=s).sort_stats("cumulative").print_stats(35)
+pstats.Stats(pr, stream=s).sort_stats(sys.argv[2] if len(sys.argv) > 2 else "cumulative").print_stats(35)
 print(s.getvalue()[:6000])
