@@ -13,9 +13,12 @@
 // — the true near residual plus the same-colour far residuals of block row i
 // (SURVEY.md F11). Two kernels: S_p = sum_j' C_ij' V_j'^T (k x m, DMMA) per
 // pair, then B_p = sum_j' A_ij' - U_i S_p with A generated on the fly.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "optile.cuh"
 #include "gemm_core.cuh"
+#include "ws.cuh"
 
 namespace ublr {
 namespace {
@@ -275,6 +278,206 @@ __global__ void __launch_bounds__(Cfg::NT) k_coupling2(ublr_op_t op, const int32
   }
 }
 
+// ------------------------------------------------------------- coupling v3
+// Warp-specialised coupling for kernel operators with m <= 256, k <= 48
+// (configs 3-5). One CTA per (row block i, chunk of column blocks j):
+//   phase 1  T = U_i^T A_ij  (KP x 256): producer warps cp.async the k-slices
+//            of U_i and generate A_ij eight block-i rows at a time into a
+//            5-stage mbarrier ring; consumer warps (2 x 4, 24 x 64 tiles) run
+//            the DMMAs;
+//   phase 2  C_ij = T V_j   (KP x k_j): the A fragments come straight from the
+//            phase-1 accumulators by quad shuffles, V_j is staged in shared
+//            memory by the producers during phase 1; the four column-warp
+//            partials are summed in a fixed order (shared memory, aliasing
+//            V_j) and written to the core.
+// The producers run ahead into the next j while the consumers do phase 2.
+// Entries are generated as A(i_r, j_q) = k(x_jq - x_ir): the squared distance
+// is bitwise that of the row-major apply (negated differences).
+struct Cp3 {
+  static constexpr int BK = 8, STAGES = 5, KP = 48, NQ = 256;
+  static constexpr int NPROD = 256, NCONS = 256, NT = NPROD + NCONS;
+  static constexpr int SA = KP + 4, SB = NQ + 4, SV = KP + 4;
+  static constexpr int A_STAGE = BK * SA, B_STAGE = BK * SB;
+  static constexpr int WMW = 2, WNW = 4, WM = KP / WMW, WN = NQ / WNW, MI = WM / 8, NJ = WN / 8, NC = KP / 8;
+  static constexpr int CONS_REGS = 200, PROD_REGS = 56;
+  static constexpr size_t smem_bytes() {
+    return (size_t)(STAGES * (A_STAGE + B_STAGE) + NQ * SV + 3 * NQ) * sizeof(double);
+  }
+  static_assert(4 * KP * KP <= NQ * SV, "phase-2 partials alias the V_j buffer");
+};
+
+template <int KIND, int DIM>
+__global__ void __launch_bounds__(Cp3::NT, 1) k_coupling3(ublr_op_t op, const int32_t* __restrict__ off,
+                                                          const int32_t* __restrict__ roff,
+                                                          const double* __restrict__ U,
+                                                          const double* __restrict__ V, int64_t lduv,
+                                                          double* __restrict__ core, int64_t ldc, int i0, int b,
+                                                          int jchunk, int vec2) {
+  using C = Cp3;
+  constexpr int BK = C::BK, STAGES = C::STAGES, KP = C::KP, NQ = C::NQ, SA = C::SA, SB = C::SB, SV = C::SV;
+  constexpr int MI = C::MI, NJ = C::NJ, NC = C::NC;
+  __shared__ LogTables lt;
+  __shared__ uint64_t full[STAGES], empty[STAGES], vfull, vempty;
+  extern __shared__ double dsm[];
+  double* As0 = dsm;
+  double* Bs0 = dsm + STAGES * C::A_STAGE;
+  double* Vs = Bs0 + STAGES * C::B_STAGE;
+  double* xi = Vs + NQ * SV;  // coordinates of block i's points, [3][NQ]
+  const int i = i0 + blockIdx.x;
+  const int j0 = blockIdx.y * jchunk;
+  const int j1 = min(b, j0 + jchunk);
+  const int ri0 = off[i], mi = off[i + 1] - ri0;
+  const int ki = roff[i + 1] - roff[i];
+  const int nk = (mi + BK - 1) / BK;
+  const int n = (int)op.n;
+  if (KIND == UBLR_OP_LOG) init_log_tables(&lt);
+  for (int e = threadIdx.x; e < 3 * NQ; e += C::NT) {
+    const int a = e / NQ, r = e - a * NQ;
+    xi[e] = (r < mi && a < DIM) ? op.coords[(int64_t)a * n + ri0 + r] : 0.0;
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      ws::mbar_init(&full[s], 2 * C::NPROD);  // cp.async (U slice) + generator arrivals
+      ws::mbar_init(&empty[s], C::NCONS);
+    }
+    ws::mbar_init(&vfull, C::NPROD);
+    ws::mbar_init(&vempty, C::NCONS);
+  }
+  __syncthreads();
+
+  if (threadIdx.x < C::NPROD) {
+    // ---------------- producers: one column q of block j each
+    ws::regs_dec<C::PROD_REGS>();
+    const int q = threadIdx.x;
+    const double diag = op.diag;
+    int it = 0;
+    for (int j = j0; j < j1; ++j) {
+      const int jl = j - j0;
+      const int cj0 = off[j], mj = off[j + 1] - cj0, kj = roff[j + 1] - roff[j];
+      const bool qok = q < mj;
+      const RowPoint rp = load_row_point(op, qok ? cj0 + q : cj0, true);
+      for (int ks = 0; ks < nk; ++ks, ++it) {
+        const int s = it % STAGES;
+        ws::mbar_wait(&empty[s], ((uint32_t)(it / STAGES) & 1) ^ 1);
+        tile_copy<C::NPROD>(As0 + s * C::A_STAGE, SA, U, lduv, BK, KP, ks * BK, 0, mi, ki, OffsetRows{ri0},
+                            vec2 != 0);
+        cp_async_commit();
+        ws::mbar_cp_async_arrive(&full[s]);
+        double v[BK];
+#pragma unroll
+        for (int e = 0; e < BK; ++e) {
+          const int r = ks * BK + e;
+          const double a = kernel_entry_dim<KIND, DIM>(rp, ri0 + r, xi[r], DIM > 1 ? xi[NQ + r] : 0.0,
+                                                       DIM > 2 ? xi[2 * NQ + r] : 0.0, diag, &lt);
+          v[e] = (qok && r < mi) ? a : 0.0;
+        }
+        double* Bs = Bs0 + s * C::B_STAGE;
+#pragma unroll
+        for (int e = 0; e < BK; ++e) Bs[e * SB + q] = v[e];
+        ws::mbar_arrive(&full[s]);
+        if (ks == min(2, nk - 1)) {
+          // V_j for phase 2, once the consumers have released phase 2 of j - 1
+          ws::mbar_wait(&vempty, ((uint32_t)jl & 1) ^ 1);
+          tile_copy<C::NPROD>(Vs, SV, V, lduv, NQ, KP, 0, 0, mj, kj, OffsetRows{cj0}, vec2 != 0);
+          cp_async_commit();
+          ws::mbar_cp_async_arrive(&vfull);
+        }
+      }
+    }
+    cp_async_wait<0>();
+    return;
+  }
+
+  // ---------------- consumers
+  ws::regs_inc<C::CONS_REGS>();
+  const int ct = threadIdx.x - C::NPROD;
+  const int warp = ct >> 5, lane = ct & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wr = warp / C::WNW, wc = warp % C::WNW;
+  const int am0 = wr * C::WM + g, bn0 = wc * C::WN + g;
+  double acc[MI][NJ][2];
+#pragma unroll
+  for (int a = 0; a < MI; ++a)
+#pragma unroll
+    for (int c = 0; c < NJ; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
+  int it = 0;
+  for (int j = j0; j < j1; ++j) {
+    const int jl = j - j0;
+    for (int ks = 0; ks < nk; ++ks, ++it) {
+      const int s = it % STAGES;
+      ws::mbar_wait(&full[s], (uint32_t)(it / STAGES) & 1);
+      const double* As = As0 + s * C::A_STAGE;
+      const double* Bs = Bs0 + s * C::B_STAGE;
+#pragma unroll
+      for (int k4 = 0; k4 < BK / 4; ++k4) {
+        const int kr = k4 * 4 + t;
+        double av[MI], bv[NJ];
+#pragma unroll
+        for (int a = 0; a < MI; ++a) av[a] = As[kr * SA + am0 + a * 8];
+#pragma unroll
+        for (int c = 0; c < NJ; ++c) bv[c] = Bs[kr * SB + bn0 + c * 8];
+#pragma unroll
+        for (int a = 0; a < MI; ++a)
+#pragma unroll
+          for (int c = 0; c < NJ; ++c) mma8x8x4(acc[a][c][0], acc[a][c][1], av[a], bv[c]);
+      }
+      ws::mbar_arrive(&empty[s]);
+    }
+    // phase 2: partial C (rows of this warp) over this warp's 64 columns q
+    ws::mbar_wait(&vfull, (uint32_t)jl & 1);
+    double cp[MI][NC][2];
+#pragma unroll
+    for (int a = 0; a < MI; ++a)
+#pragma unroll
+      for (int c = 0; c < NC; ++c) cp[a][c][0] = cp[a][c][1] = 0.0;
+#pragma unroll
+    for (int c = 0; c < NJ; ++c) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int src = (g << 2) + 2 * h + (t >> 1);
+        double av[MI];
+#pragma unroll
+        for (int a = 0; a < MI; ++a) {
+          const double v0 = __shfl_sync(0xffffffffu, acc[a][c][0], src);
+          const double v1 = __shfl_sync(0xffffffffu, acc[a][c][1], src);
+          av[a] = (t & 1) ? v1 : v0;
+        }
+        const double* vrow = Vs + (wc * C::WN + c * 8 + 4 * h + t) * SV + g;
+#pragma unroll
+        for (int nn = 0; nn < NC; ++nn) {
+          const double bvv = vrow[nn * 8];
+#pragma unroll
+          for (int a = 0; a < MI; ++a) mma8x8x4(cp[a][nn][0], cp[a][nn][1], av[a], bvv);
+        }
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < MI; ++a)
+#pragma unroll
+      for (int c = 0; c < NJ; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
+    ws::named_sync(2, C::NCONS);  // every consumer is done reading V_j
+    double* red = Vs;             // [wc][KP][KP]
+#pragma unroll
+    for (int a = 0; a < MI; ++a)
+#pragma unroll
+      for (int nn = 0; nn < NC; ++nn) {
+        const int ra = wr * C::WM + a * 8 + g, cc = nn * 8 + 2 * t;
+        red[(wc * KP + ra) * KP + cc] = cp[a][nn][0];
+        red[(wc * KP + ra) * KP + cc + 1] = cp[a][nn][1];
+      }
+    ws::named_sync(2, C::NCONS);
+    const int kj = roff[j + 1] - roff[j];
+    double* crow = core + (int64_t)roff[i] * ldc + roff[j];
+    for (int e = ct; e < ki * kj; e += C::NCONS) {
+      const int a = e / kj, c = e - a * kj;
+      const int o = a * KP + c;
+      const double sum = ((red[o] + red[KP * KP + o]) + red[2 * KP * KP + o]) + red[3 * KP * KP + o];
+      crow[(int64_t)a * ldc + c] = sum;
+    }
+    ws::mbar_arrive(&vempty);
+  }
+}
+
 // ------------------------------------------------------- near field: S_p
 // S_p (k x m_max) = sum_{j' in colour(j)} C_{i j'} V_{j'}^T, columns q < m_j'.
 // One CTA per near pair; 8 warps split the m_max columns, each warp holds
@@ -455,9 +658,36 @@ extern "C" int ublr_coupling(const ublr_op_t* op, const int32_t* off, const int3
   UBLR_REQUIRE(b <= 65535, UBLR_ERR_VALUE, "ublr_coupling: b <= 65535");
   cudaStream_t st = (cudaStream_t)stream;
   UBLR_REQUIRE(0 <= i0 && i0 < i1 && i1 <= b, UBLR_ERR_VALUE, "ublr_coupling: bad block-row range");
-  dim3 grid(b, i1 - i0);
   int kk = k < m_max ? k : m_max;  // effective ranks never exceed min(k, m)
   int vec2 = ((ld_uv % 2) == 0 && ((uintptr_t)V) % 16 == 0) ? 1 : 0;
+  static const int cp_ver = [] {
+    const char* e = getenv("UBLR_COUPLING_VERSION");
+    return e ? atoi(e) : 3;
+  }();
+  if (cp_ver == 3 && op->kind != UBLR_OP_DENSE && m_max > 64 && m_max <= Cp3::NQ && kk <= Cp3::KP) {
+    // column-block chunks per CTA: enough CTAs for the 148 SMs, long runs per CTA
+    const int rows = i1 - i0;
+    int chunks = (148 * 4 + rows - 1) / rows;
+    if (chunks > b) chunks = b;
+    const int jchunk = (b + chunks - 1) / chunks;
+    dim3 g3((unsigned)rows, (unsigned)((b + jchunk - 1) / jchunk));
+    const int v2 = vec2 && ((uintptr_t)U) % 16 == 0;
+    size_t sm = Cp3::smem_bytes();
+#define UBLR_CP3(KIND, DIM)                                                                                     \
+  {                                                                                                             \
+    UBLR_CUDA(cudaFuncSetAttribute(k_coupling3<KIND, DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
+    k_coupling3<KIND, DIM><<<g3, Cp3::NT, sm, st>>>(*op, off, roff, U, V, ld_uv, core, ld_c, i0, b, jchunk, v2);  \
+  }
+    if (op->kind == UBLR_OP_LOG) {
+      if (op->dim == 1) UBLR_CP3(UBLR_OP_LOG, 1) else if (op->dim == 2) UBLR_CP3(UBLR_OP_LOG, 2) else UBLR_CP3(UBLR_OP_LOG, 3)
+    } else {
+      if (op->dim == 1) UBLR_CP3(UBLR_OP_INV, 1) else if (op->dim == 2) UBLR_CP3(UBLR_OP_INV, 2) else UBLR_CP3(UBLR_OP_INV, 3)
+    }
+#undef UBLR_CP3
+    UBLR_LAUNCH_CHECK();
+    return UBLR_OK;
+  }
+  dim3 grid(b, i1 - i0);
 #define UBLR_CP2(BM, BN)                                                                                     \
   UBLR_DISPATCH_KIND(op->kind, KIND, {                                                                      \
     using Cfg = TileCfg<BM, BN, 32, 8, 1, 2>;                                                               \

@@ -245,3 +245,34 @@ def test_nullspace_samples_match_reference_null_basis():
         want = Yh[tess.blocks[i]] @ Pk
         got = Sh[tess.blocks[i]]
         assert np.abs(got - want).max() <= 1e-11 * np.abs(want).max(), i
+
+
+@pytest.mark.parametrize("kind,k,per,nb", [("inv", 48, 64, 16), ("log", 40, 64, 16), ("log", 33, 50, 16)])
+def test_coupling_matches_numpy(kind, k, per, nb):
+    """C_ij = U_i^T A_ij V_j for every block pair (the m = 256 warp-specialised
+    coupling, and ragged 256-point blocks for per = 48)."""
+    from paper_2501_05528_b200.bases import BlockBases
+    from paper_2501_05528_b200.reconstruction import direct_core
+    pts = P.grid_points(per, 2)
+    tess = P.build_tessellation(pts, nb)
+    dt = device_tess(tess, torch.device(DEV))
+    diag = -np.log(0.5 / per) if kind == "log" else 2.0 * per
+    op = P.KernelOperator(pts, kind, diag)
+    rng = np.random.default_rng(17)
+    n = dt.n
+    Uh, Vh = rng.standard_normal((n, k)), rng.standard_normal((n, k))
+    bs = BlockBases(dt, torch.from_numpy(Uh).cuda(), torch.from_numpy(Vh).cuda(), k, "tag", (0, 0))
+    core = direct_core(op, tess, bs).cpu().numpy()
+    coords = pts.coords if hasattr(pts, "coords") else np.asarray(pts)
+    perm = dt.perm_h if hasattr(dt, "perm_h") else None
+    off = dt.off_h
+    roff = dt.roff(k)[0]
+    for i in range(dt.b):
+        for j in range(dt.b):
+            ri = perm[off[i]:off[i + 1]] if perm is not None else np.arange(off[i], off[i + 1])
+            cj = perm[off[j]:off[j + 1]] if perm is not None else np.arange(off[j], off[j + 1])
+            A = O.kernel_block(coords, ri, cj, kind, diag)
+            ki, kj = roff[i + 1] - roff[i], roff[j + 1] - roff[j]
+            ref = Uh[off[i]:off[i + 1], :ki].T @ A @ Vh[off[j]:off[j + 1], :kj]
+            got = core[roff[i]:roff[i + 1], roff[j]:roff[j + 1]]
+            assert np.abs(got - ref).max() <= 1e-11 * max(1.0, np.abs(ref).max()), (i, j)
