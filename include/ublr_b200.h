@@ -207,6 +207,10 @@ int ublr_gather(const double* src, int64_t ld, int64_t s_src, const int32_t* map
 /* Gram assembly from shared neighbour-pair products: block (a, b) of G_c is
  * P[pid] or P[-pid-1]^T, pid = map[c][a][b] (nb x nb blocks of m x m). */
 int ublr_assemble_gram(const double* P, const int32_t* map, int nb, int m, double* G, int batch, void* stream);
+/* W_b[r][c] += d_b[r] * R_b[r][c] on a rows x cols block (the D R12 rows of a
+ * sign-LU panel, when ublr_lu_sign_diag_r is called with n = j0 + nb). */
+int ublr_add_scaled_rows(double* W, int64_t ldw, int64_t s_w, const double* R, int64_t ldr, int64_t s_r,
+                         const double* d, int64_t s_d, int rows, int cols, int batch, void* stream);
 /* X_b[r][c] *= d_b[r]. */
 int ublr_scale_rows(double* X, int64_t ldx, int64_t s_x, const double* d, int64_t s_d, int rows, int cols,
                     int batch, void* stream);

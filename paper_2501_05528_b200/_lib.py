@@ -59,6 +59,7 @@ SIGNATURES = {
     "ublr_lu_sign_diag": (INT, [P, I64, I64, INT, INT, P, I64, I64, P, P, P, I64, P, INT, P]),
     "ublr_lu_sign_diag_r": (INT, [P, I64, I64, INT, INT, P, I64, I64, P, P, P, I64, P, P, I64, I64, INT, INT, P]),
     "ublr_syrk_upper_batched": (INT, [INT, INT, C.c_double, P, I64, I64, C.c_double, P, I64, I64, INT, P]),
+    "ublr_add_scaled_rows": (INT, [P, I64, I64, P, I64, I64, P, I64, INT, INT, INT, P]),
     "ublr_gather": (INT, [P, I64, I64, P, I64, INT, INT, INT, INT, P, I64, I64, INT, P]),
     "ublr_scale_rows": (INT, [P, I64, I64, P, I64, INT, INT, INT, P]),
     "ublr_assemble_gram": (INT, [P, P, INT, INT, P, INT, P]),
@@ -109,7 +110,8 @@ def check(rc: int, what: str = ""):
 LAUNCHES = {"ublr_rng_normals": 7, "ublr_sketch_tagged": 1, "ublr_sketch_tagged_pair": 1, "ublr_apply": 1,
             "ublr_block_qr": 1, "ublr_coupling": 1, "ublr_nearfield_colour": 2,
             "ublr_blr_apply": 3, "ublr_gemm_batched": 1, "ublr_potrf_diag": 1, "ublr_lu_sign_diag": 1,
-            "ublr_lu_sign_diag_r": 1, "ublr_syrk_upper_batched": 1, "ublr_gather": 1, "ublr_scale_rows": 1, "ublr_tag_combine_pairs": 1, "ublr_assemble_tagged": 1}
+            "ublr_lu_sign_diag_r": 1, "ublr_syrk_upper_batched": 1, "ublr_add_scaled_rows": 1,
+            "ublr_gather": 1, "ublr_scale_rows": 1, "ublr_tag_combine_pairs": 1, "ublr_assemble_tagged": 1}
 launch_count = 0
 _events = None  # name -> list of (start, end) CUDA events when instrumentation is on
 

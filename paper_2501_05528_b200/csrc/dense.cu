@@ -316,6 +316,19 @@ __global__ void k_gather(const double* __restrict__ src, int64_t ld, int64_t s_s
   }
 }
 
+// W[b][r][c] += d[b*s_d + r] * R[b][r][c] on a rows x cols sub-block
+__global__ void k_add_scaled_rows(double* __restrict__ W, int64_t ldw, int64_t s_w, const double* __restrict__ R,
+                                  int64_t ldr, int64_t s_r, const double* __restrict__ d, int64_t s_d, int rows,
+                                  int cols) {
+  const int bz = blockIdx.y;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)rows * cols;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e / cols), c = (int)(e % cols);
+    double* w = W + bz * s_w + (int64_t)r * ldw + c;
+    *w = fma(d[bz * s_d + r], R[bz * s_r + (int64_t)r * ldr + c], *w);
+  }
+}
+
 // X[b][r][c] *= d[b*s_d + r]
 __global__ void k_scale_rows(double* __restrict__ X, int64_t ldx, int64_t s_x, const double* __restrict__ d,
                              int64_t s_d, int rows, int cols) {
@@ -342,6 +355,18 @@ extern "C" int ublr_gather(const double* src, int64_t ld, int64_t s_src, const i
   dim3 grid((unsigned)((tot + 255) / 256 < 4096 ? (tot + 255) / 256 : 4096), batch);
   k_gather<<<grid, 256, 0, (cudaStream_t)stream>>>(src, ld, s_src, map, s_map, rows, cols, col0, transpose, out, ldo,
                                                    s_out);
+  UBLR_LAUNCH_CHECK();
+  return UBLR_OK;
+}
+
+extern "C" int ublr_add_scaled_rows(double* W, int64_t ldw, int64_t s_w, const double* R, int64_t ldr, int64_t s_r,
+                                    const double* d, int64_t s_d, int rows, int cols, int batch, void* stream) {
+  UBLR_REQUIRE(W && R && d && rows >= 0 && cols >= 0 && batch >= 0 && batch <= 65535, UBLR_ERR_VALUE,
+               "ublr_add_scaled_rows: bad arguments");
+  if (!rows || !cols || !batch) return UBLR_OK;
+  int64_t tot = (int64_t)rows * cols;
+  dim3 grid((unsigned)((tot + 255) / 256 < 1024 ? (tot + 255) / 256 : 1024), batch);
+  k_add_scaled_rows<<<grid, 256, 0, (cudaStream_t)stream>>>(W, ldw, s_w, R, ldr, s_r, d, s_d, rows, cols);
   UBLR_LAUNCH_CHECK();
   return UBLR_OK;
 }

@@ -575,9 +575,6 @@ __global__ void __launch_bounds__(Cfg::NT, 1) k_sketch_tagged3(ublr_op_t op, con
   const int ncols = (H ? 2 : 1) * gc;
   const int row0 = row_begin + blockIdx.x * Cfg::BM;
   const int col0 = blockIdx.y * Cfg::BN;
-  // a G | H straddling column tile splits into two 16-byte-aligned copies
-  // when both parts start on even columns (smem +4 padding keeps rows 16B aligned)
-  const bool split_vec = vec2 != 0 && (gc % 2) == 0 && ((gc - col0) % 2) == 0;
   // A producer (absolute columns q0.. masked by qend), interleavable
   __shared__ double ringbuf[9 * BK];
   struct AP {
@@ -605,16 +602,36 @@ __global__ void __launch_bounds__(Cfg::NT, 1) k_sketch_tagged3(ublr_op_t op, con
     }
   } ap{op, &lt, load_row_point(op, row0 + (int)(threadIdx.x % Cfg::BM), row0 + (int)(threadIdx.x % Cfg::BM) < row_end),
        (int)(threadIdx.x % Cfg::BM), (int)(threadIdx.x / Cfg::BM), 0, 0, 0, ColRing<BK>{ringbuf}};
+  // test-block panel stage: BK rows x BN columns of [G | H]. Each thread's
+  // 16-byte pair slots are fixed for the whole kernel, so their source
+  // pointers (minus the k-step row offset) are computed once here.
+  constexpr int HALF = Cfg::BN / 2;
+  constexpr int PPT = (BK * HALF + Cfg::NT - 1) / Cfg::NT;
+  const bool vec_pairs = vec2 != 0 && (gc % 2) == 0;
+  const double* bsrc[PPT];
+  int bmeta[PPT];  // smem offset | kk << 16 | (column valid) << 30
+#pragma unroll
+  for (int z = 0; z < PPT; ++z) {
+    const int e = threadIdx.x + z * Cfg::NT;
+    const int kk = e / HALF, c = 2 * (e % HALF);
+    const int col = col0 + c;
+    const bool valid = e < BK * HALF && col < ncols;
+    bsrc[z] = ((col < gc || !H) ? G + col : H + (col - gc)) + (int64_t)kk * ldx;
+    bmeta[z] = (kk * Cfg::SB + c) | (kk << 16) | (valid ? (1 << 30) : 0);
+  }
   auto b_stage = [&](double* Bs, int q0, int qend) {
-    if (col0 + Cfg::BN <= gc || !H) {
+    if (vec_pairs) {
+      const int64_t roff = (int64_t)q0 * ldx;
+#pragma unroll
+      for (int z = 0; z < PPT; ++z) {
+        const int meta = bmeta[z];
+        const bool ok = (meta >> 30) && q0 + ((meta >> 16) & 0x3fff) < qend;
+        cp_async16(Bs + (meta & 0xffff), ok ? (const void*)(bsrc[z] + roff) : (const void*)G, ok);
+      }
+    } else if (col0 + Cfg::BN <= gc || !H) {
       tile_copy<Cfg::NT>(Bs, Cfg::SB, G, ldx, BK, Cfg::BN, q0, col0, qend, gc, IdentityRows{}, vec2 != 0);
     } else if (col0 >= gc) {
       tile_copy<Cfg::NT>(Bs, Cfg::SB, H, ldx, BK, Cfg::BN, q0, col0 - gc, qend, gc, IdentityRows{}, vec2 != 0);
-    } else if (split_vec) {
-      // the tile straddles G | H: two strided copies (16-byte cp.async)
-      tile_copy<Cfg::NT>(Bs, Cfg::SB, G, ldx, BK, gc - col0, q0, col0, qend, gc, IdentityRows{}, true);
-      tile_copy<Cfg::NT>(Bs + (gc - col0), Cfg::SB, H, ldx, BK, Cfg::BN - (gc - col0), q0, 0, qend, gc,
-                         IdentityRows{}, true);
     } else {
       for (int e = threadIdx.x; e < BK * Cfg::BN; e += Cfg::NT) {
         int kk = e / Cfg::BN, c = e - kk * Cfg::BN;

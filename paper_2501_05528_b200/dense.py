@@ -50,27 +50,71 @@ class Factors:
         self.inv2 = None  # second set (U^-1 for LU)
 
 
+def _split(w, nb):
+    """Left part of a recursive split of w columns, on an nb boundary."""
+    nblk = -(-w // nb)
+    return nb * ((nblk + 1) // 2)
+
+
+def _syrk_upper(M, K, alpha, A, lda, sA, beta, C, ldc, sC, batch):
+    _lib.call("ublr_syrk_upper_batched", int(M), int(K), float(alpha), A, int(lda), int(sA), float(beta), C,
+              int(ldc), int(sC), int(batch), _lib.stream_handle())
+
+
+def _trsm_rec(T, n, f, inv_set, j0, a, X, ldx, Y, ldy, N, batch, lower_unit):
+    """Y = op(T11)^-1 X for the diagonal range [j0, j0 + a) of T (n x n,
+    batch stride n*n): lower_unit -> T11 is the unit-lower L of an LU; else
+    T11 = R^T with R upper (Cholesky). X and Y are addresses inside n x n
+    matrices (batch stride n*n) of the range's rows, N columns. Recursive: the
+    off-diagonal update is one GEMM with K = a/2 at the top; the nb x nb leaves
+    multiply by the stored diagonal-block inverses. X is consumed; Y must not
+    alias it."""
+    nn = n * n
+    if a <= f.nb:
+        bi = j0 // f.nb
+        gemm(0 if lower_unit else 1, 0, a, N, a, 1.0, addr(inv_set[bi]), a, a * a, X, ldx, nn, 0.0, Y, ldy, nn,
+             batch)
+        return
+    h = _split(a, f.nb)
+    _trsm_rec(T, n, f, inv_set, j0, h, X, ldx, Y, ldy, N, batch, lower_unit)
+    if lower_unit:   # X_bot -= L[j0+h:j0+a, j0:j0+h] Y_top
+        gemm(0, 0, a - h, N, h, -1.0, addr(T, (j0 + h) * n + j0), n, nn, Y, ldy, nn, 1.0, X + 8 * h * ldx, ldx, nn,
+             batch)
+    else:            # X_bot -= R[j0:j0+h, j0+h:j0+a]^T Y_top
+        gemm(1, 0, a - h, N, h, -1.0, addr(T, j0 * n + j0 + h), n, nn, Y, ldy, nn, 1.0, X + 8 * h * ldx, ldx, nn,
+             batch)
+    _trsm_rec(T, n, f, inv_set, j0 + h, a - h, X + 8 * h * ldx, ldx, Y + 8 * h * ldy, ldy, N, batch, lower_unit)
+
+
 def cholesky_upper(G, R, nb=NB):
-    """G_b = R_b^T R_b (G overwritten as workspace, R zero-initialised by the
-    caller). Returns Factors with R_jj^-1. Raises LinAlgError if not SPD."""
+    """G_b = R_b^T R_b (G overwritten as workspace, only its upper triangle is
+    read; R zero-initialised by the caller). Recursive: chol(G11); R12 =
+    R11^-T G12; G22 -= R12^T R12 (upper tiles, K = half the range); chol(G22)
+    — the updates are large-K GEMMs instead of a rank-64 update per panel.
+    Returns Factors with R_jj^-1 of the nb x nb diagonal blocks. Raises
+    LinAlgError (check_status) if not SPD."""
     torch = _torch()
     _dense(G, R)
     batch, n, _ = G.shape
     f = Factors(n, nb, batch, G.device)
     status = torch.zeros(1, dtype=torch.int32, device=G.device)
     nn = n * n
-    for bi, (j0, jb) in enumerate(f.blocks):
-        _lib.call("ublr_potrf_diag", addr(G), n, nn, j0, jb, addr(R), n, nn, addr(f.inv[bi]), addr(status), batch,
-                  _lib.stream_handle())
-        if j0 + jb < n:
-            n2 = n - j0 - jb
-            # R12 = R11^-T G12
-            gemm(1, 0, jb, n2, jb, 1.0, addr(f.inv[bi]), jb, jb * jb, addr(G, j0 * n + j0 + jb), n, nn,
-                 0.0, addr(R, j0 * n + j0 + jb), n, nn, batch)
-            # G22 -= R12^T R12 (upper-triangle tiles only: the panel steps read
-            # nothing below the diagonal)
-            _lib.call("ublr_syrk_upper_batched", n2, jb, -1.0, addr(R, j0 * n + j0 + jb), n, nn, 1.0,
-                      addr(G, (j0 + jb) * n + j0 + jb), n, nn, batch, _lib.stream_handle())
+
+    def rec(j0, w):
+        if w <= nb:
+            bi = j0 // nb
+            _lib.call("ublr_potrf_diag", addr(G), n, nn, j0, w, addr(R), n, nn, addr(f.inv[bi]), addr(status),
+                      batch, _lib.stream_handle())
+            return
+        a = _split(w, nb)
+        rec(j0, a)
+        _trsm_rec(R, n, f, f.inv, j0, a, addr(G, j0 * n + j0 + a), n, addr(R, j0 * n + j0 + a), n, w - a, batch,
+                  lower_unit=False)
+        _syrk_upper(w - a, a, -1.0, addr(R, j0 * n + j0 + a), n, nn, 1.0, addr(G, (j0 + a) * n + j0 + a), n, nn,
+                    batch)
+        rec(j0 + a, w - a)
+
+    rec(0, n)
     f.status = status
     return f
 
@@ -78,12 +122,15 @@ def cholesky_upper(G, R, nb=NB):
 def lu_sign(W, LU, D, nb=NB, R=None):
     """No-pivot LU of W + diag(D) with D_jj = sign(w_jj) picked at pivot time
     (W overwritten). LU holds unit-L (strict lower) and U. Returns Factors
-    with L_jj^-1 (inv) and U_jj^-1 (inv2).
+    with L_jj^-1 (inv) and U_jj^-1 (inv2) of the nb x nb diagonal blocks.
 
     With an upper-triangular R (batch x n x n) the factored matrix is
     W + diag(D) R instead (row j of D R joins when j becomes the pivot row):
     for W = -B1^T and R the Cholesky factor of B B^T this is (D - Q_top) R,
-    whose L is the L of D - Q_top (bn null space)."""
+    whose L is the L of D - Q_top (bn null space).
+
+    Recursive on columns: LU of the left half (all rows), U12 = L11^-1 W12,
+    W22 -= L21 U12 (K = half the range), LU of the right half."""
     torch = _torch()
     _dense(W, LU, D, R)
     batch, n, _ = W.shape
@@ -91,24 +138,34 @@ def lu_sign(W, LU, D, nb=NB, R=None):
     f.inv2 = torch.zeros_like(f.inv)
     status = torch.zeros(1, dtype=torch.int32, device=W.device)
     nn = n * n
-    for bi, (j0, jb) in enumerate(f.blocks):
-        if R is None:
-            _lib.call("ublr_lu_sign_diag", addr(W), n, nn, j0, jb, addr(LU), n, nn, addr(f.inv[bi]),
-                      addr(f.inv2[bi]), addr(D), n, addr(status), batch, _lib.stream_handle())
-        else:
-            _lib.call("ublr_lu_sign_diag_r", addr(W), n, nn, j0, jb, addr(LU), n, nn, addr(f.inv[bi]),
-                      addr(f.inv2[bi]), addr(D), n, addr(status), addr(R), n, nn, n, batch, _lib.stream_handle())
-        if j0 + jb < n:
-            n2 = n - j0 - jb
-            # U12 = L11^-1 W12
-            gemm(0, 0, jb, n2, jb, 1.0, addr(f.inv[bi]), jb, jb * jb, addr(W, j0 * n + j0 + jb), n, nn,
-                 0.0, addr(LU, j0 * n + j0 + jb), n, nn, batch)
-            # L21 = W21 U11^-1
-            gemm(0, 0, n2, jb, jb, 1.0, addr(W, (j0 + jb) * n + j0), n, nn, addr(f.inv2[bi]), jb, jb * jb,
-                 0.0, addr(LU, (j0 + jb) * n + j0), n, nn, batch)
-            # W22 -= L21 U12
-            gemm(0, 0, n2, n2, jb, -1.0, addr(LU, (j0 + jb) * n + j0), n, nn, addr(LU, j0 * n + j0 + jb), n, nn,
-                 1.0, addr(W, (j0 + jb) * n + j0 + jb), n, nn, batch)
+
+    def rec(j0, w):
+        if w <= nb:
+            bi = j0 // nb
+            if R is None:
+                _lib.call("ublr_lu_sign_diag", addr(W), n, nn, j0, w, addr(LU), n, nn, addr(f.inv[bi]),
+                          addr(f.inv2[bi]), addr(D), n, addr(status), batch, _lib.stream_handle())
+            else:
+                # panel only (n = j0 + w); the rows' D R12 to the right in one parallel pass
+                _lib.call("ublr_lu_sign_diag_r", addr(W), n, nn, j0, w, addr(LU), n, nn, addr(f.inv[bi]),
+                          addr(f.inv2[bi]), addr(D), n, addr(status), addr(R), n, nn, j0 + w, batch,
+                          _lib.stream_handle())
+                if j0 + w < n:
+                    _lib.call("ublr_add_scaled_rows", addr(W, j0 * n + j0 + w), n, nn, addr(R, j0 * n + j0 + w), n,
+                              nn, addr(D, j0), n, w, n - j0 - w, batch, _lib.stream_handle())
+            if j0 + w < n:   # L21 = W21 U11^-1 for every row below
+                gemm(0, 0, n - j0 - w, w, w, 1.0, addr(W, (j0 + w) * n + j0), n, nn, addr(f.inv2[bi]), w, w * w,
+                     0.0, addr(LU, (j0 + w) * n + j0), n, nn, batch)
+            return
+        a = _split(w, nb)
+        rec(j0, a)
+        _trsm_rec(LU, n, f, f.inv, j0, a, addr(W, j0 * n + j0 + a), n, addr(LU, j0 * n + j0 + a), n, w - a, batch,
+                  lower_unit=True)
+        gemm(0, 0, n - j0 - a, w - a, a, -1.0, addr(LU, (j0 + a) * n + j0), n, nn, addr(LU, j0 * n + j0 + a), n, nn,
+             1.0, addr(W, (j0 + a) * n + j0 + a), n, nn, batch)
+        rec(j0 + a, w - a)
+
+    rec(0, n)
     f.status = status
     return f
 
