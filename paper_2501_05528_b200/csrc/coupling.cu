@@ -636,6 +636,175 @@ __global__ void __launch_bounds__(CP_THREADS) k_nf_B(ublr_op_t op, const int32_t
   }
 }
 
+
+// ------------------------------------------------- near field v3 (m <= 256)
+// S_p = sum_{j' in colour} C_ij' V_j'^T as one GEMM per pair: K runs over
+// (member j', b) in BK = 16 slices, A = the C_ij' slices (rows of the core,
+// m-major cp.async), B = V_j'^T (n-major: V_j' rows), on the shared DMMA
+// main loop. 48 x 256 CTA tile, 8 warps of 24 x 64.
+constexpr int NFS_KP = 48;
+using NfsCfg = TileCfg<NFS_KP, 256, 16, 2, 4, 3, false, false>;
+
+struct NfSA {
+  const double* crow; int64_t ldc; const int32_t* cidx; const int32_t* roff; int mem0, ki; bool vec;
+  __device__ __forceinline__ void stage(double* As, int ks) {
+    constexpr int KS = NFS_KP / NfsCfg::BK;
+    const int jp = cidx[mem0 + ks / KS], b0 = (ks % KS) * NfsCfg::BK;
+    const int kj = roff[jp + 1] - roff[jp];
+    tile_copy<NfsCfg::NT>(As, NfsCfg::SA, crow + roff[jp] + b0, ldc, NfsCfg::BM, NfsCfg::BK, 0, 0, ki, kj - b0,
+                          IdentityRows{}, vec);
+  }
+};
+struct NfSB {
+  const double* V; int64_t lduv; const int32_t* cidx; const int32_t* off; const int32_t* roff; int mem0; bool vec;
+  __device__ __forceinline__ void stage(double* Bs, int ks) {
+    constexpr int KS = NFS_KP / NfsCfg::BK;
+    const int jp = cidx[mem0 + ks / KS], b0 = (ks % KS) * NfsCfg::BK;
+    const int kj = roff[jp + 1] - roff[jp], mj = off[jp + 1] - off[jp];
+    tile_copy<NfsCfg::NT>(Bs, NfsCfg::SB, V + (int64_t)off[jp] * lduv + b0, lduv, NfsCfg::BN, NfsCfg::BK, 0, 0, mj,
+                          kj - b0, IdentityRows{}, vec);
+  }
+};
+
+__global__ void __launch_bounds__(NfsCfg::NT) k_nf_S3(const int32_t* __restrict__ off,
+                                                      const int32_t* __restrict__ roff,
+                                                      const double* __restrict__ V, int64_t lduv,
+                                                      const double* __restrict__ core, int64_t ldc,
+                                                      const int32_t* __restrict__ colour,
+                                                      const int32_t* __restrict__ cptr,
+                                                      const int32_t* __restrict__ cidx,
+                                                      const int32_t* __restrict__ pair_i,
+                                                      const int32_t* __restrict__ nidx, int m_max, int KA,
+                                                      double* __restrict__ S, int vec) {
+  using Cfg = NfsCfg;
+  extern __shared__ double dsm[];
+  const int p = blockIdx.x;
+  const int i = pair_i[p];
+  const int c = colour[nidx[p]];
+  const int ki = roff[i + 1] - roff[i];
+  const int mem0 = cptr[c], nmem = cptr[c + 1] - mem0;
+  NfSA ap{core + (int64_t)roff[i] * ldc, ldc, cidx, roff, mem0, ki, vec != 0};
+  NfSB bp{V, lduv, cidx, off, roff, mem0, vec != 0};
+  double acc[Cfg::MI][Cfg::NJ][2];
+#pragma unroll
+  for (int a = 0; a < Cfg::MI; ++a)
+#pragma unroll
+    for (int b = 0; b < Cfg::NJ; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  WholeStage<NfSA> apw{ap};
+  dmma_mainloop<Cfg>(apw, bp, nmem * (NFS_KP / Cfg::BK), dsm, acc);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wr = warp / Cfg::WNW, wc = warp % Cfg::WNW;
+  double* Sp = S + (int64_t)p * KA * m_max;
+#pragma unroll
+  for (int a = 0; a < Cfg::MI; ++a) {
+    const int row = wr * Cfg::WM + a * 8 + g;
+    if (row >= KA) continue;
+#pragma unroll
+    for (int b = 0; b < Cfg::NJ; ++b) {
+      const int q = wc * Cfg::WN + b * 8 + 2 * t;
+      if (q < m_max) Sp[(int64_t)row * m_max + q] = acc[a][b][0];
+      if (q + 1 < m_max) Sp[(int64_t)row * m_max + q + 1] = acc[a][b][1];
+    }
+  }
+}
+
+// B_p[r][q] = sum_{j' in colour} A(i_r, j'_q) - (U_i S_p)[r][q]: thread = column
+// q, 16 rows per CTA; the next member's column point is loaded one member
+// ahead, the row points of the slab are shared-memory broadcasts, and the
+// diagonal select is only evaluated for the member j' = i.
+constexpr int NFB_RT = 16;  // rows per CTA (accumulators + broadcast row points stay in registers)
+template <int KIND, int DIM>
+__global__ void __launch_bounds__(256, 2) k_nf_B3(ublr_op_t op, const int32_t* __restrict__ off,
+                                               const int32_t* __restrict__ roff, int KA,
+                                               const double* __restrict__ U, int64_t lduv,
+                                               const int32_t* __restrict__ colour,
+                                               const int32_t* __restrict__ cptr,
+                                               const int32_t* __restrict__ cidx,
+                                               const int32_t* __restrict__ pair_i,
+                                               const int32_t* __restrict__ nidx,
+                                               const int64_t* __restrict__ b_off, int m_max,
+                                               const double* __restrict__ S, double* __restrict__ B) {
+  constexpr int RT = NFB_RT;
+  __shared__ LogTables lt;
+  __shared__ double xr[DIM][RT];
+  __shared__ double us[RT][65];
+  if (KIND == UBLR_OP_LOG) init_log_tables(&lt);
+  const int p = blockIdx.x;
+  const int i = pair_i[p];
+  const int jn = nidx[p];
+  const int c = colour[jn];
+  const int ri0 = off[i], mi = off[i + 1] - ri0;
+  const int mjn = off[jn + 1] - off[jn];
+  const int r0 = blockIdx.y * RT;
+  if (r0 >= mi) return;
+  const int ki = roff[i + 1] - roff[i];
+  const int q = threadIdx.x;
+  const int n = (int)op.n;
+  for (int e = threadIdx.x; e < DIM * RT; e += blockDim.x) {
+    const int a = e / RT, r = e - a * RT;
+    xr[a][r] = (r0 + r < mi) ? op.coords[(int64_t)a * n + ri0 + r0 + r] : 0.0;
+  }
+  for (int e = threadIdx.x; e < RT * ki; e += blockDim.x) {
+    const int r = e / ki, a = e - r * ki;
+    us[r][a] = (r0 + r < mi) ? U[(int64_t)(ri0 + r0 + r) * lduv + a] : 0.0;
+  }
+  __syncthreads();
+  double acc[RT];
+#pragma unroll
+  for (int r = 0; r < RT; ++r) acc[r] = 0.0;
+  const int mem0 = cptr[c], mem1 = cptr[c + 1];
+  const double diag = op.diag;
+  // column point of member mem (one ahead)
+  auto colpt = [&](int mem, double (&x)[DIM], int& col, bool& ok) {
+    const int jp = cidx[mem];
+    ok = q < off[jp + 1] - off[jp];
+    col = off[jp] + (ok ? q : 0);
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) x[a] = op.coords[(int64_t)a * n + col];
+  };
+  double xc[DIM], xn[DIM];
+  int colc, coln = 0;
+  bool okc, okn = false;
+  colpt(mem0, xc, colc, okc);
+  for (int mem = mem0; mem < mem1; ++mem) {
+    if (mem + 1 < mem1) colpt(mem + 1, xn, coln, okn);
+    if (okc) {
+      const bool self = cidx[mem] == i;
+#pragma unroll
+      for (int r = 0; r < RT; ++r) {
+        double d = xr[0][r] - xc[0];
+        double r2 = d * d;
+        if (DIM > 1) {
+          d = xr[1][r] - xc[1];
+          r2 = fma(d, d, r2);
+        }
+        if (DIM > 2) {
+          d = xr[2][r] - xc[2];
+          r2 = fma(d, d, r2);
+        }
+        double v = (KIND == UBLR_OP_LOG) ? -0.5 * fast_log(r2, &lt) : rsqrt(r2);
+        if (self && ri0 + r0 + r == colc) v = diag;
+        acc[r] += v;
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) xc[a] = xn[a];
+    colc = coln;
+    okc = okn;
+  }
+  if (q >= mjn) return;
+  const double* Sp = S + (int64_t)p * KA * m_max;
+  double* Bp = B + b_off[p];
+  for (int a = 0; a < ki; ++a) {
+    const double sa = Sp[(int64_t)a * m_max + q];
+#pragma unroll
+    for (int r = 0; r < RT; ++r) acc[r] = fma(-us[r][a], sa, acc[r]);
+  }
+#pragma unroll
+  for (int r = 0; r < RT; ++r)
+    if (r0 + r < mi) Bp[(int64_t)(r0 + r) * mjn + q] = acc[r];
+}
 }  // namespace
 }  // namespace ublr
 
@@ -736,6 +905,33 @@ extern "C" int ublr_nearfield_colour(const ublr_op_t* op, const int32_t* off, co
   cudaStream_t st = (cudaStream_t)stream;
   double* S = (double*)workspace;
   const int KA = ka_of(k);
+  static const int nf_ver = [] {
+    const char* e = getenv("UBLR_NEARFIELD_VERSION");
+    return e ? atoi(e) : 3;
+  }();
+  const int kk = k < m_max ? k : m_max;
+  if (nf_ver == 3 && op->kind != UBLR_OP_DENSE && m_max > 64 && kk <= NFS_KP) {
+    const int vec = ((ld_uv % 2) == 0 && (ld_c % 2) == 0 && (k % 2) == 0 && ((uintptr_t)V) % 16 == 0 &&
+                     ((uintptr_t)core) % 16 == 0) ? 1 : 0;
+    size_t sm = NfsCfg::smem_bytes();
+    UBLR_CUDA(cudaFuncSetAttribute(k_nf_S3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k_nf_S3<<<n_pairs, NfsCfg::NT, sm, st>>>(off, roff, V, ld_uv, core, ld_c, colour, cptr, cidx, pair_i, nidx, m_max,
+                                            KA, S, vec);
+    UBLR_LAUNCH_CHECK();
+    dim3 gb(n_pairs, (m_max + NFB_RT - 1) / NFB_RT);
+    const int nthr = (m_max + 31) / 32 * 32;
+#define UBLR_NFB3(KIND, DIM)                                                                                   \
+  k_nf_B3<KIND, DIM><<<gb, nthr, 0, st>>>(*op, off, roff, KA, U, ld_uv, colour, cptr, cidx, pair_i, nidx, b_off, \
+                                          m_max, S, B)
+    if (op->kind == UBLR_OP_LOG) {
+      if (op->dim == 1) UBLR_NFB3(UBLR_OP_LOG, 1); else if (op->dim == 2) UBLR_NFB3(UBLR_OP_LOG, 2); else UBLR_NFB3(UBLR_OP_LOG, 3);
+    } else {
+      if (op->dim == 1) UBLR_NFB3(UBLR_OP_INV, 1); else if (op->dim == 2) UBLR_NFB3(UBLR_OP_INV, 2); else UBLR_NFB3(UBLR_OP_INV, 3);
+    }
+#undef UBLR_NFB3
+    UBLR_LAUNCH_CHECK();
+    return UBLR_OK;
+  }
   // S_p: 8 warps x NQ 8-col groups cover m_max
   int nq = (m_max + 63) / 64;  // per warp groups of 8 columns: 8 warps * 8 * nq >= m_max
 #define UBLR_NFS(NA, NQ)                                                                                   \

@@ -136,3 +136,25 @@ def test_exact_rank_recovery_all_methods(mid):
         _, report = P.compress(P.DenseOperator(A), tess, k, mid, p=10, stream=P.RandomStream(55),
                                error_iterations=20)
         assert report.relative_error <= 1e-7, (d, b, m, k, report.relative_error)
+
+
+@pytest.mark.parametrize("per,b,kind,k,mid", [(64, 16, "inv", 48, "A2"), (50, 16, "log", 20, "A2"),
+                                              (48, 9, "log", 30, "A1")])
+def test_large_blocks_vs_oracle(per, b, kind, k, mid):
+    """m > 64 blocks (the warp-specialised coupling and the v3 near-field
+    kernels), uniform m = 256 and ragged 144-169-point blocks, GPU vs the
+    oracle's dense compression on the same inputs."""
+    pts = P.grid_points(per, 2)
+    tess = P.build_tessellation(pts, b)
+    diag = -np.log(0.5 / per) if kind == "log" else 2.0 * per
+    rep, _ = P.compress(P.KernelOperator(pts, kind, diag), tess, k, mid, p=10, stream=P.RandomStream(5),
+                        compute_error=False)
+    coords = O.cell_centres(per, 2)
+    bx = O.partition(coords, b)
+    n = per * per
+    A = O.kernel_block(coords, np.arange(n), np.arange(n), kind, diag)
+    orep, _ = O.compress(O.Dense(A), bx, k, mid, p=10, stream=O.Stream(5), compute_error=False)
+    nA = np.linalg.norm(A)
+    D_gpu, D_ref = rep.to_dense(), orep.to_dense()
+    assert np.linalg.norm(D_gpu - D_ref) / nA <= TOL
+    assert np.linalg.norm(A - D_gpu) / nA <= 1.05 * np.linalg.norm(A - D_ref) / nA + 1e-15
