@@ -74,6 +74,7 @@ class Tessellation:
     grid_coords: np.ndarray
     full_grid: bool
     points: PointCloud | None = None
+    colors: np.ndarray | None = None   # stored colouring (read from a UBLR1 container), else computed
     _far_fields: list = field(default=None, repr=False)
     _device: dict = field(default_factory=dict, repr=False)
 
@@ -172,6 +173,9 @@ def build_tessellation(points: PointCloud, target_block_count: int) -> Tessellat
 
 def color_boxes(tess: Tessellation) -> BoxColoring:
     """Distance-2 colouring (ref/tessellation.py:188-219)."""
+    if tess.colors is not None:
+        colours = np.asarray(tess.colors, dtype=np.int64)
+        return BoxColoring(colors=colours, num_colors=int(colours.max()) + 1)
     if tess.full_grid:
         code = np.zeros(tess.b, dtype=np.int64)
         for a in range(tess.dim):
