@@ -233,7 +233,7 @@ def run_sharded(args, rank, world, local):
     stream = P.RandomStream(W.COMPRESS_SEED)
     other_V = None
     if emulate:   # V rows of the other shards, untimed
-        plan0 = plan_tagging(wl.tess, 0, "gaussian", stream.child(1))
+        plan0 = plan_tagging(wl.tess, 0, "gaussian", stream.child(1), device=True)
         parts = []
         for sh in shards:
             if sh.rank == me:

@@ -93,6 +93,12 @@ int ublr_seedseq_keys(const uint32_t* run, int nrun, const uint32_t* prefix, int
  * Householder Q of T[rows]^T and res[s] = ||T[rows] Z[s]||. Host function. */
 int ublr_null_vectors(const double* T, int ell, const int32_t* ptr, const int32_t* idx, int nsets, double* Z,
                       double* res);
+/* Tagging-plan aspect ratios (ref/tagging.py:110-123): rho[i] = max/min over
+ * the far field j of |T[j] . Z[i]| (T, Z: b x ell row-major device arrays;
+ * neighbour CSR nptr/nidx), 1 if the max is 0, inf if the min is 0, NaN if
+ * the far field is empty. ell <= 32. */
+int ublr_tag_aspect(const double* T, const double* Z, int ell, const int32_t* nptr, const int32_t* nidx, int b,
+                    double* rho, void* stream);
 
 /* K1 — ref/linalg.py:38-52 (`RandomStream.normal` / `gaussian`), called at
  * ref/bases.py:97-98, :163-168, :229-230 and ref/reconstruction.py:405.
@@ -131,6 +137,11 @@ int ublr_apply(const ublr_op_t* op, const double* X, int64_t ld_x, int w, double
 int ublr_block_qr(const double* Y, int64_t ld_y, int mode, const double* z, int ell, int gc,
                   const int32_t* col0, const int32_t* off, int b, int k, double* U, int64_t ld_u,
                   void* stream, int m_max);
+/* Both sides of a tagging bases step in one launch: U_i from Y and V_i from
+ * Z (mode 0 of ublr_block_qr, the same z^(i)); grid b x 2. */
+int ublr_block_qr_pair(const double* Y, const double* Z, int64_t ld_y, const double* z, int ell, int gc,
+                       const int32_t* off, int b, int k, double* U, double* V, int64_t ld_u, void* stream,
+                       int m_max);
 
 /* K6 — coupling (ref/reconstruction.py:185-198, direct_core):
  * core[roff[i]:, roff[j]:] = U_i^T A_ij V_j for block rows i0 <= i < i1 and all

@@ -44,12 +44,14 @@ SIGNATURES = {
     "ublr_device_check": (INT, []),
     "ublr_seedseq_keys": (INT, [P, INT, P, INT, P, INT, I64, P]),
     "ublr_null_vectors": (INT, [P, INT, P, P, INT, P, P]),
+    "ublr_tag_aspect": (INT, [P, P, INT, P, P, INT, P, P]),
     "ublr_rng_workspace_bytes": (I64, [P, INT]),
     "ublr_rng_normals": (INT, [P, P, INT, P, P, I64, P]),
     "ublr_sketch_tagged": (INT, [C.POINTER(OpDesc), P, INT, P, INT, P, I64, INT, P, I64, INT, INT, P]),
     "ublr_sketch_tagged_pair": (INT, [C.POINTER(OpDesc), P, INT, P, INT, P, P, I64, INT, P, P, I64, INT, INT, P]),
     "ublr_apply": (INT, [C.POINTER(OpDesc), P, I64, INT, P, I64, P]),
     "ublr_block_qr": (INT, [P, I64, INT, P, INT, INT, P, P, INT, INT, P, I64, P, INT]),
+    "ublr_block_qr_pair": (INT, [P, P, I64, P, INT, INT, P, INT, INT, P, P, I64, P, INT]),
     "ublr_coupling": (INT, [C.POINTER(OpDesc), P, P, INT, INT, P, P, I64, P, I64, P, INT, INT, INT]),
     "ublr_nearfield_workspace_bytes": (I64, [INT, INT, INT]),
     "ublr_blr_apply_workspace_bytes": (I64, [I64, INT]),
@@ -108,10 +110,10 @@ def check(rc: int, what: str = ""):
 
 # kernels each C-ABI entry point launches (for bench.py's `gpu_launches`)
 LAUNCHES = {"ublr_rng_normals": 7, "ublr_sketch_tagged": 1, "ublr_sketch_tagged_pair": 1, "ublr_apply": 1,
-            "ublr_block_qr": 1, "ublr_coupling": 1, "ublr_nearfield_colour": 2,
+            "ublr_block_qr": 1, "ublr_block_qr_pair": 1, "ublr_coupling": 1, "ublr_nearfield_colour": 2,
             "ublr_blr_apply": 3, "ublr_gemm_batched": 1, "ublr_potrf_diag": 1, "ublr_lu_sign_diag": 1,
             "ublr_lu_sign_diag_r": 1, "ublr_syrk_upper_batched": 1, "ublr_add_scaled_rows": 1,
-            "ublr_gather": 1, "ublr_scale_rows": 1, "ublr_tag_combine_pairs": 1, "ublr_assemble_tagged": 1}
+            "ublr_gather": 1, "ublr_scale_rows": 1, "ublr_tag_combine_pairs": 1, "ublr_assemble_tagged": 1, "ublr_tag_aspect": 1}
 launch_count = 0
 _events = None  # name -> list of (start, end) CUDA events when instrumentation is on
 

@@ -13,6 +13,7 @@ import numpy as np
 from . import _lib
 from .linalg import RandomStream, device_normals
 from .operators import CountingOperator, unwrap
+from .tagging import DEVICE_PLAN_MIN_B
 from .tessellation import Tessellation, device_tess
 
 
@@ -192,9 +193,8 @@ def block_bases_from_tagged(dt, Y, Z, Z_dev, ell, gc, k):
     V = alloc((dt.n, k), dtype=torch.float64, device=dt.device)
     stream = _lib.stream_handle()
     kq = max(1, min(k, dt.m_max))
-    for src, dst in ((Y, U), (Z, V)):
-        _lib.call("ublr_block_qr", _lib.ptr(src), s, 0, _lib.ptr(Z_dev), ell, gc, None, _lib.ptr(dt.off), dt.b,
-                  kq, _lib.ptr(dst), k, stream, dt.m_max)
+    _lib.call("ublr_block_qr_pair", _lib.ptr(Y), _lib.ptr(Z), s, _lib.ptr(Z_dev), ell, gc, _lib.ptr(dt.off), dt.b,
+              kq, _lib.ptr(U), _lib.ptr(V), k, stream, dt.m_max)
     return U, V
 
 
@@ -216,6 +216,10 @@ def tagging_bases(op, tess: Tessellation, k: int, p: int, plan, stream: RandomSt
     r = k + p
     gc = r if group_cols is None else group_cols
     planner = plan if callable(plan) else None
+    if planner is not None and tess.b >= DEVICE_PLAN_MIN_B:
+        # large b: the planner's aspect ratios run on the GPU, so plan before
+        # the sketch occupies it (no speculative sketch)
+        plan, planner = planner(), None
     matrix = first if planner is not None else plan.matrix
     T_entries = matrix.entries
     ell = T_entries.shape[1]

@@ -29,9 +29,14 @@ __global__ void __launch_bounds__(QR_THREADS) k_block_qr(const double* __restric
                                                          const double* __restrict__ z, int ell, int gc,
                                                          const int32_t* __restrict__ col0,
                                                          const int32_t* __restrict__ off, int k,
-                                                         double* __restrict__ U, int64_t ldu) {
+                                                         double* __restrict__ U, int64_t ldu,
+                                                         const double* __restrict__ Y2, double* __restrict__ U2) {
   extern __shared__ double smem[];
   const int i = blockIdx.x;
+  if (blockIdx.y == 1) {  // second side of a pair launch (Z -> V)
+    Y = Y2;
+    U = U2;
+  }
   const int r0 = off[i];
   const int m = off[i + 1] - r0;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -155,7 +160,23 @@ extern "C" int ublr_block_qr(const double* Y, int64_t ld_y, int mode, const doub
   UBLR_REQUIRE(smem <= 220 * 1024, UBLR_ERR_VALUE, "ublr_block_qr: m*k sample exceeds shared memory");
   cudaStream_t st = (cudaStream_t)stream;
   UBLR_CUDA(cudaFuncSetAttribute(k_block_qr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_block_qr<<<b, QR_THREADS, smem, st>>>(Y, ld_y, mode, z, ell, gc, col0, off, k, U, ld_u);
+  k_block_qr<<<b, QR_THREADS, smem, st>>>(Y, ld_y, mode, z, ell, gc, col0, off, k, U, ld_u, nullptr, nullptr);
+  UBLR_LAUNCH_CHECK();
+  return UBLR_OK;
+}
+
+extern "C" int ublr_block_qr_pair(const double* Y, const double* Z, int64_t ld_y, const double* z, int ell, int gc,
+                                  const int32_t* off, int b, int k, double* U, double* V, int64_t ld_u, void* stream,
+                                  int m_max) {
+  UBLR_REQUIRE(b > 0 && off && U && V && Y && Z && z && k >= 1 && m_max >= 1 && ell >= 1 && gc >= k,
+               UBLR_ERR_VALUE, "ublr_block_qr_pair: bad arguments");
+  UBLR_REQUIRE(ld_u >= k && ld_u >= (k < m_max ? k : m_max), UBLR_ERR_VALUE, "ublr_block_qr_pair: ld_u too small");
+  int lds = k | 1;
+  size_t smem = (size_t)(m_max * lds + k) * sizeof(double);
+  UBLR_REQUIRE(smem <= 220 * 1024, UBLR_ERR_VALUE, "ublr_block_qr_pair: m*k sample exceeds shared memory");
+  cudaStream_t st = (cudaStream_t)stream;
+  UBLR_CUDA(cudaFuncSetAttribute(k_block_qr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_block_qr<<<dim3(b, 2), QR_THREADS, smem, st>>>(Y, ld_y, 0, z, ell, gc, nullptr, off, k, U, ld_u, Z, V);
   UBLR_LAUNCH_CHECK();
   return UBLR_OK;
 }

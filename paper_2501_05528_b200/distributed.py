@@ -123,7 +123,7 @@ def phase1_local(op, tess, k, p, stream, shard, plan=None):
     _lib.require_device()
     dt = device_tess(tess, torch.device("cuda"))
     if plan is None:
-        plan = plan_tagging(tess, 0, "gaussian", stream.child(1))
+        plan = plan_tagging(tess, 0, "gaussian", stream.child(1), device=True)
     r = k + p
     gc = r
     T = plan.matrix.entries
@@ -148,9 +148,9 @@ def phase1_local(op, tess, k, p, stream, shard, plan=None):
     U = torch.zeros((nloc, k), **f64)
     V = torch.zeros((nloc, k), **f64)
     ushift = 8 * shard.r0 * k
-    for src, dst in ((Y, U), (Z, V)):
-        _lib.call("ublr_block_qr", _lib.ptr(src) - shift, s, 0, _lib.ptr(Z_dev) + 8 * shard.i0 * ell, ell, gc, None,
-                  _lib.ptr(dt.off) + 4 * shard.i0, shard.i1 - shard.i0, kq, _lib.ptr(dst) - ushift, k, st, dt.m_max)
+    _lib.call("ublr_block_qr_pair", _lib.ptr(Y) - shift, _lib.ptr(Z) - shift, s, _lib.ptr(Z_dev) + 8 * shard.i0 * ell,
+              ell, gc, _lib.ptr(dt.off) + 4 * shard.i0, shard.i1 - shard.i0, kq, _lib.ptr(U) - ushift,
+              _lib.ptr(V) - ushift, k, st, dt.m_max)
     del Y, Z
     return plan, U, V, dt
 
@@ -207,7 +207,7 @@ def compress_emulated(op, tess, k, p=10, stream=None, world=2):
     torch = _torch()
     stream = stream or RandomStream(0)
     shards = shard_ranges(tess, world, k)
-    plan = plan_tagging(tess, 0, "gaussian", stream.child(1))
+    plan = plan_tagging(tess, 0, "gaussian", stream.child(1), device=True)
     locs = [phase1_local(op, tess, k, p, stream, sh, plan) for sh in shards]
     V_all = torch.cat([loc[2] for loc in locs], 0)
     out = []

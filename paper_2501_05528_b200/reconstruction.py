@@ -406,7 +406,7 @@ def compress_type_a(op, tess, k, p=10, method="tag", stream=None, distribution="
             first = make_tagging_matrix(tess.b, tess.dim, extra_cols, distribution, stream.child(1).child(0))
             bases, bundle = tagging_bases(
                 cop, tess, k, p,
-                lambda: plan_tagging(tess, extra_cols, distribution, stream.child(1), max_redraws=max_tag_redraws,
+                lambda: plan_tagging(tess, extra_cols, distribution, stream.child(1), max_redraws=max_tag_redraws, device="auto",
                                      first=first),
                 stream.child(0), extra_samples=extra_samples, first=first)
             plan = bundle.plan
@@ -460,7 +460,7 @@ def compress_type_b(op, tess, k, p=10, method="bn", stream=None, distribution="g
             first = make_tagging_matrix(tess.b, tess.dim, 0, distribution, stream.child(1).child(0))
             bases, bundle = tagging_bases(
                 cop, tess, k, p,
-                lambda: plan_tagging(tess, 0, distribution, stream.child(1), max_redraws=max_tag_redraws,
+                lambda: plan_tagging(tess, 0, distribution, stream.child(1), max_redraws=max_tag_redraws, device="auto",
                                      extra_check=lambda T: b2_denominators_ok(T, tess), first=first),
                 stream.child(0), group_cols=tess.max_block_size + p, first=first)
             plan = bundle.plan

@@ -120,6 +120,14 @@ def _csr(rows_list):
     return ptr, np.ascontiguousarray(idx, dtype=np.int32)
 
 
+def _fro(E) -> float:
+    """||E||_F. np.linalg.norm of a 2-D array goes through a BLAS dot that
+    cost 30+ ms for a 4096 x 10 tagging matrix on the bench hosts (thread
+    start-up); the residual limits only need the value to rounding."""
+    E = np.asarray(E, dtype=np.float64)
+    return float(np.sqrt(np.einsum("ij,ij->", E, E)))
+
+
 def _neighbour_csr(tess):
     """CSR of the neighbour lists, cached on the tessellation."""
     c = tess._device.get("nbr_csr")
@@ -186,7 +194,7 @@ def tag_null_vector(T: TaggingMatrix, tess: Tessellation, i: int) -> NullVector:
     Z, res, ok = batched_null_vectors(T.entries, [tess.neighbor_lists[i]])
     if not ok[0]:
         raise DegenerateTagsError(f"block {i}: requested null space does not exist")
-    limit = 1e-12 * max(1.0, np.linalg.norm(T.entries))
+    limit = 1e-12 * max(1.0, _fro(T.entries))
     if res[0] > limit:
         raise DegenerateTagsError(f"block {i}: null-vector residual {res[0]:.3e} exceeds {limit:.3e}")
     return NullVector(block=i, vector=Z[0], residual=float(res[0]))
@@ -211,18 +219,40 @@ def aspect_ratio(pt: ProjectedTags, tess: Tessellation, i: int | None = None) ->
     return float(hi / lo)
 
 
-def _evaluate(T: TaggingMatrix, tess: Tessellation, attempts: int) -> TaggingPlan:
+DEVICE_PLAN_MIN_B = 1024
+
+
+def _aspect_device(E, Z, tess):
+    """rho per block by the C-ABI kernel ublr_tag_aspect (b x b dot products on
+    the GPU; the host form below is the CPU-test path)."""
+    import torch
+
+    from . import _lib
+    from .tessellation import device_tess
+    dt = device_tess(tess, torch.device("cuda"))
+    Ed, Zd = _lib.h2d(E, dt.device), _lib.h2d(Z, dt.device)
+    rho = torch.empty(tess.b, dtype=torch.float64, device=dt.device)
+    _lib.call("ublr_tag_aspect", _lib.ptr(Ed), _lib.ptr(Zd), E.shape[1], _lib.ptr(dt.nptr), _lib.ptr(dt.nidx),
+              tess.b, _lib.ptr(rho), _lib.stream_handle())
+    return rho.cpu().numpy()
+
+
+def _evaluate(T: TaggingMatrix, tess: Tessellation, attempts: int, device: bool = False) -> TaggingPlan:
     """ref/tagging.py:355-379 for optimize=False, batched."""
     E = T.entries
     Z, res, ok = batched_null_vectors(E, tess.neighbor_lists, csr=_neighbour_csr(tess))
     if not ok.all():
         i = int(np.flatnonzero(~ok)[0])
         raise DegenerateTagsError(f"block {i}: requested null space does not exist")
-    limit = 1e-12 * max(1.0, np.linalg.norm(E))
+    limit = 1e-12 * max(1.0, _fro(E))
     if (res > limit).any():
         i = int(np.flatnonzero(res > limit)[0])
         raise DegenerateTagsError(f"block {i}: null-vector residual {res[i]:.3e} exceeds {limit:.3e}")
     b = tess.b
+    nvs = NullVectors(Z, res)
+    if device:
+        return TaggingPlan(matrix=T, null_vectors=nvs, rho_base=_aspect_device(E, Z, tess), rho_optimized=None,
+                           attempts=attempts)
     ptr, idx = _neighbour_csr(tess)
     P = np.abs(E @ Z.T)                     # P[j, i] = |<t_j, z^(i)>|
     nl = np.diff(ptr)
@@ -237,15 +267,18 @@ def _evaluate(T: TaggingMatrix, tess: Tessellation, attempts: int) -> TaggingPla
     with np.errstate(divide="ignore", invalid="ignore"):
         r = np.where(hi == 0.0, 1.0, np.where(lo == 0.0, np.inf, hi / lo))
     rho[far_any] = r[far_any]
-    nvs = NullVectors(Z, res)
     return TaggingPlan(matrix=T, null_vectors=nvs, rho_base=rho, rho_optimized=None, attempts=attempts)
 
 
 def plan_tagging(tess, extra_cols=0, distribution="gaussian", stream=None, optimize=False,
-                 max_redraws=5, ratio_limit=1e6, extra_check=None, first=None) -> TaggingPlan:
+                 max_redraws=5, ratio_limit=1e6, extra_check=None, first=None, device=False) -> TaggingPlan:
     """Redraw policy of ref/tagging.py:306-352. `first` may carry the policy's
     first draw (make_tagging_matrix(..., stream.child(0))) when the caller has
-    already made it."""
+    already made it. `device`: aspect ratios by the GPU kernel; "auto" uses it
+    for b >= DEVICE_PLAN_MIN_B (the b x b host product dominates there, ~70 ms
+    per draw at b = 4096); False keeps the host form (CPU tests)."""
+    if device == "auto":
+        device = tess.b >= DEVICE_PLAN_MIN_B
     if optimize:
         raise NotImplementedError("null-vector optimisation (ref/tagging.py:142-292) is outside the B200 hot path")
     stream = stream or RandomStream(0)
@@ -259,7 +292,7 @@ def plan_tagging(tess, extra_cols=0, distribution="gaussian", stream=None, optim
             last = DegenerateTagsError("extra_check rejected the draw")
             continue
         try:
-            plan = _evaluate(T, tess, attempt + 1)
+            plan = _evaluate(T, tess, attempt + 1, device=device)
         except DegenerateTagsError as exc:
             last = exc
             continue
@@ -278,7 +311,7 @@ def pair_vectors(T_entries: np.ndarray, tess: Tessellation, denom_rtol: float = 
     """Per near pair p = (i, j) in neighbour-CSR order: unit null vector of
     T(N_i \\ {j}, :) and denominator <t_j, z> (ref/reconstruction.py:344-355).
     Raises DegenerateTagsError like the reference."""
-    limit = denom_rtol * max(1.0, np.linalg.norm(T_entries))
+    limit = denom_rtol * max(1.0, _fro(T_entries))
     sets, excl = [], []
     for i, nb in enumerate(tess.neighbor_lists):
         for j in nb:

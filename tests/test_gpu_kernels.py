@@ -276,3 +276,21 @@ def test_coupling_matches_numpy(kind, k, per, nb):
             ref = Uh[off[i]:off[i + 1], :ki].T @ A @ Vh[off[j]:off[j + 1], :kj]
             got = core[roff[i]:roff[i + 1], roff[j]:roff[j + 1]]
             assert np.abs(got - ref).max() <= 1e-11 * max(1.0, np.abs(ref).max()), (i, j)
+
+
+@pytest.mark.parametrize("per,nb,d", [(64, 64, 2), (256, 1024, 2), (16, 64, 3)])
+def test_tag_aspect_device_matches_host(per, nb, d):
+    """GPU aspect ratios (ublr_tag_aspect) against the host |T Z^T| form, and
+    the same redraw decisions for the whole policy."""
+    from paper_2501_05528_b200.tagging import _evaluate, make_tagging_matrix
+    tess = P.build_tessellation(P.grid_points(per, d), nb)
+    T = make_tagging_matrix(tess.b, d, 0, "gaussian", P.RandomStream(3).child(1).child(0))
+    h = _evaluate(T, tess, 1, device=False).rho_base
+    g = _evaluate(T, tess, 1, device=True).rho_base
+    assert np.array_equal(np.isnan(h), np.isnan(g))
+    fin = np.isfinite(h)
+    assert np.array_equal(fin, np.isfinite(g))
+    assert np.allclose(g[fin], h[fin], rtol=1e-12, atol=0)
+    ph = P.plan_tagging(tess, 0, "gaussian", P.RandomStream(3).child(1))
+    pg = P.plan_tagging(tess, 0, "gaussian", P.RandomStream(3).child(1), device=True)
+    assert ph.attempts == pg.attempts and np.array_equal(ph.matrix.entries, pg.matrix.entries)

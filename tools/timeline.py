@@ -7,9 +7,19 @@ import torch
 import paper_2501_05528_b200 as P
 from paper_2501_05528_b200 import _lib, workloads as W
 
-wl = W.build(sys.argv[1] if len(sys.argv) > 1 else "c2")
+cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
+wl = W.build(cfg)
 run = lambda: P.compress(wl.op, wl.tess, wl.k, wl.method, p=wl.p, stream=P.RandomStream(7), compute_error=False)
-for _ in range(5):
+if cfg == "c5":   # one rank's share of an 8-way job (bench.py run_sharded step)
+    from paper_2501_05528_b200.distributed import phase1_local, phase23_local, shard_ranges
+    sh = shard_ranges(wl.tess, 8, wl.k)[3]
+    V_all = torch.zeros((wl.tess.n_points, wl.k), dtype=torch.float64, device="cuda")
+
+    def run():
+        plan, U, V, dt = phase1_local(wl.op, wl.tess, wl.k, wl.p, P.RandomStream(W.COMPRESS_SEED), sh)
+        V_all[sh.r0:sh.r1] = V
+        phase23_local(wl.op, wl.k, sh, dt, U, V_all)
+for _ in range(2 if cfg == "c5" else 5):
     run()
 torch.cuda.synchronize()
 orig = _lib.call
