@@ -814,6 +814,267 @@ __global__ void __launch_bounds__(Cfg::NT, 1) k_sketch_tagged3(ublr_op_t op, con
   if (warp == 0) tmem::dealloc(tbase, 512);
 }
 
+
+// ------------------------------------------------- tagged sketch v4 (warp-specialised)
+// Same product as v3 (Y(I, c gc + q) = sum_j T[j,c] (A_Ij G_j)(:, q), both
+// sides) with the roles split: 8 producer warps generate the BM x BK A tile
+// (kernel operators) and cp.async the BK x BN [G | H] panel into a STAGES-deep
+// full/empty mbarrier ring; 8 consumer warps (2 x 4, warp tile 16 x BN/4) run
+// the DMMAs and, after the last k-step of every block j, fold W into the ell
+// tag groups (TG of them in TMEM, the rest in registers). Producers run ahead
+// across block boundaries while the consumers fold.
+template <int BN_, int STAGES_>
+struct Sk4Cfg {
+  static constexpr int BM = 32, BN = BN_, BK = 16, STAGES = STAGES_;
+  static constexpr int NPROD = 256, NCONS = 256, NT = NPROD + NCONS;
+  static constexpr int WMW = 2, WNW = 4, WM = BM / WMW, WN = BN / WNW, MI = WM / 8, NJ = WN / 8;
+  static constexpr int SA = BM + 4, SB = BN + 4;
+  static constexpr int A_STAGE = BK * SA, B_STAGE = BK * SB;
+  static constexpr int CONS_REGS = 200, PROD_REGS = 56;
+  static constexpr size_t smem_bytes() { return (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double); }
+};
+
+template <int KIND, int DIM, int L, class C>
+__global__ void __launch_bounds__(C::NT, 1) k_sketch_tagged4(ublr_op_t op, const int32_t* __restrict__ off, int b,
+                                                             const double* __restrict__ T, int ell,
+                                                             const double* __restrict__ G,
+                                                             const double* __restrict__ H, int64_t ldx, int gc,
+                                                             double* __restrict__ Y, double* __restrict__ Z,
+                                                             int64_t ldy, int row_begin, int row_end) {
+  constexpr int BM = C::BM, BN = C::BN, BK = C::BK, STAGES = C::STAGES, SA = C::SA, SB = C::SB;
+  constexpr int MI = C::MI, NJ = C::NJ;
+  constexpr int WD = MI * NJ * 2;                       // W doubles per consumer thread
+  constexpr int WCOLS = 512 / (C::NCONS / 32 / 4);      // TMEM columns per consumer warp
+  constexpr int WDP = (WD + 7) / 8 * 8;
+  constexpr int TCAP = (WCOLS / 2) / WDP;
+  constexpr int TG = (L < TCAP) ? L : TCAP;
+  constexpr int RG = L - TG;
+  __shared__ LogTables lt;
+  __shared__ uint64_t full[STAGES], empty[STAGES];
+  __shared__ uint32_t tbase_slot;
+  extern __shared__ double dsm[];
+  double* As0 = dsm;
+  double* Bs0 = dsm + STAGES * C::A_STAGE;
+  const int ncols = (H ? 2 : 1) * gc;
+  const int row0 = row_begin + blockIdx.x * BM;
+  const int col0 = blockIdx.y * BN;
+  const int n = (int)op.n;
+  if (KIND == UBLR_OP_LOG) init_log_tables(&lt);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      ws::mbar_init(&full[s], 2 * C::NPROD);
+      ws::mbar_init(&empty[s], C::NCONS);
+    }
+  }
+  if (threadIdx.x / 32 == C::NPROD / 32) tmem::alloc(&tbase_slot, 512);  // first consumer warp
+  tmem::fence_before();
+  __syncthreads();
+  tmem::fence_after();
+  const uint32_t tbase = tbase_slot;
+
+  if (threadIdx.x < C::NPROD) {
+    // ---------------- producers
+    ws::regs_dec<C::PROD_REGS>();
+    const int p = threadIdx.x;
+    const int r = p % BM;               // A-tile row
+    const int kq = p / BM;              // k lane (BM x BK / NPROD = 2 entries per thread: kq, kq + 8)
+    constexpr int KL = C::NPROD / BM;
+    constexpr int EPT = BK / KL;
+    const bool rok = row0 + r < row_end;
+    const RowPoint rp = load_row_point(op, rok ? row0 + r : row_begin, true);
+    const double diag = op.diag;
+    // panel pair slots, fixed for the kernel (see v3)
+    constexpr int HALF = BN / 2;
+    constexpr int PPT = (BK * HALF + C::NPROD - 1) / C::NPROD;
+    const double* bsrc[PPT];
+    int bmeta[PPT];
+#pragma unroll
+    for (int z = 0; z < PPT; ++z) {
+      const int e = p + z * C::NPROD;
+      const int kk = e / HALF, c = 2 * (e % HALF);
+      const int col = col0 + c;
+      const bool valid = e < BK * HALF && col < ncols;
+      bsrc[z] = ((col < gc || !H) ? G + col : H + (col - gc)) + (int64_t)kk * ldx;
+      bmeta[z] = (kk * SB + c) | (kk << 16) | (valid ? (1 << 30) : 0);
+    }
+    int it = 0;
+    for (int j = 0; j < b; ++j) {
+      const int qe = off[j + 1];
+      for (int q0 = off[j]; q0 < qe; q0 += BK, ++it) {
+        const int s = it % STAGES;
+        double v[EPT];
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) {
+          const int q = q0 + kq + e * KL;
+          const bool ok = q < qe;
+          const int qc = ok ? q : q0;
+          const double c0 = __ldg(op.coords + qc);
+          const double c1 = DIM > 1 ? __ldg(op.coords + n + qc) : 0.0;
+          const double c2 = DIM > 2 ? __ldg(op.coords + 2 * n + qc) : 0.0;
+          const double a = kernel_entry_dim<KIND, DIM>(rp, qc, c0, c1, c2, diag, &lt);
+          v[e] = ok ? a : 0.0;
+        }
+        ws::mbar_wait(&empty[s], ((uint32_t)(it / STAGES) & 1) ^ 1);
+        double* Bs = Bs0 + s * C::B_STAGE;
+        const int64_t roff = (int64_t)q0 * ldx;
+#pragma unroll
+        for (int z = 0; z < PPT; ++z) {
+          const int meta = bmeta[z];
+          const bool ok = (meta >> 30) && q0 + ((meta >> 16) & 0x3fff) < qe;
+          cp_async16(Bs + (meta & 0xffff), ok ? (const void*)(bsrc[z] + roff) : (const void*)G, ok);
+        }
+        cp_async_commit();
+        ws::mbar_cp_async_arrive(&full[s]);
+        double* As = As0 + s * C::A_STAGE;
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) As[(kq + e * KL) * SA + r] = v[e];
+        ws::mbar_arrive(&full[s]);
+      }
+    }
+    cp_async_wait<0>();
+  } else {
+    // ---------------- consumers
+    ws::regs_inc<C::CONS_REGS>();
+    const int ct = threadIdx.x - C::NPROD;
+    const int warp = ct >> 5, lane = ct & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int wr = warp / C::WNW, wc = warp % C::WNW;
+    const int am0 = wr * C::WM + g, bn0 = wc * C::WN + g;
+    const int twarp = warp;                       // lane quarter = warp & 3
+    const int colbase = (warp >> 2) * WCOLS;
+    double w[MI][NJ][2];
+    double racc[RG > 0 ? RG : 1][MI][NJ][2];
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+      for (int jj = 0; jj < NJ; ++jj) {
+        w[i][jj][0] = w[i][jj][1] = 0.0;
+#pragma unroll
+        for (int c = 0; c < (RG > 0 ? RG : 1); ++c) racc[c][i][jj][0] = racc[c][i][jj][1] = 0.0;
+      }
+    {
+      double z8[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) z8[q] = 0.0;
+#pragma unroll
+      for (int c = 0; c < TG; ++c)
+#pragma unroll
+        for (int h = 0; h < WDP / 8; ++h) tmem::st8(tmem::addr(tbase, twarp, colbase + (c * WDP + h * 8) * 2), z8);
+      tmem::wait_st();
+    }
+    int it = 0;
+    for (int j = 0; j < b; ++j) {
+      const int qe = off[j + 1];
+      for (int q0 = off[j]; q0 < qe; q0 += BK, ++it) {
+        const int s = it % STAGES;
+        ws::mbar_wait(&full[s], (uint32_t)(it / STAGES) & 1);
+        const double* As = As0 + s * C::A_STAGE;
+        const double* Bs = Bs0 + s * C::B_STAGE;
+        double a[2][MI], bb[2][NJ];
+#pragma unroll
+        for (int i = 0; i < MI; ++i) a[0][i] = As[t * SA + am0 + i * 8];
+#pragma unroll
+        for (int jj = 0; jj < NJ; ++jj) bb[0][jj] = Bs[t * SB + bn0 + jj * 8];
+#pragma unroll
+        for (int k4 = 0; k4 < BK / 4; ++k4) {
+          const int cur = k4 & 1;
+          if (k4 + 1 < BK / 4) {
+            const int kr = (k4 + 1) * 4 + t;
+#pragma unroll
+            for (int i = 0; i < MI; ++i) a[cur ^ 1][i] = As[kr * SA + am0 + i * 8];
+#pragma unroll
+            for (int jj = 0; jj < NJ; ++jj) bb[cur ^ 1][jj] = Bs[kr * SB + bn0 + jj * 8];
+          }
+#pragma unroll
+          for (int i = 0; i < MI; ++i)
+#pragma unroll
+            for (int jj = 0; jj < NJ; ++jj) mma8x8x4(w[i][jj][0], w[i][jj][1], a[cur][i], bb[cur][jj]);
+        }
+        ws::mbar_arrive(&empty[s]);
+      }
+      // block j complete: acc_c += T[j, c] W
+      const double* Tj = T + (int64_t)j * ell;
+      double wf[WDP];
+#pragma unroll
+      for (int q = WD; q < WDP; ++q) wf[q] = 0.0;
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int jj = 0; jj < NJ; ++jj) {
+          wf[(i * NJ + jj) * 2] = w[i][jj][0];
+          wf[(i * NJ + jj) * 2 + 1] = w[i][jj][1];
+          w[i][jj][0] = w[i][jj][1] = 0.0;
+        }
+#pragma unroll
+      for (int c = 0; c < TG; ++c) {
+        const double tc = (c < ell) ? __ldg(&Tj[c]) : 0.0;
+#pragma unroll
+        for (int h = 0; h < WDP / 8; ++h) {
+          double v[8];
+          const uint32_t ta = tmem::addr(tbase, twarp, colbase + (c * WDP + h * 8) * 2);
+          tmem::ld8(ta, v);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) v[q] = fma(tc, wf[h * 8 + q], v[q]);
+          tmem::st8(ta, v);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < RG; ++c) {
+        const double tc = (TG + c < ell) ? __ldg(&Tj[TG + c]) : 0.0;
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+          for (int jj = 0; jj < NJ; ++jj) {
+            racc[c][i][jj][0] = fma(tc, wf[(i * NJ + jj) * 2], racc[c][i][jj][0]);
+            racc[c][i][jj][1] = fma(tc, wf[(i * NJ + jj) * 2 + 1], racc[c][i][jj][1]);
+          }
+      }
+    }
+    tmem::wait_st();
+    // epilogue: Y / Z rows of this warp
+#pragma unroll
+    for (int c = 0; c < L; ++c) {
+      if (c >= ell) break;
+      double accv[WDP];
+      if (c < TG) {
+#pragma unroll
+        for (int h = 0; h < WDP / 8; ++h) {
+          double v[8];
+          tmem::ld8(tmem::addr(tbase, twarp, colbase + (c * WDP + h * 8) * 2), v);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) accv[h * 8 + q] = v[q];
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+          for (int jj = 0; jj < NJ; ++jj) {
+            accv[(i * NJ + jj) * 2] = racc[(c - TG) < 0 ? 0 : (c - TG)][i][jj][0];
+            accv[(i * NJ + jj) * 2 + 1] = racc[(c - TG) < 0 ? 0 : (c - TG)][i][jj][1];
+          }
+      }
+#pragma unroll
+      for (int i = 0; i < MI; ++i) {
+        const int row = row0 + wr * C::WM + i * 8 + g;
+        if (row >= row_end) continue;
+#pragma unroll
+        for (int jj = 0; jj < NJ; ++jj)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int col = col0 + wc * C::WN + jj * 8 + 2 * t + h;
+            if (col >= ncols) continue;
+            double* dst = (col < gc) ? Y : Z;
+            const int q = (col < gc) ? col : col - gc;
+            dst[(int64_t)row * ldy + c * gc + q] = accv[(i * NJ + jj) * 2 + h];
+          }
+      }
+    }
+  }
+  tmem::fence_before();
+  __syncthreads();
+  tmem::fence_after();
+  if (threadIdx.x / 32 == C::NPROD / 32) tmem::dealloc(tbase, 512);
+}
 }  // namespace
 }  // namespace ublr
 
@@ -894,10 +1155,24 @@ int sketch_common_v3(const ublr_op_t* op, const int32_t* off, int b, const doubl
   const int ncols = (H ? 2 : 1) * gc;
   int vec2 = ((ld_x % 2) == 0 && ((uintptr_t)G) % 16 == 0 && (!H || ((uintptr_t)H) % 16 == 0)) ? 1 : 0;
   dim3 grid;
+  static const int ts_cfg = [] {
+    const char* e = getenv("UBLR_SKETCH_CFG");
+    return e ? atoi(e) : 0;
+  }();
 #define UBLR_TS3(L, BNv)                                                                                        \
-  {                                                                                                             \
+  { if (ts_cfg == 1 && (BNv) == 128) {                                                                          \
+    using Cfg = TileCfg<32, BNv, 32, 2, 4, 2>;                                                                  \
+    UBLR_TS3_LAUNCH(L)                                                                                          \
+  } else if (ts_cfg == 2 && (BNv) == 128) {                                                                     \
+    using Cfg = TileCfg<32, BNv, 32, 2, 4, 3>;                                                                  \
+    UBLR_TS3_LAUNCH(L)                                                                                          \
+  } else {                                                                                                      \
     using Cfg = TileCfg<32, BNv, 32, 2, 8, 2>;                                                                  \
-    grid.y = (unsigned)((ncols + (BNv) - 1) / (BNv));                                                           \
+    UBLR_TS3_LAUNCH(L)                                                                                          \
+  } }
+#define UBLR_TS3_LAUNCH(L)                                                                                      \
+  {                                                                                                             \
+    grid.y = (unsigned)((ncols + Cfg::BN - 1) / Cfg::BN);                                                        \
     grid.x = (unsigned)((row_end - row_begin + 31) / 32);                                                       \
     UBLR_DISPATCH_KIND(op->kind, KIND, {                                                                        \
       size_t sm = Cfg::smem_bytes();                                                                            \
@@ -913,6 +1188,41 @@ int sketch_common_v3(const ublr_op_t* op, const int32_t* off, int b, const doubl
     if (ell <= 4) UBLR_TS3(4, 128) else UBLR_TS3(10, 128)
   }
 #undef UBLR_TS3
+#undef UBLR_TS3_LAUNCH
+  UBLR_LAUNCH_CHECK();
+  return UBLR_OK;
+}
+
+int sketch_common_v4(const ublr_op_t* op, const int32_t* off, int b, const double* T, int ell, const double* G,
+                     const double* H, int64_t ld_x, int gc, double* Y, double* Z, int64_t ld_y, int row_begin,
+                     int row_end, cudaStream_t st) {
+  const int ncols = (H ? 2 : 1) * gc;
+  dim3 grid((unsigned)((row_end - row_begin + 31) / 32), 0);
+#define UBLR_TS4(KIND, DIM, L, BNv)                                                                              \
+  {                                                                                                              \
+    using C = Sk4Cfg<BNv, 6>;                                                                                    \
+    grid.y = (unsigned)((ncols + C::BN - 1) / C::BN);                                                            \
+    size_t sm = C::smem_bytes();                                                                                 \
+    UBLR_CUDA(cudaFuncSetAttribute(k_sketch_tagged4<KIND, DIM, L, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                   (int)sm));                                                                   \
+    k_sketch_tagged4<KIND, DIM, L, C><<<grid, C::NT, sm, st>>>(*op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y,   \
+                                                               row_begin, row_end);                              \
+  }
+#define UBLR_TS4_L(KIND, DIM)                                                                                    \
+  {                                                                                                              \
+    if (ncols <= 64) {                                                                                           \
+      if (ell <= 4) UBLR_TS4(KIND, DIM, 4, 64) else UBLR_TS4(KIND, DIM, 10, 64)                                  \
+    } else {                                                                                                     \
+      if (ell <= 4) UBLR_TS4(KIND, DIM, 4, 128) else UBLR_TS4(KIND, DIM, 10, 128)                                \
+    }                                                                                                            \
+  }
+  if (op->kind == UBLR_OP_LOG) {
+    if (op->dim == 1) UBLR_TS4_L(UBLR_OP_LOG, 1) else if (op->dim == 2) UBLR_TS4_L(UBLR_OP_LOG, 2) else UBLR_TS4_L(UBLR_OP_LOG, 3)
+  } else {
+    if (op->dim == 1) UBLR_TS4_L(UBLR_OP_INV, 1) else if (op->dim == 2) UBLR_TS4_L(UBLR_OP_INV, 2) else UBLR_TS4_L(UBLR_OP_INV, 3)
+  }
+#undef UBLR_TS4_L
+#undef UBLR_TS4
   UBLR_LAUNCH_CHECK();
   return UBLR_OK;
 }
@@ -922,8 +1232,14 @@ int sketch_common(const ublr_op_t* op, const int32_t* off, int b, const double* 
                   int row_end, cudaStream_t st) {
   UBLR_REQUIRE(row_begin >= 0 && row_begin < row_end && row_end <= op->n, UBLR_ERR_VALUE, "sketch: bad row range");
   static const char* ver = getenv("UBLR_SKETCH_VERSION");
-  const int v = ver ? atoi(ver) : 3;
-  if (v == 3 && ell <= 10) return sketch_common_v3(op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y, row_begin, row_end, st);
+  const int v = ver ? atoi(ver) : 4;
+  const bool vec_ok = (ld_x % 2) == 0 && (gc % 2) == 0 && ((uintptr_t)G) % 16 == 0 && (!H || ((uintptr_t)H) % 16 == 0);
+  // v4 (warp-specialised) where the entry evaluation is expensive (table log,
+  // ~22 FP64 ops): c2 0.246 -> 0.210 ms, c4 325 -> 274 ms; for 1/r (~9 ops) the
+  // synchronous v3 with 16 DMMA warps stays faster (c5 shard 1.98 s vs 2.09 s)
+  if (v == 4 && ell <= 10 && op->kind == UBLR_OP_LOG && vec_ok)
+    return sketch_common_v4(op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y, row_begin, row_end, st);
+  if (v >= 3 && ell <= 10) return sketch_common_v3(op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y, row_begin, row_end, st);
   return sketch_common_v1(op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y, row_begin, row_end, st);
 }
 
