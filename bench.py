@@ -19,6 +19,7 @@ reference algorithm (oracle/, numpy + OpenBLAS on all host cores).
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -303,7 +304,7 @@ def run_sharded(args, rank, world, local):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=None, help="timed steps (default: 30 for c1/c2, 5 for c3-c5)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
@@ -312,6 +313,8 @@ def main():
     ap.add_argument("--shard-rank", type=int, default=3, help="c5 on one GPU: which shard to time")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.steps is None:
+        args.steps = 30 if args.config in ("c1", "c2") else 5
     rank, world, local = dist_env()
 
     if args.impl == "reference":
@@ -362,6 +365,8 @@ def main():
     _lib.instrument(True, only={dominant} if dominant else None)
     launches0 = _lib.launch_count
     step_ms = []
+    gc.collect()
+    gc.disable()   # no collector pauses inside millisecond steps (re-enabled below)
     with ClockSampler(local) as clocks:
         for _ in range(args.steps):
             flush_l2(l2buf)
@@ -372,6 +377,7 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             step_ms.append(e0.elapsed_time(e1))
+    gc.enable()
     ev = _lib.event_times()
     _lib.instrument(False)
     launches = (_lib.launch_count - launches0) // args.steps
@@ -419,11 +425,13 @@ def main():
             "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {**wl.describe(), "parallelism": f"replicas{world}" if world > 1 else "single",
-                       "l2": "flushed between timed steps (256 MB write)"},
+                       "l2": "flushed between timed steps (256 MB write)", "python_gc": "disabled in the timed loop"},
             "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(launches),
             "roofline": roof,
             "kernel_ms_per_step": kernel_ms,
+            "step_ms": {"min": float(np.min(step_ms)), "median": float(np.median(step_ms)),
+                        "max": float(np.max(step_ms))},
             "phase_s": dict(report.times_s),
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,

@@ -99,6 +99,11 @@ int ublr_null_vectors(const double* T, int ell, const int32_t* ptr, const int32_
  * the far field is empty. ell <= 32. */
 int ublr_tag_aspect(const double* T, const double* Z, int ell, const int32_t* nptr, const int32_t* nidx, int b,
                     double* rho, void* stream);
+/* One evaluation of the tagging redraw policy on the host: null vectors Z and
+ * residuals res (ublr_null_vectors), scale[i] = max(1, ||T[rows_i]||_F), and
+ * (if rho != NULL) the aspect ratios as ublr_tag_aspect. Host pointers. */
+int ublr_tag_plan_host(const double* T, int ell, const int32_t* ptr, const int32_t* idx, int b, double* Z,
+                       double* res, double* scale, double* rho);
 
 /* K1 — ref/linalg.py:38-52 (`RandomStream.normal` / `gaussian`), called at
  * ref/bases.py:97-98, :163-168, :229-230 and ref/reconstruction.py:405.

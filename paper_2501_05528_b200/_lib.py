@@ -44,6 +44,7 @@ SIGNATURES = {
     "ublr_device_check": (INT, []),
     "ublr_seedseq_keys": (INT, [P, INT, P, INT, P, INT, I64, P]),
     "ublr_null_vectors": (INT, [P, INT, P, P, INT, P, P]),
+    "ublr_tag_plan_host": (INT, [P, INT, P, P, INT, P, P, P, P]),
     "ublr_tag_aspect": (INT, [P, P, INT, P, P, INT, P, P]),
     "ublr_rng_workspace_bytes": (I64, [P, INT]),
     "ublr_rng_normals": (INT, [P, P, INT, P, P, I64, P]),
@@ -109,7 +110,7 @@ def check(rc: int, what: str = ""):
 
 
 # kernels each C-ABI entry point launches (for bench.py's `gpu_launches`)
-LAUNCHES = {"ublr_rng_normals": 7, "ublr_sketch_tagged": 1, "ublr_sketch_tagged_pair": 1, "ublr_apply": 1,
+LAUNCHES = {"ublr_rng_normals": 8, "ublr_sketch_tagged": 1, "ublr_sketch_tagged_pair": 1, "ublr_apply": 1,
             "ublr_block_qr": 1, "ublr_block_qr_pair": 1, "ublr_coupling": 1, "ublr_nearfield_colour": 2,
             "ublr_blr_apply": 3, "ublr_gemm_batched": 1, "ublr_potrf_diag": 1, "ublr_lu_sign_diag": 1,
             "ublr_lu_sign_diag_r": 1, "ublr_syrk_upper_batched": 1, "ublr_add_scaled_rows": 1,
@@ -212,15 +213,77 @@ def ptr(t) -> int:
     return 0 if t is None else int(t.data_ptr())
 
 
+class _PinnedRing:
+    """Small host->device transfers staged through a ring of pinned slots.
+    A slot is reused only after the copy that last read it has completed
+    (its CUDA event), so the caller never blocks on the GPU in practice and a
+    pageable copy (which would wait for all queued work) is never issued."""
+
+    SLOT = 1 << 20
+    NSLOT = 16
+
+    def __init__(self):
+        import torch
+        self.buf = torch.empty(self.SLOT * self.NSLOT, dtype=torch.uint8, pin_memory=True)
+        self.np = self.buf.numpy()
+        self.events = [torch.cuda.Event() for _ in range(self.NSLOT)]
+        self.used = [False] * self.NSLOT
+        self.i = 0
+
+    def h2d(self, a, device):
+        import torch
+        a = np.ascontiguousarray(a)
+        nb = a.nbytes
+        if nb > self.SLOT or nb == 0:
+            t = torch.from_numpy(a)
+            return t.pin_memory().to(device, non_blocking=True) if nb else t.to(device)
+        s = self.i
+        self.i = (self.i + 1) % self.NSLOT
+        if self.used[s]:
+            self.events[s].synchronize()
+        off = s * self.SLOT
+        view = self.np[off:off + nb].view(a.dtype).reshape(a.shape)
+        view[...] = a
+        out = torch.from_numpy(view).to(device, non_blocking=True)
+        self.events[s].record()
+        self.used[s] = True
+        return out
+
+
+_ring = None
+
+
 def h2d(a, device):
-    """Host array -> device tensor without blocking the host: staged through
-    torch's pinned-memory cache and copied with non_blocking=True (a pageable
-    copy would wait for all work queued before it)."""
-    import torch
-    t = torch.from_numpy(np.ascontiguousarray(a))
-    return t.pin_memory().to(device, non_blocking=True)
+    """Host array -> device tensor without blocking the host (pinned staging
+    ring, non_blocking copy on the current stream)."""
+    global _ring
+    if _ring is None:
+        _ring = _PinnedRing()
+    return _ring.h2d(a, device)
+
+
+_stream_cached = None
+
+
+class stream_scope:
+    """Within the scope, stream_handle() returns the current stream captured
+    at entry (torch.cuda.current_stream() costs ~10 us per call; a compression
+    issues dozens of launches on one stream)."""
+
+    def __enter__(self):
+        global _stream_cached
+        import torch
+        self._prev = _stream_cached
+        _stream_cached = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        return self
+
+    def __exit__(self, *exc):
+        global _stream_cached
+        _stream_cached = self._prev
 
 
 def stream_handle():
+    if _stream_cached is not None:
+        return _stream_cached
     import torch
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)

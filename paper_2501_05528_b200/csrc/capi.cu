@@ -88,14 +88,23 @@ extern "C" int ublr_null_vectors(const double* T, int ell, const int32_t* ptr, c
                                  double* Z, double* res) {
   UBLR_REQUIRE(T && ell >= 1 && ptr && idx && nsets >= 0 && Z && res, UBLR_ERR_VALUE,
                "ublr_null_vectors: bad arguments");
-  std::vector<double> A, tau;
+  // column-major ell x sz work matrix A[i + j*ell] = T[idx[r0+j], i]; fixed
+  // storage for the usual ell <= 32 (no per-set allocation)
+  std::vector<double> Aheap, tauheap;
+  double Afix[32 * 32], taufix[32];
+  const bool small = ell <= 32;
+  if (!small) {
+    Aheap.resize((size_t)ell * ell);
+    tauheap.resize(ell);
+  }
+  double* A = small ? Afix : Aheap.data();
+  double* tau = small ? taufix : tauheap.data();
   for (int s = 0; s < nsets; ++s) {
     const int r0 = ptr[s], sz = ptr[s + 1] - ptr[s];
     UBLR_REQUIRE(sz >= 0 && sz < ell, UBLR_ERR_VALUE, "ublr_null_vectors: a set has >= ell rows (no null vector)");
-    A.assign((size_t)ell * sz, 0.0);  // column-major ell x sz: A[i + j*ell] = T[idx[r0+j], i]
     for (int j = 0; j < sz; ++j)
       for (int i = 0; i < ell; ++i) A[i + (size_t)j * ell] = T[(size_t)idx[r0 + j] * ell + i];
-    tau.assign(sz, 0.0);
+    for (int j = 0; j < sz; ++j) tau[j] = 0.0;
     for (int j = 0; j < sz; ++j) {
       double* col = &A[(size_t)j * ell];
       const double alpha = col[j];
@@ -142,6 +151,48 @@ extern "C" int ublr_null_vectors(const double* T, int ell, const int32_t* ptr, c
       r2 += d * d;
     }
     res[s] = sqrt(r2);
+  }
+  return UBLR_OK;
+}
+
+// One redraw-policy evaluation on the host (ref/tagging.py:355-379 with
+// :110-139): null vectors and residuals (ublr_null_vectors), the residual
+// scale max(1, ||T[rows]||_F) per set, and the aspect ratios rho_i over the
+// far field of block i (1 if the max is 0, inf if the min is 0, NaN for an
+// empty far field). The Python planner is a thin wrapper around it; for
+// b >= 1024 the aspect ratios run on the GPU (ublr_tag_aspect) instead.
+extern "C" int ublr_tag_plan_host(const double* T, int ell, const int32_t* ptr, const int32_t* idx, int b,
+                                  double* Z, double* res, double* scale, double* rho) {
+  int rc = ublr_null_vectors(T, ell, ptr, idx, b, Z, res);
+  if (rc) return rc;
+  std::vector<double> rn2(b);
+  for (int j = 0; j < b; ++j) {
+    double s2 = 0.0;
+    for (int c = 0; c < ell; ++c) s2 += T[(size_t)j * ell + c] * T[(size_t)j * ell + c];
+    rn2[j] = s2;
+  }
+  std::vector<char> nearm(b, 0);
+  for (int i = 0; i < b; ++i) {
+    double seg = 0.0;
+    for (int p = ptr[i]; p < ptr[i + 1]; ++p) seg += rn2[idx[p]];
+    scale[i] = fmax(1.0, sqrt(seg));
+    if (!rho) continue;
+    for (int p = ptr[i]; p < ptr[i + 1]; ++p) nearm[idx[p]] = 1;
+    const double* z = Z + (size_t)i * ell;
+    double lo = INFINITY, hi = -INFINITY;
+    for (int j = 0; j < b; ++j) {
+      if (nearm[j]) continue;
+      double d = 0.0;
+      for (int c = 0; c < ell; ++c) d += T[(size_t)j * ell + c] * z[c];  // host: no libm fma call
+      d = fabs(d);
+      lo = fmin(lo, d);
+      hi = fmax(hi, d);
+    }
+    for (int p = ptr[i]; p < ptr[i + 1]; ++p) nearm[idx[p]] = 0;
+    if (ptr[i + 1] - ptr[i] >= b) rho[i] = NAN;
+    else if (hi == 0.0) rho[i] = 1.0;
+    else if (lo == 0.0) rho[i] = INFINITY;
+    else rho[i] = hi / lo;
   }
   return UBLR_OK;
 }

@@ -307,6 +307,37 @@ __global__ void k_rng_serial(RngPlan P, double* out) {
 inline int64_t words_for(int64_t count) { return count + count / 24 + 256; }
 inline int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 
+// chunk_start[s] = sum_{t < s} ceil(words(count_t) / C), from the device
+// stream records (one block; replaces a pageable host->device copy, which
+// would block the host behind queued work)
+__global__ void k_chunk_starts(const ublr_rng_stream_t* __restrict__ streams, int n, int64_t* __restrict__ out,
+                               int* __restrict__ flag) {
+  __shared__ int64_t part[1024];
+  const int T = blockDim.x;
+  const int per = (n + T - 1) / T;
+  const int s0 = threadIdx.x * per, s1 = min(n, s0 + per);
+  int64_t sum = 0;
+  for (int s = s0; s < s1; ++s) sum += (streams[s].count + streams[s].count / 24 + 256 + C - 1) / C;
+  part[threadIdx.x] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t run = 0;
+    for (int t = 0; t < T; ++t) {
+      const int64_t v = part[t];
+      part[t] = run;
+      run += v;
+    }
+    out[n] = run;
+    *flag = 0;
+  }
+  __syncthreads();
+  int64_t run = part[threadIdx.x];
+  for (int s = s0; s < s1; ++s) {
+    out[s] = run;
+    run += (streams[s].count + streams[s].count / 24 + 256 + C - 1) / C;
+  }
+}
+
 struct Layout {
   int64_t n_chunks, chunk_start_off, summary_off, counts_off, prefix_off, bsum_off, total_off, flag_off, bytes;
 };
@@ -349,13 +380,9 @@ extern "C" int ublr_rng_normals(const ublr_rng_stream_t* streams_dev, const int6
   UBLR_REQUIRE(workspace_bytes >= L.bytes, UBLR_ERR_VALUE, "rng workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
   char* ws = (char*)workspace;
-  // host-computed chunk starts (tiny) -> workspace
-  std::string hstarts((size_t)8 * (n_streams + 1), '\0');
-  int64_t* hs = (int64_t*)hstarts.data();
-  hs[0] = 0;
-  for (int s = 0; s < n_streams; ++s) hs[s + 1] = hs[s] + (words_for(counts_host[s]) + C - 1) / C;
-  UBLR_CUDA(cudaMemcpyAsync(ws + L.chunk_start_off, hs, 8 * (n_streams + 1), cudaMemcpyHostToDevice, st));
-  UBLR_CUDA(cudaMemsetAsync(ws + L.flag_off, 0, 8, st));
+  // chunk starts and the fallback flag, computed on the device
+  k_chunk_starts<<<1, 1024, 0, st>>>(streams_dev, n_streams, (int64_t*)(ws + L.chunk_start_off), (int*)(ws + L.flag_off));
+  UBLR_LAUNCH_CHECK();
   RngPlan P;
   P.streams = streams_dev;
   P.chunk_start = (const int64_t*)(ws + L.chunk_start_off);

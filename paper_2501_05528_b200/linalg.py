@@ -109,6 +109,17 @@ def device_normals_keys(seed, keys, rows, cols, offsets, ld, rowmap, out, suffix
     from .seedseq import philox_keys, philox_keys_suffixed
 
     _lib.require_device()
+    # the stream records (keys, counts, layout) are a pure function of the
+    # arguments: built and uploaded once, the normals are drawn every call
+    ck = (int(seed), tuple(keys) if suffix is not None else tuple(map(tuple, keys)),
+          np.asarray(rows, dtype=np.int64).tobytes(), int(cols), np.asarray(offsets, dtype=np.int64).tobytes(),
+          int(ld), _lib.ptr(rowmap), None if suffix is None else np.asarray(suffix).tobytes(), str(out.device))
+    hit = _RNG_CACHE.get(ck)
+    if hit is not None:
+        rec_d, counts, ns, ws, ws_bytes = hit
+        _lib.call("ublr_rng_normals", _lib.ptr(rec_d), counts.ctypes.data, ns, _lib.ptr(out), _lib.ptr(ws), ws_bytes,
+                  _lib.stream_handle())
+        return out
     if suffix is not None:
         kk = philox_keys_suffixed(seed, keys, suffix)
     else:
@@ -129,7 +140,13 @@ def device_normals_keys(seed, keys, rows, cols, offsets, ld, rowmap, out, suffix
     rec_d = _lib.h2d(rec.view(np.uint8), out.device)
     _lib.call("ublr_rng_normals", _lib.ptr(rec_d), counts.ctypes.data, ns, _lib.ptr(out), _lib.ptr(ws), ws_bytes,
               _lib.stream_handle())
+    if len(_RNG_CACHE) > 64:
+        _RNG_CACHE.clear()
+    _RNG_CACHE[ck] = (rec_d, counts, ns, ws, ws_bytes)
     return out
+
+
+_RNG_CACHE = {}
 
 
 def col_basis(B, k: int) -> np.ndarray:

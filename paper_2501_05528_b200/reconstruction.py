@@ -246,9 +246,13 @@ def structured_identity_discrepancy(op, tess: Tessellation, bases: BlockBases, c
     (ref/reconstruction.py:201-244). Returns a flat device buffer
     of near blocks in neighbour-CSR order."""
     torch = _torch()
-    _check_coloring(tess, coloring.colors)
     dt = bases.dt
-    if not np.array_equal(np.asarray(coloring.colors), dt.colours_h):
+    cols = np.asarray(coloring.colors)
+    checked = tess._device.get("coloring_checked")
+    if checked is None or not np.array_equal(checked, cols):
+        _check_coloring(tess, cols)          # pure function of (tess, colours): validated once
+        tess._device["coloring_checked"] = cols.copy()
+    if not np.array_equal(cols, dt.colours_h):
         raise NotImplementedError("custom colourings: only color_boxes(tess) is supported on the GPU path")
     k = bases.rank
     K = bases.total_rank
@@ -389,6 +393,18 @@ class _PhaseTimer:
         self.times._record(self.name, self.e0, e1)
 
 
+def _stream_scoped(fn):
+    """Run a compressor with the CUDA stream handle captured once (_lib.stream_scope)."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapped(*args, **kwargs):
+        with _lib.stream_scope():
+            return fn(*args, **kwargs)
+    return wrapped
+
+
+@_stream_scoped
 def compress_type_a(op, tess, k, p=10, method="tag", stream=None, distribution="gaussian", extra_cols=0,
                     optimize=False, extra_samples=False, max_tag_redraws=5, compute_error=True,
                     error_iterations=20):
@@ -437,6 +453,7 @@ def compress_type_a(op, tess, k, p=10, method="tag", stream=None, distribution="
     return rep, report
 
 
+@_stream_scoped
 def compress_type_b(op, tess, k, p=10, method="bn", stream=None, distribution="gaussian", optimize=False,
                     max_tag_redraws=5, compute_error=True, error_iterations=20, max_width=None):
     """ref/reconstruction.py:586-677 on the GPU: bases, near field from the

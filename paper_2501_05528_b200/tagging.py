@@ -238,7 +238,39 @@ def _aspect_device(E, Z, tess):
 
 
 def _evaluate(T: TaggingMatrix, tess: Tessellation, attempts: int, device: bool = False) -> TaggingPlan:
-    """ref/tagging.py:355-379 for optimize=False, batched."""
+    """ref/tagging.py:355-379 for optimize=False, batched: one C-ABI host call
+    (ublr_tag_plan_host) for the null vectors, residuals and, unless `device`
+    (GPU aspect ratios for large b), the aspect ratios."""
+    from . import _lib
+    E = np.ascontiguousarray(T.entries, dtype=np.float64)
+    b, ell = E.shape
+    ptr, idx = _neighbour_csr(tess)
+    if len(ptr) > 1 and int(np.diff(ptr).max()) >= ell:
+        raise DegenerateTagsError("requested null space of dimension 1 does not exist")
+    Z = np.zeros((b, ell))
+    res = np.zeros(b)
+    scale = np.zeros(b)
+    rho = None if device else np.zeros(b)
+    _lib.check(_lib.load().ublr_tag_plan_host(E.ctypes.data, ell, ptr.ctypes.data, idx.ctypes.data, b, Z.ctypes.data,
+                                              res.ctypes.data, scale.ctypes.data,
+                                              None if rho is None else rho.ctypes.data), "ublr_tag_plan_host")
+    ok = res <= 1e-12 * scale
+    if not ok.all():
+        i = int(np.flatnonzero(~ok)[0])
+        raise DegenerateTagsError(f"block {i}: requested null space does not exist")
+    limit = 1e-12 * max(1.0, _fro(E))
+    if (res > limit).any():
+        i = int(np.flatnonzero(res > limit)[0])
+        raise DegenerateTagsError(f"block {i}: null-vector residual {res[i]:.3e} exceeds {limit:.3e}")
+    if device:
+        rho = _aspect_device(E, Z, tess)
+    return TaggingPlan(matrix=T, null_vectors=NullVectors(Z, res), rho_base=rho, rho_optimized=None,
+                       attempts=attempts)
+
+
+def _evaluate_numpy(T: TaggingMatrix, tess: Tessellation, attempts: int) -> TaggingPlan:
+    """The same evaluation with numpy (batched_null_vectors + |T Z^T|): the
+    cross-check of ublr_tag_plan_host in the CPU tests."""
     E = T.entries
     Z, res, ok = batched_null_vectors(E, tess.neighbor_lists, csr=_neighbour_csr(tess))
     if not ok.all():
@@ -250,9 +282,6 @@ def _evaluate(T: TaggingMatrix, tess: Tessellation, attempts: int, device: bool 
         raise DegenerateTagsError(f"block {i}: null-vector residual {res[i]:.3e} exceeds {limit:.3e}")
     b = tess.b
     nvs = NullVectors(Z, res)
-    if device:
-        return TaggingPlan(matrix=T, null_vectors=nvs, rho_base=_aspect_device(E, Z, tess), rho_optimized=None,
-                           attempts=attempts)
     ptr, idx = _neighbour_csr(tess)
     P = np.abs(E @ Z.T)                     # P[j, i] = |<t_j, z^(i)>|
     nl = np.diff(ptr)

@@ -172,7 +172,17 @@ def build_tessellation(points: PointCloud, target_block_count: int) -> Tessellat
 
 
 def color_boxes(tess: Tessellation) -> BoxColoring:
-    """Distance-2 colouring (ref/tessellation.py:188-219)."""
+    """Distance-2 colouring (ref/tessellation.py:188-219); cached on the
+    tessellation (a pure function of it)."""
+    cached = tess._device.get("color_boxes")
+    if cached is not None:
+        return cached
+    out = _color_boxes(tess)
+    tess._device["color_boxes"] = out
+    return out
+
+
+def _color_boxes(tess: Tessellation) -> BoxColoring:
     if tess.colors is not None:
         colours = np.asarray(tess.colors, dtype=np.int64)
         return BoxColoring(colors=colours, num_colors=int(colours.max()) + 1)

@@ -290,7 +290,9 @@ def test_tag_aspect_device_matches_host(per, nb, d):
     assert np.array_equal(np.isnan(h), np.isnan(g))
     fin = np.isfinite(h)
     assert np.array_equal(fin, np.isfinite(g))
-    assert np.allclose(g[fin], h[fin], rtol=1e-12, atol=0)
+    # fma (device) vs separate multiply-add (host) dot products: rho = hi/lo
+    # amplifies the rounding of a small lo
+    assert np.allclose(g[fin], h[fin], rtol=1e-8, atol=0)
     ph = P.plan_tagging(tess, 0, "gaussian", P.RandomStream(3).child(1))
     pg = P.plan_tagging(tess, 0, "gaussian", P.RandomStream(3).child(1), device=True)
     assert ph.attempts == pg.attempts and np.array_equal(ph.matrix.entries, pg.matrix.entries)

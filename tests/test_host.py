@@ -171,3 +171,15 @@ def test_quantile_restatement_matches_numpy():
     for n in list(range(1, 30)) + [64, 255, 4096]:
         x = np.sort(rng.standard_normal(n) * rng.uniform(0.1, 1e6))
         assert np.array_equal(np.array(_quantiles(x, (0.25, 0.5, 0.75))), np.quantile(x, (0.25, 0.5, 0.75)))
+
+
+@pytest.mark.parametrize("per,nb,d", [(64, 64, 2), (16, 64, 3), (48, 16, 2)])
+def test_plan_evaluation_c_abi_matches_numpy(per, nb, d):
+    """ublr_tag_plan_host (null vectors, residuals, aspect ratios in C) against
+    the numpy form of the same evaluation."""
+    from paper_2501_05528_b200.tagging import _evaluate, _evaluate_numpy, make_tagging_matrix
+    tess = P.build_tessellation(P.grid_points(per, d), nb)
+    T = make_tagging_matrix(tess.b, d, 0, "gaussian", P.RandomStream(5).child(1).child(0))
+    a, b = _evaluate(T, tess, 1), _evaluate_numpy(T, tess, 1)
+    assert np.allclose(np.abs(a.null_vectors.Z), np.abs(b.null_vectors.Z), rtol=0, atol=1e-13)
+    assert np.allclose(a.rho_base, b.rho_base, rtol=1e-12, equal_nan=True)
