@@ -1005,17 +1005,26 @@ __global__ void __launch_bounds__(C::NT, 1) k_sketch_tagged4(ublr_op_t op, const
           wf[(i * NJ + jj) * 2 + 1] = w[i][jj][1];
           w[i][jj][0] = w[i][jj][1] = 0.0;
         }
+      // TMEM groups in batches of FB chunks: issue the loads, one wait, FMAs, stores
+      constexpr int NCH = TG * (WDP / 8);           // 8-double chunks held in TMEM
+      constexpr int FB = NCH < (WDP > 8 ? 2 : 4) ? NCH : (WDP > 8 ? 2 : 4);
 #pragma unroll
-      for (int c = 0; c < TG; ++c) {
-        const double tc = (c < ell) ? __ldg(&Tj[c]) : 0.0;
+      for (int c0 = 0; c0 < NCH; c0 += FB) {
+        uint32_t raw[FB][16];
 #pragma unroll
-        for (int h = 0; h < WDP / 8; ++h) {
+        for (int f = 0; f < FB; ++f)
+          if (c0 + f < NCH) tmem::ld8_async(tmem::addr(tbase, twarp, colbase + (c0 + f) * 16), raw[f]);
+        tmem::wait_ld();
+#pragma unroll
+        for (int f = 0; f < FB; ++f) {
+          if (c0 + f >= NCH) break;
+          const int c = (c0 + f) / (WDP / 8), h = (c0 + f) % (WDP / 8);
+          const double tc = (c < ell) ? __ldg(&Tj[c]) : 0.0;
           double v[8];
-          const uint32_t ta = tmem::addr(tbase, twarp, colbase + (c * WDP + h * 8) * 2);
-          tmem::ld8(ta, v);
+          tmem::unpack8(raw[f], v);
 #pragma unroll
           for (int q = 0; q < 8; ++q) v[q] = fma(tc, wf[h * 8 + q], v[q]);
-          tmem::st8(ta, v);
+          tmem::st8(tmem::addr(tbase, twarp, colbase + (c0 + f) * 16), v);
         }
       }
 #pragma unroll

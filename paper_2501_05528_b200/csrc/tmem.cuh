@@ -59,6 +59,24 @@ __device__ __forceinline__ void ld8(uint32_t taddr, double (&v)[8]) {
   for (int i = 0; i < 8; ++i) v[i] = __hiloint2double(static_cast<int>(r[2 * i + 1]), static_cast<int>(r[2 * i]));
 }
 
+// 16 x 32-bit columns per lane without waiting: issue several, then one
+// wait_ld(), then unpack with unpack8 (hides the TMEM load latency once per
+// batch instead of once per load).
+__device__ __forceinline__ void ld8_async(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+}
+
+__device__ __forceinline__ void unpack8(const uint32_t (&r)[16], double (&v)[8]) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __hiloint2double(static_cast<int>(r[2 * i + 1]), static_cast<int>(r[2 * i]));
+}
+
 // address of (lane base of this warp's quarter, column)
 __device__ __forceinline__ uint32_t addr(uint32_t base, int warp, int col) {
   return base + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + static_cast<uint32_t>(col);
