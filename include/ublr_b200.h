@@ -171,6 +171,19 @@ int ublr_nearfield_colour(const ublr_op_t* op, const int32_t* off, const int32_t
                           const int64_t* b_off, double* B, void* workspace, int64_t workspace_bytes,
                           void* stream);
 
+/* K6 + K7 fused for small blocks (m_max <= 64, effective rank <= 32; configs
+ * 1-2): one CTA per (block row i, colour c) writes C_ij = U_i^T A_ij V_j for
+ * every j of colour c (as ublr_coupling) and, when block row i has a near pair
+ * p = (i, j*) with colour(j*) = c, B_p exactly as ublr_nearfield_colour, from
+ * the same generated A_ij (one operator pass instead of two, no workspace).
+ * pair_of[i * n_colours + c] = p, or -1 when block row i has no near pair of
+ * colour c (a valid colouring has at most one). Rows i0 <= i < i1. */
+int ublr_coupling_nearfield(const ublr_op_t* op, const int32_t* off, const int32_t* roff, int b, int k,
+                            const double* U, const double* V, int64_t ld_uv, double* core, int64_t ld_c,
+                            const int32_t* cptr, const int32_t* cidx, int n_colours, int m_max,
+                            const int32_t* pair_of, const int32_t* nidx, const int64_t* b_off, double* B,
+                            void* stream, int i0, int i1);
+
 /* K12 — A_hat X (adjoint = 0) or A_hat^T X (adjoint = 1) for the compressed
  * representation (ref/reconstruction.py:93-119): blockwise U C V^T X + B X.
  * tpair[q] for q in the CSR row of j gives the pair index of (nidx[q], j).

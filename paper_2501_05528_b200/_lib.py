@@ -55,6 +55,8 @@ SIGNATURES = {
     "ublr_block_qr_pair": (INT, [P, P, I64, P, INT, INT, P, INT, INT, P, P, I64, P, INT]),
     "ublr_coupling": (INT, [C.POINTER(OpDesc), P, P, INT, INT, P, P, I64, P, I64, P, INT, INT, INT]),
     "ublr_nearfield_workspace_bytes": (I64, [INT, INT, INT]),
+    "ublr_coupling_nearfield": (INT, [C.POINTER(OpDesc), P, P, INT, INT, P, P, I64, P, I64, P, P, INT, INT, P, P, P,
+                                      P, P, INT, INT]),
     "ublr_blr_apply_workspace_bytes": (I64, [I64, INT]),
     "ublr_gemm_batched": (INT, [INT, INT, INT, INT, INT, C.c_double, P, I64, I64, P, I64, P, I64, I64, P, I64,
                                 C.c_double, P, I64, I64, P, I64, INT, P]),
@@ -112,10 +114,22 @@ def check(rc: int, what: str = ""):
 # kernels each C-ABI entry point launches (for bench.py's `gpu_launches`)
 LAUNCHES = {"ublr_rng_normals": 8, "ublr_sketch_tagged": 1, "ublr_sketch_tagged_pair": 1, "ublr_apply": 1,
             "ublr_block_qr": 1, "ublr_block_qr_pair": 1, "ublr_coupling": 1, "ublr_nearfield_colour": 2,
+            "ublr_coupling_nearfield": 1,
             "ublr_blr_apply": 3, "ublr_gemm_batched": 1, "ublr_potrf_diag": 1, "ublr_lu_sign_diag": 1,
             "ublr_lu_sign_diag_r": 1, "ublr_syrk_upper_batched": 1, "ublr_add_scaled_rows": 1,
             "ublr_gather": 1, "ublr_scale_rows": 1, "ublr_tag_combine_pairs": 1, "ublr_assemble_tagged": 1, "ublr_tag_aspect": 1}
 launch_count = 0
+RNG_CTA_MAX_CHUNKS = 4096   # rng.cu CTA_MAX_CHUNKS: one-launch per-CTA decode of short streams
+
+
+def _launches_of(name, args):
+    if name == "ublr_rng_normals" and os.environ.get("UBLR_RNG_PATH", "0") in ("0", "2"):
+        ns = int(args[2])
+        counts = np.ctypeslib.as_array((C.c_int64 * ns).from_address(int(args[1]))) if ns else np.zeros(1, np.int64)
+        mx = int(counts.max())
+        if os.environ.get("UBLR_RNG_PATH", "0") == "2" or (mx + mx // 24 + 256 + 31) // 32 <= RNG_CTA_MAX_CHUNKS:
+            return 1
+    return LAUNCHES.get(name, 0)
 _events = None  # name -> list of (start, end) CUDA events when instrumentation is on
 
 
@@ -171,6 +185,10 @@ def _work_of(name, args):
             n, b, k, m = args[0].n, int(args[3]), int(args[4]), int(args[11])
             rows = (int(args[13]) - int(args[12])) * m
             return 2.0 * rows * n * k + 2.0 * rows * (b * k) * k
+        if name == "ublr_coupling_nearfield":
+            n, b, k, m = args[0].n, int(args[3]), int(args[4]), int(args[13])
+            rows = (int(args[20]) - int(args[19])) * m
+            return 2.0 * rows * n * k + 2.0 * rows * (b * k) * k
     except Exception:  # pragma: no cover - accounting only
         return 0.0
     return 0.0
@@ -179,7 +197,7 @@ def _work_of(name, args):
 def call(name: str, *args):
     """Call a status-returning C-ABI function and raise on failure."""
     global launch_count
-    launch_count += LAUNCHES.get(name, 0)
+    launch_count += _launches_of(name, args)
     if _events is not None and (_only is None or name in _only):
         add_work(name, _work_of(name, args))
         import torch

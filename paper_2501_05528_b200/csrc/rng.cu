@@ -43,7 +43,9 @@ __device__ __forceinline__ void load_tables(Tables* t) {
   }
 }
 
+template <int CC>
 struct WindowWords {
+  static constexpr int WIN = CC + 16;
   uint64_t k0, k1;
   int64_t base;  // absolute word index of rel 0
   uint64_t buf[WIN];
@@ -91,35 +93,28 @@ __device__ __forceinline__ int find_stream(const int64_t* chunk_start, int n, in
   return lo;
 }
 
-// A. chunk summaries
-__global__ void __launch_bounds__(RNG_THREADS) k_rng_summary(RngPlan P) {
-  __shared__ Tables tb;
-  load_tables(&tb);
-  __syncthreads();
-  int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= P.n_chunks) return;
-  int s = find_stream(P.chunk_start, P.n_streams, g);
-  const ublr_rng_stream_t st = P.streams[s];
-  int64_t local = g - P.chunk_start[s];
-  WindowWords ws;
-  ws.k0 = st.key0; ws.k1 = st.key1; ws.base = local * C;
+// A. chunk summaries: chunk `local` of stream st parsed from entries 0..D-1
+template <int CC>
+__device__ uint64_t chunk_summary(const Tables& tb, const ublr_rng_stream_t& st, int64_t local) {
+  WindowWords<CC> ws;
+  ws.k0 = st.key0; ws.k1 = st.key1; ws.base = local * CC;
   ws.fill();
   // parse from entry 0: token starts and accepted-suffix counts
-  uint32_t starts = 0;        // bit p set if parse-0 token starts at rel p < C
-  uint8_t acc_at[C];          // accepted flag of the token starting at p
+  uint32_t starts = 0;        // bit p set if parse-0 token starts at rel p < CC
+  uint8_t acc_at[CC];          // accepted flag of the token starting at p
   int64_t p = 0;
   double v; bool ok;
-  while (p < C) {
+  while (p < CC) {
     int len = rng::zig_token(ws, p, tb.ki, tb.wi, tb.fi, v, ok);
     starts |= 1u << p;
     acc_at[p] = ok ? 1 : 0;
     p += len;
   }
-  int exit0 = (int)(p - C);
-  uint8_t suffix[C + 1];      // accepted parse-0 tokens starting at >= q (q a start)
-  suffix[C] = 0;
+  int exit0 = (int)(p - CC);
+  uint8_t suffix[CC + 1];      // accepted parse-0 tokens starting at >= q (q a start)
+  suffix[CC] = 0;
   int run = 0;
-  for (int q = C - 1; q >= 0; --q) {
+  for (int q = CC - 1; q >= 0; --q) {
     if (starts & (1u << q)) run += acc_at[q];
     suffix[q] = (uint8_t)run;
   }
@@ -131,32 +126,43 @@ __global__ void __launch_bounds__(RNG_THREADS) k_rng_summary(RngPlan P) {
     } else {
       int64_t q = e;
       int before = 0;
-      while (q < C && !(starts & (1u << q))) {
+      while (q < CC && !(starts & (1u << q))) {
         int len = rng::zig_token(ws, q, tb.ki, tb.wi, tb.fi, v, ok);
         before += ok ? 1 : 0;
         q += len;
       }
-      if (q < C) cnt = before + suffix[q];          // merged with parse 0
-      else if (q - C == exit0) cnt = before;         // same exit, no merge inside
+      if (q < CC) cnt = before + suffix[q];          // merged with parse 0
+      else if (q - CC == exit0) cnt = before;         // same exit, no merge inside
       else cnt = 0xff;                               // diverged
     }
     rec |= (uint64_t)(cnt & 0xff) << (16 + 8 * e);
   }
-  P.summary[g] = rec;
+  return rec;
+}
+
+__global__ void __launch_bounds__(RNG_THREADS) k_rng_summary(RngPlan P) {
+  __shared__ Tables tb;
+  load_tables(&tb);
+  __syncthreads();
+  int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= P.n_chunks) return;
+  int s = find_stream(P.chunk_start, P.n_streams, g);
+  P.summary[g] = chunk_summary<C>(tb, P.streams[s], g - P.chunk_start[s]);
 }
 
 // Exact parse of chunk g from entry `entry` (slow path).
+template <int CC>
 __device__ int parse_count(const Tables& tb, const ublr_rng_stream_t& st, int64_t local, int64_t entry,
                            int64_t* exit_rel) {
-  DirectWords ws{st.key0, st.key1, local * C};
+  DirectWords ws{st.key0, st.key1, local * CC};
   int64_t p = entry;
   int cnt = 0;
   double v; bool ok;
-  while (p < C) {
+  while (p < CC) {
     p += rng::zig_token(ws, p, tb.ki, tb.wi, tb.fi, v, ok);
     cnt += ok ? 1 : 0;
   }
-  *exit_rel = p - C;
+  *exit_rel = p - CC;
   return cnt;
 }
 
@@ -165,7 +171,29 @@ __device__ __forceinline__ int64_t chunk_entry(const RngPlan& P, int64_t g, int 
   return (int64_t)(P.summary[g - 1] & 0xffff);
 }
 
-// B. resolve per-chunk counts
+// B. resolve: normals produced by chunk `local` entered at `entry` (rec =
+// its summary); sets *bad when the summaries are inconsistent (serial fallback)
+template <int CC>
+__device__ int chunk_count(const Tables& tb, const ublr_rng_stream_t& st, int64_t local, int64_t entry,
+                           uint64_t rec, bool* bad) {
+  int cnt = 0xff;
+  if (entry == 0xffff) {
+    *bad = true;
+    return 0;
+  }
+  if (entry < D) cnt = (int)((rec >> (16 + 8 * entry)) & 0xff);
+  if (cnt == 0xff) {
+    if (entry >= CC) {
+      *bad = true;  // a token spanning a whole chunk: serial fallback
+      return 0;
+    }
+    int64_t ex;
+    cnt = parse_count<CC>(tb, st, local, entry, &ex);
+    if (ex != (int64_t)(rec & 0xffff)) *bad = true;
+  }
+  return cnt;
+}
+
 __global__ void __launch_bounds__(RNG_THREADS) k_rng_resolve(RngPlan P) {
   __shared__ Tables tb;
   load_tables(&tb);
@@ -173,26 +201,9 @@ __global__ void __launch_bounds__(RNG_THREADS) k_rng_resolve(RngPlan P) {
   int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= P.n_chunks) return;
   int s = find_stream(P.chunk_start, P.n_streams, g);
-  uint64_t rec = P.summary[g];
-  int64_t entry = chunk_entry(P, g, s);
-  int cnt = 0xff;
-  if (entry == 0xffff) {
-    atomicExch(P.flag, 1);
-    cnt = 0;
-  } else if (entry < D) {
-    cnt = (int)((rec >> (16 + 8 * entry)) & 0xff);
-  }
-  if (cnt == 0xff) {
-    if (entry >= C) {
-      atomicExch(P.flag, 1);  // a token spanning a whole chunk: serial fallback
-      cnt = 0;
-    } else {
-      int64_t ex;
-      cnt = parse_count(tb, P.streams[s], g - P.chunk_start[s], entry, &ex);
-      if (ex != (int64_t)(rec & 0xffff)) atomicExch(P.flag, 1);
-    }
-  }
-  P.counts[g] = cnt;
+  bool bad = false;
+  P.counts[g] = chunk_count<C>(tb, P.streams[s], g - P.chunk_start[s], chunk_entry(P, g, s), P.summary[g], &bad);
+  if (bad) atomicExch(P.flag, 1);
 }
 
 // C. scan (exclusive, int32 -> int64), two levels.
@@ -257,7 +268,26 @@ __device__ __forceinline__ void store_normal(const ublr_rng_stream_t& st, int64_
   out[st.out_offset + row * st.ld + c] = v;
 }
 
-// D. emit
+// D. emit: chunk `local` entered at `entry` writes its normals from index n;
+// returns the index after its last normal
+template <int CC>
+__device__ int64_t chunk_emit(const Tables& tb, const ublr_rng_stream_t& st, int64_t local, int64_t entry, int64_t n,
+                              double* out) {
+  WindowWords<CC> ws;
+  ws.k0 = st.key0; ws.k1 = st.key1; ws.base = local * CC;
+  ws.fill();
+  int64_t p = entry;
+  double v; bool ok;
+  while (p < CC) {
+    p += rng::zig_token(ws, p, tb.ki, tb.wi, tb.fi, v, ok);
+    if (ok) {
+      if (n < st.count) store_normal(st, n, v, out);
+      ++n;
+    }
+  }
+  return n;
+}
+
 __global__ void __launch_bounds__(RNG_THREADS) k_rng_emit(RngPlan P, double* out) {
   __shared__ Tables tb;
   load_tables(&tb);
@@ -268,21 +298,9 @@ __global__ void __launch_bounds__(RNG_THREADS) k_rng_emit(RngPlan P, double* out
   int s = find_stream(P.chunk_start, P.n_streams, g);
   const ublr_rng_stream_t st = P.streams[s];
   int64_t first = P.chunk_start[s];
-  int64_t n = P.prefix[g] - P.prefix[first];
   int64_t entry = chunk_entry(P, g, s);
   if (entry >= C) return;
-  WindowWords ws;
-  ws.k0 = st.key0; ws.k1 = st.key1; ws.base = (g - first) * C;
-  ws.fill();
-  int64_t p = entry;
-  double v; bool ok;
-  while (p < C) {
-    p += rng::zig_token(ws, p, tb.ki, tb.wi, tb.fi, v, ok);
-    if (ok) {
-      if (n < st.count) store_normal(st, n, v, out);
-      ++n;
-    }
-  }
+  int64_t n = chunk_emit<C>(tb, st, g - first, entry, P.prefix[g] - P.prefix[first], out);
   if (g + 1 == P.chunk_start[s + 1] && n < st.count) atomicExch(P.flag, 1);  // ran out of words
 }
 
@@ -301,6 +319,72 @@ __global__ void k_rng_serial(RngPlan P, double* out) {
       p += rng::zig_token(ws, p, tb.ki, tb.wi, tb.fi, v, ok);
       if (ok) store_normal(st, n++, v, out);
     }
+  }
+}
+
+
+// One CTA per stream for many short streams (the test blocks G_i, H_i: one
+// stream per block of m_i x gc normals): the four phases above run inside
+// the CTA on its stream's chunks (summaries and counts in shared memory, a
+// block scan), so a whole launch set is one kernel. A chunk's entry is the
+// previous chunk's parse-0 exit, so every phase is chunk-parallel; an
+// inconsistency makes thread 0 re-decode the stream serially.
+constexpr int CTA_MAX_CHUNKS = 4096;   // longest stream decoded by one CTA (~125k normals)
+constexpr int CTA_THREADS = 256;
+
+__host__ __device__ inline int64_t chunks_for(int64_t count, int cc) { return (count + count / 24 + 256 + cc - 1) / cc; }
+
+template <int CC>
+__global__ void __launch_bounds__(CTA_THREADS) k_rng_cta(const ublr_rng_stream_t* __restrict__ streams,
+                                                         int n_streams, double* __restrict__ out) {
+  __shared__ Tables tb;
+  __shared__ uint64_t rec[CTA_MAX_CHUNKS];
+  __shared__ int32_t part[CTA_THREADS];
+  __shared__ int bad_any;
+  load_tables(&tb);
+  const int T = blockDim.x, tid = threadIdx.x;
+  for (int s = blockIdx.x; s < n_streams; s += gridDim.x) {
+    const ublr_rng_stream_t st = streams[s];
+    const int nch = (int)chunks_for(st.count, CC);
+    if (tid == 0) bad_any = 0;
+    __syncthreads();
+    for (int g = tid; g < nch; g += T) rec[g] = chunk_summary<CC>(tb, st, g);
+    __syncthreads();
+    bool bad = false;
+    // counts, then a block scan over contiguous per-thread runs of chunks
+    const int per = (nch + T - 1) / T, g0 = tid * per, g1 = min(nch, g0 + per);
+    int run = 0;
+    for (int g = g0; g < g1; ++g) {
+      const int64_t entry = g == 0 ? 0 : (int64_t)(rec[g - 1] & 0xffff);
+      run += chunk_count<CC>(tb, st, g, entry, rec[g], &bad);
+    }
+    part[tid] = run;
+    __syncthreads();
+    for (int o = 1; o < T; o <<= 1) {
+      const int v = tid >= o ? part[tid - o] : 0;
+      __syncthreads();
+      part[tid] += v;
+      __syncthreads();
+    }
+    int64_t n = part[tid] - run;
+    for (int g = g0; g < g1 && !bad; ++g) {
+      const int64_t entry = g == 0 ? 0 : (int64_t)(rec[g - 1] & 0xffff);
+      if (entry >= CC) { bad = true; break; }
+      n = chunk_emit<CC>(tb, st, g, entry, n, out);
+    }
+    if (tid == T - 1 && part[T - 1] < st.count) bad = true;   // ran out of words
+    if (bad) atomicExch(&bad_any, 1);
+    __syncthreads();
+    if (bad_any && tid == 0) {
+      DirectWords ws{st.key0, st.key1, 0};
+      int64_t p = 0;
+      double v; bool ok;
+      for (int64_t q = 0; q < st.count;) {
+        p += rng::zig_token(ws, p, tb.ki, tb.wi, tb.fi, v, ok);
+        if (ok) store_normal(st, q++, v, out);
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -376,9 +460,28 @@ extern "C" int ublr_rng_normals(const ublr_rng_stream_t* streams_dev, const int6
   if (n_streams == 0) return UBLR_OK;
   UBLR_REQUIRE(streams_dev && counts_host && out && workspace, UBLR_ERR_VALUE, "null pointer argument");
   for (int s = 0; s < n_streams; ++s) UBLR_REQUIRE(counts_host[s] >= 0, UBLR_ERR_VALUE, "negative stream count");
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t max_count = 0;
+  for (int s = 0; s < n_streams; ++s) max_count = counts_host[s] > max_count ? counts_host[s] : max_count;
+  static const int path = [] {
+    const char* e = getenv("UBLR_RNG_PATH");  // 0 auto, 1 chunked multi-kernel, 2 one CTA per stream
+    return e ? atoi(e) : 0;
+  }();
+  // chunk size: enough chunks per stream to give every stream a CTA of threads
+  const int cc = chunks_for(max_count, 8) <= CTA_THREADS ? 8 : chunks_for(max_count, 16) <= 2 * CTA_THREADS ? 16 : C;
+  const int64_t max_chunks = chunks_for(max_count, cc);
+  if (path == 2 || (path == 0 && max_chunks <= CTA_MAX_CHUNKS)) {
+    UBLR_REQUIRE(max_chunks <= CTA_MAX_CHUNKS, UBLR_ERR_VALUE, "rng: stream too long for the per-CTA decode");
+    int threads = (int)((max_chunks + 31) / 32 * 32);
+    threads = threads > CTA_THREADS ? CTA_THREADS : threads;
+    if (cc == 8) k_rng_cta<8><<<n_streams, threads, 0, st>>>(streams_dev, n_streams, out);
+    else if (cc == 16) k_rng_cta<16><<<n_streams, threads, 0, st>>>(streams_dev, n_streams, out);
+    else k_rng_cta<C><<<n_streams, threads, 0, st>>>(streams_dev, n_streams, out);
+    UBLR_LAUNCH_CHECK();
+    return UBLR_OK;
+  }
   Layout L = layout(counts_host, n_streams);
   UBLR_REQUIRE(workspace_bytes >= L.bytes, UBLR_ERR_VALUE, "rng workspace too small");
-  cudaStream_t st = (cudaStream_t)stream;
   char* ws = (char*)workspace;
   // chunk starts and the fallback flag, computed on the device
   k_chunk_starts<<<1, 1024, 0, st>>>(streams_dev, n_streams, (int64_t*)(ws + L.chunk_start_off), (int*)(ws + L.flag_off));

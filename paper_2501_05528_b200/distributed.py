@@ -28,6 +28,7 @@ from . import _lib
 from .bases import _bill, draw_test_pair
 from .linalg import RandomStream
 from .operators import counting_wrapper, unwrap
+from .reconstruction import FUSED_NEAR_K_MAX, FUSED_NEAR_M_MAX
 from .tagging import plan_tagging
 from .tessellation import device_tess
 
@@ -166,11 +167,18 @@ def phase23_local(op, k, shard, dt, U, V_all):
     core = torch.empty((kloc, K), **f64)
     st = _lib.stream_handle()
     desc = inner.device_op(dt.perm)
-    _lib.call("ublr_coupling", desc, _lib.ptr(dt.off), _lib.ptr(roff), dt.b, k, _lib.ptr(U) - 8 * shard.r0 * k,
-              _lib.ptr(V_all), k, _lib.ptr(core) - 8 * shard.K0 * K, K, st, dt.m_max, shard.i0, shard.i1)
     npairs = shard.p1 - shard.p0
     bbase = int(dt.b_off_h[shard.p0])
     B = torch.empty(int(dt.b_off_h[shard.p1]) - bbase, **f64)
+    if dt.m_max <= FUSED_NEAR_M_MAX and min(k, dt.m_max) <= FUSED_NEAR_K_MAX and dt.pair_of is not None:
+        # small blocks: core rows and near blocks from one pass over A (as direct_core)
+        _lib.call("ublr_coupling_nearfield", desc, _lib.ptr(dt.off), _lib.ptr(roff), dt.b, k,
+                  _lib.ptr(U) - 8 * shard.r0 * k, _lib.ptr(V_all), k, _lib.ptr(core) - 8 * shard.K0 * K, K,
+                  _lib.ptr(dt.cptr), _lib.ptr(dt.cidx), dt.n_colours, dt.m_max, _lib.ptr(dt.pair_of),
+                  _lib.ptr(dt.nidx), _lib.ptr(dt.b_off), _lib.ptr(B) - 8 * bbase, st, shard.i0, shard.i1)
+        return core, B
+    _lib.call("ublr_coupling", desc, _lib.ptr(dt.off), _lib.ptr(roff), dt.b, k, _lib.ptr(U) - 8 * shard.r0 * k,
+              _lib.ptr(V_all), k, _lib.ptr(core) - 8 * shard.K0 * K, K, st, dt.m_max, shard.i0, shard.i1)
     lib = _lib.load()
     ws_bytes = int(lib.ublr_nearfield_workspace_bytes(npairs, max(k, 1), dt.m_max))
     ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device=dt.device)

@@ -221,10 +221,30 @@ def direct_core(op, tess: Tessellation, bases: BlockBases):
         return core
     if not hasattr(inner, "device_op"):
         raise NotImplementedError("direct_core needs a GPU operator (DenseOperator / KernelOperator)")
+    if dt.m_max <= FUSED_NEAR_M_MAX and min(k, dt.m_max) <= FUSED_NEAR_K_MAX and dt.pair_of is not None:
+        # small blocks: the colour-probe near field (phase III) comes out of the
+        # same pass over A (ublr_coupling_nearfield); structured_identity_discrepancy
+        # returns it for this core
+        B = torch.empty(max(int(dt.b_off_h[-1]), 1), dtype=torch.float64, device=dt.device)
+        _lib.call("ublr_coupling_nearfield", inner.device_op(dt.perm), _lib.ptr(dt.off), _lib.ptr(roff), dt.b, k,
+                  _lib.ptr(bases.U), _lib.ptr(bases.V), bases.U.stride(0), _lib.ptr(core), K, _lib.ptr(dt.cptr),
+                  _lib.ptr(dt.cidx), dt.n_colours, dt.m_max, _lib.ptr(dt.pair_of), _lib.ptr(dt.nidx),
+                  _lib.ptr(dt.b_off), _lib.ptr(B), _lib.stream_handle(), 0, dt.b)
+        bases.fused_near = (core, _versions(core, bases), inner, B[:int(dt.b_off_h[-1])])
+        return core
     _lib.call("ublr_coupling", inner.device_op(dt.perm), _lib.ptr(dt.off), _lib.ptr(roff), dt.b, k,
               _lib.ptr(bases.U), _lib.ptr(bases.V), bases.U.stride(0), _lib.ptr(core), K, _lib.stream_handle(),
               dt.m_max, 0, dt.b)
     return core
+
+
+def _versions(core, bases):
+    """In-place modification counters of the fused near field's inputs."""
+    return (core._version, bases.U._version, bases.V._version)
+
+
+FUSED_NEAR_M_MAX = 64   # ublr_coupling_nearfield limits
+FUSED_NEAR_K_MAX = 32
 
 
 def _check_coloring(tess, colors):
@@ -263,6 +283,9 @@ def structured_identity_discrepancy(op, tess: Tessellation, bases: BlockBases, c
     inner = unwrap(op)
     if not hasattr(inner, "device_op"):
         raise NotImplementedError("structured_identity_discrepancy needs a GPU operator")
+    fused = getattr(bases, "fused_near", None)
+    if fused is not None and fused[0] is core and fused[1] == _versions(core, bases) and fused[2] is inner:
+        return fused[3]   # computed with this core by direct_core's fused pass
     B = torch.empty(int(dt.b_off_h[-1]), dtype=torch.float64, device=dt.device)
     lib = _lib.load()
     ws_bytes = int(lib.ublr_nearfield_workspace_bytes(dt.n_pairs, max(k, 1), dt.m_max))

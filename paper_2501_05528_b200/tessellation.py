@@ -239,6 +239,15 @@ class DeviceTess:
         counts = np.bincount(self.colours_h, minlength=self.n_colours)
         self.cptr_h = np.concatenate(([0], np.cumsum(counts))).astype(np.int32)
         self.cidx_h = order.astype(np.int32)
+        # pair_of[i, c]: the near pair (i, j) with colour(j) = c, or -1; None if
+        # a neighbourhood repeats a colour (invalid colouring, see _check_coloring)
+        key = self.pair_i_h.astype(np.int64) * self.n_colours + self.colours_h[self.nidx_h]
+        if np.unique(key).size == key.size:
+            po = np.full(b * self.n_colours, -1, dtype=np.int32)
+            po[key] = np.arange(self.n_pairs, dtype=np.int32)
+            self.pair_of_h = po
+        else:
+            self.pair_of_h = None
 
         def t(a):
             return torch.from_numpy(np.ascontiguousarray(a)).to(device)
@@ -254,6 +263,7 @@ class DeviceTess:
         self.colours = t(self.colours_h)
         self.cptr = t(self.cptr_h)
         self.cidx = t(self.cidx_h)
+        self.pair_of = None if self.pair_of_h is None else t(self.pair_of_h)
         self._roff = {}
 
     def ranks(self, k: int) -> np.ndarray:

@@ -58,6 +58,19 @@ def test_rng_many_small_streams():
         assert np.array_equal(got[i], P.RandomStream(7).child(0).child(0, i).normal(m, gc))
 
 
+@pytest.mark.parametrize("rows,cols", [(1, 1), (7, 3), (50, 30), (64, 30), (100, 50), (256, 266)])
+def test_rng_per_cta_decode_bitwise(rows, cols):
+    """Short streams take the one-launch per-CTA decode (chunk sizes 8, 16 and
+    32 words by stream length); bitwise against numpy for every stream."""
+    nst = 9
+    specs = [(P.RandomStream(11).child(3, i), rows, cols, i * rows * cols, cols, None) for i in range(nst)]
+    out = torch.full((nst * rows * cols,), np.nan, dtype=torch.float64, device=DEV)
+    device_normals(specs, out)
+    got = out.cpu().numpy().reshape(nst, rows, cols)
+    for i in range(nst):
+        assert np.array_equal(got[i], P.RandomStream(11).child(3, i).normal(rows, cols)), i
+
+
 def _dense_apply_case(kind):
     coords = O.cell_centres(24, 2)
     n = len(coords)
@@ -296,3 +309,58 @@ def test_tag_aspect_device_matches_host(per, nb, d):
     ph = P.plan_tagging(tess, 0, "gaussian", P.RandomStream(3).child(1))
     pg = P.plan_tagging(tess, 0, "gaussian", P.RandomStream(3).child(1), device=True)
     assert ph.attempts == pg.attempts and np.array_equal(ph.matrix.entries, pg.matrix.entries)
+
+
+def _fused_case(name):
+    if name == "dense1d":
+        pts = P.grid_points(512, 1)
+        tess = P.build_tessellation(pts, 8)
+        A = np.random.default_rng(3).standard_normal((512, 512))
+        return tess, P.DenseOperator(A)
+    if name == "log2d":
+        pts = P.grid_points(32, 2)
+        return P.build_tessellation(pts, 16), P.KernelOperator(pts, "log", -np.log(0.5 / 32))
+    if name == "inv_ragged":
+        pts = P.grid_points(48, 2)   # 36-point blocks
+        return P.build_tessellation(pts, 64), P.KernelOperator(pts, "inv", 96.0)
+    if name == "log_rand":
+        pts = P.random_points(500, 2, P.RandomStream(21))
+        return P.build_tessellation(pts, 16), P.KernelOperator(pts, "log", 3.0)
+    raise KeyError(name)
+
+
+@pytest.mark.parametrize("name,k", [("dense1d", 10), ("log2d", 20), ("inv_ragged", 32), ("log_rand", 20),
+                                    ("log2d", 7), ("log_rand", 30)])
+def test_coupling_nearfield_fused_matches_separate(name, k):
+    """ublr_coupling_nearfield (one pass over A for m <= 64) against the
+    separate coupling + colour-probe kernels on the same U, V."""
+    from paper_2501_05528_b200.bases import BlockBases
+    from paper_2501_05528_b200.reconstruction import direct_core, structured_identity_discrepancy
+    from paper_2501_05528_b200.tessellation import color_boxes
+    tess, op = _fused_case(name)
+    dt = device_tess(tess, torch.device(DEV))
+    assert dt.m_max <= 64 and dt.pair_of is not None
+    rng = np.random.default_rng(5)
+    U = torch.from_numpy(rng.standard_normal((dt.n, k))).cuda()
+    V = torch.from_numpy(rng.standard_normal((dt.n, k))).cuda()
+    bs = BlockBases(dt, U, V, k, "tag", (0, 0))
+    core_f = direct_core(op, tess, bs)
+    assert getattr(bs, "fused_near", None) is not None
+    B_f = structured_identity_discrepancy(op, tess, bs, core_f, color_boxes(tess)).cpu().numpy()
+    # separate kernels
+    K = bs.total_rank
+    roff = dt.roff(k)[1]
+    core_s = torch.empty_like(core_f)
+    _lib.call("ublr_coupling", op.device_op(dt.perm), _lib.ptr(dt.off), _lib.ptr(roff), dt.b, k, _lib.ptr(U),
+              _lib.ptr(V), k, _lib.ptr(core_s), K, _lib.stream_handle(), dt.m_max, 0, dt.b)
+    bs.fused_near = None
+    B_s = structured_identity_discrepancy(op, tess, bs, core_s, color_boxes(tess)).cpu().numpy()
+    cf, cs = core_f.cpu().numpy(), core_s.cpu().numpy()
+    assert np.abs(cf - cs).max() <= 1e-12 * np.abs(cs).max()
+    assert B_f.shape == B_s.shape
+    assert np.abs(B_f - B_s).max() <= 1e-12 * np.abs(B_s).max()
+    # a modified core is not served from the fused pass
+    direct_core(op, tess, bs)
+    core2 = direct_core(op, tess, bs)
+    core2.mul_(2.0)
+    assert structured_identity_discrepancy(op, tess, bs, core2, color_boxes(tess)) is not bs.fused_near[3]
