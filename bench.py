@@ -366,7 +366,9 @@ def main():
     launches0 = _lib.launch_count
     step_ms = []
     gc.collect()
-    gc.disable()   # no collector pauses inside millisecond steps (re-enabled below)
+    if args.config in ("c1", "c2"):
+        gc.disable()   # no collector pauses inside millisecond steps (re-enabled below); c3/c4 steps
+                       # allocate tens of GB, so the collector stays on there
     with ClockSampler(local) as clocks:
         for _ in range(args.steps):
             flush_l2(l2buf)
@@ -377,6 +379,7 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             step_ms.append(e0.elapsed_time(e1))
+            rep = report = None
     gc.enable()
     ev = _lib.event_times()
     _lib.instrument(False)

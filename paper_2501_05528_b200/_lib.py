@@ -119,16 +119,19 @@ LAUNCHES = {"ublr_rng_normals": 8, "ublr_sketch_tagged": 1, "ublr_sketch_tagged_
             "ublr_lu_sign_diag_r": 1, "ublr_syrk_upper_batched": 1, "ublr_add_scaled_rows": 1,
             "ublr_gather": 1, "ublr_scale_rows": 1, "ublr_tag_combine_pairs": 1, "ublr_assemble_tagged": 1, "ublr_tag_aspect": 1}
 launch_count = 0
-RNG_CTA_MAX_CHUNKS = 4096   # rng.cu CTA_MAX_CHUNKS: one-launch per-CTA decode of short streams
+
+
+def rng_launches(counts) -> int:
+    """Kernels one ublr_rng_normals call launches (rng.cu: one per-CTA decode
+    kernel for short streams, else the 8-kernel chunk-parallel set)."""
+    path = os.environ.get("UBLR_RNG_PATH", "0")
+    mx = int(np.max(counts)) if len(counts) else 0
+    if path == "2" or (path == "0" and (mx + mx // 24 + 256 + 15) // 16 <= 512):
+        return 1
+    return LAUNCHES["ublr_rng_normals"]
 
 
 def _launches_of(name, args):
-    if name == "ublr_rng_normals" and os.environ.get("UBLR_RNG_PATH", "0") in ("0", "2"):
-        ns = int(args[2])
-        counts = np.ctypeslib.as_array((C.c_int64 * ns).from_address(int(args[1]))) if ns else np.zeros(1, np.int64)
-        mx = int(counts.max())
-        if os.environ.get("UBLR_RNG_PATH", "0") == "2" or (mx + mx // 24 + 256 + 31) // 32 <= RNG_CTA_MAX_CHUNKS:
-            return 1
     return LAUNCHES.get(name, 0)
 _events = None  # name -> list of (start, end) CUDA events when instrumentation is on
 
@@ -194,17 +197,18 @@ def _work_of(name, args):
     return 0.0
 
 
-def call(name: str, *args):
-    """Call a status-returning C-ABI function and raise on failure."""
+def call(name: str, *args, launches=None):
+    """Call a status-returning C-ABI function and raise on failure
+    (`launches`: kernels it launches when that depends on the arguments)."""
     global launch_count
-    launch_count += _launches_of(name, args)
+    launch_count += _launches_of(name, args) if launches is None else launches
     if _events is not None and (_only is None or name in _only):
         add_work(name, _work_of(name, args))
         import torch
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
+        a.record(current_stream())
         check(getattr(load(), name)(*args), name)
-        b.record()
+        b.record(current_stream())
         _events.setdefault(name, []).append((a, b))
         return
     check(getattr(load(), name)(*args), name)
@@ -263,7 +267,7 @@ class _PinnedRing:
         view = self.np[off:off + nb].view(a.dtype).reshape(a.shape)
         view[...] = a
         out = torch.from_numpy(view).to(device, non_blocking=True)
-        self.events[s].record()
+        self.events[s].record(current_stream())
         self.used[s] = True
         return out
 
@@ -289,15 +293,28 @@ class stream_scope:
     issues dozens of launches on one stream)."""
 
     def __enter__(self):
-        global _stream_cached
+        global _stream_cached, _stream_obj
         import torch
-        self._prev = _stream_cached
-        _stream_cached = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        self._prev = (_stream_cached, _stream_obj)
+        _stream_obj = torch.cuda.current_stream()
+        _stream_cached = C.c_void_p(_stream_obj.cuda_stream)
         return self
 
     def __exit__(self, *exc):
-        global _stream_cached
-        _stream_cached = self._prev
+        global _stream_cached, _stream_obj
+        _stream_cached, _stream_obj = self._prev
+
+
+_stream_obj = None
+
+
+def current_stream():
+    """torch.cuda.current_stream(), cached inside a stream_scope (pass it to
+    Event.record: without an argument, record() queries the current stream)."""
+    if _stream_obj is not None:
+        return _stream_obj
+    import torch
+    return torch.cuda.current_stream()
 
 
 def stream_handle():

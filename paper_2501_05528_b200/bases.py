@@ -143,28 +143,40 @@ def draw_test_pair(dt, stream: RandomStream, cols: int):
     """(G, H) with G_i = gaussian(m_i, cols, stream.child(0, i)) and
     H_i = ...child(1, i) (ref/bases.py:163-168), drawn in ONE launch set into
     a (2, N, cols) buffer."""
-    from .linalg import device_normals_keys
+    from .linalg import launch_normals, rng_launch_record
 
     torch = _torch()
     GH = torch.empty((2, dt.n, cols), dtype=torch.float64, device=dt.device)
-    b = dt.b
-    suffix = np.stack([np.repeat(np.arange(2), b), np.tile(np.arange(b), 2)], axis=1)  # (side, i)
-    rows = np.concatenate([dt.sizes, dt.sizes])
-    offs = np.concatenate([dt.off_h[:-1].astype(np.int64) * cols, dt.n * cols + dt.off_h[:-1].astype(np.int64) * cols])
-    device_normals_keys(stream.seed, stream.key, rows, cols, offs, cols, None, GH, suffix=suffix)
+    ck = ("test_pair", stream.seed, tuple(stream.key), cols)
+    rec = dt.rng_records.get(ck)
+    if rec is None:
+        b = dt.b
+        suffix = np.stack([np.repeat(np.arange(2), b), np.tile(np.arange(b), 2)], axis=1)  # (side, i)
+        rows = np.concatenate([dt.sizes, dt.sizes])
+        offs = np.concatenate([dt.off_h[:-1].astype(np.int64) * cols,
+                               dt.n * cols + dt.off_h[:-1].astype(np.int64) * cols])
+        rec = rng_launch_record(stream.seed, stream.key, rows, cols, offs, cols, None, dt.device, suffix=suffix)
+        if len(dt.rng_records) > 16:
+            dt.rng_records.clear()
+        dt.rng_records[ck] = rec
+    launch_normals(rec, GH)
     return GH[0], GH[1]
 
 
-def tagged_sketch(op, dt, T_dev, T_entries, G, H, gc):
-    """Y = A Omega, Z = A^* Psi for the tagged test matrices; returns (Y, Z)."""
+def tagged_sketch(op, dt, T_dev, T_entries, G, H, gc, out=None):
+    """Y = A Omega, Z = A^* Psi for the tagged test matrices; returns (Y, Z)
+    (into `out` = (Y, Z) when given)."""
     torch = _torch()
     inner = unwrap(op)
     ell = T_entries.shape[1]
     s = ell * gc
     stream = _lib.stream_handle()
     if hasattr(inner, "device_op"):
-        Y = torch.empty((dt.n, s), dtype=torch.float64, device=dt.device)
-        Z = torch.empty((dt.n, s), dtype=torch.float64, device=dt.device)
+        if out is not None:
+            Y, Z = out
+        else:
+            Y = torch.empty((dt.n, s), dtype=torch.float64, device=dt.device)
+            Z = torch.empty((dt.n, s), dtype=torch.float64, device=dt.device)
         if getattr(inner, "symmetric", False):
             _lib.call("ublr_sketch_tagged_pair", inner.device_op(dt.perm), _lib.ptr(dt.off), dt.b,
                       _lib.ptr(T_dev), ell, _lib.ptr(G), _lib.ptr(H), gc, gc, _lib.ptr(Y), _lib.ptr(Z), s, 0, dt.n,
@@ -199,7 +211,7 @@ def block_bases_from_tagged(dt, Y, Z, Z_dev, ell, gc, k):
 
 
 def tagging_bases(op, tess: Tessellation, k: int, p: int, plan, stream: RandomStream,
-                  group_cols: int | None = None, extra_samples: bool = False, first=None):
+                  group_cols: int | None = None, extra_samples: bool = False, first=None, test_pair=None):
     """ref/bases.py:140-204 on the GPU. Returns (BlockBases, SketchBundle).
 
     `plan` is a TaggingPlan, or a zero-argument callable producing one (the
@@ -207,7 +219,9 @@ def tagging_bases(op, tess: Tessellation, k: int, p: int, plan, stream: RandomSt
     policy's first draw. The sketch depends only on the tagging matrix, not on
     the null vectors, so with a callable the sketch of `first` is launched
     before the host evaluates the plan and runs on the GPU meanwhile; if the
-    policy redraws, the sketch is recomputed for the accepted matrix."""
+    policy redraws, the sketch is recomputed for the accepted matrix.
+    `test_pair` = (G, H) already drawn by draw_test_pair(dt, stream, gc)
+    (compress_type_a launches it before the host draws the tagging matrix)."""
     torch = _torch()
     if extra_samples:
         raise NotImplementedError("extra_samples (ref/bases.py:177-182) is not on the B200 hot path (SURVEY F12)")
@@ -224,10 +238,14 @@ def tagging_bases(op, tess: Tessellation, k: int, p: int, plan, stream: RandomSt
     T_entries = matrix.entries
     ell = T_entries.shape[1]
     s = ell * gc
-    G, H = draw_test_pair(dt, stream, gc)
+    # everything the sketch launch needs is staged before the RNG launch, so
+    # the two kernels follow each other on the GPU without a host gap
     T_dev = _lib.h2d(T_entries, dt.device)
+    Y = torch.empty((dt.n, s), dtype=torch.float64, device=dt.device)
+    Z = torch.empty((dt.n, s), dtype=torch.float64, device=dt.device)
     _bill(op, s, s)
-    Y, Z = tagged_sketch(op, dt, T_dev, T_entries, G, H, gc)
+    G, H = draw_test_pair(dt, stream, gc) if test_pair is None else test_pair
+    Y, Z = tagged_sketch(op, dt, T_dev, T_entries, G, H, gc, out=(Y, Z))
     if planner is not None:
         plan = planner()                     # host work, overlapping the sketch
         if plan.matrix is not matrix:        # redrawn: sketch the accepted matrix

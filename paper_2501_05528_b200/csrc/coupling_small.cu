@@ -91,14 +91,32 @@ __global__ void __launch_bounds__(CS_THREADS) k_coupling_nf_small(
   const bool near = p >= 0;
   __syncthreads();
 
-  for (int mem = cptr[c]; mem < cptr[c + 1]; ++mem) {
+  const int mem0 = cptr[c], mem1 = cptr[c + 1];
+  // the column point of the first member; later ones are loaded one member ahead
+  RowPoint cp_next;
+  {
+    const int j = cidx[mem0];
+    cp_next = load_row_point(op, off[j] + q, q < off[j + 1] - off[j]);
+  }
+  for (int mem = mem0; mem < mem1; ++mem) {
     const int j = cidx[mem];
     const int cj0 = off[j], mj = off[j + 1] - cj0;
     const int kj = roff[j + 1] - roff[j];
-    // ---- A_ij -> shared (and D), V_j -> shared
+    // ---- V_j -> shared (cp.async, zero-filled padding), overlapping the generation
+    for (int e = tid; e < CS_M * KP; e += CS_THREADS) {
+      const int r = e / KP, a = e - r * KP;
+      const bool ok = r < mj && a < kj;
+      cp_async8(&Vs[r * SU + a], ok ? (const void*)(V + (int64_t)(cj0 + r) * lduv + a) : (const void*)V, ok);
+    }
+    cp_async_commit();
+    // ---- A_ij -> shared (and D)
     {
       const bool qok = q < mj;
-      RowPoint cp = load_row_point(op, cj0 + q, qok);   // the column point
+      const RowPoint cp = cp_next;   // the column point
+      if (mem + 1 < mem1) {
+        const int jn = cidx[mem + 1];
+        cp_next = load_row_point(op, off[jn] + q, q < off[jn + 1] - off[jn]);
+      }
 #pragma unroll
       for (int s = 0; s < 16; ++s) {
         const int r = r0 + 4 * s;
@@ -114,11 +132,8 @@ __global__ void __launch_bounds__(CS_THREADS) k_coupling_nf_small(
         As[r * CS_SA + q] = v;
         D[s] += v;
       }
-      for (int e = tid; e < CS_M * KP; e += CS_THREADS) {
-        const int r = e / KP, a = e - r * KP;
-        Vs[r * SU + a] = (r < mj && a < kj) ? V[(int64_t)(cj0 + r) * lduv + a] : 0.0;
-      }
     }
+    cp_async_wait<0>();
     __syncthreads();
     // ---- T = U_i^T A_ij: warp owns columns q0 = 8 warp, all KP rows; K = 64 rows r
     {

@@ -470,7 +470,10 @@ extern "C" int ublr_rng_normals(const ublr_rng_stream_t* streams_dev, const int6
   // chunk size: enough chunks per stream to give every stream a CTA of threads
   const int cc = chunks_for(max_count, 8) <= CTA_THREADS ? 8 : chunks_for(max_count, 16) <= 2 * CTA_THREADS ? 16 : C;
   const int64_t max_chunks = chunks_for(max_count, cc);
-  if (path == 2 || (path == 0 && max_chunks <= CTA_MAX_CHUNKS)) {
+  // the per-CTA decode wins for short streams (c2: 0.081 -> 0.033 ms); for
+  // long ones (c5: 8192 streams of 16k normals) the chunk-parallel kernels do
+  // (2.8 vs 3.8 ms)
+  if (path == 2 || (path == 0 && cc < C)) {
     UBLR_REQUIRE(max_chunks <= CTA_MAX_CHUNKS, UBLR_ERR_VALUE, "rng: stream too long for the per-CTA decode");
     int threads = (int)((max_chunks + 31) / 32 * 32);
     threads = threads > CTA_THREADS ? CTA_THREADS : threads;

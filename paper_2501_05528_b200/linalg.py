@@ -93,7 +93,7 @@ def device_normals(specs, out):
     ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device=out.device)
     rec_d = _lib.h2d(rec.view(np.uint8), out.device)
     _lib.call("ublr_rng_normals", _lib.ptr(rec_d), counts.ctypes.data, len(specs), _lib.ptr(out),
-              _lib.ptr(ws), ws_bytes, _lib.stream_handle())
+              _lib.ptr(ws), ws_bytes, _lib.stream_handle(), launches=_lib.rng_launches(counts))
     # keep host/device descriptors alive until the stream has consumed them
     out._ublr_keepalive = (rec_d, ws, keep)
     return out
@@ -106,20 +106,24 @@ def device_normals_keys(seed, keys, rows, cols, offsets, ld, rowmap, out, suffix
     With `suffix` ((n, ns) ints), `keys` is one prefix tuple and stream s is
     RandomStream(seed, keys + tuple(suffix[s])); the keys are derived by the
     C-ABI host function ublr_seedseq_keys."""
-    from .seedseq import philox_keys, philox_keys_suffixed
 
     _lib.require_device()
-    # the stream records (keys, counts, layout) are a pure function of the
-    # arguments: built and uploaded once, the normals are drawn every call
+    launch_normals(rng_launch_record(seed, keys, rows, cols, offsets, ld, rowmap, out.device, suffix), out)
+    return out
+
+
+def rng_launch_record(seed, keys, rows, cols, offsets, ld, rowmap, device, suffix=None):
+    """Device stream records + workspace of a device_normals_keys launch set.
+    They are a pure function of the arguments: built and uploaded once, the
+    normals are drawn on every launch_normals call."""
+    from .seedseq import philox_keys, philox_keys_suffixed
+
     ck = (int(seed), tuple(keys) if suffix is not None else tuple(map(tuple, keys)),
           np.asarray(rows, dtype=np.int64).tobytes(), int(cols), np.asarray(offsets, dtype=np.int64).tobytes(),
-          int(ld), _lib.ptr(rowmap), None if suffix is None else np.asarray(suffix).tobytes(), str(out.device))
+          int(ld), _lib.ptr(rowmap), None if suffix is None else np.asarray(suffix).tobytes(), str(device))
     hit = _RNG_CACHE.get(ck)
     if hit is not None:
-        rec_d, counts, ns, ws, ws_bytes = hit
-        _lib.call("ublr_rng_normals", _lib.ptr(rec_d), counts.ctypes.data, ns, _lib.ptr(out), _lib.ptr(ws), ws_bytes,
-                  _lib.stream_handle())
-        return out
+        return hit
     if suffix is not None:
         kk = philox_keys_suffixed(seed, keys, suffix)
     else:
@@ -136,13 +140,19 @@ def device_normals_keys(seed, keys, rows, cols, offsets, ld, rowmap, out, suffix
     lib = _lib.load()
     ws_bytes = int(lib.ublr_rng_workspace_bytes(counts.ctypes.data, ns))
     import torch
-    ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device=out.device)
-    rec_d = _lib.h2d(rec.view(np.uint8), out.device)
-    _lib.call("ublr_rng_normals", _lib.ptr(rec_d), counts.ctypes.data, ns, _lib.ptr(out), _lib.ptr(ws), ws_bytes,
-              _lib.stream_handle())
+    ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device=device)
+    rec_d = _lib.h2d(rec.view(np.uint8), device)
     if len(_RNG_CACHE) > 64:
         _RNG_CACHE.clear()
-    _RNG_CACHE[ck] = (rec_d, counts, ns, ws, ws_bytes)
+    hit = _RNG_CACHE[ck] = (rec_d, counts, ns, ws, ws_bytes, rowmap)
+    return hit
+
+
+def launch_normals(record, out):
+    """Draw the normals of a rng_launch_record into `out` (K1)."""
+    rec_d, counts, ns, ws, ws_bytes, _ = record
+    _lib.call("ublr_rng_normals", _lib.ptr(rec_d), counts.ctypes.data, ns, _lib.ptr(out), _lib.ptr(ws), ws_bytes,
+              _lib.stream_handle(), launches=_lib.rng_launches(counts))
     return out
 
 

@@ -15,7 +15,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .bases import BlockBases, block_nullification_bases, naive_bases, tagging_bases
+from .bases import BlockBases, block_nullification_bases, draw_test_pair, naive_bases, tagging_bases
 from .linalg import RandomStream, device_normals
 from .operators import CountingOperator, DifferenceOperator, LinearOperatorHandle, counting_wrapper, unwrap
 from .tagging import DegenerateTagsError, make_tagging_matrix, plan_tagging
@@ -408,11 +408,11 @@ class _PhaseTimer:
 
     def __enter__(self):
         self.e0 = _torch().cuda.Event(enable_timing=True)
-        self.e0.record()
+        self.e0.record(_lib.current_stream())
 
     def __exit__(self, *exc):
         e1 = _torch().cuda.Event(enable_timing=True)
-        e1.record()
+        e1.record(_lib.current_stream())
         self.times._record(self.name, self.e0, e1)
 
 
@@ -441,13 +441,18 @@ def compress_type_a(op, tess, k, p=10, method="tag", stream=None, distribution="
             if optimize:
                 raise NotImplementedError("null-vector optimisation (ref/tagging.py:142-292) is outside the "
                                           "B200 hot path")
-            # the sketch of the policy's first draw runs while the host evaluates the plan
+            # the test blocks are drawn on the GPU while the host draws the
+            # tagging matrix; the sketch of the policy's first draw runs while
+            # the host evaluates the plan
+            test_pair = None
+            if not extra_samples:
+                test_pair = draw_test_pair(device_tess(tess, _torch().device("cuda")), stream.child(0), k + p)
             first = make_tagging_matrix(tess.b, tess.dim, extra_cols, distribution, stream.child(1).child(0))
             bases, bundle = tagging_bases(
                 cop, tess, k, p,
                 lambda: plan_tagging(tess, extra_cols, distribution, stream.child(1), max_redraws=max_tag_redraws, device="auto",
                                      first=first),
-                stream.child(0), extra_samples=extra_samples, first=first)
+                stream.child(0), extra_samples=extra_samples, first=first, test_pair=test_pair)
             plan = bundle.plan
         elif method == "bn":
             bases, _ = block_nullification_bases(cop, tess, k, p, stream.child(0))

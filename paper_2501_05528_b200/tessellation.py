@@ -265,6 +265,7 @@ class DeviceTess:
         self.cidx = t(self.cidx_h)
         self.pair_of = None if self.pair_of_h is None else t(self.pair_of_h)
         self._roff = {}
+        self.rng_records = {}   # memoised launch records of the test-block draws (bases.draw_test_pair)
 
     def ranks(self, k: int) -> np.ndarray:
         return np.minimum(k, self.sizes)

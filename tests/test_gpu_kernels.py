@@ -137,7 +137,7 @@ def test_tagged_sketch_matches_oracle(case):
     assert np.linalg.norm(Zh - bundle.z) <= 1e-13 * np.linalg.norm(bundle.z)
 
 
-@pytest.mark.parametrize("m,n,k", [(64, 20, 10), (256, 60, 48), (33, 33, 33), (100, 7, 7)])
+@pytest.mark.parametrize("m,n,k", [(64, 20, 10), (256, 60, 48), (33, 33, 33), (100, 7, 7), (64, 40, 32), (17, 5, 5)])
 def test_col_basis_matches_numpy(m, n, k):
     B = np.random.default_rng(m + n).standard_normal((m, n))
     got = P.col_basis(B, k)

@@ -11,13 +11,13 @@ run = lambda: P.compress(wl.op, wl.tess, wl.k, wl.method, p=wl.p, stream=P.Rando
 run(); torch.cuda.synchronize()
 orig = _lib.call
 shapes = {}
-def call(name, *args):
+def call(name, *args, **kw):
     if name == "ublr_gemm_batched":
         key = f"gemm t{args[0]}{args[1]} M{args[2]} N{args[3]} K{args[4]} b{args[22]}"
     else:
         key = name
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(); orig(name, *args); b.record()
+    a.record(); orig(name, *args, **kw); b.record()
     shapes.setdefault(key, []).append((a, b, _lib._work_of(name, args)))
 _lib.call = call
 import paper_2501_05528_b200.dense as D

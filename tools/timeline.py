@@ -24,10 +24,10 @@ for _ in range(2 if cfg == "c5" else 5):
 torch.cuda.synchronize()
 orig = _lib.call
 rec = []
-def call(name, *args):
+def call(name, *args, **kw):
     h0 = time.perf_counter()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(); orig(name, *args); b.record()
+    a.record(); orig(name, *args, **kw); b.record()
     rec.append((name, h0, time.perf_counter(), a, b))
 _lib.call = call
 e0 = torch.cuda.Event(enable_timing=True)
