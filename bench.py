@@ -182,14 +182,21 @@ def cpu_baseline(wl, budget_s=12.0):
                       f"(dense operator prebuilt, OpenBLAS on all cores)"}
 
 
-KERNEL_OF = {"ublr_sketch_tagged_pair": "k_sketch_tagged3 (Kronecker-restructured tagged sketch, TMEM tag groups)",
-             "ublr_sketch_tagged": "k_sketch_tagged3 (Kronecker-restructured tagged sketch, TMEM tag groups)",
+KERNEL_OF = {"ublr_sketch_tagged_pair": "k_sketch_tagged{v} (Kronecker-restructured tagged sketch, TMEM tag groups)",
+             "ublr_sketch_tagged": "k_sketch_tagged{v} (Kronecker-restructured tagged sketch, TMEM tag groups)",
              "ublr_apply": "k_apply3 (operator apply, warp-specialised: A generated by producer warps, DMMA consumers)",
              "ublr_gemm_batched": "k_gemm2 (batched DMMA GEMM)",
-             "ublr_coupling": "k_coupling2 (C_ij = U_i^T A_ij V_j)"}
+             "ublr_coupling": "k_coupling3 (C_ij = U_i^T A_ij V_j, warp-specialised)",
+             "ublr_coupling_nearfield": "k_coupling_nf_small (coupling + colour-probe near field, one pass over A)"}
 
 
-def roofline_of(ev, work, config):
+def kernel_label(entry, operator):
+    """The kernel an entry point dispatches to for this workload (sketch.cu:
+    v4 warp-specialised for the table log, v3 for 1/r and dense)."""
+    return KERNEL_OF.get(entry, entry).replace("{v}", "4" if operator.startswith("-log") else "3")
+
+
+def roofline_of(ev, work, config, operator):
     """Dominant C-ABI kernel by device time among those with an algorithmic
     flop count; achieved = flops / CUDA-event time of that kernel."""
     cands = [(float(np.sum(ev[k])), k) for k in ev if work.get(k, 0.0) > 0]
@@ -204,7 +211,7 @@ def roofline_of(ev, work, config):
         if tj.get("entry") == name:
             traffic = tj.get("dram_bytes_per_launch")
     n_launch = len(ev[name])
-    return {"kernel": KERNEL_OF.get(name, name), "entry": name, "bound": "fp64", "achieved": achieved,
+    return {"kernel": kernel_label(name, operator), "entry": name, "bound": "fp64", "achieved": achieved,
             "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
             "peak_source": "measured DMMA m8n8k4 burst (profiles/fp64_peak_r01.txt); MEASURED_PEAKS.json has no "
                            "fp64 entry",
@@ -282,7 +289,7 @@ def run_sharded(args, rank, world, local):
         tt = torch.tensor([t], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t = float(tt.item())
-    roof = roofline_of(ev, _lib.work, args.config)
+    roof = roofline_of(ev, _lib.work, args.config, wl.describe().get("operator", ""))
     sh = shards[me]
     rows = sh.r1 - sh.r0
     if rank == 0:
@@ -418,7 +425,7 @@ def main():
         e2e = float(t.item())
 
     # --- roofline of the dominant kernel -------------------------------------
-    roof = roofline_of(ev, _lib.work, args.config)
+    roof = roofline_of(ev, _lib.work, args.config, wl.describe().get("operator", ""))
     kernel_ms = {k: float(np.sum(v)) for k, v in ev0.items()}   # one untimed instrumented step
 
     if rank == 0:

@@ -139,36 +139,55 @@ def draw_test_blocks(dt, stream: RandomStream, side: int, cols: int):
     return device_normals(specs, out)
 
 
-def draw_test_pair(dt, stream: RandomStream, cols: int):
+def draw_test_pair(dt, stream: RandomStream, cols: int, tag_stream: RandomStream | None = None, tag_cols: int = 0):
     """(G, H) with G_i = gaussian(m_i, cols, stream.child(0, i)) and
     H_i = ...child(1, i) (ref/bases.py:163-168), drawn in ONE launch set into
-    a (2, N, cols) buffer."""
+    a (2, N, cols) buffer. With `tag_stream`, the same launch also draws the
+    gaussian tagging matrix T = gaussian(b, tag_cols, tag_stream)
+    (ref/tagging.py:61-91) on the device and (G, H, T) is returned: the host
+    draws the same bits with numpy for its planning, and the sketch can be
+    launched without waiting for a host-to-device copy of T."""
     from .linalg import launch_normals, rng_launch_record
 
     torch = _torch()
-    GH = torch.empty((2, dt.n, cols), dtype=torch.float64, device=dt.device)
-    ck = ("test_pair", stream.seed, tuple(stream.key), cols)
+    n2 = 2 * dt.n * cols
+    tn = dt.b * tag_cols if tag_stream is not None else 0
+    buf = torch.empty(n2 + tn, dtype=torch.float64, device=dt.device)
+    ck = ("test_pair", stream.seed, tuple(stream.key), cols,
+          None if tag_stream is None else (tag_stream.seed, tuple(tag_stream.key), tag_cols))
     rec = dt.rng_records.get(ck)
     if rec is None:
         b = dt.b
-        suffix = np.stack([np.repeat(np.arange(2), b), np.tile(np.arange(b), 2)], axis=1)  # (side, i)
-        rows = np.concatenate([dt.sizes, dt.sizes])
+        keys = [tuple(stream.key) + (side, i) for side in (0, 1) for i in range(b)]
+        rows = np.concatenate([dt.sizes, dt.sizes]).astype(np.int64)
         offs = np.concatenate([dt.off_h[:-1].astype(np.int64) * cols,
                                dt.n * cols + dt.off_h[:-1].astype(np.int64) * cols])
-        rec = rng_launch_record(stream.seed, stream.key, rows, cols, offs, cols, None, dt.device, suffix=suffix)
+        if tag_stream is None:
+            suffix = np.stack([np.repeat(np.arange(2), b), np.tile(np.arange(b), 2)], axis=1)  # (side, i)
+            rec = rng_launch_record(stream.seed, stream.key, rows, cols, offs, cols, None, dt.device, suffix=suffix)
+        else:
+            if tag_stream.seed != stream.seed:
+                raise ValueError("tagging and test-block streams must share the seed")
+            rec = rng_launch_record(stream.seed, keys + [tuple(tag_stream.key)], np.append(rows, b),
+                                    np.append(np.full(2 * b, cols), tag_cols), np.append(offs, n2),
+                                    np.append(np.full(2 * b, cols), tag_cols), None, dt.device)
         if len(dt.rng_records) > 16:
             dt.rng_records.clear()
         dt.rng_records[ck] = rec
-    launch_normals(rec, GH)
-    return GH[0], GH[1]
+    launch_normals(rec, buf)
+    GH = buf[:n2].view(2, dt.n, cols)
+    if tag_stream is None:
+        return GH[0], GH[1]
+    return GH[0], GH[1], buf[n2:].view(dt.b, tag_cols)
 
 
-def tagged_sketch(op, dt, T_dev, T_entries, G, H, gc, out=None):
+def tagged_sketch(op, dt, T_dev, T_entries, G, H, gc, out=None, ell=None):
     """Y = A Omega, Z = A^* Psi for the tagged test matrices; returns (Y, Z)
-    (into `out` = (Y, Z) when given)."""
+    (into `out` = (Y, Z) when given). T_entries (host) is needed only by a
+    black-box operator."""
     torch = _torch()
     inner = unwrap(op)
-    ell = T_entries.shape[1]
+    ell = T_entries.shape[1] if ell is None else ell
     s = ell * gc
     stream = _lib.stream_handle()
     if hasattr(inner, "device_op"):
@@ -234,18 +253,29 @@ def tagging_bases(op, tess: Tessellation, k: int, p: int, plan, stream: RandomSt
         # large b: the planner's aspect ratios run on the GPU, so plan before
         # the sketch occupies it (no speculative sketch)
         plan, planner = planner(), None
-    matrix = first if planner is not None else plan.matrix
-    T_entries = matrix.entries
-    ell = T_entries.shape[1]
+    first_fn = first if callable(first) else (lambda: first)
+    device_T = (planner is not None and test_pair is not None and len(test_pair) == 3
+                and hasattr(unwrap(op), "device_op"))
+    if device_T:
+        # the device draw of the policy's first matrix (draw_test_pair with
+        # tag_stream): the sketch is launched before the host has drawn it
+        T_dev = test_pair[2]
+        ell = T_dev.shape[1]
+        matrix = None
+    else:
+        matrix = first_fn() if planner is not None else plan.matrix
+        ell = matrix.entries.shape[1]
+        T_dev = _lib.h2d(matrix.entries, dt.device)
     s = ell * gc
-    # everything the sketch launch needs is staged before the RNG launch, so
-    # the two kernels follow each other on the GPU without a host gap
-    T_dev = _lib.h2d(T_entries, dt.device)
     Y = torch.empty((dt.n, s), dtype=torch.float64, device=dt.device)
     Z = torch.empty((dt.n, s), dtype=torch.float64, device=dt.device)
     _bill(op, s, s)
-    G, H = draw_test_pair(dt, stream, gc) if test_pair is None else test_pair
-    Y, Z = tagged_sketch(op, dt, T_dev, T_entries, G, H, gc, out=(Y, Z))
+    G, H = draw_test_pair(dt, stream, gc) if test_pair is None else test_pair[:2]
+    Y, Z = tagged_sketch(op, dt, T_dev, None if matrix is None else matrix.entries, G, H, gc, out=(Y, Z), ell=ell)
+    if matrix is None:
+        matrix = first_fn()                  # host draw of the same bits, while the sketch runs
+        if matrix.entries.shape != tuple(T_dev.shape):
+            raise RuntimeError("device and host tagging draws disagree in shape")
     if planner is not None:
         plan = planner()                     # host work, overlapping the sketch
         if plan.matrix is not matrix:        # redrawn: sketch the accepted matrix

@@ -111,14 +111,18 @@ extern "C" int ublr_null_vectors(const double* T, int ell, const int32_t* ptr, c
       double ss = 0.0, scale = 0.0;
       for (int i = j + 1; i < ell; ++i) scale = fmax(scale, fabs(col[i]));
       if (scale > 0.0) {
-        for (int i = j + 1; i < ell; ++i) ss += (col[i] / scale) * (col[i] / scale);
+        const double inv_scale = 1.0 / scale;   // one division per column (dnrm2-style scaling)
+        for (int i = j + 1; i < ell; ++i) ss += (col[i] * inv_scale) * (col[i] * inv_scale);
       }
       const double xnorm = scale * sqrt(ss);
       if (xnorm == 0.0) {
         tau[j] = 0.0;
         continue;
       }
-      const double beta = -copysign(hypot(alpha, xnorm), alpha);
+      // dlapy2: w sqrt(1 + (z / w)^2) with w = max(|alpha|, xnorm) (no libm hypot call)
+      const double aa = fabs(alpha), wmax = fmax(aa, xnorm), zmin = fmin(aa, xnorm);
+      const double ratio = zmin / wmax;
+      const double beta = -copysign(wmax * sqrt(1.0 + ratio * ratio), alpha);
       tau[j] = (beta - alpha) / beta;
       const double inv = 1.0 / (alpha - beta);
       for (int i = j + 1; i < ell; ++i) col[i] *= inv;
@@ -180,10 +184,28 @@ extern "C" int ublr_tag_plan_host(const double* T, int ell, const int32_t* ptr, 
     for (int p = ptr[i]; p < ptr[i + 1]; ++p) nearm[idx[p]] = 1;
     const double* z = Z + (size_t)i * ell;
     double lo = INFINITY, hi = -INFINITY;
-    for (int j = 0; j < b; ++j) {
+    int j = 0;
+    for (; j + 4 <= b; j += 4) {   // four independent dot products (ILP; same per-dot order)
+      const double* t0 = T + (size_t)j * ell;
+      double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+      for (int c = 0; c < ell; ++c) {   // host: no libm fma call
+        const double zc = z[c];
+        d0 += t0[c] * zc;
+        d1 += t0[ell + c] * zc;
+        d2 += t0[2 * ell + c] * zc;
+        d3 += t0[3 * ell + c] * zc;
+      }
+      const double dv[4] = {fabs(d0), fabs(d1), fabs(d2), fabs(d3)};
+      for (int u = 0; u < 4; ++u) {
+        if (nearm[j + u]) continue;
+        lo = fmin(lo, dv[u]);
+        hi = fmax(hi, dv[u]);
+      }
+    }
+    for (; j < b; ++j) {
       if (nearm[j]) continue;
       double d = 0.0;
-      for (int c = 0; c < ell; ++c) d += T[(size_t)j * ell + c] * z[c];  // host: no libm fma call
+      for (int c = 0; c < ell; ++c) d += T[(size_t)j * ell + c] * z[c];
       d = fabs(d);
       lo = fmin(lo, d);
       hi = fmax(hi, d);

@@ -118,9 +118,11 @@ def rng_launch_record(seed, keys, rows, cols, offsets, ld, rowmap, device, suffi
     normals are drawn on every launch_normals call."""
     from .seedseq import philox_keys, philox_keys_suffixed
 
+    cols_a = np.broadcast_to(np.asarray(cols, dtype=np.int64), np.shape(rows))   # scalar or per stream
+    ld_a = np.broadcast_to(np.asarray(ld, dtype=np.int64), np.shape(rows))
     ck = (int(seed), tuple(keys) if suffix is not None else tuple(map(tuple, keys)),
-          np.asarray(rows, dtype=np.int64).tobytes(), int(cols), np.asarray(offsets, dtype=np.int64).tobytes(),
-          int(ld), _lib.ptr(rowmap), None if suffix is None else np.asarray(suffix).tobytes(), str(device))
+          np.asarray(rows, dtype=np.int64).tobytes(), cols_a.tobytes(), np.asarray(offsets, dtype=np.int64).tobytes(),
+          ld_a.tobytes(), _lib.ptr(rowmap), None if suffix is None else np.asarray(suffix).tobytes(), str(device))
     hit = _RNG_CACHE.get(ck)
     if hit is not None:
         return hit
@@ -131,10 +133,10 @@ def rng_launch_record(seed, keys, rows, cols, offsets, ld, rowmap, device, suffi
     ns = kk.shape[0]
     rec = np.zeros(ns, dtype=_lib.RNG_STREAM_DTYPE)
     rec["key0"], rec["key1"] = kk[:, 0], kk[:, 1]
-    counts = np.asarray(rows, dtype=np.int64) * int(cols)
+    counts = np.asarray(rows, dtype=np.int64) * cols_a
     rec["count"] = counts
-    rec["cols"] = max(int(cols), 1)
-    rec["ld"] = int(ld)
+    rec["cols"] = np.maximum(cols_a, 1)
+    rec["ld"] = ld_a
     rec["out_offset"] = np.asarray(offsets, dtype=np.int64)
     rec["rowmap"] = _lib.ptr(rowmap)
     lib = _lib.load()

@@ -416,6 +416,19 @@ class _PhaseTimer:
         self.times._record(self.name, self.e0, e1)
 
 
+class _Lazy:
+    """A value computed on first call (the host tagging draw, deferred until
+    the sketch of its device twin has been launched)."""
+
+    def __init__(self, fn):
+        self._fn, self._done, self._v = fn, False, None
+
+    def __call__(self):
+        if not self._done:
+            self._v, self._done = self._fn(), True
+        return self._v
+
+
 def _stream_scoped(fn):
     """Run a compressor with the CUDA stream handle captured once (_lib.stream_scope)."""
     import functools
@@ -446,12 +459,16 @@ def compress_type_a(op, tess, k, p=10, method="tag", stream=None, distribution="
             # the host evaluates the plan
             test_pair = None
             if not extra_samples:
-                test_pair = draw_test_pair(device_tess(tess, _torch().device("cuda")), stream.child(0), k + p)
-            first = make_tagging_matrix(tess.b, tess.dim, extra_cols, distribution, stream.child(1).child(0))
+                # gaussian tagging: T is drawn in the same launch (the host draws the same bits below)
+                ell = 3 ** tess.dim + 1 + extra_cols
+                tag = (stream.child(1).child(0), ell) if distribution == "gaussian" and tess.b >= ell else (None, 0)
+                test_pair = draw_test_pair(device_tess(tess, _torch().device("cuda")), stream.child(0), k + p, *tag)
+            first = _Lazy(lambda: make_tagging_matrix(tess.b, tess.dim, extra_cols, distribution,
+                                                      stream.child(1).child(0)))
             bases, bundle = tagging_bases(
                 cop, tess, k, p,
                 lambda: plan_tagging(tess, extra_cols, distribution, stream.child(1), max_redraws=max_tag_redraws, device="auto",
-                                     first=first),
+                                     first=first()),
                 stream.child(0), extra_samples=extra_samples, first=first, test_pair=test_pair)
             plan = bundle.plan
         elif method == "bn":
