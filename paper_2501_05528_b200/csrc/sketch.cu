@@ -898,20 +898,38 @@ __global__ void __launch_bounds__(C::NT, 1) k_sketch_tagged4(ublr_op_t op, const
       bmeta[z] = (kk * SB + c) | (kk << 16) | (valid ? (1 << 30) : 0);
     }
     int it = 0;
+    // column coordinates are loaded one stage ahead (software pipelining: the
+    // global-load latency of stage it + 1 hides behind the evaluations of it)
+    double cn[EPT][DIM];
+    auto load_cols = [&](int q0, int qe) {
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) {
+        const int q = q0 + kq + e * KL;
+        const int qc = q < qe ? q : q0;
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) cn[e][d] = __ldg(op.coords + (int64_t)d * n + qc);
+      }
+    };
+    load_cols(off[0], off[1]);
     for (int j = 0; j < b; ++j) {
       const int qe = off[j + 1];
       for (int q0 = off[j]; q0 < qe; q0 += BK, ++it) {
         const int s = it % STAGES;
+        double cc[EPT][DIM];
+#pragma unroll
+        for (int e = 0; e < EPT; ++e)
+#pragma unroll
+          for (int d = 0; d < DIM; ++d) cc[e][d] = cn[e][d];
+        if (q0 + BK < qe) load_cols(q0 + BK, qe);
+        else if (j + 1 < b) load_cols(qe, off[j + 2]);
         double v[EPT];
 #pragma unroll
         for (int e = 0; e < EPT; ++e) {
           const int q = q0 + kq + e * KL;
           const bool ok = q < qe;
           const int qc = ok ? q : q0;
-          const double c0 = __ldg(op.coords + qc);
-          const double c1 = DIM > 1 ? __ldg(op.coords + n + qc) : 0.0;
-          const double c2 = DIM > 2 ? __ldg(op.coords + 2 * n + qc) : 0.0;
-          const double a = kernel_entry_dim<KIND, DIM>(rp, qc, c0, c1, c2, diag, &lt);
+          const double a = kernel_entry_dim<KIND, DIM>(rp, qc, cc[e][0], DIM > 1 ? cc[e][DIM > 1 ? 1 : 0] : 0.0,
+                                                       DIM > 2 ? cc[e][DIM > 2 ? 2 : 0] : 0.0, diag, &lt);
           v[e] = ok ? a : 0.0;
         }
         ws::mbar_wait(&empty[s], ((uint32_t)(it / STAGES) & 1) ^ 1);
@@ -970,25 +988,19 @@ __global__ void __launch_bounds__(C::NT, 1) k_sketch_tagged4(ublr_op_t op, const
         ws::mbar_wait(&full[s], (uint32_t)(it / STAGES) & 1);
         const double* As = As0 + s * C::A_STAGE;
         const double* Bs = Bs0 + s * C::B_STAGE;
-        double a[2][MI], bb[2][NJ];
+        static_assert(MI == 2, "the m16n8k8 fragments cover the warp's two 8-row blocks");
+        // m16n8k8 DMMA: a0..a3 = A[g][t], A[g+8][t], A[g][t+4], A[g+8][t+4];
+        // b0, b1 = B[t][g], B[t+4][g]; d = (w[0][jj], w[1][jj]) -- the m8n8k4 layout
 #pragma unroll
-        for (int i = 0; i < MI; ++i) a[0][i] = As[t * SA + am0 + i * 8];
+        for (int k8 = 0; k8 < BK / 8; ++k8) {
+          const int kr = k8 * 8 + t;
+          const double a0 = As[kr * SA + am0], a1 = As[kr * SA + am0 + 8];
+          const double a2 = As[(kr + 4) * SA + am0], a3 = As[(kr + 4) * SA + am0 + 8];
 #pragma unroll
-        for (int jj = 0; jj < NJ; ++jj) bb[0][jj] = Bs[t * SB + bn0 + jj * 8];
-#pragma unroll
-        for (int k4 = 0; k4 < BK / 4; ++k4) {
-          const int cur = k4 & 1;
-          if (k4 + 1 < BK / 4) {
-            const int kr = (k4 + 1) * 4 + t;
-#pragma unroll
-            for (int i = 0; i < MI; ++i) a[cur ^ 1][i] = As[kr * SA + am0 + i * 8];
-#pragma unroll
-            for (int jj = 0; jj < NJ; ++jj) bb[cur ^ 1][jj] = Bs[kr * SB + bn0 + jj * 8];
+          for (int jj = 0; jj < NJ; ++jj) {
+            const double b0 = Bs[kr * SB + bn0 + jj * 8], b1 = Bs[(kr + 4) * SB + bn0 + jj * 8];
+            mma16x8x8(w[0][jj][0], w[0][jj][1], w[1][jj][0], w[1][jj][1], a0, a1, a2, a3, b0, b1);
           }
-#pragma unroll
-          for (int i = 0; i < MI; ++i)
-#pragma unroll
-            for (int jj = 0; jj < NJ; ++jj) mma8x8x4(w[i][jj][0], w[i][jj][1], a[cur][i], bb[cur][jj]);
         }
         ws::mbar_arrive(&empty[s]);
       }
@@ -1243,10 +1255,15 @@ int sketch_common(const ublr_op_t* op, const int32_t* off, int b, const double* 
   static const char* ver = getenv("UBLR_SKETCH_VERSION");
   const int v = ver ? atoi(ver) : 4;
   const bool vec_ok = (ld_x % 2) == 0 && (gc % 2) == 0 && ((uintptr_t)G) % 16 == 0 && (!H || ((uintptr_t)H) % 16 == 0);
-  // v4 (warp-specialised) where the entry evaluation is expensive (table log,
-  // ~22 FP64 ops): c2 0.246 -> 0.210 ms, c4 325 -> 274 ms; for 1/r (~9 ops) the
-  // synchronous v3 with 16 DMMA warps stays faster (c5 shard 1.98 s vs 2.09 s)
-  if (v == 4 && ell <= 10 && op->kind == UBLR_OP_LOG && vec_ok)
+  // v4 (warp-specialised): c2 0.246 -> 0.196 ms, c4 325 -> 263 ms (table log);
+  // c5 shard 1.98 -> 1.57 s (1/r)
+  // 1/r: v4 since its m16n8k8 consumers and one-stage-ahead column loads
+  // (c5 shard 1.98 s with v3 -> 1.57 s); UBLR_SKETCH_V4_INV=0 restores v3
+  static const bool v4_inv = [] {
+    const char* e = getenv("UBLR_SKETCH_V4_INV");
+    return !e || atoi(e) != 0;
+  }();
+  if (v == 4 && ell <= 10 && (op->kind == UBLR_OP_LOG || (v4_inv && op->kind == UBLR_OP_INV)) && vec_ok)
     return sketch_common_v4(op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y, row_begin, row_end, st);
   if (v >= 3 && ell <= 10) return sketch_common_v3(op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y, row_begin, row_end, st);
   return sketch_common_v1(op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y, row_begin, row_end, st);

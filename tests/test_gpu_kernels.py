@@ -105,7 +105,7 @@ def test_fast_log_accuracy():
     assert err.max() <= 4e-16 * max(1.0, np.abs(A).max()) * 8
 
 
-@pytest.mark.parametrize("case", ["c1s", "log1k", "rand500"])
+@pytest.mark.parametrize("case", ["c1s", "log1k", "rand500", "inv1k", "inv_rand500", "inv3d"])
 def test_tagged_sketch_matches_oracle(case):
     if case == "c1s":
         from cases import c1_problem
@@ -117,11 +117,23 @@ def test_tagged_sketch_matches_oracle(case):
         bx, coords, oop = log_problem(32, 16)
         tess = P.build_tessellation(P.grid_points(32, 2), 16)
         op, gc = P.KernelOperator(coords, "log", oop.diag), 15
+    elif case == "inv1k":
+        coords = O.cell_centres(32, 2)
+        bx, oop = O.partition(coords, 16), O.KernelOp(coords, "inv", 64.0)
+        tess = P.build_tessellation(P.grid_points(32, 2), 16)
+        op, gc = P.KernelOperator(coords, "inv", 64.0), 15
+    elif case == "inv3d":
+        coords = O.cell_centres(12, 3)   # ell = 28: the general (v1) sketch
+        bx, oop = O.partition(coords, 64), O.KernelOp(coords, "inv", 24.0)
+        tess = P.build_tessellation(P.grid_points(12, 3), 64)
+        op, gc = P.KernelOperator(coords, "inv", 24.0), 8
     else:
         from cases import rand500_problem
         bx, coords, oop = rand500_problem()
         tess = P.build_tessellation(P.PointCloud(coords, 2), 16)
-        op, gc = P.KernelOperator(coords, "log", 3.0), 12
+        kind, diag = ("inv", 40.0) if case.startswith("inv") else ("log", 3.0)
+        oop = O.KernelOp(coords, kind, diag)
+        op, gc = P.KernelOperator(coords, kind, diag), 12
     dt = device_tess(tess, torch.device(DEV))
     st = P.RandomStream(7).child(0)
     plan = P.plan_tagging(tess, 0, "gaussian", P.RandomStream(7).child(1))
