@@ -172,52 +172,76 @@ def lu_sign(W, LU, D, nb=NB, R=None):
 
 def trsm_right_upper(X, R, f: Factors, tmp):
     """X_b <- X_b R_b^-1 in place (X: batch x rows x n, R upper n x n).
-    tmp: (batch, rows, nb) scratch."""
+    tmp: (batch, rows, nb) scratch. Recursive on columns: Y1 = X1 R11^-1,
+    X2 -= Y1 R12 (one GEMM with K = half the range), Y2 = X2 R22^-1; the
+    nb-column leaves multiply by the stored diagonal-block inverses."""
     batch, rows, n = X.shape
     nn = n * n
     sx = rows * n
     st = tmp.shape[1] * tmp.shape[2]
-    for bi, (j0, jb) in enumerate(f.blocks):
-        if j0 > 0:  # X[:, j] -= Z[:, :j0] R[:j0, j]
-            gemm(0, 0, rows, jb, j0, -1.0, addr(X), n, sx, addr(R, j0), n, nn, 1.0, addr(X, j0), n, sx, batch)
-        _lib.call("ublr_gather", addr(X, j0), n, sx, None, 0, rows, jb, 0, 0, addr(tmp), tmp.shape[2], st, batch,
-                  _lib.stream_handle())
-        gemm(0, 0, rows, jb, jb, 1.0, addr(tmp), tmp.shape[2], st, addr(f.inv[bi]), jb, jb * jb,
-             0.0, addr(X, j0), n, sx, batch)
+
+    def rec(j0, a):
+        if a <= f.nb:
+            bi = j0 // f.nb
+            _lib.call("ublr_gather", addr(X, j0), n, sx, None, 0, rows, a, 0, 0, addr(tmp), tmp.shape[2], st, batch,
+                      _lib.stream_handle())
+            gemm(0, 0, rows, a, a, 1.0, addr(tmp), tmp.shape[2], st, addr(f.inv[bi]), a, a * a,
+                 0.0, addr(X, j0), n, sx, batch)
+            return
+        h = _split(a, f.nb)
+        rec(j0, h)
+        gemm(0, 0, rows, a - h, h, -1.0, addr(X, j0), n, sx, addr(R, j0 * n + j0 + h), n, nn, 1.0,
+             addr(X, j0 + h), n, sx, batch)
+        rec(j0 + h, a - h)
+
+    rec(0, n)
 
 
 def trsm_left(T, X, f: Factors, inv_set, upper: bool, trans: bool, tmp):
     """X_b <- op(T_b)^-1 X_b in place, op = transpose if `trans`.
     T: batch x n x n (only the triangle selected by `upper` is read; the
     diagonal blocks come from the stored inverses `inv_set` of T's own
-    diagonal blocks). X: batch x n x w. tmp: batch x nb x w."""
+    diagonal blocks). X: batch x n x w. tmp: batch x nb x w.
+    Recursive on rows (forward for a lower op(T), backward for an upper one):
+    the off-diagonal update is one GEMM with K = half the range, so the
+    flops run at large-K GEMM rates instead of rank-nb panel updates."""
     batch, n, w = X.shape
     nn = n * n
     sx = n * w
     stt = tmp.shape[1] * tmp.shape[2]
     eff_lower = (not upper) != trans  # lower-triangular after op
-    order = list(enumerate(f.blocks))
-    if not eff_lower:
-        order = order[::-1]
-    for bi, (j0, jb) in order:
-        if eff_lower and j0 > 0:
-            # X_j -= op(T)[j, :j0] X[:j0]; op(T)[j, :j0] = T[j, :j0] or T[:j0, j]^T
-            if not trans:
-                gemm(0, 0, jb, w, j0, -1.0, addr(T, j0 * n), n, nn, addr(X), w, sx, 1.0, addr(X, j0 * w), w, sx, batch)
-            else:
-                gemm(1, 0, jb, w, j0, -1.0, addr(T, j0), n, nn, addr(X), w, sx, 1.0, addr(X, j0 * w), w, sx, batch)
-        elif not eff_lower and j0 + jb < n:
-            rest = n - j0 - jb
-            if not trans:
-                gemm(0, 0, jb, w, rest, -1.0, addr(T, j0 * n + j0 + jb), n, nn, addr(X, (j0 + jb) * w), w, sx,
-                     1.0, addr(X, j0 * w), w, sx, batch)
-            else:
-                gemm(1, 0, jb, w, rest, -1.0, addr(T, (j0 + jb) * n + j0), n, nn, addr(X, (j0 + jb) * w), w, sx,
-                     1.0, addr(X, j0 * w), w, sx, batch)
+
+    def leaf(j0, jb):
+        bi = j0 // f.nb
         _lib.call("ublr_gather", addr(X, j0 * w), w, sx, None, 0, jb, w, 0, 0, addr(tmp), w, stt, batch,
                   _lib.stream_handle())
         gemm(1 if trans else 0, 0, jb, w, jb, 1.0, addr(inv_set[bi]), jb, jb * jb, addr(tmp), w, stt,
              0.0, addr(X, j0 * w), w, sx, batch)
+
+    def update(r0, r1, c0, c1):
+        # X[r0:r1] -= op(T)[r0:r1, c0:c1] X[c0:c1]; op(T)[r, c] = T[r, c] or T[c, r]
+        if not trans:
+            gemm(0, 0, r1 - r0, w, c1 - c0, -1.0, addr(T, r0 * n + c0), n, nn, addr(X, c0 * w), w, sx,
+                 1.0, addr(X, r0 * w), w, sx, batch)
+        else:
+            gemm(1, 0, r1 - r0, w, c1 - c0, -1.0, addr(T, c0 * n + r0), n, nn, addr(X, c0 * w), w, sx,
+                 1.0, addr(X, r0 * w), w, sx, batch)
+
+    def rec(j0, a):
+        if a <= f.nb:
+            leaf(j0, a)
+            return
+        h = _split(a, f.nb)
+        if eff_lower:
+            rec(j0, h)
+            update(j0 + h, j0 + a, j0, j0 + h)
+            rec(j0 + h, a - h)
+        else:
+            rec(j0 + h, a - h)
+            update(j0, j0 + h, j0 + h, j0 + a)
+            rec(j0, h)
+
+    rec(0, n)
 
 
 def check_status(f: Factors, what: str):

@@ -266,17 +266,18 @@ def lstsq_right(LHS, M):
     torch = _torch()
     K, L = M.shape
     f64 = _f64(M.device)
-    G1 = torch.empty((1, K, K), **f64)
-    R1 = torch.zeros_like(G1)
-    D.gemm(0, 1, K, K, L, 1.0, D.addr(M), L, 0, D.addr(M), L, 0, 0.0, D.addr(G1), K, 0, 1)
-    f1 = D.cholesky_upper(G1, R1)
-    D.check_status(f1, "pinv_core: V^T Omega is rank deficient")
+    # Gram matrices by SYRK on M^T (upper tiles only: the Cholesky reads the upper triangle)
     Q1 = torch.empty((1, L, K), **f64)
     _lib.call("ublr_gather", D.addr(M), L, 0, None, 0, K, L, 0, 1, D.addr(Q1), K, 0, 1, _lib.stream_handle())
+    G1 = torch.empty((1, K, K), **f64)
+    R1 = torch.zeros_like(G1)
+    D._syrk_upper(K, L, 1.0, D.addr(Q1), K, 0, 0.0, D.addr(G1), K, 0, 1)
+    f1 = D.cholesky_upper(G1, R1)
+    D.check_status(f1, "pinv_core: V^T Omega is rank deficient")
     D.trsm_right_upper(Q1, R1, f1, torch.empty((1, L, D.NB), **f64))
     G2 = torch.empty((1, K, K), **f64)
     R2 = torch.zeros_like(G2)
-    D.gemm(1, 0, K, K, L, 1.0, D.addr(Q1), K, 0, D.addr(Q1), K, 0, 0.0, D.addr(G2), K, 0, 1)
+    D._syrk_upper(K, L, 1.0, D.addr(Q1), K, 0, 0.0, D.addr(G2), K, 0, 1)
     f2 = D.cholesky_upper(G2, R2)
     D.check_status(f2, "pinv_core: second CholeskyQR pass")
     C1t = torch.empty((1, K, LHS.shape[0]), **f64)      # (LHS Q1)^T = Q1^T LHS^T
