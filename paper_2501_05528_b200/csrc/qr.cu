@@ -54,7 +54,6 @@ __global__ void __launch_bounds__(QR_THREADS) k_block_qr(const double* __restric
   const int lds = k | 1;
   double* S = smem;                 // m x lds
   double* tau = smem + m * lds;     // k
-  __shared__ double sh_beta;
 
   // 1. sample
   if (mode == 0) {
@@ -75,62 +74,77 @@ __global__ void __launch_bounds__(QR_THREADS) k_block_qr(const double* __restric
   }
   __syncthreads();
 
-  // 2. dgeqr2
-  for (int j = 0; j < k; ++j) {
-    if (warp == 0) {
-      double ss = 0.0;
-      for (int r = j + 1 + lane; r < m; r += 32) {
-        double x = S[r * lds + j];
-        ss = fma(x, x, ss);
-      }
-      ss = warp_sum(ss);
-      double alpha = S[j * lds + j];
-      double beta, t, scal;
-      if (ss == 0.0) {
-        t = 0.0; beta = alpha; scal = 1.0;
-      } else {
-        double nrm = sqrt(fma(alpha, alpha, ss));
-        beta = alpha >= 0.0 ? -nrm : nrm;
-        t = (beta - alpha) / beta;
-        scal = 1.0 / (alpha - beta);
-      }
-      for (int r = j + 1 + lane; r < m; r += 32) S[r * lds + j] *= scal;
-      if (lane == 0) { tau[j] = t; sh_beta = beta; }
+  // 2. dgeqr2 with look-ahead: warp 0 owns column j + 1 of step j's trailing
+  // update (c = j + 1 + warp), so it forms reflector j + 1 right after
+  // updating that column; one barrier per step.
+  double* vbuf = tau + k;                // dorg2r: two reflector copies of m doubles
+  auto reflector = [&](int j) {          // warp 0: dlarfg on column j (rows j..m-1)
+    double ss = 0.0;
+    for (int r = j + 1 + lane; r < m; r += 32) {
+      double x = S[r * lds + j];
+      ss = fma(x, x, ss);
     }
-    __syncthreads();
+    ss = warp_sum(ss);
+    double alpha = S[j * lds + j];
+    double beta, t, scal;
+    if (ss == 0.0) {
+      t = 0.0; beta = alpha; scal = 1.0;
+    } else {
+      double nrm = sqrt(fma(alpha, alpha, ss));
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      t = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    for (int r = j + 1 + lane; r < m; r += 32) S[r * lds + j] *= scal;
+    if (lane == 0) { tau[j] = t; S[j * lds + j] = beta; }
+  };
+  if (warp == 0) reflector(0);
+  __syncthreads();
+  for (int j = 0; j < k; ++j) {
     const double tj = tau[j];
-    // trailing columns c > j: w = v^T S(:, c); S(:, c) -= tj * v * w
+    // trailing columns c > j: w = v^T S(:, c); S(:, c) -= tj * v * w (v = [1; S(j+1:, j)])
     for (int c = j + 1 + warp; c < k; c += QR_WARPS) {
       double w = (lane == 0) ? S[j * lds + c] : 0.0;
       for (int r = j + 1 + lane; r < m; r += 32) w = fma(S[r * lds + j], S[r * lds + c], w);
       w = warp_sum(w) * tj;
       if (lane == 0) S[j * lds + c] -= w;
       for (int r = j + 1 + lane; r < m; r += 32) S[r * lds + c] = fma(-w, S[r * lds + j], S[r * lds + c]);
+      if (c == j + 1) {                  // warp 0: the next pivot column is final
+        __syncwarp();
+        reflector(j + 1);
+      }
     }
-    __syncthreads();
-    if (tid == 0) S[j * lds + j] = sh_beta;
     __syncthreads();
   }
 
-  // 3. dorg2r: Q = H_0 ... H_{k-1} [I; 0], in place, right to left
+  // 3. dorg2r: Q = H_0 ... H_{k-1} [I; 0], in place, right to left. v_j is
+  // read from a copy (vbuf, double-buffered) so that column j can be formed
+  // in the same step as the update of columns c > j: one barrier per step.
+  const int fw = QR_WARPS - 1;           // the warp that forms columns and stages reflectors
+  if (warp == fw)
+    for (int r = lane; r < m; r += 32) vbuf[((k - 1) & 1) * m + r] = r > k - 1 ? S[r * lds + k - 1] : 0.0;
+  __syncthreads();
   for (int j = k - 1; j >= 0; --j) {
     const double tj = tau[j];
+    const double* v = vbuf + (j & 1) * m;   // v_j below the diagonal (v_j[j] = 1 implicit)
     for (int c = j + 1 + warp; c < k; c += QR_WARPS) {
-      // column c of the partially formed Q: apply H_j (v = [1; S(j+1:, j)])
+      // column c of the partially formed Q: apply H_j (rows < c of column c are zero)
       double w = (lane == 0) ? S[j * lds + c] : 0.0;
-      for (int r = j + 1 + lane; r < m; r += 32) w = fma(S[r * lds + j], S[r * lds + c], w);
+      for (int r = j + 1 + lane; r < m; r += 32) w = fma(v[r], S[r * lds + c], w);
       w = warp_sum(w) * tj;
       if (lane == 0) S[j * lds + c] -= w;
-      for (int r = j + 1 + lane; r < m; r += 32) S[r * lds + c] = fma(-w, S[r * lds + j], S[r * lds + c]);
+      for (int r = j + 1 + lane; r < m; r += 32) S[r * lds + c] = fma(-w, v[r], S[r * lds + c]);
     }
-    __syncthreads();
-    // column j itself: e_j - tau v
-    for (int r = tid; r < m; r += QR_THREADS) {
-      double v;
-      if (r < j) v = 0.0;
-      else if (r == j) v = 1.0 - tj;
-      else v = -tj * S[r * lds + j];
-      S[r * lds + j] = v;
+    if (warp == fw) {
+      // column j itself: e_j - tau v; and stage v_{j-1} for the next step
+      for (int r = lane; r < m; r += 32) {
+        double x;
+        if (r < j) x = 0.0;
+        else if (r == j) x = 1.0 - tj;
+        else x = -tj * v[r];
+        S[r * lds + j] = x;
+        if (j > 0) vbuf[((j - 1) & 1) * m + r] = r > j - 1 ? S[r * lds + j - 1] : 0.0;
+      }
     }
     __syncthreads();
   }
@@ -156,7 +170,7 @@ extern "C" int ublr_block_qr(const double* Y, int64_t ld_y, int mode, const doub
   UBLR_REQUIRE(!(mode & 1) || col0, UBLR_ERR_VALUE, "ublr_block_qr: cols mode needs col0");
   UBLR_REQUIRE(ld_u >= k && ld_u >= (k < m_max ? k : m_max), UBLR_ERR_VALUE, "ublr_block_qr: ld_u too small");
   int lds = k | 1;
-  size_t smem = (size_t)(m_max * lds + k) * sizeof(double);
+  size_t smem = (size_t)(m_max * lds + k + 2 * m_max) * sizeof(double);
   UBLR_REQUIRE(smem <= 220 * 1024, UBLR_ERR_VALUE, "ublr_block_qr: m*k sample exceeds shared memory");
   cudaStream_t st = (cudaStream_t)stream;
   UBLR_CUDA(cudaFuncSetAttribute(k_block_qr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -172,7 +186,7 @@ extern "C" int ublr_block_qr_pair(const double* Y, const double* Z, int64_t ld_y
                UBLR_ERR_VALUE, "ublr_block_qr_pair: bad arguments");
   UBLR_REQUIRE(ld_u >= k && ld_u >= (k < m_max ? k : m_max), UBLR_ERR_VALUE, "ublr_block_qr_pair: ld_u too small");
   int lds = k | 1;
-  size_t smem = (size_t)(m_max * lds + k) * sizeof(double);
+  size_t smem = (size_t)(m_max * lds + k + 2 * m_max) * sizeof(double);
   UBLR_REQUIRE(smem <= 220 * 1024, UBLR_ERR_VALUE, "ublr_block_qr_pair: m*k sample exceeds shared memory");
   cudaStream_t st = (cudaStream_t)stream;
   UBLR_CUDA(cudaFuncSetAttribute(k_block_qr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
