@@ -184,6 +184,7 @@ def cpu_baseline(wl, budget_s=12.0):
 
 KERNEL_OF = {"ublr_sketch_tagged_pair": "k_sketch_tagged{v} (Kronecker-restructured tagged sketch, TMEM tag groups)",
              "ublr_sketch_tagged": "k_sketch_tagged{v} (Kronecker-restructured tagged sketch, TMEM tag groups)",
+             "ublr_sketch_tagged_two": "k_sketch_tagged3 (both sides of a non-symmetric A in one launch, TMEM tag groups)",
              "ublr_apply": "k_apply3 (operator apply, warp-specialised: A generated by producer warps, DMMA consumers)",
              "ublr_gemm_batched": "k_gemm2 (batched DMMA GEMM)",
              "ublr_coupling": "k_coupling3 (C_ij = U_i^T A_ij V_j, warp-specialised)",

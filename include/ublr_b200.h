@@ -122,6 +122,12 @@ int ublr_rng_normals(const ublr_rng_stream_t* streams_dev, const int64_t* counts
 int ublr_sketch_tagged(const ublr_op_t* op, const int32_t* off, int b, const double* T, int ell,
                        const double* X, int64_t ld_x, int gc, double* Y, int64_t ld_y, int row_begin,
                        int row_end, void* stream);
+/* Both sides of a NON-symmetric tagged sketch in one launch: Y = A Omega
+ * (op, test blocks G) and Z = A^T Psi (op_adj = the adjoint descriptor, H),
+ * the same tagging matrix T. Replaces two ublr_sketch_tagged calls. */
+int ublr_sketch_tagged_two(const ublr_op_t* op, const ublr_op_t* op_adj, const int32_t* off, int b, const double* T,
+                           int ell, const double* G, const double* H, int64_t ld_x, int gc, double* Y, double* Z,
+                           int64_t ld_y, int row_begin, int row_end, void* stream);
 /* Symmetric operator: [Y | Z] = A [Omega | Psi] in one pass over A. */
 int ublr_sketch_tagged_pair(const ublr_op_t* op, const int32_t* off, int b, const double* T, int ell,
                             const double* G, const double* H, int64_t ld_x, int gc,

@@ -50,6 +50,8 @@ SIGNATURES = {
     "ublr_rng_normals": (INT, [P, P, INT, P, P, I64, P]),
     "ublr_sketch_tagged": (INT, [C.POINTER(OpDesc), P, INT, P, INT, P, I64, INT, P, I64, INT, INT, P]),
     "ublr_sketch_tagged_pair": (INT, [C.POINTER(OpDesc), P, INT, P, INT, P, P, I64, INT, P, P, I64, INT, INT, P]),
+    "ublr_sketch_tagged_two": (INT, [C.POINTER(OpDesc), C.POINTER(OpDesc), P, INT, P, INT, P, P, I64, INT, P, P, I64,
+                                     INT, INT, P]),
     "ublr_apply": (INT, [C.POINTER(OpDesc), P, I64, INT, P, I64, P]),
     "ublr_block_qr": (INT, [P, I64, INT, P, INT, INT, P, P, INT, INT, P, I64, P, INT]),
     "ublr_block_qr_pair": (INT, [P, P, I64, P, INT, INT, P, INT, INT, P, P, I64, P, INT]),
@@ -112,7 +114,7 @@ def check(rc: int, what: str = ""):
 
 
 # kernels each C-ABI entry point launches (for bench.py's `gpu_launches`)
-LAUNCHES = {"ublr_rng_normals": 8, "ublr_sketch_tagged": 1, "ublr_sketch_tagged_pair": 1, "ublr_apply": 1,
+LAUNCHES = {"ublr_rng_normals": 8, "ublr_sketch_tagged": 1, "ublr_sketch_tagged_pair": 1, "ublr_sketch_tagged_two": 1, "ublr_apply": 1,
             "ublr_block_qr": 1, "ublr_block_qr_pair": 1, "ublr_coupling": 1, "ublr_nearfield_colour": 2,
             "ublr_coupling_nearfield": 1,
             "ublr_blr_apply": 3, "ublr_gemm_batched": 1, "ublr_potrf_diag": 1, "ublr_lu_sign_diag": 1,
@@ -173,6 +175,10 @@ def _work_of(name, args):
         if name == "ublr_apply":
             n = args[0].n
             return 2.0 * n * n * int(args[3])
+        if name == "ublr_sketch_tagged_two":
+            n, b, ell, gc = args[0].n, int(args[3]), int(args[5]), int(args[9])
+            r0, r1 = int(args[13]), int(args[14])
+            return 2 * (2.0 * (r1 - r0) * n * gc + 2.0 * (r1 - r0) * b * gc * ell)
         if name in ("ublr_sketch_tagged", "ublr_sketch_tagged_pair"):
             pair = name.endswith("pair")
             n, b, ell = args[0].n, int(args[2]), int(args[4])

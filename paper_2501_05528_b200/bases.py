@@ -200,11 +200,10 @@ def tagged_sketch(op, dt, T_dev, T_entries, G, H, gc, out=None, ell=None):
             _lib.call("ublr_sketch_tagged_pair", inner.device_op(dt.perm), _lib.ptr(dt.off), dt.b,
                       _lib.ptr(T_dev), ell, _lib.ptr(G), _lib.ptr(H), gc, gc, _lib.ptr(Y), _lib.ptr(Z), s, 0, dt.n,
                       stream)
-        else:
-            _lib.call("ublr_sketch_tagged", inner.device_op(dt.perm), _lib.ptr(dt.off), dt.b, _lib.ptr(T_dev),
-                      ell, _lib.ptr(G), gc, gc, _lib.ptr(Y), s, 0, dt.n, stream)
-            _lib.call("ublr_sketch_tagged", inner.device_op(dt.perm, adjoint=True), _lib.ptr(dt.off), dt.b,
-                      _lib.ptr(T_dev), ell, _lib.ptr(H), gc, gc, _lib.ptr(Z), s, 0, dt.n, stream)
+        else:   # both sides in one launch (A, A^T descriptors)
+            _lib.call("ublr_sketch_tagged_two", inner.device_op(dt.perm), inner.device_op(dt.perm, adjoint=True),
+                      _lib.ptr(dt.off), dt.b, _lib.ptr(T_dev), ell, _lib.ptr(G), _lib.ptr(H), gc, gc, _lib.ptr(Y),
+                      _lib.ptr(Z), s, 0, dt.n, stream)
         return Y, Z
     # black-box host operator: explicit test matrices through its apply
     om = assemble_tagged(dt, T_entries, G, gc)

@@ -543,12 +543,21 @@ __global__ void __launch_bounds__(TS_THREADS) k_sketch_tagged(ublr_op_t op, cons
 // (row tile, column tile) — once per row tile when 2gc <= BN — and every
 // test-block panel is reused by BM rows.
 template <int KIND, int L, class Cfg>
-__global__ void __launch_bounds__(Cfg::NT, 1) k_sketch_tagged3(ublr_op_t op, const int32_t* __restrict__ off, int b,
+__global__ void __launch_bounds__(Cfg::NT, 1) k_sketch_tagged3(ublr_op_t op_a, const int32_t* __restrict__ off, int b,
                                                                const double* __restrict__ T, int ell,
                                                                const double* __restrict__ G,
                                                                const double* __restrict__ H, int64_t ldx, int gc,
                                                                double* __restrict__ Y, double* __restrict__ Z,
-                                                               int64_t ldy, int row_begin, int row_end, int vec2) {
+                                                               int64_t ldy, int row_begin, int row_end, int vec2,
+                                                               ublr_op_t op_b, const double* __restrict__ G_b,
+                                                               double* __restrict__ Y_b) {
+  // gridDim.z == 2: blockIdx.z = 1 sketches a second operator (the adjoint of a
+  // non-symmetric A) against its own test blocks in the same launch
+  const ublr_op_t op = blockIdx.z ? op_b : op_a;
+  if (blockIdx.z) {
+    G = G_b;
+    Y = Y_b;
+  }
   constexpr int BK = Cfg::BK, STAGES = Cfg::STAGES;
   constexpr int WD = Cfg::MI * Cfg::NJ * 2;            // W doubles per thread
   constexpr int NWARP = Cfg::NT / 32;
@@ -582,11 +591,29 @@ __global__ void __launch_bounds__(Cfg::NT, 1) k_sketch_tagged3(ublr_op_t op, con
     int q0n, qendn;   // columns of the stage being produced
     int sidx;         // its stage index (ring slot)
     ColRing<BK> ring;
+    // dense, not transposed: thread = (column kk, rows dr[e]) so a warp reads
+    // consecutive columns of one row of A (coalesced); dorig[e] = perm[row] or -1
+    int dorig[(BK * Cfg::BM + Cfg::NT - 1) / Cfg::NT];
     __device__ __forceinline__ void stage_part(double* As, int, int part, int nparts) {
       constexpr int KL = Cfg::NT / Cfg::BM;
       constexpr int E = BK / KL;
       int e0, e1;
       chunk_range<E, 2>(part, nparts, e0, e1);
+      if (KIND == UBLR_OP_DENSE && !op.transpose) {
+        static_assert(BK * Cfg::BM % Cfg::NT == 0 && Cfg::NT % BK == 0, "dense tile mapping");
+        const int kk = threadIdx.x % BK;
+        const int q = q0n + kk;
+        const bool qok = q < qendn;
+        const int oq = qok ? (op.perm ? op.perm[q] : q) : 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          if (e < e0 || e >= e1) continue;
+          const int rr = threadIdx.x / BK + e * (Cfg::NT / BK);
+          const double v = (qok && dorig[e] >= 0) ? op.A[(int64_t)dorig[e] * op.lda + oq] : 0.0;
+          As[Cfg::ai(rr, kk)] = v;
+        }
+        return;
+      }
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         if (e < e0 || e >= e1) continue;
@@ -601,7 +628,14 @@ __global__ void __launch_bounds__(Cfg::NT, 1) k_sketch_tagged3(ublr_op_t op, con
       }
     }
   } ap{op, &lt, load_row_point(op, row0 + (int)(threadIdx.x % Cfg::BM), row0 + (int)(threadIdx.x % Cfg::BM) < row_end),
-       (int)(threadIdx.x % Cfg::BM), (int)(threadIdx.x / Cfg::BM), 0, 0, 0, ColRing<BK>{ringbuf}};
+       (int)(threadIdx.x % Cfg::BM), (int)(threadIdx.x / Cfg::BM), 0, 0, 0, ColRing<BK>{ringbuf}, {}};
+  if (KIND == UBLR_OP_DENSE) {
+#pragma unroll
+    for (int e = 0; e < (int)(sizeof(ap.dorig) / sizeof(int)); ++e) {
+      const int row = row0 + (int)(threadIdx.x / BK) + e * (Cfg::NT / BK);
+      ap.dorig[e] = row < row_end ? (op.perm ? op.perm[row] : row) : -1;
+    }
+  }
   // test-block panel stage: BK rows x BN columns of [G | H]. Each thread's
   // 16-byte pair slots are fixed for the whole kernel, so their source
   // pointers (minus the k-step row offset) are computed once here.
@@ -1172,10 +1206,14 @@ int sketch_common_v1(const ublr_op_t* op, const int32_t* off, int b, const doubl
 
 int sketch_common_v3(const ublr_op_t* op, const int32_t* off, int b, const double* T, int ell, const double* G,
                      const double* H, int64_t ld_x, int gc, double* Y, double* Z, int64_t ld_y, int row_begin,
-                     int row_end, cudaStream_t st) {
+                     int row_end, cudaStream_t st, const ublr_op_t* op2 = nullptr, const double* G2 = nullptr,
+                     double* Y2 = nullptr) {
   const int ncols = (H ? 2 : 1) * gc;
-  int vec2 = ((ld_x % 2) == 0 && ((uintptr_t)G) % 16 == 0 && (!H || ((uintptr_t)H) % 16 == 0)) ? 1 : 0;
+  int vec2 = ((ld_x % 2) == 0 && ((uintptr_t)G) % 16 == 0 && (!H || ((uintptr_t)H) % 16 == 0) &&
+              (!G2 || ((uintptr_t)G2) % 16 == 0)) ? 1 : 0;
   dim3 grid;
+  grid.z = op2 ? 2 : 1;
+  const ublr_op_t opb = op2 ? *op2 : *op;
   static const int ts_cfg = [] {
     const char* e = getenv("UBLR_SKETCH_CFG");
     return e ? atoi(e) : 0;
@@ -1200,7 +1238,7 @@ int sketch_common_v3(const ublr_op_t* op, const int32_t* off, int b, const doubl
       UBLR_CUDA(cudaFuncSetAttribute(k_sketch_tagged3<KIND, L, Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                      (int)sm));                                                                \
       k_sketch_tagged3<KIND, L, Cfg><<<grid, Cfg::NT, sm, st>>>(*op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y,   \
-                                                                row_begin, row_end, vec2);                     \
+                                                                row_begin, row_end, vec2, opb, G2, Y2);        \
     })                                                                                                          \
   }
   if (ncols <= 64) {
@@ -1280,6 +1318,28 @@ extern "C" int ublr_sketch_tagged(const ublr_op_t* op, const int32_t* off, int b
                UBLR_ERR_VALUE, "ublr_sketch_tagged: bad arguments");
   return sketch_common(op, off, b, T, ell, X, nullptr, ld_x, gc, Y, nullptr, ld_y, row_begin, row_end,
                        (cudaStream_t)stream);
+}
+
+extern "C" int ublr_sketch_tagged_two(const ublr_op_t* op, const ublr_op_t* op_adj, const int32_t* off, int b,
+                                      const double* T, int ell, const double* G, const double* H, int64_t ld_x, int gc,
+                                      double* Y, double* Z, int64_t ld_y, int row_begin, int row_end, void* stream) {
+  int rc = check_op(op);
+  if (rc) return rc;
+  rc = check_op(op_adj);
+  if (rc) return rc;
+  UBLR_REQUIRE(b > 0 && off && T && G && H && Y && Z && gc > 0 && ell > 0 && ld_x >= gc &&
+                   ld_y >= (int64_t)ell * gc && op->kind == op_adj->kind && op->n == op_adj->n,
+               UBLR_ERR_VALUE, "ublr_sketch_tagged_two: bad arguments");
+  UBLR_REQUIRE(row_begin >= 0 && row_begin < row_end && row_end <= op->n, UBLR_ERR_VALUE, "sketch: bad row range");
+  cudaStream_t st = (cudaStream_t)stream;
+  static const char* ver = getenv("UBLR_SKETCH_VERSION");
+  const int v = ver ? atoi(ver) : 4;
+  if (v >= 3 && ell <= 10)
+    return sketch_common_v3(op, off, b, T, ell, G, nullptr, ld_x, gc, Y, nullptr, ld_y, row_begin, row_end, st,
+                            op_adj, H, Z);
+  rc = sketch_common(op, off, b, T, ell, G, nullptr, ld_x, gc, Y, nullptr, ld_y, row_begin, row_end, st);
+  if (rc) return rc;
+  return sketch_common(op_adj, off, b, T, ell, H, nullptr, ld_x, gc, Z, nullptr, ld_y, row_begin, row_end, st);
 }
 
 extern "C" int ublr_sketch_tagged_pair(const ublr_op_t* op, const int32_t* off, int b, const double* T, int ell,
