@@ -93,6 +93,11 @@ int ublr_seedseq_keys(const uint32_t* run, int nrun, const uint32_t* prefix, int
  * Householder Q of T[rows]^T and res[s] = ||T[rows] Z[s]||. Host function. */
 int ublr_null_vectors(const double* T, int ell, const int32_t* ptr, const int32_t* idx, int nsets, double* Z,
                       double* res);
+/* Device twin of ublr_null_vectors (device pointers; every set must have
+ * fewer than ell rows, ell <= 32): bitwise the same Z and residuals as the
+ * host function (shared explicitly-rounded arithmetic). */
+int ublr_null_vectors_device(const double* T, int ell, const int32_t* ptr, const int32_t* idx, int nsets, double* Z,
+                             double* res, void* stream);
 /* Tagging-plan aspect ratios (ref/tagging.py:110-123): rho[i] = max/min over
  * the far field j of |T[j] . Z[i]| (T, Z: b x ell row-major device arrays;
  * neighbour CSR nptr/nidx), 1 if the max is 0, inf if the min is 0, NaN if

@@ -46,6 +46,7 @@ SIGNATURES = {
     "ublr_null_vectors": (INT, [P, INT, P, P, INT, P, P]),
     "ublr_tag_plan_host": (INT, [P, INT, P, P, INT, P, P, P, P]),
     "ublr_tag_aspect": (INT, [P, P, INT, P, P, INT, P, P]),
+    "ublr_null_vectors_device": (INT, [P, INT, P, P, INT, P, P, P]),
     "ublr_rng_workspace_bytes": (I64, [P, INT]),
     "ublr_rng_normals": (INT, [P, P, INT, P, P, I64, P]),
     "ublr_sketch_tagged": (INT, [C.POINTER(OpDesc), P, INT, P, INT, P, I64, INT, P, I64, INT, INT, P]),
@@ -119,7 +120,7 @@ LAUNCHES = {"ublr_rng_normals": 8, "ublr_sketch_tagged": 1, "ublr_sketch_tagged_
             "ublr_coupling_nearfield": 1,
             "ublr_blr_apply": 3, "ublr_gemm_batched": 1, "ublr_potrf_diag": 1, "ublr_lu_sign_diag": 1,
             "ublr_lu_sign_diag_r": 1, "ublr_syrk_upper_batched": 1, "ublr_add_scaled_rows": 1,
-            "ublr_gather": 1, "ublr_scale_rows": 1, "ublr_tag_combine_pairs": 1, "ublr_assemble_tagged": 1, "ublr_tag_aspect": 1}
+            "ublr_gather": 1, "ublr_scale_rows": 1, "ublr_tag_combine_pairs": 1, "ublr_assemble_tagged": 1, "ublr_tag_aspect": 1, "ublr_null_vectors_device": 1}
 launch_count = 0
 
 

@@ -228,6 +228,9 @@ def block_bases_from_tagged(dt, Y, Z, Z_dev, ell, gc, k):
     return U, V
 
 
+NULLVEC_DEVICE_MAX_ELL = 32   # ublr_null_vectors_device
+
+
 def tagging_bases(op, tess: Tessellation, k: int, p: int, plan, stream: RandomStream,
                   group_cols: int | None = None, extra_samples: bool = False, first=None, test_pair=None):
     """ref/bases.py:140-204 on the GPU. Returns (BlockBases, SketchBundle).
@@ -271,6 +274,17 @@ def tagging_bases(op, tess: Tessellation, k: int, p: int, plan, stream: RandomSt
     _bill(op, s, s)
     G, H = draw_test_pair(dt, stream, gc) if test_pair is None else test_pair[:2]
     Y, Z = tagged_sketch(op, dt, T_dev, None if matrix is None else matrix.entries, G, H, gc, out=(Y, Z), ell=ell)
+    UV = None
+    if matrix is None and ell <= NULLVEC_DEVICE_MAX_ELL:
+        # speculative bases: the first draw's null vectors on the device (the
+        # same bits as the host planner's, csrc/nullvec.cuh) and the block QR,
+        # queued behind the sketch; the host evaluates the plan meanwhile and
+        # they are recomputed only if the redraw policy rejects the draw
+        Z_spec = torch.empty((dt.b, ell), dtype=torch.float64, device=dt.device)
+        res_spec = torch.empty(dt.b, dtype=torch.float64, device=dt.device)
+        _lib.call("ublr_null_vectors_device", _lib.ptr(T_dev), ell, _lib.ptr(dt.nptr), _lib.ptr(dt.nidx), dt.b,
+                  _lib.ptr(Z_spec), _lib.ptr(res_spec), _lib.stream_handle())
+        UV = block_bases_from_tagged(dt, Y, Z, Z_spec, ell, gc, k)
     if matrix is None:
         matrix = first_fn()                  # host draw of the same bits, while the sketch runs
         if matrix.entries.shape != tuple(T_dev.shape):
@@ -278,11 +292,14 @@ def tagging_bases(op, tess: Tessellation, k: int, p: int, plan, stream: RandomSt
     if planner is not None:
         plan = planner()                     # host work, overlapping the sketch
         if plan.matrix is not matrix:        # redrawn: sketch the accepted matrix
+            UV = None
             T_entries = plan.matrix.entries
             T_dev = _lib.h2d(T_entries, dt.device)
             Y, Z = tagged_sketch(op, dt, T_dev, T_entries, G, H, gc)
-    Z_dev = _lib.h2d(plan.Z, dt.device)
-    U, V = block_bases_from_tagged(dt, Y, Z, Z_dev, ell, gc, k)
+    if UV is None:
+        Z_dev = _lib.h2d(plan.Z, dt.device)
+        UV = block_bases_from_tagged(dt, Y, Z, Z_dev, ell, gc, k)
+    U, V = UV
     bases = BlockBases(dt, U, V, k, "tag", (s, s))
     bundle = SketchBundle("tag", dt, s, Y, Z, G=G, H=H, tagging=plan.matrix, group_cols=gc)
     bundle.plan = plan

@@ -1,5 +1,6 @@
 // C-ABI plumbing: error text, version, device check.
 #include "common.cuh"
+#include "nullvec.cuh"
 #include <cmath>
 #include <vector>
 
@@ -88,73 +89,18 @@ extern "C" int ublr_null_vectors(const double* T, int ell, const int32_t* ptr, c
                                  double* Z, double* res) {
   UBLR_REQUIRE(T && ell >= 1 && ptr && idx && nsets >= 0 && Z && res, UBLR_ERR_VALUE,
                "ublr_null_vectors: bad arguments");
-  // column-major ell x sz work matrix A[i + j*ell] = T[idx[r0+j], i]; fixed
-  // storage for the usual ell <= 32 (no per-set allocation)
-  std::vector<double> Aheap, tauheap;
-  double Afix[32 * 32], taufix[32];
-  const bool small = ell <= 32;
-  if (!small) {
+  double Afix[ublr::nullvec::MAX_ELL * ublr::nullvec::MAX_ELL], taufix[ublr::nullvec::MAX_ELL];
+  std::vector<double> Aheap, tauheap;   // ell > 32 (extra tagging columns in 3-D)
+  if (ell > ublr::nullvec::MAX_ELL) {
     Aheap.resize((size_t)ell * ell);
     tauheap.resize(ell);
   }
-  double* A = small ? Afix : Aheap.data();
-  double* tau = small ? taufix : tauheap.data();
+  double* A = ell > ublr::nullvec::MAX_ELL ? Aheap.data() : Afix;
+  double* tau = ell > ublr::nullvec::MAX_ELL ? tauheap.data() : taufix;
   for (int s = 0; s < nsets; ++s) {
     const int r0 = ptr[s], sz = ptr[s + 1] - ptr[s];
     UBLR_REQUIRE(sz >= 0 && sz < ell, UBLR_ERR_VALUE, "ublr_null_vectors: a set has >= ell rows (no null vector)");
-    for (int j = 0; j < sz; ++j)
-      for (int i = 0; i < ell; ++i) A[i + (size_t)j * ell] = T[(size_t)idx[r0 + j] * ell + i];
-    for (int j = 0; j < sz; ++j) tau[j] = 0.0;
-    for (int j = 0; j < sz; ++j) {
-      double* col = &A[(size_t)j * ell];
-      const double alpha = col[j];
-      double ss = 0.0, scale = 0.0;
-      for (int i = j + 1; i < ell; ++i) scale = fmax(scale, fabs(col[i]));
-      if (scale > 0.0) {
-        const double inv_scale = 1.0 / scale;   // one division per column (dnrm2-style scaling)
-        for (int i = j + 1; i < ell; ++i) ss += (col[i] * inv_scale) * (col[i] * inv_scale);
-      }
-      const double xnorm = scale * sqrt(ss);
-      if (xnorm == 0.0) {
-        tau[j] = 0.0;
-        continue;
-      }
-      // dlapy2: w sqrt(1 + (z / w)^2) with w = max(|alpha|, xnorm) (no libm hypot call)
-      const double aa = fabs(alpha), wmax = fmax(aa, xnorm), zmin = fmin(aa, xnorm);
-      const double ratio = zmin / wmax;
-      const double beta = -copysign(wmax * sqrt(1.0 + ratio * ratio), alpha);
-      tau[j] = (beta - alpha) / beta;
-      const double inv = 1.0 / (alpha - beta);
-      for (int i = j + 1; i < ell; ++i) col[i] *= inv;
-      col[j] = beta;
-      // apply H_j = I - tau v v^T (v = [1, col[j+1:]]) to the remaining columns
-      for (int c = j + 1; c < sz; ++c) {
-        double* a = &A[(size_t)c * ell];
-        double w = a[j];
-        for (int i = j + 1; i < ell; ++i) w += col[i] * a[i];
-        w *= tau[j];
-        a[j] -= w;
-        for (int i = j + 1; i < ell; ++i) a[i] -= w * col[i];
-      }
-    }
-    double* z = Z + (size_t)s * ell;
-    for (int i = 0; i < ell; ++i) z[i] = (i == ell - 1) ? 1.0 : 0.0;
-    for (int j = sz - 1; j >= 0; --j) {
-      const double* v = &A[(size_t)j * ell];
-      double w = z[j];
-      for (int i = j + 1; i < ell; ++i) w += v[i] * z[i];
-      w *= tau[j];
-      z[j] -= w;
-      for (int i = j + 1; i < ell; ++i) z[i] -= w * v[i];
-    }
-    double r2 = 0.0;
-    for (int j = 0; j < sz; ++j) {
-      const double* t = T + (size_t)idx[r0 + j] * ell;
-      double d = 0.0;
-      for (int i = 0; i < ell; ++i) d += t[i] * z[i];
-      r2 += d * d;
-    }
-    res[s] = sqrt(r2);
+    res[s] = ublr::nullvec::null_vector(T, ell, idx + r0, sz, A, tau, Z + (size_t)s * ell);
   }
   return UBLR_OK;
 }

@@ -9,6 +9,7 @@
 #include <cmath>
 
 #include "common.cuh"
+#include "nullvec.cuh"
 
 namespace ublr {
 namespace {
@@ -77,6 +78,38 @@ extern "C" int ublr_tag_aspect(const double* T, const double* Z, int ell, const 
   size_t sm = (size_t)((b + 31) / 32) * sizeof(uint32_t);
   UBLR_REQUIRE(sm <= 48 * 1024, UBLR_ERR_VALUE, "ublr_tag_aspect: b too large for the near-set bitmask");
   k_tag_aspect<<<b, TA_THREADS, sm, (cudaStream_t)stream>>>(T, Z, ell, nptr, nidx, b, rho);
+  UBLR_LAUNCH_CHECK();
+  return UBLR_OK;
+}
+
+// Device twin of ublr_null_vectors (same arithmetic, same bits: nullvec.cuh),
+// one thread per row set. Lets the pipeline launch the block QR right after
+// the sketch while the host evaluates the same plan for its redraw decision.
+namespace ublr {
+namespace {
+__global__ void k_null_vectors(const double* __restrict__ T, int ell, const int32_t* __restrict__ ptr,
+                               const int32_t* __restrict__ idx, int nsets, double* __restrict__ Z,
+                               double* __restrict__ res) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nsets) return;
+  double A[ublr::nullvec::MAX_ELL * ublr::nullvec::MAX_ELL], tau[ublr::nullvec::MAX_ELL];
+  const int r0 = ptr[s], sz = ptr[s + 1] - r0;
+  if (sz >= ell) {   // no null vector (the host planner raises DegenerateTagsError)
+    for (int i = 0; i < ell; ++i) Z[(int64_t)s * ell + i] = 0.0;
+    res[s] = INFINITY;
+    return;
+  }
+  res[s] = ublr::nullvec::null_vector(T, ell, idx + r0, sz, A, tau, Z + (int64_t)s * ell);
+}
+}  // namespace
+}  // namespace ublr
+
+extern "C" int ublr_null_vectors_device(const double* T, int ell, const int32_t* ptr, const int32_t* idx, int nsets,
+                                        double* Z, double* res, void* stream) {
+  UBLR_REQUIRE(T && ell >= 1 && ell <= ublr::nullvec::MAX_ELL && ptr && idx && nsets >= 0 && Z && res,
+               UBLR_ERR_VALUE, "ublr_null_vectors_device: bad arguments (ell <= 32)");
+  if (nsets == 0) return UBLR_OK;
+  ublr::k_null_vectors<<<(nsets + 63) / 64, 64, 0, (cudaStream_t)stream>>>(T, ell, ptr, idx, nsets, Z, res);
   UBLR_LAUNCH_CHECK();
   return UBLR_OK;
 }

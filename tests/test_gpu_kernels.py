@@ -376,3 +376,27 @@ def test_coupling_nearfield_fused_matches_separate(name, k):
     core2 = direct_core(op, tess, bs)
     core2.mul_(2.0)
     assert structured_identity_discrepancy(op, tess, bs, core2, color_boxes(tess)) is not bs.fused_near[3]
+
+
+@pytest.mark.parametrize("per,nb,d,extra", [(64, 64, 2, 0), (32, 16, 2, 0), (12, 64, 3, 0), (64, 64, 2, 3),
+                                           (64, 256, 2, 0)])
+def test_null_vectors_device_bitwise_equal_host(per, nb, d, extra):
+    """ublr_null_vectors_device gives the host planner's null vectors and
+    residuals bit for bit (the pipeline's speculative block QR relies on it)."""
+    from paper_2501_05528_b200.tagging import _neighbour_csr, make_tagging_matrix
+    tess = P.build_tessellation(P.grid_points(per, d), nb)
+    T = make_tagging_matrix(tess.b, d, extra, "gaussian", P.RandomStream(3).child(1).child(0))
+    E = np.ascontiguousarray(T.entries)
+    b, ell = E.shape
+    ptr, idx = _neighbour_csr(tess)
+    Zh, rh = np.zeros((b, ell)), np.zeros(b)
+    _lib.check(_lib.load().ublr_null_vectors(E.ctypes.data, ell, ptr.ctypes.data, idx.ctypes.data, b,
+                                             Zh.ctypes.data, rh.ctypes.data))
+    dt = device_tess(tess, torch.device(DEV))
+    Ed = torch.from_numpy(E).to(DEV)
+    Zd = torch.empty((b, ell), dtype=torch.float64, device=DEV)
+    rd = torch.empty(b, dtype=torch.float64, device=DEV)
+    _lib.call("ublr_null_vectors_device", _lib.ptr(Ed), ell, _lib.ptr(dt.nptr), _lib.ptr(dt.nidx), b, _lib.ptr(Zd),
+              _lib.ptr(rd), _lib.stream_handle())
+    assert np.array_equal(Zd.cpu().numpy(), Zh)
+    assert np.array_equal(rd.cpu().numpy(), rh)

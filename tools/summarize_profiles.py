@@ -21,7 +21,7 @@ def run(args):
     return subprocess.run(args, capture_output=True, text=True).stdout
 
 
-for cfg in ("c2_bench", "c2", "c3", "c5"):
+for cfg in ("c2_bench", "c2", "c3", "c4", "c5"):
     f = os.path.join(SRC, f"launches_{cfg}.csv")
     if os.path.exists(f):
         shutil.copy(f, os.path.join(DST, f"launches_{cfg}.csv"))
@@ -32,7 +32,7 @@ for cfg in ("c2_bench", "c2", "c3", "c5"):
 # capture -> (bench config, C-ABI entry the bench attributes it to)
 CAPS = {"c2_sketch4": ("c2", "ublr_sketch_tagged_pair"), "c2_cnf": (None, "ublr_coupling_nearfield"),
         "c3_apply3": ("c3", "ublr_apply"),
-        "c5_sketch3": ("c5", "ublr_sketch_tagged_pair"), "c5_coupling3": (None, "ublr_coupling")}
+        "c4_apply3": ("c4", "ublr_apply"), "c5_sketch4": ("c5", "ublr_sketch_tagged_pair"), "c5_coupling3": (None, "ublr_coupling")}
 for cap, (cfg, entry) in CAPS.items():
     rep = os.path.join(SRC, f"{cap}.ncu-rep")
     if not os.path.exists(rep):
