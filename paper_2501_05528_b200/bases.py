@@ -229,10 +229,22 @@ def block_bases_from_tagged(dt, Y, Z, Z_dev, ell, gc, k):
 
 
 NULLVEC_DEVICE_MAX_ELL = 32   # ublr_null_vectors_device
+_PLAN_WORKER = None
+
+
+def _plan_worker():
+    """One persistent worker thread for the host tagging plan (tagging_bases
+    with defer_plan)."""
+    global _PLAN_WORKER
+    if _PLAN_WORKER is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _PLAN_WORKER = ThreadPoolExecutor(max_workers=1, thread_name_prefix="ublr-plan")
+    return _PLAN_WORKER
 
 
 def tagging_bases(op, tess: Tessellation, k: int, p: int, plan, stream: RandomStream,
-                  group_cols: int | None = None, extra_samples: bool = False, first=None, test_pair=None):
+                  group_cols: int | None = None, extra_samples: bool = False, first=None, test_pair=None,
+                  defer_plan: bool = False):
     """ref/bases.py:140-204 on the GPU. Returns (BlockBases, SketchBundle).
 
     `plan` is a TaggingPlan, or a zero-argument callable producing one (the
@@ -242,7 +254,12 @@ def tagging_bases(op, tess: Tessellation, k: int, p: int, plan, stream: RandomSt
     before the host evaluates the plan and runs on the GPU meanwhile; if the
     policy redraws, the sketch is recomputed for the accepted matrix.
     `test_pair` = (G, H) already drawn by draw_test_pair(dt, stream, gc)
-    (compress_type_a launches it before the host draws the tagging matrix)."""
+    (compress_type_a launches it before the host draws the tagging matrix).
+    `defer_plan`: when the bases were built speculatively from the device draw,
+    return with bundle.plan = None and leave the host plan evaluation to
+    bundle.resolve_plan() (the caller queues more GPU work first); it returns
+    (plan, None) if the first draw was accepted, else (plan, ((U, V), Y, Z))
+    recomputed for the accepted matrix."""
     torch = _torch()
     if extra_samples:
         raise NotImplementedError("extra_samples (ref/bases.py:177-182) is not on the B200 hot path (SURVEY F12)")
@@ -285,20 +302,53 @@ def tagging_bases(op, tess: Tessellation, k: int, p: int, plan, stream: RandomSt
         _lib.call("ublr_null_vectors_device", _lib.ptr(T_dev), ell, _lib.ptr(dt.nptr), _lib.ptr(dt.nidx), dt.b,
                   _lib.ptr(Z_spec), _lib.ptr(res_spec), _lib.stream_handle())
         UV = block_bases_from_tagged(dt, Y, Z, Z_spec, ell, gc, k)
-    if matrix is None:
-        matrix = first_fn()                  # host draw of the same bits, while the sketch runs
-        if matrix.entries.shape != tuple(T_dev.shape):
-            raise RuntimeError("device and host tagging draws disagree in shape")
-    if planner is not None:
-        plan = planner()                     # host work, overlapping the sketch
-        if plan.matrix is not matrix:        # redrawn: sketch the accepted matrix
-            UV = None
-            T_entries = plan.matrix.entries
-            T_dev = _lib.h2d(T_entries, dt.device)
-            Y, Z = tagged_sketch(op, dt, T_dev, T_entries, G, H, gc)
-    if UV is None:
-        Z_dev = _lib.h2d(plan.Z, dt.device)
-        UV = block_bases_from_tagged(dt, Y, Z, Z_dev, ell, gc, k)
+    def evaluate(speculative_matrix):
+        """Host draw + redraw policy; (plan, Y, Z, UV) for the accepted matrix."""
+        nonlocal Y, Z
+        m0 = speculative_matrix
+        if m0 is None:
+            m0 = first_fn()                  # host draw of the same bits, while the GPU works
+            if m0.entries.shape != tuple(T_dev.shape):
+                raise RuntimeError("device and host tagging draws disagree in shape")
+        pl, uv = plan, UV
+        if planner is not None:
+            pl = planner()                   # host work, overlapping the sketch
+            if pl.matrix is not m0:          # redrawn: sketch the accepted matrix
+                uv = None
+                T_entries = pl.matrix.entries
+                Y, Z = tagged_sketch(op, dt, _lib.h2d(T_entries, dt.device), T_entries, G, H, gc)
+        if uv is None:
+            uv = block_bases_from_tagged(dt, Y, Z, _lib.h2d(pl.Z, dt.device), ell, gc, k)
+        return pl, uv
+
+    if defer_plan and UV is not None and planner is not None:
+        bases = BlockBases(dt, UV[0], UV[1], k, "tag", (s, s))
+        bundle = SketchBundle("tag", dt, s, Y, Z, G=G, H=H, tagging=None, group_cols=gc)
+        bundle.plan = None
+        def host_plan():                     # worker thread: host numpy + C only, no CUDA calls
+            m0 = first_fn()
+            if m0.entries.shape != tuple(T_dev.shape):
+                raise RuntimeError("device and host tagging draws disagree in shape")
+            return m0, planner()
+
+        # the host draw and the redraw policy (its C evaluation releases the
+        # GIL) run on a worker thread while this thread queues phases II-III
+        fut = _plan_worker().submit(host_plan)
+
+        def resolve_plan():
+            # (no reference to bundle / bases here: a cycle through this
+            # closure would keep the compression's device buffers alive until
+            # the cyclic collector runs)
+            m0, pl = fut.result()
+            if pl.matrix is m0:
+                return pl, None
+            T_entries = pl.matrix.entries   # redrawn: sketch and bases of the accepted matrix
+            Y2, Z2 = tagged_sketch(op, dt, _lib.h2d(T_entries, dt.device), T_entries, G, H, gc)
+            uv = block_bases_from_tagged(dt, Y2, Z2, _lib.h2d(pl.Z, dt.device), ell, gc, k)
+            return pl, (uv, Y2, Z2)
+        bundle.resolve_plan = resolve_plan
+        return bases, bundle
+    plan, UV = evaluate(matrix)
     U, V = UV
     bases = BlockBases(dt, U, V, k, "tag", (s, s))
     bundle = SketchBundle("tag", dt, s, Y, Z, G=G, H=H, tagging=plan.matrix, group_cols=gc)

@@ -87,19 +87,112 @@ extern "C" int ublr_tag_aspect(const double* T, const double* Z, int ell, const 
 // the sketch while the host evaluates the same plan for its redraw decision.
 namespace ublr {
 namespace {
-__global__ void k_null_vectors(const double* __restrict__ T, int ell, const int32_t* __restrict__ ptr,
-                               const int32_t* __restrict__ idx, int nsets, double* __restrict__ Z,
-                               double* __restrict__ res) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+// One warp per row set, the set's ell x sz matrix in shared memory. Every
+// sum keeps the host routine's sequential order (nullvec::null_vector):
+// lanes only split loops whose iterations are independent (elementwise
+// scaling, the trailing columns, the entries of z), so the bits agree.
+constexpr int NV_WARPS = 4;
+__global__ void __launch_bounds__(NV_WARPS * 32) k_null_vectors(const double* __restrict__ T, int ell,
+                                                                const int32_t* __restrict__ ptr,
+                                                                const int32_t* __restrict__ idx, int nsets,
+                                                                double* __restrict__ Z, double* __restrict__ res) {
+  using namespace nullvec;
+  constexpr int ME = MAX_ELL;
+  __shared__ double Ash[NV_WARPS][ME * ME];
+  __shared__ double zsh[NV_WARPS][ME], tsh[NV_WARPS][ME], wsh[NV_WARPS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = blockIdx.x * NV_WARPS + warp;
   if (s >= nsets) return;
-  double A[ublr::nullvec::MAX_ELL * ublr::nullvec::MAX_ELL], tau[ublr::nullvec::MAX_ELL];
+  double* A = Ash[warp];
+  double* z = zsh[warp];
+  double* tau = tsh[warp];
   const int r0 = ptr[s], sz = ptr[s + 1] - r0;
+  double* zo = Z + (int64_t)s * ell;
   if (sz >= ell) {   // no null vector (the host planner raises DegenerateTagsError)
-    for (int i = 0; i < ell; ++i) Z[(int64_t)s * ell + i] = 0.0;
-    res[s] = INFINITY;
+    for (int i = lane; i < ell; i += 32) zo[i] = 0.0;
+    if (lane == 0) res[s] = INFINITY;
     return;
   }
-  res[s] = ublr::nullvec::null_vector(T, ell, idx + r0, sz, A, tau, Z + (int64_t)s * ell);
+  for (int e = lane; e < ell * sz; e += 32) {
+    const int j = e / ell, i = e - j * ell;
+    A[i + j * ell] = T[(int64_t)idx[r0 + j] * ell + i];
+  }
+  for (int j = lane; j < sz; j += 32) tau[j] = 0.0;
+  __syncwarp();
+  for (int j = 0; j < sz; ++j) {
+    double* col = &A[j * ell];
+    double inv = 0.0, beta = 0.0;
+    bool skip = false;
+    if (lane == 0) {
+      const double alpha = col[j];
+      double ss = 0.0, scale = 0.0;
+      for (int i = j + 1; i < ell; ++i) scale = fmax(scale, fabs(col[i]));
+      if (scale > 0.0) {
+        const double inv_scale = div(1.0, scale);
+        for (int i = j + 1; i < ell; ++i) {
+          const double x = mul(col[i], inv_scale);
+          ss = add(ss, mul(x, x));
+        }
+      }
+      const double xnorm = mul(scale, sqrt_(ss));
+      if (xnorm == 0.0) {
+        skip = true;
+      } else {
+        const double aa = fabs(alpha), wmax = fmax(aa, xnorm), zmin = fmin(aa, xnorm);
+        const double ratio = div(zmin, wmax);
+        beta = -copysign(mul(wmax, sqrt_(add(1.0, mul(ratio, ratio)))), alpha);
+        tau[j] = div(sub(beta, alpha), beta);
+        inv = div(1.0, sub(alpha, beta));
+      }
+    }
+    skip = __shfl_sync(0xffffffffu, skip, 0);
+    if (skip) continue;   // tau_j = 0, column untouched
+    inv = __shfl_sync(0xffffffffu, inv, 0);
+    beta = __shfl_sync(0xffffffffu, beta, 0);
+    for (int i = j + 1 + lane; i < ell; i += 32) col[i] = mul(col[i], inv);
+    __syncwarp();
+    if (lane == 0) col[j] = beta;
+    const double tj = tau[j];
+    for (int c = j + 1 + lane; c < sz; c += 32) {   // trailing columns, one lane each
+      double* a = &A[c * ell];
+      double w = a[j];
+      for (int i = j + 1; i < ell; ++i) w = add(w, mul(col[i], a[i]));
+      w = mul(w, tj);
+      a[j] = sub(a[j], w);
+      for (int i = j + 1; i < ell; ++i) a[i] = sub(a[i], mul(w, col[i]));
+    }
+    __syncwarp();
+  }
+  for (int i = lane; i < ell; i += 32) z[i] = (i == ell - 1) ? 1.0 : 0.0;
+  __syncwarp();
+  for (int j = sz - 1; j >= 0; --j) {
+    const double* v = &A[j * ell];
+    if (lane == 0) {
+      double w = z[j];
+      for (int i = j + 1; i < ell; ++i) w = add(w, mul(v[i], z[i]));
+      wsh[warp] = mul(w, tau[j]);
+    }
+    __syncwarp();
+    const double w = wsh[warp];
+    if (lane == 0) z[j] = sub(z[j], w);
+    for (int i = j + 1 + lane; i < ell; i += 32) z[i] = sub(z[i], mul(w, v[i]));
+    __syncwarp();
+  }
+  // residual ||T[rows] z||: per-row dots by lanes, sum of squares in order by lane 0
+  double* d = tau;   // reuse
+  for (int j = lane; j < sz; j += 32) {
+    const double* t = T + (int64_t)idx[r0 + j] * ell;
+    double dd = 0.0;
+    for (int i = 0; i < ell; ++i) dd = add(dd, mul(t[i], z[i]));
+    d[j] = dd;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    double r2 = 0.0;
+    for (int j = 0; j < sz; ++j) r2 = add(r2, mul(d[j], d[j]));
+    res[s] = sqrt_(r2);
+  }
+  for (int i = lane; i < ell; i += 32) zo[i] = z[i];
 }
 }  // namespace
 }  // namespace ublr
@@ -109,7 +202,7 @@ extern "C" int ublr_null_vectors_device(const double* T, int ell, const int32_t*
   UBLR_REQUIRE(T && ell >= 1 && ell <= ublr::nullvec::MAX_ELL && ptr && idx && nsets >= 0 && Z && res,
                UBLR_ERR_VALUE, "ublr_null_vectors_device: bad arguments (ell <= 32)");
   if (nsets == 0) return UBLR_OK;
-  ublr::k_null_vectors<<<(nsets + 63) / 64, 64, 0, (cudaStream_t)stream>>>(T, ell, ptr, idx, nsets, Z, res);
+  ublr::k_null_vectors<<<(nsets + ublr::NV_WARPS - 1) / ublr::NV_WARPS, ublr::NV_WARPS * 32, 0, (cudaStream_t)stream>>>(T, ell, ptr, idx, nsets, Z, res);
   UBLR_LAUNCH_CHECK();
   return UBLR_OK;
 }

@@ -469,7 +469,7 @@ def compress_type_a(op, tess, k, p=10, method="tag", stream=None, distribution="
                 cop, tess, k, p,
                 lambda: plan_tagging(tess, extra_cols, distribution, stream.child(1), max_redraws=max_tag_redraws, device="auto",
                                      first=first()),
-                stream.child(0), extra_samples=extra_samples, first=first, test_pair=test_pair)
+                stream.child(0), extra_samples=extra_samples, first=first, test_pair=test_pair, defer_plan=True)
             plan = bundle.plan
         elif method == "bn":
             bases, _ = block_nullification_bases(cop, tess, k, p, stream.child(0))
@@ -483,6 +483,19 @@ def compress_type_a(op, tess, k, p=10, method="tag", stream=None, distribution="
         coloring = color_boxes(tess)
         with cop.ledger.phase("III"):
             B = structured_identity_discrepancy(cop, tess, bases, core, coloring)
+    if method == "tag" and plan is None:
+        # the bases were built from the device draw of the first tagging
+        # matrix and phases II-III are queued behind them; the host evaluates
+        # the redraw policy now, overlapping that GPU work, and everything is
+        # recomputed (without billing the ledger twice) if it redrew
+        plan, redo = bundle.resolve_plan()
+        bundle.resolve_plan = None
+        bundle.plan, bundle.tagging = plan, plan.matrix
+        if redo is not None:
+            (bases.U, bases.V), bundle.Y, bundle.Z = redo
+            inner = unwrap(cop)
+            core = direct_core(inner, tess, bases)
+            B = structured_identity_discrepancy(inner, tess, bases, core, coloring)
     rep = UniformBLR(tess, k, bases.U, bases.V, core, B, bases.dt, {"method": METHOD_IDS[("A", method)]})
     rel = relative_error(op, rep, error_iterations, stream.child(9)) if compute_error else None
     aspect, ell = None, None

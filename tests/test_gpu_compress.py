@@ -158,3 +158,31 @@ def test_large_blocks_vs_oracle(per, b, kind, k, mid):
     D_gpu, D_ref = rep.to_dense(), orep.to_dense()
     assert np.linalg.norm(D_gpu - D_ref) / nA <= TOL
     assert np.linalg.norm(A - D_gpu) / nA <= 1.05 * np.linalg.norm(A - D_ref) / nA + 1e-15
+
+
+def test_redraw_after_speculative_bases(monkeypatch):
+    """The tag pipeline builds bases and queues phases II-III from the device
+    draw of the first tagging matrix before the host evaluates the redraw
+    policy; when the policy redraws, everything is recomputed for the accepted
+    matrix (same result as building from that plan directly) and the ledger
+    is not billed twice."""
+    import warnings
+    import torch
+    import paper_2501_05528_b200.reconstruction as R
+    from paper_2501_05528_b200.bases import tagging_bases
+    pts = P.grid_points(32, 2)
+    tess = P.build_tessellation(pts, 16)
+    op = P.KernelOperator(pts, "log", -np.log(0.5 / 32))
+    _, normal = P.compress(op, tess, 10, "A2", p=5, stream=P.RandomStream(7), compute_error=False)
+    orig = R.plan_tagging
+    monkeypatch.setattr(R, "plan_tagging", lambda *a, **kw: orig(*a, **{**kw, "ratio_limit": 0.0}))
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", UserWarning)
+        rep, report = P.compress(op, tess, 10, "A2", p=5, stream=P.RandomStream(7), compute_error=False)
+        plan = orig(tess, 0, "gaussian", P.RandomStream(7).child(1), max_redraws=5, ratio_limit=0.0)
+    assert report.aspect_ratios["draws"] == 6
+    assert report.matvecs == normal.matvecs
+    bases, _ = tagging_bases(op, tess, 10, 5, plan, P.RandomStream(7).child(0))
+    assert torch.equal(bases.U, rep.U[:, :10]) and torch.equal(bases.V, rep.V[:, :10])
+    core = R.direct_core(op, tess, bases)
+    assert torch.equal(core, rep.core_d)

@@ -25,7 +25,8 @@ def wrap(mod, name, label=None):
     setattr(mod, name, g)
 
 
-for mod, names in ((reconstruction, ["direct_core", "structured_identity_discrepancy", "UniformBLR", "CompressionReport"]),
+for mod, names in ((reconstruction, ["direct_core", "structured_identity_discrepancy", "UniformBLR", "CompressionReport",
+                                     "_base_config", "_ratio_summary", "color_boxes"]),
                    (bases, ["tagging_bases", "draw_test_pair", "tagged_sketch", "block_bases_from_tagged"]),
                    (tagging, ["plan_tagging", "make_tagging_matrix", "_evaluate"]),
                    (_lib, ["h2d"])):
