@@ -195,6 +195,26 @@ __global__ void __launch_bounds__(CS_THREADS) k_coupling_nf_small(
     }
   }
   __syncthreads();
+  // U_i S (64 x 64) by DMMA: warp w owns rows 8w .. 8w + 7; the padding
+  // columns of U_i and rows of S are zero, so K = KP adds exact zeros only
+  double* US = As;   // free after the member loop
+  {
+    double acc[8][2];
+#pragma unroll
+    for (int qb = 0; qb < 8; ++qb) acc[qb][0] = acc[qb][1] = 0.0;
+#pragma unroll
+    for (int k4 = 0; k4 < KP; k4 += 4) {
+      const double av = Us[(warp * 8 + g) * SU + k4 + t];
+#pragma unroll
+      for (int qb = 0; qb < 8; ++qb) mma8x8x4(acc[qb][0], acc[qb][1], av, Ss[(k4 + t) * CS_SA + qb * 8 + g]);
+    }
+#pragma unroll
+    for (int qb = 0; qb < 8; ++qb) {
+      US[(warp * 8 + g) * CS_SA + qb * 8 + 2 * t] = acc[qb][0];
+      US[(warp * 8 + g) * CS_SA + qb * 8 + 2 * t + 1] = acc[qb][1];
+    }
+  }
+  __syncthreads();
   const int jn = nidx[p];
   const int mjn = off[jn + 1] - off[jn];
   if (q >= mjn) return;
@@ -202,10 +222,7 @@ __global__ void __launch_bounds__(CS_THREADS) k_coupling_nf_small(
 #pragma unroll
   for (int s = 0; s < 16; ++s) {
     const int r = r0 + 4 * s;
-    if (r >= mi) continue;
-    double v = D[s];
-    for (int a = 0; a < ki; ++a) v = fma(-Us[r * SU + a], Ss[a * CS_SA + q], v);
-    Bp[(int64_t)r * mjn + q] = v;
+    if (r < mi) Bp[(int64_t)r * mjn + q] = D[s] - US[r * CS_SA + q];
   }
 }
 
