@@ -261,13 +261,18 @@ def tagging_bases(op, tess: Tessellation, k: int, p: int, plan, stream: RandomSt
     (plan, None) if the first draw was accepted, else (plan, ((U, V), Y, Z))
     recomputed for the accepted matrix."""
     torch = _torch()
-    if extra_samples:
-        raise NotImplementedError("extra_samples (ref/bases.py:177-182) is not on the B200 hot path (SURVEY F12)")
     _lib.require_device()
     dt = device_tess(tess, torch.device("cuda"))
     r = k + p
     gc = r if group_cols is None else group_cols
     planner = plan if callable(plan) else None
+    from .tagging import extra_sample_vectors
+
+    def combine(pl):
+        """Per-block combination vectors: the plan's z^(i), or with
+        extra_samples the first null direction (tagging.extra_sample_vectors)."""
+        return extra_sample_vectors(pl, tess) if extra_samples else pl.Z
+
     if planner is not None and tess.b >= DEVICE_PLAN_MIN_B:
         # large b: the planner's aspect ratios run on the GPU, so plan before
         # the sketch occupies it (no speculative sketch)
@@ -292,7 +297,7 @@ def tagging_bases(op, tess: Tessellation, k: int, p: int, plan, stream: RandomSt
     G, H = draw_test_pair(dt, stream, gc) if test_pair is None else test_pair[:2]
     Y, Z = tagged_sketch(op, dt, T_dev, None if matrix is None else matrix.entries, G, H, gc, out=(Y, Z), ell=ell)
     UV = None
-    if matrix is None and ell <= NULLVEC_DEVICE_MAX_ELL:
+    if matrix is None and ell <= NULLVEC_DEVICE_MAX_ELL and not extra_samples:
         # speculative bases: the first draw's null vectors on the device (the
         # same bits as the host planner's, csrc/nullvec.cuh) and the block QR,
         # queued behind the sketch; the host evaluates the plan meanwhile and
@@ -318,7 +323,7 @@ def tagging_bases(op, tess: Tessellation, k: int, p: int, plan, stream: RandomSt
                 T_entries = pl.matrix.entries
                 Y, Z = tagged_sketch(op, dt, _lib.h2d(T_entries, dt.device), T_entries, G, H, gc)
         if uv is None:
-            uv = block_bases_from_tagged(dt, Y, Z, _lib.h2d(pl.Z, dt.device), ell, gc, k)
+            uv = block_bases_from_tagged(dt, Y, Z, _lib.h2d(combine(pl), dt.device), ell, gc, k)
         return pl, uv
 
     if defer_plan and UV is not None and planner is not None:
@@ -344,7 +349,7 @@ def tagging_bases(op, tess: Tessellation, k: int, p: int, plan, stream: RandomSt
                 return pl, None
             T_entries = pl.matrix.entries   # redrawn: sketch and bases of the accepted matrix
             Y2, Z2 = tagged_sketch(op, dt, _lib.h2d(T_entries, dt.device), T_entries, G, H, gc)
-            uv = block_bases_from_tagged(dt, Y2, Z2, _lib.h2d(pl.Z, dt.device), ell, gc, k)
+            uv = block_bases_from_tagged(dt, Y2, Z2, _lib.h2d(combine(pl), dt.device), ell, gc, k)
             return pl, (uv, Y2, Z2)
         bundle.resolve_plan = resolve_plan
         return bases, bundle

@@ -451,9 +451,6 @@ def compress_type_a(op, tess, k, p=10, method="tag", stream=None, distribution="
     times, plan = PhaseTimes(), None
     with _PhaseTimer(times, "I"), cop.ledger.phase("I"):
         if method == "tag":
-            if optimize:
-                raise NotImplementedError("null-vector optimisation (ref/tagging.py:142-292) is outside the "
-                                          "B200 hot path")
             # the test blocks are drawn on the GPU while the host draws the
             # tagging matrix; the sketch of the policy's first draw runs while
             # the host evaluates the plan
@@ -461,14 +458,16 @@ def compress_type_a(op, tess, k, p=10, method="tag", stream=None, distribution="
             if not extra_samples:
                 # gaussian tagging: T is drawn in the same launch (the host draws the same bits below)
                 ell = 3 ** tess.dim + 1 + extra_cols
-                tag = (stream.child(1).child(0), ell) if distribution == "gaussian" and tess.b >= ell else (None, 0)
+                # (not with optimize: the device null vectors are the base ones)
+                tag = ((stream.child(1).child(0), ell) if distribution == "gaussian" and tess.b >= ell
+                       and not optimize else (None, 0))
                 test_pair = draw_test_pair(device_tess(tess, _torch().device("cuda")), stream.child(0), k + p, *tag)
             first = _Lazy(lambda: make_tagging_matrix(tess.b, tess.dim, extra_cols, distribution,
                                                       stream.child(1).child(0)))
             bases, bundle = tagging_bases(
                 cop, tess, k, p,
-                lambda: plan_tagging(tess, extra_cols, distribution, stream.child(1), max_redraws=max_tag_redraws, device="auto",
-                                     first=first()),
+                lambda: plan_tagging(tess, extra_cols, distribution, stream.child(1), optimize=optimize,
+                                     max_redraws=max_tag_redraws, device="auto", first=first()),
                 stream.child(0), extra_samples=extra_samples, first=first, test_pair=test_pair, defer_plan=True)
             plan = bundle.plan
         elif method == "bn":
@@ -502,6 +501,8 @@ def compress_type_a(op, tess, k, p=10, method="tag", stream=None, distribution="
     if plan is not None:
         ell = plan.matrix.n_cols
         aspect = {"base": _ratio_summary(plan.rho_base), "draws": plan.attempts}
+        if plan.rho_optimized is not None:
+            aspect["optimized"] = _ratio_summary(plan.rho_optimized)
     report = CompressionReport(
         method=METHOD_IDS[("A", method)],
         config=_base_config(tess, k, p, stream, ell=ell, distribution=distribution if method == "tag" else None,
@@ -529,14 +530,11 @@ def compress_type_b(op, tess, k, p=10, method="bn", stream=None, distribution="g
         if method == "bn":
             bases, bundle = block_nullification_bases(cop, tess, k, p, stream.child(0))
         else:
-            if optimize:
-                raise NotImplementedError("null-vector optimisation (ref/tagging.py:142-292) is outside the "
-                                          "B200 hot path")
             first = make_tagging_matrix(tess.b, tess.dim, 0, distribution, stream.child(1).child(0))
             bases, bundle = tagging_bases(
                 cop, tess, k, p,
-                lambda: plan_tagging(tess, 0, distribution, stream.child(1), max_redraws=max_tag_redraws, device="auto",
-                                     extra_check=lambda T: b2_denominators_ok(T, tess), first=first),
+                lambda: plan_tagging(tess, 0, distribution, stream.child(1), optimize=optimize,
+                                     max_redraws=max_tag_redraws, device="auto", extra_check=lambda T: b2_denominators_ok(T, tess), first=first),
                 stream.child(0), group_cols=tess.max_block_size + p, first=first)
             plan = bundle.plan
     with _PhaseTimer(times, "III"), cop.ledger.phase("III"):
@@ -552,6 +550,8 @@ def compress_type_b(op, tess, k, p=10, method="bn", stream=None, distribution="g
     if plan is not None:
         ell = plan.matrix.n_cols
         aspect = {"base": _ratio_summary(plan.rho_base), "draws": plan.attempts}
+        if plan.rho_optimized is not None:
+            aspect["optimized"] = _ratio_summary(plan.rho_optimized)
     report = CompressionReport(
         method=METHOD_IDS[("B", method)],
         config=_base_config(tess, k, p, stream, ell=ell, distribution=distribution if method == "tag" else None,

@@ -107,10 +107,35 @@ def make_tagging_matrix(b, d, extra_cols=0, distribution="gaussian", stream=None
         signs[signs == 0] = 1.0
         entries = q * signs
     elif distribution == "equidistributed":
-        raise NotImplementedError("equidistributed tagging rows are not part of the B200 hot path")
+        entries = equidistributed_rows(b, ell, stream)
     else:
         raise ValueError(f"unknown distribution {distribution!r}; expected one of {DISTRIBUTIONS}")
     return TaggingMatrix(entries, d, extra_cols, distribution, stream.seed)
+
+
+def equidistributed_rows(b, ell, stream, iterations=200):
+    """ref/tagging.py:94-123: normalised Gaussian rows spread over the unit
+    sphere by Riesz-energy descent against the other rows and their antipodes
+    (step 0.25 d_min^3, displacement capped at d_min / 2, renormalised after
+    each step). Host planning: b x b x ell work per iteration, done once per
+    draw before any kernel runs."""
+    rows = gaussian(b, ell, stream)
+    rows /= np.linalg.norm(rows, axis=1, keepdims=True)
+    for _ in range(iterations):
+        force = np.zeros_like(rows)
+        d_min = np.inf
+        for sgn in (1.0, -1.0):
+            diff = rows[:, None, :] - sgn * rows[None, :, :]
+            d2 = (diff ** 2).sum(axis=2)
+            d2[d2 < 1e-30] = np.inf
+            dist = np.sqrt(d2)
+            force += (diff / dist[:, :, None] ** 3).sum(axis=1)
+            d_min = min(d_min, dist.min())
+        disp = (0.25 * d_min ** 3) * force
+        dlen = np.linalg.norm(disp, axis=1, keepdims=True)
+        rows = rows + disp * np.minimum(1.0, (0.5 * d_min) / np.maximum(dlen, 1e-300))
+        rows /= np.linalg.norm(rows, axis=1, keepdims=True)
+    return rows
 
 
 def _csr(rows_list):
@@ -219,6 +244,148 @@ def aspect_ratio(pt: ProjectedTags, tess: Tessellation, i: int | None = None) ->
     return float(hi / lo)
 
 
+def null_basis_host(sub: np.ndarray, k: int, rtol: float = 1e-12) -> np.ndarray:
+    """ref/linalg.py:72-94 for the tiny host tagging problems: the last k
+    columns of numpy's complete QR of sub^T (the reference's own
+    orthonormalisation, so nullity >= 2 picks the same directions)."""
+    n = sub.shape[1]
+    if k > n:
+        raise DegenerateTagsError(f"k={k} exceeds column count {n}")
+    q = np.linalg.qr(sub.T, mode="complete")[0]
+    X = q[:, n - k:]
+    if np.linalg.norm(sub @ X) > rtol * max(1.0, np.linalg.norm(sub)):
+        raise DegenerateTagsError(f"requested null space of dimension {k} does not exist")
+    return X
+
+
+def _ratio_cols(far_vals: np.ndarray) -> np.ndarray:
+    """ref/tagging.py:157-166: aspect ratio of each column of (|F|, n)."""
+    mags = np.abs(far_vals)
+    hi, lo = mags.max(axis=0), mags.min(axis=0)
+    out = np.full(far_vals.shape[1], np.inf)
+    np.divide(hi, lo, out=out, where=lo > 0)
+    out[hi == 0] = 1.0
+    return out
+
+
+def _golden_min(f, a, b, tol=1e-10, max_iter=200):
+    """ref/tagging.py:169-191: golden-section minimisation on [a, b]."""
+    g = (np.sqrt(5.0) - 1.0) / 2.0
+    x1, x2 = b - g * (b - a), a + g * (b - a)
+    f1, f2 = f(x1), f(x2)
+    for _ in range(max_iter):
+        if b - a < tol:
+            break
+        if f1 <= f2:
+            b, x2, f2 = x2, x1, f1
+            x1 = b - g * (b - a)
+            f1 = f(x1)
+        else:
+            a, x1, f1 = x1, x2, f2
+            x2 = a + g * (b - a)
+            f2 = f(x2)
+    return (x1, f1) if f1 <= f2 else (x2, f2)
+
+
+def _search_circle(P, grid_points):
+    """ref/tagging.py:241-262: nullity 2 -- grid over the half circle, then
+    golden-section refinement inside the best grid cell."""
+    th = np.linspace(0.0, np.pi, grid_points, endpoint=False)
+    ratios = _ratio_cols(P @ np.vstack((np.cos(th), np.sin(th))))
+    best = int(np.argmin(ratios))
+    h = np.pi / grid_points
+    t_ref, r_ref = _golden_min(lambda t: _ratio_cols((P @ np.array([np.cos(t), np.sin(t)]))[:, None])[0],
+                               th[best] - h, th[best] + h)
+    t, r = (t_ref, r_ref) if r_ref <= ratios[best] else (th[best], ratios[best])
+    return np.array([np.cos(t), np.sin(t)]), float(r)
+
+
+def _search_sphere(P, coarse=64, zoom_rounds=3):
+    """ref/tagging.py:265-289: nullity >= 3 -- (phi, psi) grid over the
+    sphere of the first three null directions with three zoom rounds."""
+    phi_c, phi_h, psi_c, psi_h = np.pi / 2, np.pi / 2, np.pi, np.pi
+    best_a, best_r = None, np.inf
+    n = coarse
+    for _ in range(zoom_rounds + 1):
+        pp, ss = np.meshgrid(np.linspace(phi_c - phi_h, phi_c + phi_h, n),
+                             np.linspace(psi_c - psi_h, psi_c + psi_h, n), indexing="ij")
+        pp, ss = pp.ravel(), ss.ravel()
+        A = np.column_stack((np.cos(pp), np.sin(pp) * np.cos(ss), np.sin(pp) * np.sin(ss)))
+        ratios = _ratio_cols(P @ A.T)
+        idx = int(np.argmin(ratios))
+        if ratios[idx] < best_r:
+            best_r, best_a = float(ratios[idx]), A[idx]
+        phi_c, psi_c = pp[idx], ss[idx]
+        phi_h /= n / 4.0
+        psi_h /= n / 4.0
+        n = 17
+    return best_a, best_r
+
+
+def optimize_null_vector(T: TaggingMatrix, tess: Tessellation, i: int, grid_points: int = 4096,
+                         base: NullVector | None = None) -> NullVector:
+    """ref/tagging.py:194-238: the unit vector of null(T(N_i, :)) with the
+    smallest far-field aspect ratio (searched over the first <= 3 null
+    directions); the unoptimised vector is kept when it is at least as good.
+    Nullity 1 returns the base vector with a warning."""
+    if base is None:
+        base = tag_null_vector(T, tess, i)
+    far, nbrs = tess.far_fields[i], tess.neighbor_lists[i]
+    nullity = T.n_cols - len(nbrs)
+    if nullity < 2:
+        warnings.warn(f"block {i}: null space is one-dimensional, nothing to optimize")
+        return base
+    if len(far) == 0:
+        return base
+    sub = T.entries[nbrs, :]
+    X = null_basis_host(sub, nullity)[:, :min(nullity, 3)]
+    P = T.entries[far, :] @ X
+    coeffs, ratio = _search_circle(P, grid_points) if X.shape[1] == 2 else _search_sphere(P)
+    if aspect_ratio(projected_tags(T, tess, base), tess) <= ratio:
+        return base
+    z = X @ coeffs
+    z /= np.linalg.norm(z)
+    return NullVector(block=i, vector=z, residual=float(np.linalg.norm(sub @ z)))
+
+
+def _optimize_plan(plan: TaggingPlan, tess: Tessellation) -> TaggingPlan:
+    """The optimize=True branch of ref/tagging.py:355-379 over an evaluated
+    plan: blocks of nullity >= 2 get optimize_null_vector, every block with a
+    far field gets rho_optimized. Host planning only -- the chosen vectors
+    feed the same GPU block-QR launch as the base ones."""
+    T = plan.matrix
+    Z, res = plan.Z.copy(), np.array([nv.residual for nv in plan.null_vectors])
+    rho_opt = np.full(tess.b, np.nan)
+    nl = np.array([len(x) for x in tess.neighbor_lists])
+    for i in range(tess.b):
+        far = tess.far_fields[i]
+        if T.n_cols - nl[i] >= 2:
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore")
+                nv = optimize_null_vector(T, tess, i, base=NullVector(i, Z[i], float(res[i])))
+            Z[i], res[i] = nv.vector, nv.residual
+        if len(far) > 0:
+            rho_opt[i] = _ratio_cols((T.entries[far, :] @ Z[i])[:, None])[0]
+    return TaggingPlan(matrix=T, null_vectors=NullVectors(Z, res), rho_base=plan.rho_base, rho_optimized=rho_opt,
+                       attempts=plan.attempts)
+
+
+def extra_sample_vectors(plan: TaggingPlan, tess: Tessellation) -> np.ndarray:
+    """Per-block combination vectors of tagging_bases(extra_samples=True)
+    (ref/bases.py:177-188). The reference concatenates the samples of every
+    orthonormal null direction, but U_i = the first k columns of an unpivoted
+    QR depends only on the first sample (k <= group width), so
+    the GPU path combines with the first column of null_basis(T(N_i,:),
+    nullity) where nullity >= 2 and with the plan's z^(i) elsewhere."""
+    T = plan.matrix.entries
+    Z = plan.Z.copy()
+    for i, nb in enumerate(tess.neighbor_lists):
+        nullity = T.shape[1] - len(nb)
+        if nullity >= 2:
+            Z[i] = null_basis_host(T[nb, :], nullity)[:, 0]
+    return Z
+
+
 DEVICE_PLAN_MIN_B = 1024
 
 
@@ -308,8 +475,6 @@ def plan_tagging(tess, extra_cols=0, distribution="gaussian", stream=None, optim
     per draw at b = 4096); False keeps the host form (CPU tests)."""
     if device == "auto":
         device = tess.b >= DEVICE_PLAN_MIN_B
-    if optimize:
-        raise NotImplementedError("null-vector optimisation (ref/tagging.py:142-292) is outside the B200 hot path")
     stream = stream or RandomStream(0)
     last, plan = None, None
     for attempt in range(max_redraws + 1):
@@ -322,10 +487,13 @@ def plan_tagging(tess, extra_cols=0, distribution="gaussian", stream=None, optim
             continue
         try:
             plan = _evaluate(T, tess, attempt + 1, device=device)
+            if optimize:
+                plan = _optimize_plan(plan, tess)
         except DegenerateTagsError as exc:
             last = exc
             continue
-        fin = plan.rho_base[~np.isnan(plan.rho_base)]
+        eff = plan.rho_optimized if plan.rho_optimized is not None else plan.rho_base
+        fin = eff[~np.isnan(eff)]
         worst = fin.max() if fin.size else 1.0
         if np.isfinite(worst) and worst <= ratio_limit:
             return plan

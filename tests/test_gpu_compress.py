@@ -186,3 +186,31 @@ def test_redraw_after_speculative_bases(monkeypatch):
     assert torch.equal(bases.U, rep.U[:, :10]) and torch.equal(bases.V, rep.V[:, :10])
     core = R.direct_core(op, tess, bases)
     assert torch.equal(core, rep.core_d)
+
+
+# tests/golden/make_golden_options.py: the 32 x 32 log grid, 16 boxes
+OPTION_CASES = {
+    "A2_opt": ("A2", 10, 5, {"optimize": True}),
+    "A2_xs": ("A2", 10, 5, {"extra_samples": True}),
+    "A2_equi": ("A2", 10, 5, {"distribution": "equidistributed"}),
+    "A2_haar_x1": ("A2", 10, 5, {"distribution": "haar", "extra_cols": 1}),
+    "A2_x2_opt": ("A2", 10, 5, {"extra_cols": 2, "optimize": True}),
+    "B2_opt": ("B2", 8, 4, {"optimize": True}),
+}
+
+
+@pytest.mark.parametrize("name", sorted(OPTION_CASES))
+def test_tagging_options_match_reference(name):
+    """Null-vector optimisation, extra_samples, equidistributed / haar rows and
+    extra tagging columns through the GPU path against the reference's own
+    compressions of the same matrix (same seeds)."""
+    mid, k, p, kw = OPTION_CASES[name]
+    tess, op, _ = gpu_problem("log1k_" + mid)
+    rep, report = P.compress(op, tess, k, mid, p=p, stream=P.RandomStream(7), compute_error=False, **kw)
+    g = golden("opt_" + name)
+    assert ahat_error_vs_golden(rep, g) <= TOL
+    mv = np.array([[report.matvecs.get(ph, {"A": 0})["A"], report.matvecs.get(ph, {"Astar": 0})["Astar"]]
+                   for ph in ("I", "II", "III")])
+    assert np.array_equal(mv, g["matvecs"])
+    if kw.get("optimize"):
+        assert report.aspect_ratios["optimized"]["max"] == pytest.approx(float(g["rho_opt_max"]), rel=1e-8)

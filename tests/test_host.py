@@ -183,3 +183,50 @@ def test_plan_evaluation_c_abi_matches_numpy(per, nb, d):
     a, b = _evaluate(T, tess, 1), _evaluate_numpy(T, tess, 1)
     assert np.allclose(np.abs(a.null_vectors.Z), np.abs(b.null_vectors.Z), rtol=0, atol=1e-13)
     assert np.allclose(a.rho_base, b.rho_base, rtol=1e-12, equal_nan=True)
+
+
+# name -> (per_axis, b, extra_cols, distribution, optimize); tests/golden/make_golden_options.py
+PLAN_OPTIONS = {
+    "g16_opt": (32, 16, 0, "gaussian", True),
+    "g64_opt": (64, 64, 0, "gaussian", True),
+    "g16_x2_opt": (32, 16, 2, "gaussian", True),
+    "g16_equi": (32, 16, 0, "equidistributed", False),
+    "g16_haar_x1": (32, 16, 1, "haar", False),
+}
+
+
+@pytest.mark.parametrize("name", sorted(PLAN_OPTIONS))
+def test_tagging_plan_options_match_reference(name):
+    """Null-vector optimisation (ref/tagging.py:194-289), equidistributed and
+    haar rows (ref/tagging.py:61-123), extra columns, and the extra_samples
+    combination vectors (ref/bases.py:177-182) against the reference's plans."""
+    per, b, xc, dist, opt = PLAN_OPTIONS[name]
+    g = golden("plans_options")
+    t = P.build_tessellation(P.grid_points(per, 2), b)
+    plan = P.plan_tagging(t, xc, dist, P.RandomStream(7).child(1), optimize=opt)
+    assert int(g[f"{name}_attempts"]) == plan.attempts
+    T = plan.matrix.entries
+    if dist == "gaussian":
+        assert np.array_equal(T, g[f"{name}_T"])
+    else:   # numpy QR / Riesz descent: the same operations, rounding-level agreement
+        assert np.abs(T - g[f"{name}_T"]).max() <= 1e-13
+    assert np.abs(plan.Z - g[f"{name}_Z"]).max() <= 1e-10
+    assert np.allclose(plan.rho_base, g[f"{name}_rho"], rtol=1e-8, equal_nan=True)
+    if opt:
+        assert np.allclose(plan.rho_optimized, g[f"{name}_rho_opt"], rtol=1e-8, equal_nan=True)
+        fin = ~np.isnan(plan.rho_base)
+        assert (plan.rho_optimized[fin] <= plan.rho_base[fin] * (1 + 1e-12)).all()
+    else:
+        assert plan.rho_optimized is None
+    X = P.tagging.extra_sample_vectors(plan, t)
+    assert np.abs(X - g[f"{name}_X"]).max() <= 1e-10
+
+
+def test_optimize_nullity_one_warns_and_keeps_base():
+    t = P.build_tessellation(P.grid_points(32, 2), 16)
+    plan = P.plan_tagging(t, 0, "gaussian", P.RandomStream(7).child(1))
+    interior = next(i for i, nb in enumerate(t.neighbor_lists) if len(nb) == 9)
+    base = plan.null_vectors[interior]
+    with pytest.warns(UserWarning, match="one-dimensional"):
+        nv = P.tagging.optimize_null_vector(plan.matrix, t, interior)
+    assert np.abs(nv.vector - base.vector).max() <= 1e-14
