@@ -238,8 +238,12 @@ def require_device():
 
 
 def ptr(t) -> int:
-    """Device pointer of a torch tensor (or 0 for None)."""
-    return 0 if t is None else int(t.data_ptr())
+    """Device pointer of a torch tensor (0 for None; ints pass through)."""
+    if t is None:
+        return 0
+    if isinstance(t, int):    # already a raw device address
+        return t
+    return int(t.data_ptr())
 
 
 class _PinnedRing:
@@ -303,8 +307,17 @@ class stream_scope:
         global _stream_cached, _stream_obj
         import torch
         self._prev = (_stream_cached, _stream_obj)
-        _stream_obj = torch.cuda.current_stream()
-        _stream_cached = C.c_void_p(_stream_obj.cuda_stream)
+        # the raw handle is a cheap query; the torch Stream object (for
+        # Event.record) is memoised per (device, handle)
+        dev = torch._C._cuda_getDevice()
+        raw = torch._C._cuda_getCurrentRawStream(dev)
+        hit = _STREAMS.get((dev, raw))
+        if hit is None:
+            obj = torch.cuda.current_stream()
+            if len(_STREAMS) > 64:
+                _STREAMS.clear()
+            hit = _STREAMS[(dev, raw)] = (obj, C.c_void_p(raw))
+        _stream_obj, _stream_cached = hit
         return self
 
     def __exit__(self, *exc):
@@ -313,6 +326,7 @@ class stream_scope:
 
 
 _stream_obj = None
+_STREAMS = {}   # (device, raw handle) -> (torch Stream, c_void_p)
 
 
 def current_stream():

@@ -139,12 +139,43 @@ def draw_test_blocks(dt, stream: RandomStream, side: int, cols: int):
     return device_normals(specs, out)
 
 
+class TestPair:
+    """(G, H, T) drawn into one buffer by draw_test_pair with a tagging
+    stream. The launches that follow need only the device addresses
+    (G_ptr, H_ptr, T_ptr); the torch views are built on first access, after
+    those launches are queued (each view op costs microseconds of host time
+    on the compression's critical path)."""
+
+    def __init__(self, buf, n, cols, b, tag_cols):
+        self.buf, self.n, self.cols, self.b, self.tag_cols = buf, n, cols, b, tag_cols
+        self.G_ptr = int(buf.data_ptr())
+        self.H_ptr = self.G_ptr + 8 * n * cols
+        self.T_ptr = self.G_ptr + 16 * n * cols
+        self._views = None
+
+    def views(self):
+        if self._views is None:
+            n2 = 2 * self.n * self.cols
+            GH = self.buf[:n2].view(2, self.n, self.cols)
+            self._views = (GH[0], GH[1], self.buf[n2:].view(self.b, self.tag_cols))
+        return self._views
+
+    def __len__(self):
+        return 3
+
+    def __getitem__(self, i):
+        return self.views()[i]
+
+    def __iter__(self):
+        return iter(self.views())
+
+
 def draw_test_pair(dt, stream: RandomStream, cols: int, tag_stream: RandomStream | None = None, tag_cols: int = 0):
     """(G, H) with G_i = gaussian(m_i, cols, stream.child(0, i)) and
     H_i = ...child(1, i) (ref/bases.py:163-168), drawn in ONE launch set into
     a (2, N, cols) buffer. With `tag_stream`, the same launch also draws the
     gaussian tagging matrix T = gaussian(b, tag_cols, tag_stream)
-    (ref/tagging.py:61-91) on the device and (G, H, T) is returned: the host
+    (ref/tagging.py:61-91) on the device and a TestPair (G, H, T) is returned: the host
     draws the same bits with numpy for its planning, and the sketch can be
     launched without waiting for a host-to-device copy of T."""
     from .linalg import launch_normals, rng_launch_record
@@ -175,10 +206,10 @@ def draw_test_pair(dt, stream: RandomStream, cols: int, tag_stream: RandomStream
             dt.rng_records.clear()
         dt.rng_records[ck] = rec
     launch_normals(rec, buf)
-    GH = buf[:n2].view(2, dt.n, cols)
     if tag_stream is None:
+        GH = buf[:n2].view(2, dt.n, cols)
         return GH[0], GH[1]
-    return GH[0], GH[1], buf[n2:].view(dt.b, tag_cols)
+    return TestPair(buf, dt.n, cols, dt.b, tag_cols)
 
 
 def tagged_sketch(op, dt, T_dev, T_entries, G, H, gc, out=None, ell=None):
@@ -282,20 +313,33 @@ def tagging_bases(op, tess: Tessellation, k: int, p: int, plan, stream: RandomSt
                 and hasattr(unwrap(op), "device_op"))
     if device_T:
         # the device draw of the policy's first matrix (draw_test_pair with
-        # tag_stream): the sketch is launched before the host has drawn it
-        T_dev = test_pair[2]
-        ell = T_dev.shape[1]
+        # tag_stream): the sketch is launched before the host has drawn it,
+        # from raw addresses (the tensor views are built after the launches)
+        T_dev = test_pair.T_ptr
+        ell = test_pair.tag_cols
         matrix = None
     else:
         matrix = first_fn() if planner is not None else plan.matrix
         ell = matrix.entries.shape[1]
         T_dev = _lib.h2d(matrix.entries, dt.device)
+    T_shape = (dt.b, ell)
     s = ell * gc
-    Y = torch.empty((dt.n, s), dtype=torch.float64, device=dt.device)
-    Z = torch.empty((dt.n, s), dtype=torch.float64, device=dt.device)
+    if device_T:
+        YZ = torch.empty(2 * dt.n * s, dtype=torch.float64, device=dt.device)
+        yp = int(YZ.data_ptr())
+        tagged_sketch(op, dt, T_dev, None, test_pair.G_ptr, test_pair.H_ptr, gc, out=(yp, yp + 8 * dt.n * s),
+                      ell=ell)
+    else:
+        Y = torch.empty((dt.n, s), dtype=torch.float64, device=dt.device)
+        Z = torch.empty((dt.n, s), dtype=torch.float64, device=dt.device)
+        G, H = draw_test_pair(dt, stream, gc) if test_pair is None else test_pair[:2]
+        Y, Z = tagged_sketch(op, dt, T_dev, None if matrix is None else matrix.entries, G, H, gc, out=(Y, Z),
+                             ell=ell)
     _bill(op, s, s)
-    G, H = draw_test_pair(dt, stream, gc) if test_pair is None else test_pair[:2]
-    Y, Z = tagged_sketch(op, dt, T_dev, None if matrix is None else matrix.entries, G, H, gc, out=(Y, Z), ell=ell)
+    if device_T:
+        YZv = YZ.view(2, dt.n, s)
+        Y, Z = YZv[0], YZv[1]
+        G, H = test_pair[0], test_pair[1]
     UV = None
     if matrix is None and ell <= NULLVEC_DEVICE_MAX_ELL and not extra_samples:
         # speculative bases: the first draw's null vectors on the device (the
@@ -313,7 +357,7 @@ def tagging_bases(op, tess: Tessellation, k: int, p: int, plan, stream: RandomSt
         m0 = speculative_matrix
         if m0 is None:
             m0 = first_fn()                  # host draw of the same bits, while the GPU works
-            if m0.entries.shape != tuple(T_dev.shape):
+            if m0.entries.shape != T_shape:
                 raise RuntimeError("device and host tagging draws disagree in shape")
         pl, uv = plan, UV
         if planner is not None:
@@ -332,7 +376,7 @@ def tagging_bases(op, tess: Tessellation, k: int, p: int, plan, stream: RandomSt
         bundle.plan = None
         def host_plan():                     # worker thread: host numpy + C only, no CUDA calls
             m0 = first_fn()
-            if m0.entries.shape != tuple(T_dev.shape):
+            if m0.entries.shape != T_shape:
                 raise RuntimeError("device and host tagging draws disagree in shape")
             return m0, planner()
 

@@ -146,15 +146,20 @@ def rng_launch_record(seed, keys, rows, cols, offsets, ld, rowmap, device, suffi
     rec_d = _lib.h2d(rec.view(np.uint8), device)
     if len(_RNG_CACHE) > 64:
         _RNG_CACHE.clear()
-    hit = _RNG_CACHE[ck] = (rec_d, counts, ns, ws, ws_bytes, rowmap)
+    # the launch arguments as plain ints, resolved once (the RNG launch is the
+    # first thing a compression queues: its host latency is on the step's
+    # critical path)
+    fast = (_lib.ptr(rec_d), counts.ctypes.data, ns, _lib.ptr(ws), ws_bytes, _lib.rng_launches(counts))
+    hit = _RNG_CACHE[ck] = (rec_d, counts, ns, ws, ws_bytes, rowmap, fast)
     return hit
 
 
-def launch_normals(record, out):
-    """Draw the normals of a rng_launch_record into `out` (K1)."""
-    rec_d, counts, ns, ws, ws_bytes, _ = record
-    _lib.call("ublr_rng_normals", _lib.ptr(rec_d), counts.ctypes.data, ns, _lib.ptr(out), _lib.ptr(ws), ws_bytes,
-              _lib.stream_handle(), launches=_lib.rng_launches(counts))
+def launch_normals(record, out, out_ptr=None):
+    """Draw the normals of a rng_launch_record into `out` (K1); `out_ptr`
+    overrides the destination pointer."""
+    rp, cp, ns, wp, ws_bytes, launches = record[6]
+    _lib.call("ublr_rng_normals", rp, cp, ns, _lib.ptr(out) if out_ptr is None else out_ptr, wp, ws_bytes,
+              _lib.stream_handle(), launches=launches)
     return out
 
 

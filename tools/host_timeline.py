@@ -33,6 +33,14 @@ for mod, names in ((reconstruction, ["direct_core", "structured_identity_discrep
     for nm in names:
         wrap(mod, nm)
 reconstruction.draw_test_pair = bases.draw_test_pair
+if os.environ.get("TL_FINE"):
+    wrap(reconstruction, "counting_wrapper")
+    wrap(reconstruction, "device_tess")
+    wrap(linalg, "launch_normals")
+    wrap(torch, "empty", "torch.empty")
+    wrap(reconstruction._PhaseTimer, "__enter__", "PhaseTimer.enter")
+    wrap(reconstruction._PhaseTimer, "__exit__", "PhaseTimer.exit")
+    wrap(linalg.RandomStream, "child", "RandomStream.child")
 orig = _lib.call
 
 
