@@ -327,6 +327,21 @@ class stream_scope:
 
 _stream_obj = None
 _STREAMS = {}   # (device, raw handle) -> (torch Stream, c_void_p)
+_SIDE = {}      # (device, main raw handle) -> (torch Stream, c_void_p)
+
+
+def side_stream():
+    """A second stream for work that is independent of the kernel queued
+    next on the current one (one per device and current stream, created
+    once): (torch Stream, raw handle)."""
+    import torch
+    main = current_stream()
+    key = (main.device_index, main.cuda_stream)
+    hit = _SIDE.get(key)
+    if hit is None:
+        st = torch.cuda.Stream(device=main.device)
+        hit = _SIDE[key] = (st, C.c_void_p(st.cuda_stream))
+    return hit
 
 
 def current_stream():

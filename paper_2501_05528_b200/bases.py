@@ -324,6 +324,10 @@ def tagging_bases(op, tess: Tessellation, k: int, p: int, plan, stream: RandomSt
         T_dev = _lib.h2d(matrix.entries, dt.device)
     T_shape = (dt.b, ell)
     s = ell * gc
+    speculative = matrix is None and ell <= NULLVEC_DEVICE_MAX_ELL and not extra_samples
+    if speculative:
+        ev_drawn = torch.cuda.Event()          # G, H and T drawn: the null vectors need only T
+        ev_drawn.record(_lib.current_stream())
     if device_T:
         YZ = torch.empty(2 * dt.n * s, dtype=torch.float64, device=dt.device)
         yp = int(YZ.data_ptr())
@@ -341,15 +345,22 @@ def tagging_bases(op, tess: Tessellation, k: int, p: int, plan, stream: RandomSt
         Y, Z = YZv[0], YZv[1]
         G, H = test_pair[0], test_pair[1]
     UV = None
-    if matrix is None and ell <= NULLVEC_DEVICE_MAX_ELL and not extra_samples:
+    if speculative:
         # speculative bases: the first draw's null vectors on the device (the
         # same bits as the host planner's, csrc/nullvec.cuh) and the block QR,
         # queued behind the sketch; the host evaluates the plan meanwhile and
-        # they are recomputed only if the redraw policy rejects the draw
+        # they are recomputed only if the redraw policy rejects the draw. The
+        # null vectors run on a side stream beside the sketch (whose grid
+        # leaves SMs free), so only the QR waits for both.
         Z_spec = torch.empty((dt.b, ell), dtype=torch.float64, device=dt.device)
         res_spec = torch.empty(dt.b, dtype=torch.float64, device=dt.device)
+        side, side_h = _lib.side_stream()
+        side.wait_event(ev_drawn)
         _lib.call("ublr_null_vectors_device", _lib.ptr(T_dev), ell, _lib.ptr(dt.nptr), _lib.ptr(dt.nidx), dt.b,
-                  _lib.ptr(Z_spec), _lib.ptr(res_spec), _lib.stream_handle())
+                  _lib.ptr(Z_spec), _lib.ptr(res_spec), side_h)
+        ev_nv = torch.cuda.Event()
+        ev_nv.record(side)
+        _lib.current_stream().wait_event(ev_nv)
         UV = block_bases_from_tagged(dt, Y, Z, Z_spec, ell, gc, k)
     def evaluate(speculative_matrix):
         """Host draw + redraw policy; (plan, Y, Z, UV) for the accepted matrix."""
