@@ -204,18 +204,21 @@ def _work_of(name, args):
     return 0.0
 
 
-def call(name: str, *args, launches=None):
+def call(name: str, *args, launches=None, on=None):
     """Call a status-returning C-ABI function and raise on failure
-    (`launches`: kernels it launches when that depends on the arguments)."""
+    (`launches`: kernels it launches when that depends on the arguments;
+    `on`: the torch stream it launches on when that is not the current one,
+    for the instrumentation events)."""
     global launch_count
     launch_count += _launches_of(name, args) if launches is None else launches
     if _events is not None and (_only is None or name in _only):
         add_work(name, _work_of(name, args))
         import torch
+        st = current_stream() if on is None else on
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(current_stream())
+        a.record(st)
         check(getattr(load(), name)(*args), name)
-        b.record(current_stream())
+        b.record(st)
         _events.setdefault(name, []).append((a, b))
         return
     check(getattr(load(), name)(*args), name)

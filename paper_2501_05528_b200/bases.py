@@ -357,7 +357,7 @@ def tagging_bases(op, tess: Tessellation, k: int, p: int, plan, stream: RandomSt
         side, side_h = _lib.side_stream()
         side.wait_event(ev_drawn)
         _lib.call("ublr_null_vectors_device", _lib.ptr(T_dev), ell, _lib.ptr(dt.nptr), _lib.ptr(dt.nidx), dt.b,
-                  _lib.ptr(Z_spec), _lib.ptr(res_spec), side_h)
+                  _lib.ptr(Z_spec), _lib.ptr(res_spec), side_h, on=side)
         ev_nv = torch.cuda.Event()
         ev_nv.record(side)
         _lib.current_stream().wait_event(ev_nv)
