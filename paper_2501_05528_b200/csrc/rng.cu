@@ -43,6 +43,14 @@ __device__ __forceinline__ void load_tables(Tables* t) {
   }
 }
 
+// Out-of-line Philox word for the rare reads past a window and the serial
+// fallback: inlined, every ziggurat token site carried its own copy of the
+// ten unrolled rounds and the per-CTA decode kernel outgrew the instruction
+// cache (ncu: "no instructions" was the top stall of k_rng_cta).
+__device__ __noinline__ uint64_t philox_word_ool(uint64_t k0, uint64_t k1, uint64_t w) {
+  return rng::philox_word(k0, k1, w);
+}
+
 template <int CC>
 struct WindowWords {
   static constexpr int WIN = CC + 16;
@@ -50,7 +58,7 @@ struct WindowWords {
   int64_t base;  // absolute word index of rel 0
   uint64_t buf[WIN];
   __device__ void fill() {
-#pragma unroll
+#pragma unroll 1
     for (int q = 0; q < WIN / 4; ++q) {
       uint64_t o[4];
       rng::philox4x64_10(((uint64_t)base >> 2) + q + 1, k0, k1, o);
@@ -62,14 +70,14 @@ struct WindowWords {
   }
   __device__ uint64_t operator()(int64_t rel) {
     if (rel < WIN) return buf[rel];
-    return rng::philox_word(k0, k1, (uint64_t)(base + rel));
+    return philox_word_ool(k0, k1, (uint64_t)(base + rel));
   }
 };
 
 struct DirectWords {
   uint64_t k0, k1;
   int64_t base;
-  __device__ uint64_t operator()(int64_t rel) { return rng::philox_word(k0, k1, (uint64_t)(base + rel)); }
+  __device__ uint64_t operator()(int64_t rel) { return philox_word_ool(k0, k1, (uint64_t)(base + rel)); }
 };
 
 // Per-launch descriptor arrays live in the workspace.
