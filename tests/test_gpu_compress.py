@@ -214,3 +214,20 @@ def test_tagging_options_match_reference(name):
     assert np.array_equal(mv, g["matvecs"])
     if kw.get("optimize"):
         assert report.aspect_ratios["optimized"]["max"] == pytest.approx(float(g["rho_opt_max"]), rel=1e-8)
+
+
+def test_compress_on_a_side_stream_matches_default_stream():
+    """The speculative path queues the null vectors on a side stream keyed by
+    the caller's stream: a compression issued on a user stream, back to back
+    with one on the default stream, gives the same bits."""
+    tess, op, _ = gpu_problem("c2_A2")
+    _, _, k, p, mid, seed = build_case("c2_A2")
+    rep0, _ = P.compress(op, tess, k, mid, p=p, stream=P.RandomStream(seed), compute_error=False)
+    h0 = rep0.to_host()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        rep1, _ = P.compress(op, tess, k, mid, p=p, stream=P.RandomStream(seed), compute_error=False)
+        h1 = rep1.to_host()
+    torch.cuda.synchronize()
+    for key in ("U", "V", "core", "B"):
+        assert np.array_equal(h0[key], h1[key]), key
