@@ -206,6 +206,28 @@ int ublr_blr_apply(const double* U, const double* V, int64_t ld_uv, const double
                    const double* X, int64_t ld_x, int w, int adjoint, double* out, int64_t ld_o,
                    double* work, void* stream);
 
+/* K12b — exact blockwise Frobenius norms for the parity gates (BASELINE.json;
+ * the compressed form is ref/reconstruction.py:50-132). For block rows
+ * i0 <= i < i1 and every j: err2[(i-i0)*b + j] = ||A_ij - A_hat_ij||_F^2 and
+ * (a2 != NULL) a2[...] = ||A_ij||_F^2, with A_ij generated from the operator
+ * descriptor and A_hat_ij = U_i C_ij V_j^T (+ B_ij on near pairs, neighbour
+ * CSR nptr/nidx, block p at B + b_off[p]). U and core are indexed by absolute
+ * rows (a block-row shard passes shifted pointers); V holds all rows. B may
+ * be NULL (no near blocks). Effective ranks from roff; k = max rank <= 96.
+ * Deterministic (fixed-order reductions). */
+int ublr_frob_error(const ublr_op_t* op, const int32_t* off, const int32_t* nptr, const int32_t* nidx,
+                    const int64_t* b_off, int b, const int32_t* roff, int k, const double* U, const double* V,
+                    int64_t ld_uv, const double* core, int64_t ld_c, const double* B, int i0, int i1, double* err2,
+                    double* a2, void* stream);
+/* diff2[(i-i0)*b + j] = ||A_hat1_ij - A_hat2_ij||_F^2 for two compressed
+ * representations on the same tessellation (the GPU's own rounding
+ * sensitivity, sharded vs single-GPU runs); k1 + k2 <= 96. */
+int ublr_frob_diff(const int32_t* off, const int32_t* nptr, const int32_t* nidx, const int64_t* b_off, int b,
+                   const int32_t* roff1, int k1, const double* U1, const double* V1, int64_t ld1, const double* core1,
+                   int64_t ldc1, const double* B1, const int32_t* roff2, int k2, const double* U2, const double* V2,
+                   int64_t ld2, const double* core2, int64_t ldc2, const double* B2, int i0, int i1, double* diff2,
+                   void* stream);
+
 /* Batched dense fp64 building blocks (no cuBLAS / cuSOLVER), used by the
  * block-nullification null space (ref/linalg.py:72-94 at ref/bases.py:102-110)
  * and the type-B solves (ref/reconstruction.py:252-421). Row-major;

@@ -74,6 +74,9 @@ SIGNATURES = {
     "ublr_tag_combine_pairs": (INT, [P, I64, INT, INT, P, P, P, INT, INT, P, P]),
     "ublr_assemble_tagged": (INT, [P, INT, P, I64, INT, P, INT, P, I64, I64, P]),
     "ublr_blr_apply": (INT, [P, P, I64, P, I64, P, P, P, P, P, P, P, INT, P, I64, INT, INT, P, I64, P, P]),
+    "ublr_frob_error": (INT, [C.POINTER(OpDesc), P, P, P, P, INT, P, INT, P, P, I64, P, I64, P, INT, INT, P, P, P]),
+    "ublr_frob_diff": (INT, [P, P, P, P, INT, P, INT, P, P, I64, P, I64, P, P, INT, P, P, I64, P, I64, P, INT, INT, P,
+                             P]),
     "ublr_nearfield_colour": (INT, [C.POINTER(OpDesc), P, P, INT, INT, P, P, I64, P, I64, P, P, P, INT, INT,
                                     P, P, INT, P, P, P, I64, P]),
 }
@@ -120,7 +123,8 @@ LAUNCHES = {"ublr_rng_normals": 8, "ublr_sketch_tagged": 1, "ublr_sketch_tagged_
             "ublr_coupling_nearfield": 1,
             "ublr_blr_apply": 3, "ublr_gemm_batched": 1, "ublr_potrf_diag": 1, "ublr_lu_sign_diag": 1,
             "ublr_lu_sign_diag_r": 1, "ublr_syrk_upper_batched": 1, "ublr_add_scaled_rows": 1,
-            "ublr_gather": 1, "ublr_scale_rows": 1, "ublr_tag_combine_pairs": 1, "ublr_assemble_tagged": 1, "ublr_tag_aspect": 1, "ublr_null_vectors_device": 1}
+            "ublr_gather": 1, "ublr_scale_rows": 1, "ublr_tag_combine_pairs": 1, "ublr_assemble_tagged": 1, "ublr_tag_aspect": 1, "ublr_null_vectors_device": 1,
+            "ublr_frob_error": 1, "ublr_frob_diff": 1}
 launch_count = 0
 
 

@@ -95,6 +95,10 @@ class _Stager:
             s = self.slot
             self._flush(s)
             part = flat[a:a + self.n]
+            # the source may be a temporary of the caller's stream (a per-block
+            # .contiguous()): keep its memory out of the allocator's reuse
+            # until this stream's copy has read it
+            part.record_stream(self.stream)
             with torch.cuda.stream(self.stream):
                 self.buf[s][:part.numel()].copy_(part, non_blocking=True)
                 self.ev[s].record(self.stream)

@@ -119,7 +119,9 @@ def torch_allgather(group=None):
 
 
 def phase1_local(op, tess, k, p, stream, shard, plan=None):
-    """Steps 1-2 for one shard: returns (plan, U_own, V_own, dt, G, H, T_dev)."""
+    """Steps 1-2 for one shard: returns (plan, U_own, V_own, dt) — the
+    tagging plan, the shard's rows of U and V ((r1 - r0) x k each) and the
+    device tessellation."""
     torch = _torch()
     _lib.require_device()
     dt = device_tess(tess, torch.device("cuda"))

@@ -202,6 +202,88 @@ def relative_error(op, rep: UniformBLR, iterations: int = 20, stream: RandomStre
     return num / den
 
 
+@dataclass
+class FrobeniusReport:
+    """Exact blockwise Frobenius norms (ublr_frob_error / ublr_frob_diff).
+
+    `pair2[i - i0, j]` holds the squared norm of pair (i, j) for the block
+    rows i0 <= i < i1 that were evaluated; `ref2` the squared norms of the
+    minuend (||A_ij||^2 for an error report, None for a difference)."""
+    i0: int
+    i1: int
+    pair2: np.ndarray
+    ref2: np.ndarray | None
+
+    @property
+    def fro(self) -> float:
+        return float(np.sqrt(self.pair2.sum()))
+
+    @property
+    def ref_fro(self) -> float | None:
+        return None if self.ref2 is None else float(np.sqrt(self.ref2.sum()))
+
+    @property
+    def relative(self) -> float:
+        return self.fro / self.ref_fro
+
+
+def _rep_rows(rep, i0):
+    """U / core pointers of a representation, shifted for a block-row shard
+    whose arrays start at block row `i0` (rep.row0 / rep.k0)."""
+    dt = rep.dt
+    r0 = int(dt.off_h[i0]) - int(getattr(rep, "row0", 0))
+    return r0, getattr(rep, "k0", 0)
+
+
+def frobenius_error(op, rep: UniformBLR, i0: int = 0, i1: int | None = None) -> FrobeniusReport:
+    """||A - A_hat||_F blockwise and exactly, A generated on the device
+    (ublr_frob_error). The BASELINE.json approximation-error gate; the
+    reference reports a 20-step power-method spectral estimate instead
+    (ref/reconstruction.py:160-177)."""
+    torch = _torch()
+    dt = rep.dt
+    i1 = dt.b if i1 is None else i1
+    inner = unwrap(op)
+    if not hasattr(inner, "device_op"):
+        raise NotImplementedError("frobenius_error needs an operator with a device descriptor")
+    roff_h, roff = dt.roff(rep.rank)
+    rows = max(i1 - i0, 0)
+    err2 = torch.zeros((rows, dt.b), dtype=torch.float64, device=dt.device)
+    a2 = torch.zeros_like(err2)
+    row0 = int(getattr(rep, "row0", 0))
+    k0 = int(getattr(rep, "k0", 0))
+    _lib.call("ublr_frob_error", inner.device_op(dt.perm), _lib.ptr(dt.off), _lib.ptr(dt.nptr), _lib.ptr(dt.nidx),
+              _lib.ptr(dt.b_off), dt.b, _lib.ptr(roff), int(max(rep.effective_ranks.max(initial=0), 0)),
+              _lib.ptr(rep.U) - 8 * row0 * rep.U.stride(0), _lib.ptr(rep.V), rep.U.stride(0),
+              _lib.ptr(rep.core_d) - 8 * k0 * rep.core_d.stride(0), rep.core_d.stride(0),
+              _lib.ptr(rep.B_d) - 8 * int(getattr(rep, "b0", 0)), i0, i1, _lib.ptr(err2), _lib.ptr(a2),
+              _lib.stream_handle())
+    return FrobeniusReport(i0, i1, err2.cpu().numpy(), a2.cpu().numpy())
+
+
+def frobenius_distance(rep1: UniformBLR, rep2: UniformBLR, i0: int = 0, i1: int | None = None) -> FrobeniusReport:
+    """||A_hat1 - A_hat2||_F blockwise and exactly (ublr_frob_diff), for two
+    representations on the same tessellation."""
+    torch = _torch()
+    dt = rep1.dt
+    if rep2.dt.b != dt.b or not np.array_equal(rep2.dt.off_h, dt.off_h):
+        raise ValueError("frobenius_distance: representations on different tessellations")
+    i1 = dt.b if i1 is None else i1
+    _, roff1 = dt.roff(rep1.rank)
+    _, roff2 = rep2.dt.roff(rep2.rank)
+    d2 = torch.zeros((max(i1 - i0, 0), dt.b), dtype=torch.float64, device=dt.device)
+
+    def args(rep):
+        row0, k0 = int(getattr(rep, "row0", 0)), int(getattr(rep, "k0", 0))
+        return (int(max(rep.effective_ranks.max(initial=0), 0)), _lib.ptr(rep.U) - 8 * row0 * rep.U.stride(0),
+                _lib.ptr(rep.V), rep.U.stride(0), _lib.ptr(rep.core_d) - 8 * k0 * rep.core_d.stride(0),
+                rep.core_d.stride(0), _lib.ptr(rep.B_d) - 8 * int(getattr(rep, "b0", 0)))
+
+    _lib.call("ublr_frob_diff", _lib.ptr(dt.off), _lib.ptr(dt.nptr), _lib.ptr(dt.nidx), _lib.ptr(dt.b_off), dt.b,
+              _lib.ptr(roff1), *args(rep1), _lib.ptr(roff2), *args(rep2), i0, i1, _lib.ptr(d2), _lib.stream_handle())
+    return FrobeniusReport(i0, i1, d2.cpu().numpy(), None)
+
+
 # ---------------------------------------------------------------------------
 # Type A
 # ---------------------------------------------------------------------------
