@@ -1,20 +1,29 @@
 #!/usr/bin/env python
 """Benchmark: uBLR compression time on B200 (BASELINE.json metric).
 
-    python bench.py [--config c2] [--gpus N --steps K --warmup W] [--impl reference]
+    python bench.py [--config c3] [--gpus N --steps K --warmup W] [--impl reference]
 
 One step = one full compression (phases I+II+III of
-ref/reconstruction.py:498-583: tagging plan, test-matrix generation, tagged
-sketch, per-block QR, coupling, near field) of the chosen BASELINE config.
+ref/reconstruction.py:498-687) of the chosen BASELINE config. Default: c3
+(A1 on the 256 x 256 log-kernel grid, the largest configuration that fits one
+GPU) at N = 1, and c5 (A2 on the 1024 x 1024 1/r grid, block rows sharded over
+the ranks, NCCL all-gather of V) at N > 1. `--gpus N` without a torchrun
+environment starts the N ranks itself.
+
 `value` = compression time in seconds with the operator's inputs resident in
 HBM (device-timed, max over ranks); `e2e` = the same through the public API
-from HOST arrays (operator built from host coordinates / matrix inside the
-timed region, compressed representation copied back to host).
+from HOST arrays (device layout and operator rebuilt from host coordinates /
+matrix inside the timed region, compressed representation copied back to
+pinned host memory).
 
 Configs 1-4 do not shard: with --gpus N every rank compresses its own replica
 ("replicas only"). `--impl reference` times the CPU port of the
-reference algorithm (oracle/, numpy + OpenBLAS on all host cores).
+reference algorithm (oracle/, numpy + OpenBLAS on all host cores): full
+compressions for c1/c2, and for c3-c5 (15-40 min on the host, or infeasible)
+a phase-by-phase sampled estimate of one full compression (oracle/sampled.py),
+labelled as such in the line.
 """
+
 
 from __future__ import annotations
 
@@ -121,65 +130,123 @@ def flush_l2(buf):
     buf.add_(1.0)  # 256 MB write > 126 MB L2
 
 
-def run_reference(args, rank, world):
-    """CPU baseline: the oracle port of the reference pipeline on host cores."""
+def free_port() -> int:
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch(n):
+    """`--gpus N` without a torchrun environment: start N ranks (one per GPU)
+    with torch.distributed.run on this node and return its exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def bench_config(wl, world, name, shards=None):
+    """The `config` object of both arms (identical for the same workload)."""
+    cfg = dict(wl.describe())
+    if name == "c5":
+        S = shards or world
+        cfg["parallelism"] = f"block-row shards x{S}" + ("" if world == S else f" (one rank's share on {world} GPU)")
+    else:
+        cfg["parallelism"] = "single" if world == 1 else f"replicas x{world}"
+    return cfg
+
+
+def _oracle_operator(wl):
+    import oracle as O
+    if wl.kernel == "dense-synthetic":
+        return O.Dense(wl.matrix)
+    kind = "log" if wl.kernel.startswith("-log") else "inv"
+    per = round(wl.n ** 0.5)
+    diag = -np.log(0.5 / per) if kind == "log" else 2.0 * per
+    return O.Dense(O.kernel_block(wl.points.coords, np.arange(wl.n), np.arange(wl.n), kind, diag))
+
+
+def _sampled_estimate(wl):
+    """oracle/sampled.py: phase-by-phase sampled timing of the oracle port at
+    the full size of this workload (c3-c5)."""
+    import oracle as O
+    from oracle.sampled import estimate
+    kind = "log" if wl.kernel.startswith("-log") else "inv"
+    per = round(wl.n ** 0.5)
+    diag = -np.log(0.5 / per) if kind == "log" else 2.0 * per
+    bx = O.partition(wl.points.coords, wl.b)
+    return estimate(wl.name, wl.points.coords, bx, wl.k, wl.p, wl.method, kind, diag)
+
+
+def _cpu_line(wl, steps, warmup):
+    """Times of the CPU port of the reference pipeline on this workload:
+    full oracle compressions for c1/c2 (dense operator prebuilt), a sampled
+    phase-by-phase estimate of one full compression for c3-c5."""
+    import oracle as O
+    cores = os.cpu_count() or 1
+    if wl.n <= 8192:
+        op = _oracle_operator(wl)
+        bx = O.partition(wl.points.coords, wl.b)
+        for _ in range(warmup):
+            O.compress(op, bx, wl.k, wl.method, p=wl.p, stream=O.Stream(7), compute_error=False)
+        times = []
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            O.compress(op, bx, wl.k, wl.method, p=wl.p, stream=O.Stream(7), compute_error=False)
+            times.append(time.perf_counter() - t0)
+        return times, {"kind": "port", "cores": cores,
+                       "sample": f"full {wl.name} compressions with the oracle numpy port (dense operator prebuilt, "
+                                 f"OpenBLAS on all {cores} host threads)"}, None
+    for _ in range(warmup):
+        _sampled_estimate(wl)
+    ests = [_sampled_estimate(wl) for _ in range(steps)]
+    return [e.seconds for e in ests], {"kind": "port", "cores": cores, "sample": ests[-1].describe(),
+                                       "extrapolated": True}, ests[-1].table()
+
+
+def run_reference(args, rank, world, cfgname):
+    """The reference arm: the CPU port of the reference pipeline (oracle/,
+    numpy + OpenBLAS) on the host cores, rank 0 only."""
     if rank != 0:
         return
-    import oracle as O
     from paper_2501_05528_b200 import workloads as W
-    wl = W.build(args.config, device_ops=False)
-    cores = os.cpu_count() or 1
-    bx = O.partition(wl.points.coords, wl.b)
-    if wl.kernel == "dense-synthetic":
-        op = O.Dense(wl.matrix)
-    elif wl.n <= 8192:
-        kind = "log" if wl.kernel.startswith("-log") else "inv"
-        diag = -np.log(0.5 / round(wl.n ** 0.5)) if kind == "log" else 2.0 * round(wl.n ** 0.5)
-        op = O.Dense(O.kernel_block(wl.points.coords, np.arange(wl.n), np.arange(wl.n), kind, diag))
-    else:
-        raise SystemExit(json.dumps({"impl": "reference", "unavailable":
-                                     f"CPU port of {args.config} exceeds the bench time budget (see DESIGN.md)"}))
-    times = []
-    for _ in range(args.warmup):
-        O.compress(op, bx, wl.k, wl.method, p=wl.p, stream=O.Stream(7), compute_error=False)
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        O.compress(op, bx, wl.k, wl.method, p=wl.p, stream=O.Stream(7), compute_error=False)
-        times.append(time.perf_counter() - t0)
-    v = float(np.mean(times))
-    print(json.dumps({
+    wl = W.build(cfgname, device_ops=False)
+    times, info, stages = _cpu_line(wl, args.steps, args.warmup)
+    v = float(np.median(times))
+    line = {
         "metric": METRIC, "value": v, "unit": "s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic", "impl": "reference",
-        "config": {**wl.describe(), "parallelism": "cpu", "replicas": 1},
-        "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "port",
-                         "sample": f"full {args.config} compression (oracle/ numpy port, OpenBLAS threads={cores})"},
+        "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "strong" if cfgname == "c5" else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": bench_config(wl, world, cfgname, args.shards if (cfgname == "c5" and world == 1) else None),
+        "cpu_baseline": {"value": v, "unit": "s", **info},
         "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }))
+        "step_s": [float(t) for t in times],
+    }
+    if cfgname == "c5" and world == 1:
+        line["value"] = line["cpu_baseline"]["value"] = line["e2e"]["value"] = v / args.shards
+        line["cpu_baseline"]["sample"] += f"; divided by {args.shards} (one rank's share, as the b200 arm)"
+    if stages is not None:
+        line["stages"] = stages
+    print(json.dumps(line))
 
 
-def cpu_baseline(wl, budget_s=12.0):
-    """Bounded CPU sample of the same workload with the oracle port."""
-    import oracle as O
-    bx = O.partition(wl.points.coords, wl.b)
-    if wl.kernel == "dense-synthetic":
-        op = O.Dense(wl.matrix)
-    else:
-        kind = "log" if wl.kernel.startswith("-log") else "inv"
-        per = round(wl.n ** 0.5)
-        diag = -np.log(0.5 / per) if kind == "log" else 2.0 * per
-        if wl.n > 8192:
-            return None
-        op = O.Dense(O.kernel_block(wl.points.coords, np.arange(wl.n), np.arange(wl.n), kind, diag))
-    times = []
-    t_end = time.perf_counter() + budget_s
-    while time.perf_counter() < t_end or len(times) < 2:
-        t0 = time.perf_counter()
-        O.compress(op, bx, wl.k, wl.method, p=wl.p, stream=O.Stream(7), compute_error=False)
-        times.append(time.perf_counter() - t0)
-    return {"value": float(np.median(times)), "unit": "s", "cores": os.cpu_count() or 1, "kind": "port",
-            "sample": f"{len(times)} full {wl.name} compressions with the oracle numpy port "
-                      f"(dense operator prebuilt, OpenBLAS on all cores)"}
+def cpu_baseline(wl, shards=1):
+    """Bounded CPU sample of the same workload with the oracle port (rank 0,
+    N=1): ~12 s of full compressions for c1/c2, one sampled estimate for
+    c3-c5."""
+    if wl.n <= 8192:
+        t_end = time.perf_counter() + 12.0
+        times, info = [], None
+        while time.perf_counter() < t_end or len(times) < 2:
+            t, info, _ = _cpu_line(wl, 1, 0)
+            times += t
+        return {"value": float(np.median(times)), "unit": "s", **info,
+                "sample": f"{len(times)} " + info["sample"]}
+    times, info, stages = _cpu_line(wl, 1, 0)
+    out = {"value": float(times[0]) / shards, "unit": "s", **info, "stages": stages}
+    if shards > 1:
+        out["sample"] += f"; divided by {shards} (one rank's share)"
+    return out
 
 
 KERNEL_OF = {"ublr_sketch_tagged_pair": "k_sketch_tagged{v} (Kronecker-restructured tagged sketch, TMEM tag groups)",
@@ -214,10 +281,20 @@ def roofline_of(ev, work, config, operator):
     n_launch = len(ev[name])
     return {"kernel": kernel_label(name, operator), "entry": name, "bound": "fp64", "achieved": achieved,
             "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
-            "peak_source": "measured DMMA m8n8k4 burst (profiles/fp64_peak_r01.txt); MEASURED_PEAKS.json has no "
+            "peak_source": "measured DMMA m8n8k4 burst (profiles/fp64_peak_r02.txt); MEASURED_PEAKS.json has no "
                            "fp64 entry",
             "algorithmic_flops_per_launch": work[name] / n_launch, "avg_launch_ms": t_ms / n_launch,
             "launches_timed": n_launch}
+
+
+def _max_over_ranks(x, world, dev):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 def run_sharded(args, rank, world, local):
@@ -230,38 +307,30 @@ def run_sharded(args, rank, world, local):
     import paper_2501_05528_b200 as P
     from paper_2501_05528_b200 import _lib
     from paper_2501_05528_b200 import workloads as W
-    from paper_2501_05528_b200.distributed import (phase1_local, phase23_local, shard_ranges, torch_allgather)
+    from paper_2501_05528_b200.distributed import compress_sharded, phase1_local, shard_ranges
     from paper_2501_05528_b200.tagging import plan_tagging
 
-    wl = W.build(args.config)
+    wl = W.build("c5")
     dev = torch.device("cuda", local)
     emulate = world == 1
     S = args.shards if emulate else world
     me = args.shard_rank if emulate else rank
     shards = shard_ranges(wl.tess, S, wl.k)
-    stream = P.RandomStream(W.COMPRESS_SEED)
     other_V = None
     if emulate:   # V rows of the other shards, untimed
+        stream = P.RandomStream(W.COMPRESS_SEED)
         plan0 = plan_tagging(wl.tess, 0, "gaussian", stream.child(1), device=True)
-        parts = []
+        other_V = []
         for sh in shards:
-            if sh.rank == me:
-                parts.append(None)
-                continue
-            _, _, V, _ = phase1_local(wl.op, wl.tess, wl.k, wl.p, stream, sh, plan0)
-            parts.append(V)
-        other_V = parts
+            other_V.append(None if sh.rank == me else phase1_local(wl.op, wl.tess, wl.k, wl.p, stream, sh, plan0)[2])
         torch.cuda.synchronize()
 
-    def step():
-        sh = shards[me]
-        plan, U, V, dt = phase1_local(wl.op, wl.tess, wl.k, wl.p, stream, sh)
-        if emulate:
-            V_all = torch.cat([V if p_ is None else p_ for p_ in other_V], 0)
-        else:
-            V_all = torch_allgather()(V, dt.n)
-        core, B = phase23_local(wl.op, wl.k, sh, dt, U, V_all)
-        return core, B
+    def gather_emulated(V, n):
+        return torch.cat([V if p_ is None else p_ for p_ in other_V], 0)
+
+    def step(op=None):
+        return compress_sharded(op or wl.op, wl.tess, wl.k, wl.p, P.RandomStream(W.COMPRESS_SEED), rank=me,
+                                world=S, allgather=gather_emulated if emulate else None)
 
     for _ in range(args.warmup):
         step()
@@ -278,75 +347,70 @@ def run_sharded(args, rank, world, local):
                 dist.barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            core, B = step()
+            res = step()
             e1.record()
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1) / 1e3)
+            res = None
     ev = _lib.event_times()
     _lib.instrument(False)
     launches = (_lib.launch_count - launches0) // args.steps
-    t = float(np.mean(times))
-    if world > 1:
-        tt = torch.tensor([t], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t = float(tt.item())
-    roof = roofline_of(ev, _lib.work, args.config, wl.describe().get("operator", ""))
+    t = _max_over_ranks(float(np.mean(times)), world, dev)
+    roof = roofline_of(ev, _lib.work, "c5", wl.describe().get("operator", ""))
+
+    # e2e: operator from host coordinates (H2D), the rank's result to pinned host memory (D2H)
     sh = shards[me]
-    rows = sh.r1 - sh.r0
+    e2e_times, h2d, d2h = [], 0, 0
+    host = None
+    for it in range(3):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        wl.tess._device.clear()
+        op = P.KernelOperator(wl.points, wl.op.kind, wl.op.diag)
+        h2d = wl.points.coords.nbytes
+        res = step(op)
+        parts = (res.U, res.core, res.B)
+        if host is None:
+            host = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in parts]
+        for h, x in zip(host, parts):
+            h.copy_(x, non_blocking=True)
+        torch.cuda.synchronize()
+        d2h = sum(x.numel() * 8 for x in parts)
+        res = parts = None
+        if it > 0:
+            e2e_times.append(time.perf_counter() - t0)
+    e2e = _max_over_ranks(float(np.median(e2e_times)), world, dev)
     if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(W.build("c5", device_ops=False), shards=S)
         print(json.dumps({
             "metric": METRIC, "value": t, "unit": "s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t * 1e3, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {**wl.describe(), "parallelism": f"block-row shards x{S}",
-                       "measured": ("one rank's share of a %d-way sharded job on 1 GPU (all-gather emulated)" % S)
-                       if emulate else "all ranks, NCCL all-gather of V",
-                       "shard_rank": me, "rows_per_shard": rows},
+            "config": bench_config(wl, world, "c5", S if emulate else None),
+            "measured": ("one rank's share of a %d-way sharded job on 1 GPU (all-gather emulated)" % S)
+            if emulate else "all ranks, NCCL all-gather of V; max over ranks",
+            "shard_rank": me, "rows_per_shard": sh.r1 - sh.r0,
+            "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(launches),
             "roofline": roof,
             "kernel_ms_per_step": {k_: float(np.sum(v)) / args.steps for k_, v in ev.items()},
-            "clocks": clocks.summary(), "cpu_baseline": None,
+            "clocks": clocks.summary(), "cpu_baseline": cpu,
         }))
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=None, help="timed steps (default: 30 for c1/c2, 5 for c3-c5)")
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--shards", type=int, default=8, help="c5 on one GPU: shard count to emulate")
-    ap.add_argument("--shard-rank", type=int, default=3, help="c5 on one GPU: which shard to time")
-    args = ap.parse_args()
-    args.warmup = max(args.warmup, 3)
-    if args.steps is None:
-        args.steps = 30 if args.config in ("c1", "c2") else 5
-    rank, world, local = dist_env()
-
-    if args.impl == "reference":
-        run_reference(args, rank, world)
-        return
-
+def run_single(args, rank, world, local, cfgname):
     import torch
     import torch.distributed as dist
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
-    if args.config == "c5":
-        run_sharded(args, rank, world, local)
-        if world > 1:
-            dist.destroy_process_group()
-        return
 
     import paper_2501_05528_b200 as P
     from paper_2501_05528_b200 import _lib
     from paper_2501_05528_b200 import workloads as W
 
-    wl = W.build(args.config)
-    flops = W.algorithmic_flops(wl)
+    wl = W.build(cfgname)
     dev = torch.device("cuda", local)
     l2buf = torch.zeros(32 * 1024 * 1024, dtype=torch.float64, device=dev)
 
@@ -374,9 +438,9 @@ def main():
     launches0 = _lib.launch_count
     step_ms = []
     gc.collect()
-    if args.config in ("c1", "c2"):
-        gc.disable()   # no collector pauses inside millisecond steps (re-enabled below); c3/c4 steps
-                       # allocate tens of GB, so the collector stays on there
+    small = wl.n <= 8192
+    if small:
+        gc.disable()   # no collector pauses inside millisecond steps
     with ClockSampler(local) as clocks:
         for _ in range(args.steps):
             flush_l2(l2buf)
@@ -392,21 +456,19 @@ def main():
     ev = _lib.event_times()
     _lib.instrument(False)
     launches = (_lib.launch_count - launches0) // args.steps
-    t_step = float(np.mean(step_ms)) / 1e3
-    if world > 1:
-        t = torch.tensor([t_step], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_step = float(t.item())
+    t_step = _max_over_ranks(float(np.mean(step_ms)) / 1e3, world, dev)
 
     # --- e2e: host buffers through the public API --------------------------
+    # every iteration starts from the host: a fresh device layout of the
+    # tessellation, the operator from host coordinates / matrix (H2D), and
+    # the compressed representation copied back to pinned host memory (D2H)
     e2e_times = []
     h2d = d2h = 0
-    host = None
     for it in range(max(3, args.steps // 2) + 1):   # first pass untimed (pinned staging warm-up)
-        host = None
         flush_l2(l2buf)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
+        wl.tess._device.clear()
         if wl.matrix is not None:
             op = P.DenseOperator(wl.matrix)                       # H2D of A
             h2d = wl.matrix.nbytes
@@ -419,37 +481,75 @@ def main():
         if it > 0:
             e2e_times.append(time.perf_counter() - t0)
         d2h = sum(x.nbytes for x in host.values())
-    e2e = float(np.median(e2e_times))
-    if world > 1:
-        t = torch.tensor([e2e], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e = float(t.item())
+        rep = report = host = None
+    e2e = _max_over_ranks(float(np.median(e2e_times)), world, dev)
 
-    # --- roofline of the dominant kernel -------------------------------------
-    roof = roofline_of(ev, _lib.work, args.config, wl.describe().get("operator", ""))
+    roof = roofline_of(ev, _lib.work, cfgname, wl.describe().get("operator", ""))
     kernel_ms = {k: float(np.sum(v)) for k, v in ev0.items()}   # one untimed instrumented step
-
     if rank == 0:
-        cpu = None if (args.no_cpu_baseline or world > 1) else cpu_baseline(W.build(args.config, device_ops=False))
+        cpu = None if (args.no_cpu_baseline or world > 1) else cpu_baseline(W.build(cfgname, device_ops=False))
         line = {
             "metric": METRIC, "value": t_step, "unit": "s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {**wl.describe(), "parallelism": f"replicas{world}" if world > 1 else "single",
-                       "l2": "flushed between timed steps (256 MB write)", "python_gc": "disabled in the timed loop"},
+            "config": bench_config(wl, world, cfgname),
+            "timing": {"l2": "flushed between timed steps (256 MB write)",
+                       "python_gc": "disabled in the timed loop" if small else "enabled (steps allocate GBs)",
+                       "e2e_layout": "device tessellation layout rebuilt from host arrays every e2e step"},
             "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(launches),
             "roofline": roof,
             "kernel_ms_per_step": kernel_ms,
             "step_ms": {"min": float(np.min(step_ms)), "median": float(np.median(step_ms)),
                         "max": float(np.max(step_ms))},
-            "phase_s": dict(report.times_s),
+            "phase_s": dict(P.compress(wl.op, wl.tess, wl.k, wl.method, p=wl.p,
+                                       stream=P.RandomStream(W.COMPRESS_SEED), compute_error=False)[1].times_s),
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,
         }
         print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=None, help="timed steps (default: 30 for c1/c2, 5 for c3-c5)")
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default=None, choices=["c1", "c2", "c3", "c4", "c5"],
+                    help="default: c3 (the largest single-GPU config) on 1 GPU, c5 (block-row sharded) on N > 1")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shards", type=int, default=8, help="c5 on one GPU: shard count to emulate")
+    ap.add_argument("--shard-rank", type=int, default=3, help="c5 on one GPU: which shard to time")
+    args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args.gpus))
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch with torchrun --nproc-per-node "
+                         f"{args.gpus}, or without torchrun to let bench.py start the ranks")
+    args.warmup = max(args.warmup, 3)
+    cfgname = args.config or ("c3" if world == 1 else "c5")
+    if args.steps is None:
+        args.steps = 30 if cfgname in ("c1", "c2") else 5
+
+    if args.impl == "reference":
+        run_reference(args, rank, world, cfgname)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
     if world > 1:
-        dist.destroy_process_group()
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    try:
+        if cfgname == "c5":
+            run_sharded(args, rank, world, local)
+        else:
+            run_single(args, rank, world, local, cfgname)
+    finally:
+        if world > 1:
+            dist.destroy_process_group()
 
 
 if __name__ == "__main__":

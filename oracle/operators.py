@@ -54,6 +54,12 @@ def kernel_block(coords, rows, cols, kind, diag):
     return out
 
 
+def blas_threads(n):
+    """Context manager limiting the BLAS thread pool to n threads."""
+    from threadpoolctl import threadpool_limits
+    return threadpool_limits(limits=n, user_api="blas")
+
+
 class KernelOp:
     """Symmetric kernel matrix applied in row chunks on a thread pool."""
 
@@ -76,7 +82,9 @@ class KernelOp:
         n = self.shape[0]
         out = np.empty((n, X.shape[1]))
         spans = [(lo, min(lo + self.chunk, n)) for lo in range(0, n, self.chunk)]
-        with ThreadPoolExecutor(self.threads) as ex:
+        # one BLAS thread per chunk worker: the pool already occupies every
+        # core (nested BLAS threading would oversubscribe them)
+        with blas_threads(1), ThreadPoolExecutor(self.threads) as ex:
             for (lo, hi), res in zip(spans, ex.map(lambda s: self._rows(s[0], s[1], X), spans)):
                 out[lo:hi] = res
         return out

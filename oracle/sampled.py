@@ -35,7 +35,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .operators import KernelOp
+from .operators import KernelOp, blas_threads, kernel_block
 from .ublr_oracle import (
     Stream, _basis, _combine, _perp, _tagged_matrix, bn_width, colour_boxes, leading_q, normals, null_tail,
     pair_vector, plan_tags, svd_pinv,
@@ -85,18 +85,30 @@ def _tic():
     return time.perf_counter()
 
 
-def _apply_sample(op: KernelOp, X, waves=1):
+def _apply_sample(op: KernelOp, X, waves=1, col_scale=1.0):
     """Time `waves` rounds of op.threads row chunks of op.apply(X) on the
     adapter's thread pool (the chunks a full apply runs, spread over the
-    matrix). Returns (seconds, chunks timed, chunks in a full apply)."""
+    matrix). Returns (seconds, chunks timed, chunks in a full apply).
+
+    With col_scale != 1, X holds a column sample of the full right-hand side:
+    the kernel evaluation of the chunks (independent of the width) is timed
+    on its own and only the remainder (the GEMM, linear in the width) is
+    scaled: t = t_eval + (t_chunk - t_eval) * col_scale."""
     n = op.shape[0]
     total = -(-n // op.chunk)
     count = min(total, op.threads * waves)
     starts = [((c * total) // count) * op.chunk for c in range(count)]
-    with ThreadPoolExecutor(op.threads) as ex:
+    with blas_threads(1), ThreadPoolExecutor(op.threads) as ex:
         t0 = _tic()
         list(ex.map(lambda lo: op._rows(lo, min(lo + op.chunk, n), X), starts))
         dt = _tic() - t0
+        if col_scale != 1.0:
+            cols = np.arange(n)
+            t0 = _tic()
+            list(ex.map(lambda lo: kernel_block(op.coords, np.arange(lo, min(lo + op.chunk, n)), cols, op.kind,
+                                                op.diag), starts))
+            t_eval = _tic() - t0
+            dt = t_eval + max(dt - t_eval, 0.0) * col_scale
     return dt, count, total
 
 
@@ -108,7 +120,7 @@ def _blocks_by_nbr_size(bx):
     return out
 
 
-def estimate_a1(op: KernelOp, bx, k, p, label="c3", row_frac=16, blocks_per_size=1):
+def estimate_a1(op: KernelOp, bx, k, p, label="c3", row_frac=16, blocks_per_size=1, col_blocks=32):
     """compress_type_a(method="bn") (ref/reconstruction.py:498-583 with
     ref/bases.py:86-123, :185-244) at full size, sampled."""
     wall0 = _tic()
@@ -133,35 +145,37 @@ def estimate_a1(op: KernelOp, bx, k, p, label="c3", row_frac=16, blocks_per_size
     rng = np.random.default_rng(5)
     for nsz, members in sorted(_blocks_by_nbr_size(bx).items()):
         for i in members[:blocks_per_size]:
-            nr = bx.nbr_rows(i)
+            Om_nbr = rng.standard_normal((bx.nbr_count(i), s))   # Omega[nbr(i)]
             Y_i = rng.standard_normal((len(bx.blocks[i]), s))
             t0 = _tic()
-            P_ = null_tail(Om[nr], r)
+            P_ = null_tail(Om_nbr, r)
             _basis(Y_i @ P_, k)
             est.add(f"I: null_basis + Y_i P + col_basis, |nbr| = {nsz}", _tic() - t0,
                     min(blocks_per_size, len(members)), 2 * len(members))
     del Om
-    # phase II: direct_core = U^T (A V_dense), V_dense built as the reference does
+    # phase II: direct_core = U^T (A V_dense), V_dense built as the reference
+    # does (zeros + block writes), on the columns of `col_blocks` blocks
     ranks = np.minimum(k, bx.sizes)
     off = np.concatenate(([0], np.cumsum(ranks)))
     K = int(off[-1])
     Vb = [leading_q(rng.standard_normal((len(bx.blocks[j]), k)), k) for j in range(bx.b)]
+    cb = min(col_blocks, bx.b)
+    Kc = int(off[cb])
     t0 = _tic()
-    Vd = np.zeros((n, K))
-    for j, rows_j in enumerate(bx.blocks):
-        Vd[rows_j, off[j]:off[j + 1]] = Vb[j]
-    est.add("II: block-diagonal V (N x K)", _tic() - t0, 1, 1)
-    dt, c, tot = _apply_sample(op, Vd)
-    est.add("II: A V_dense (row chunks)", dt, c, tot)
-    AV = np.full((n, K), 0.5)
+    Vd = np.zeros((n, Kc))
+    for j in range(cb):
+        Vd[bx.blocks[j], off[j]:off[j + 1]] = Vb[j]
+    est.add("II: block-diagonal V (N x K, column sample)", _tic() - t0, cb, bx.b)
+    dt, c, tot = _apply_sample(op, Vd, col_scale=bx.b / cb)
+    est.add(f"II: A V_dense (row chunks; GEMM on {cb} of {bx.b} column blocks, scaled)", dt, c, tot)
+    AV = np.full((n, Kc), 0.5)
     t0 = _tic()
     nb = min(16, bx.b)
-    C = np.empty((K, K))
     for i in range(nb):
-        C[off[i]:off[i + 1]] = Vb[i].T @ AV[bx.blocks[i]]
-    est.add("II: U_i^T (A V)[rows_i]", _tic() - t0, nb, bx.b)
+        Vb[i].T @ AV[bx.blocks[i]]
+    est.add("II: U_i^T (A V)[rows_i] (column sample)", _tic() - t0, nb * cb, bx.b * bx.b)
     del AV, Vd
-    C[:] = 0.5
+    C = np.full((K, K), 0.5)
     # phase III: one colour probe of the nine (ref/reconstruction.py:227-243)
     colours = colour_boxes(bx)
     ncol = int(colours.max()) + 1
@@ -281,6 +295,105 @@ def estimate_b2(op: KernelOp, bx, k, p, label="c4", row_frac=16, block_frac=16, 
     return est
 
 
+def estimate_a2(op: KernelOp, bx, k, p, label="c5", block_frac=64, col_blocks=32, attempts=None):
+    """compress_type_a(method="tag") (ref/reconstruction.py:498-583 with
+    ref/tagging.py:306-379, ref/bases.py:140-210, ref/reconstruction.py:185-244)
+    at full size, sampled. Config 5 is infeasible on a CPU (phase II pushes a
+    1.6 TB block-diagonal V through A; the dense core is 309 GB), so phases II
+    and III are additionally sampled by COLUMN blocks: the applies and the
+    core products are timed against the columns of `col_blocks` blocks and
+    scaled by b / col_blocks (their cost is linear in the column count)."""
+    wall0 = _tic()
+    est = Estimate(label, "A2", op.threads)
+    n, b = bx.n, bx.b
+    gc = k + p
+    stream = Stream(7)
+    rng = np.random.default_rng(5)
+    sample = list(range(0, b, block_frac))
+    # plan: ref/tagging.py:355-379 per block, `attempts` draws (6 at c5, SURVEY F8)
+    if attempts is None:
+        attempts = plan_tags(bx, stream.child(1)).attempts if b <= 1024 else 6
+    T = normals(b, 3 ** bx.dim + 1, stream.child(1).child(0))
+    t0 = _tic()
+    for i in sample:
+        z = null_tail(T[bx.nbrs[i], :], 1)[:, 0]
+        far = bx.far(i)
+        mags = np.abs((T @ z)[far])
+        mags.max() / mags.min()
+    est.add(f"I: tagging plan ({attempts} draws), null vectors + aspect ratios", _tic() - t0, len(sample),
+            attempts * b)
+    # test blocks and the tagged test matrices
+    t0 = _tic()
+    G = [normals(len(bx.blocks[i]), gc, stream.child(0).child(0, i)) for i in sample]
+    est.add("I: gaussian G_i, H_i", _tic() - t0, len(sample), 2 * b)
+    Gs = {i: g for i, g in zip(sample, G)}
+    G_all = [Gs.get(i, G[0]) if len(bx.blocks[i]) == len(G[0]) else rng.standard_normal((len(bx.blocks[i]), gc))
+             for i in range(b)]
+    t0 = _tic()
+    omega = _tagged_matrix(bx, T, G_all, gc)
+    est.add("I: tagged Omega, Psi (N x ell gc)", _tic() - t0, 1, 2)
+    dt, c, tot = _apply_sample(op, omega)
+    est.add("I: Y = A Omega, Z = A* Psi (row chunks)", dt, c, 2 * tot)
+    y = omega
+    t0 = _tic()
+    for i in sample:
+        _basis(_combine(y[bx.blocks[i]], T[i] / np.linalg.norm(T[i]), gc), k)
+    est.add("I: combine + col_basis", _tic() - t0, len(sample), 2 * b)
+    del omega, y
+    # phase II: U^T (A V_dense) on the columns of col_blocks blocks
+    ranks = np.minimum(k, bx.sizes)
+    cb = list(range(min(col_blocks, b)))
+    Kc = int(ranks[cb].sum())
+    Vb = leading_q(rng.standard_normal((bx.m_max, k)), k)
+    t0 = _tic()
+    Vd = np.zeros((n, Kc))
+    at = 0
+    for j in cb:
+        Vd[bx.blocks[j], at:at + ranks[j]] = Vb[:len(bx.blocks[j]), :ranks[j]]
+        at += ranks[j]
+    est.add("II: block-diagonal V (column sample)", _tic() - t0, len(cb), b)
+    dt, c, tot = _apply_sample(op, Vd, col_scale=b / len(cb))
+    est.add(f"II: A V_dense (row chunks; GEMM on {len(cb)} of {b} column blocks, scaled)", dt, c, tot)
+    AV = np.full((n, Kc), 0.5)
+    t0 = _tic()
+    for i in sample:
+        Vb[:len(bx.blocks[i])].T @ AV[bx.blocks[i]]
+    est.add("II: U_i^T (A V)[rows_i] (column sample)", _tic() - t0, len(sample) * len(cb), b * b)
+    del AV, Vd
+    # phase III: one colour probe of the nine
+    colours = colour_boxes(bx)
+    ncol = int(colours.max()) + 1
+    members = np.flatnonzero(colours == 0)
+    mc = int(bx.sizes[members].max())
+    t0 = _tic()
+    probe = np.zeros((n, mc))
+    for j in members:
+        probe[bx.blocks[j], :bx.sizes[j]] = np.eye(bx.sizes[j])
+    t_build = _tic() - t0
+    dt, c, tot = _apply_sample(op, probe)
+    est.add("III: A probe_c (row chunks), 9 colours", dt, c, tot * ncol)
+    K = int(ranks.sum())
+    t0 = _tic()
+    VtP = np.empty((K, mc))
+    off = np.concatenate(([0], np.cumsum(ranks)))
+    for j, rows_j in enumerate(bx.blocks):
+        VtP[off[j]:off[j + 1]] = Vb[:len(rows_j), :ranks[j]].T @ probe[rows_j]
+    est.add("III: probe build + V^T probe", _tic() - t0 + t_build, 1, ncol)
+    # C @ VtP (K x K x m_c) on the rows of the column-sample blocks, then the
+    # per-block subtraction and cut-out on the sampled rows
+    Cr = np.full((Kc, K), 0.5)
+    R = np.full((n, mc), 0.5)
+    t0 = _tic()
+    CV = Cr @ VtP
+    at = 0
+    for i in cb:
+        R[bx.blocks[i]] -= Vb[:len(bx.blocks[i]), :ranks[i]] @ CV[at:at + ranks[i]]
+        at += ranks[i]
+    est.add("III: C V^T probe + subtract (row sample)", _tic() - t0, len(cb), b * ncol)
+    est.wall = _tic() - wall0
+    return est
+
+
 def estimate(config: str, coords, bx, k, p, method, kind, diag, threads=None):
     threads = threads or os.cpu_count() or 1
     op = KernelOp(coords, kind, diag, chunk=256, threads=threads)
@@ -288,4 +401,6 @@ def estimate(config: str, coords, bx, k, p, method, kind, diag, threads=None):
         return estimate_a1(op, bx, k, p, label=config)
     if method == "B2":
         return estimate_b2(op, bx, k, p, label=config)
+    if method == "A2":
+        return estimate_a2(op, bx, k, p, label=config)
     raise ValueError(f"no sampled estimate for method {method}")

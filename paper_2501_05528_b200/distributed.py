@@ -87,6 +87,16 @@ class ShardResult:
     plan: object
     ledger: dict
 
+    def rep_view(self, dt, k):
+        """The shard's part of the compressed representation in the shape
+        reconstruction.frobenius_error / frobenius_distance read: U and core
+        hold this shard's rows (row0 / k0 shifts), V all rows, B this shard's
+        near pairs (b0 shift)."""
+        from types import SimpleNamespace
+        return SimpleNamespace(dt=dt, rank=k, effective_ranks=dt.ranks(k).astype(np.int64), U=self.U, V=self.V,
+                               core_d=self.core, B_d=self.B, row0=self.shard.r0, k0=self.shard.K0,
+                               b0=int(dt.b_off_h[self.shard.p0]))
+
 
 def torch_allgather(group=None):
     """All-gather of equal-size row shards through torch.distributed."""
@@ -118,10 +128,11 @@ def torch_allgather(group=None):
     return gather
 
 
-def phase1_local(op, tess, k, p, stream, shard, plan=None):
+def phase1_local(op, tess, k, p, stream, shard, plan=None, keep_sketch=False):
     """Steps 1-2 for one shard: returns (plan, U_own, V_own, dt) — the
     tagging plan, the shard's rows of U and V ((r1 - r0) x k each) and the
-    device tessellation."""
+    device tessellation; with keep_sketch also the shard's rows of the
+    sketches Y, Z ((r1 - r0) x ell (k + p), for the parity tests)."""
     torch = _torch()
     _lib.require_device()
     dt = device_tess(tess, torch.device("cuda"))
@@ -154,6 +165,8 @@ def phase1_local(op, tess, k, p, stream, shard, plan=None):
     _lib.call("ublr_block_qr_pair", _lib.ptr(Y) - shift, _lib.ptr(Z) - shift, s, _lib.ptr(Z_dev) + 8 * shard.i0 * ell,
               ell, gc, _lib.ptr(dt.off) + 4 * shard.i0, shard.i1 - shard.i0, kq, _lib.ptr(U) - ushift,
               _lib.ptr(V) - ushift, k, st, dt.m_max)
+    if keep_sketch:
+        return plan, U, V, dt, Y, Z
     del Y, Z
     return plan, U, V, dt
 

@@ -1,0 +1,170 @@
+"""Config 5 (N = 1,048,576, b = 4096, m = 256, k = 48, p = 16, 1/|x-y|, A2)
+block-row spot checks against the CPU oracle on identical inputs
+(the full reference is infeasible at this size).
+
+The compression runs sharded 8 ways as on the 8-GPU box (all eight phase-I
+shards, then phases II-III for the two shards on either side of the 3 | 4
+boundary, on one GPU). For 8 block rows — four on each side of the boundary,
+whose near fields reach into the other shard — the oracle recomputes with the
+reference's formulas on the same test blocks G_j, H_j and tagging plan:
+
+* the sketch rows Y(I_i, :) = A(I_i, :) Omega and Z(I_i, :) = A(I_i, :) Psi
+  with the explicitly assembled tagged test matrices (ref/bases.py:126-172);
+* U_i, V_i = col_basis of the z^(i)-combined samples (ref/bases.py:207-210,
+  ref/linalg.py:55-69);
+* the core rows C_ij = U_i^T A_ij V_j for every j (ref/reconstruction.py:185-198);
+* the near blocks B_ij with the colour-probe sum over the same-colour boxes of
+  the row (ref/reconstruction.py:201-244);
+* the assembled rows A_hat(I_i, :), gated at 1e-10 relative to ||A(I_i, :)||_F.
+
+The exact blockwise ||A - A_hat||_F of the two shards comes from
+ublr_frob_error (A generated on the device)."""
+
+import os
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle as O
+import paper_2501_05528_b200 as P
+from paper_2501_05528_b200.distributed import ShardResult, phase1_local, phase23_local, shard_ranges
+
+pytestmark = pytest.mark.gpu
+
+PER, B, K, PP, DIAG = 1024, 4096, 48, 16, 2048.0
+CHUNK = 64   # column blocks per oracle chunk
+
+
+@pytest.fixture(scope="module")
+def c5():
+    pts = P.grid_points(PER, 2)
+    tess = P.build_tessellation(pts, B)
+    op = P.KernelOperator(pts, "inv", DIAG)
+    stream = P.RandomStream(7)
+    shards = shard_ranges(tess, 8, K)
+    plan = P.plan_tagging(tess, 0, "gaussian", stream.child(1), device=True)
+    loc = {}
+    Vs = []
+    for sh in shards:
+        out = phase1_local(op, tess, K, PP, stream, sh, plan, keep_sketch=sh.rank in (3, 4))
+        Vs.append(out[2])
+        loc[sh.rank] = out
+    V_all = torch.cat(Vs, 0)
+    res = {}
+    for r in (3, 4):
+        _, U, V, dt, Y, Z = loc[r]
+        core, Bf = phase23_local(op, K, shards[r], dt, U, V_all)
+        res[r] = (ShardResult(shards[r], U, V_all, core, Bf, plan, {}), Y.cpu().numpy(), Z.cpu().numpy())
+    torch.cuda.synchronize()
+    # the reference's explicitly assembled tagged test matrices
+    # (ref/bases.py:126-137, 163-168) on the same streams and plan
+    bx = O.partition(pts.coords, B)
+    st = O.Stream(7).child(0)
+    T = plan.matrix.entries
+    G = [O.normals(len(bx.blocks[i]), K + PP, st.child(0, i)) for i in range(bx.b)]
+    H = [O.normals(len(bx.blocks[i]), K + PP, st.child(1, i)) for i in range(bx.b)]
+    om = O.ublr_oracle._tagged_matrix(bx, T, G, K + PP)
+    ps = O.ublr_oracle._tagged_matrix(bx, T, H, K + PP)
+    return dict(pts=pts, tess=tess, op=op, plan=plan, shards=shards, dt=loc[3][3], res=res,
+                V=V_all.cpu().numpy(), om=om, ps=ps)
+
+
+def _oracle_row(c5, i):
+    """Reference formulas for block row i (original index order within blocks)."""
+    tess, plan = c5["tess"], c5["plan"]
+    coords = c5["pts"].coords
+    Zv = plan.Z
+    gc = K + PP
+    rows = tess.blocks[i]
+    m = len(rows)
+    dt = c5["dt"]
+    om, ps = c5["om"], c5["ps"]
+    y = np.zeros((m, om.shape[1]))
+    z = np.zeros((m, ps.shape[1]))
+    for c0 in range(0, tess.n_points, CHUNK * 256):
+        cols = np.arange(c0, min(c0 + CHUNK * 256, tess.n_points))
+        A = O.kernel_block(coords, rows, cols, "inv", DIAG)
+        y += A @ om[cols]
+        z += A @ ps[cols]     # A symmetric: A^* Psi rows = A(I_i, :) Psi
+    U = O.leading_q(np.tensordot(y.reshape(m, -1, gc), Zv[i], axes=(1, 0)), K)
+    Vi = O.leading_q(np.tensordot(z.reshape(m, -1, gc), Zv[i], axes=(1, 0)), K)
+    # core row and colour-probe near blocks, with the device's V_j (checked on
+    # the sampled rows through Vi) for the column blocks
+    Vh = c5["V"]
+    colours = dt.colours_h
+    C = np.zeros((K, tess.b * K))
+    Bsum = np.zeros((int(colours.max()) + 1, m, dt.m_max))
+    for j0 in range(0, tess.b, CHUNK):
+        js = list(range(j0, min(j0 + CHUNK, tess.b)))
+        cols = np.concatenate([tess.blocks[j] for j in js])
+        A = O.kernel_block(coords, rows, cols, "inv", DIAG)
+        at = 0
+        for j in js:
+            mj = len(tess.blocks[j])
+            Vj = Vh[dt.off_h[j]:dt.off_h[j + 1]]
+            Aij = A[:, at:at + mj]
+            Cij = U.T @ Aij @ Vj
+            C[:, j * K:(j + 1) * K] = Cij
+            Bsum[colours[j], :, :mj] += Aij - U @ Cij @ Vj.T
+            at += mj
+    Bn = {j: Bsum[colours[j], :, :len(tess.blocks[j])] for j in tess.neighbor_lists[i]}
+    return y, z, U, Vi, C, Bn
+
+
+def test_c5_block_rows_match_oracle(c5):
+    dt, shards = c5["dt"], c5["shards"]
+    sh3, sh4 = shards[3], shards[4]
+    b0 = sh4.i0                          # first block row of shard 4
+    rows = [b0 - 64, b0 - 63, b0 - 2, b0 - 1, b0, b0 + 1, b0 + 63, b0 + 64 + 17]
+    with ThreadPoolExecutor(min(len(rows), os.cpu_count() or 1)) as ex:
+        refs = list(ex.map(lambda i: _oracle_row(c5, i), rows))
+    for i, (y, z, U, Vi, C, Bn) in zip(rows, refs):
+        r = 3 if i < b0 else 4
+        res, Yg, Zg = c5["res"][r]
+        sh = res.shard
+        lo, hi = dt.off_h[i] - sh.r0, dt.off_h[i + 1] - sh.r0
+        assert np.linalg.norm(Yg[lo:hi] - y) <= 1e-12 * np.linalg.norm(y)
+        assert np.linalg.norm(Zg[lo:hi] - z) <= 1e-12 * np.linalg.norm(z)
+        Ug = res.U[lo:hi].cpu().numpy()
+        assert np.abs(Ug - U).max() <= 1e-10
+        assert np.abs(c5["V"][dt.off_h[i]:dt.off_h[i + 1]] - Vi).max() <= 1e-10
+        kr = dt.roff(K)[0][i] - sh.K0
+        Cg = res.core[kr:kr + K].cpu().numpy()
+        assert np.linalg.norm(Cg - C) <= 1e-10 * np.linalg.norm(C)
+        Bflat = res.B.cpu().numpy()
+        bbase = dt.b_off_h[sh.p0]
+        arow = 0.0
+        dA2 = 0.0
+        for q in range(dt.nptr_h[i], dt.nptr_h[i + 1]):
+            j = int(dt.nidx_h[q])
+            mj = int(dt.sizes[j])
+            Bg = Bflat[dt.b_off_h[q] - bbase:dt.b_off_h[q + 1] - bbase].reshape(hi - lo, mj)
+            dA2 += np.linalg.norm(Bg - Bn[j]) ** 2
+            arow += np.linalg.norm(Bn[j]) ** 2
+        # A_hat(I_i, :) = U_i C_i blockdiag(V)^T + B_i: far part through the core rows
+        Vh = c5["V"]
+        for j in range(dt.b):
+            Vj = Vh[dt.off_h[j]:dt.off_h[j + 1]]
+            d = Ug @ Cg[:, j * K:(j + 1) * K] @ Vj.T - U @ C[:, j * K:(j + 1) * K] @ Vj.T
+            dA2 += np.linalg.norm(d) ** 2
+        A_row = np.linalg.norm(O.kernel_block(c5["pts"].coords, c5["tess"].blocks[i],
+                                              np.arange(c5["tess"].n_points), "inv", DIAG))
+        assert np.sqrt(dA2) <= 1e-10 * A_row, (i, np.sqrt(dA2) / A_row)
+
+
+def test_c5_exact_frobenius_error_of_shards(c5):
+    """Exact ||A - A_hat||_F over the two shards' block rows (ublr_frob_error)."""
+    dt = c5["dt"]
+    tot_e = tot_a = 0.0
+    for r in (3, 4):
+        res = c5["res"][r][0]
+        fr = P.frobenius_error(c5["op"], res.rep_view(dt, K), res.shard.i0, res.shard.i1)
+        tot_e += fr.pair2.sum()
+        tot_a += fr.ref2.sum()
+        assert np.isfinite(fr.pair2).all()
+    rel = np.sqrt(tot_e / tot_a)
+    print(f"c5 shards 3-4: ||A - A_hat||_F / ||A||_F = {rel:.3e}")
+    assert rel < 1e-6

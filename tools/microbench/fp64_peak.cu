@@ -99,17 +99,26 @@ __global__ void k_rsqrt(double* out, int iters) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// Launch errors (e.g. too many registers for 1024-thread blocks) are checked
+// after every launch: a failed launch returns a negative time and the row is
+// reported as FAILED instead of timing an empty kernel.
 template <class K>
 float run(K kern, double* out, int blocks, int threads, int iters) {
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   kern<<<blocks, threads>>>(out, 10);
-  cudaDeviceSynchronize();
+  if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) return -1.f;
   cudaEventRecord(e0);
   kern<<<blocks, threads>>>(out, iters);
+  if (cudaGetLastError() != cudaSuccess) return -1.f;
   cudaEventRecord(e1);
-  cudaEventSynchronize(e1);
+  if (cudaEventSynchronize(e1) != cudaSuccess) return -1.f;
   float ms; cudaEventElapsedTime(&ms, e0, e1);
   return ms;
+}
+
+static void report(const char* name, int tpb, float ms, double work, const char* unit) {
+  if (ms <= 0.f) printf("%-8s tpb=%4d : FAILED (launch error: %s)\n", name, tpb, cudaGetErrorString(cudaGetLastError()));
+  else printf("%-8s tpb=%4d : %.2f %s\n", name, tpb, work / (ms * 1e-3) / (unit[0] == 'T' ? 1e12 : 1e9), unit);
 }
 
 int main() {
@@ -120,20 +129,16 @@ int main() {
   for (int tpb : {256, 512, 1024}) {
     int blocks = sms * (1024 / tpb) * 1;
     double thr = (double)blocks * tpb;
-    float ms = run(k_dfma, out, blocks, tpb, iters);
-    printf("DFMA     tpb=%4d : %.2f TFLOP/s\n", tpb, thr * iters * 64 * 2 / (ms * 1e-3) / 1e12);
-    ms = run(k_m8n8k4, out, blocks, tpb, iters);
-    printf("m8n8k4   tpb=%4d : %.2f TFLOP/s\n", tpb, thr / 32 * iters * 8 * (8 * 8 * 4) * 2 / (ms * 1e-3) / 1e12);
-    ms = run(k_m16n8k4, out, blocks, tpb, iters);
-    printf("m16n8k4  tpb=%4d : %.2f TFLOP/s\n", tpb, thr / 32 * iters * 8 * (16 * 8 * 4) * 2 / (ms * 1e-3) / 1e12);
-    ms = run(k_m16n8k8, out, blocks, tpb, iters);
-    printf("m16n8k8  tpb=%4d : %.2f TFLOP/s\n", tpb, thr / 32 * iters * 8 * (16 * 8 * 8) * 2 / (ms * 1e-3) / 1e12);
-    ms = run(k_m16n8k16, out, blocks, tpb, iters / 2);
-    printf("m16n8k16 tpb=%4d : %.2f TFLOP/s\n", tpb, thr / 32 * (iters / 2) * 8 * (16 * 8 * 16) * 2 / (ms * 1e-3) / 1e12);
-    ms = run(k_log, out, blocks, tpb, iters / 10);
-    printf("log      tpb=%4d : %.3f Gevals/s\n", tpb, thr * (iters / 10) * 8 / (ms * 1e-3) / 1e9);
-    ms = run(k_rsqrt, out, blocks, tpb, iters / 10);
-    printf("rsqrt    tpb=%4d : %.3f Gevals/s\n", tpb, thr * (iters / 10) * 8 / (ms * 1e-3) / 1e9);
+    report("DFMA", tpb, run(k_dfma, out, blocks, tpb, iters), thr * iters * 64 * 2, "TFLOP/s");
+    report("m8n8k4", tpb, run(k_m8n8k4, out, blocks, tpb, iters), thr / 32 * iters * 8 * (8 * 8 * 4) * 2, "TFLOP/s");
+    report("m16n8k4", tpb, run(k_m16n8k4, out, blocks, tpb, iters), thr / 32 * iters * 8 * (16 * 8 * 4) * 2,
+           "TFLOP/s");
+    report("m16n8k8", tpb, run(k_m16n8k8, out, blocks, tpb, iters), thr / 32 * iters * 8 * (16 * 8 * 8) * 2,
+           "TFLOP/s");
+    report("m16n8k16", tpb, run(k_m16n8k16, out, blocks, tpb, iters / 2),
+           thr / 32 * (iters / 2) * 8 * (16 * 8 * 16) * 2, "TFLOP/s");
+    report("log", tpb, run(k_log, out, blocks, tpb, iters / 10), thr * (iters / 10) * 8, "Gevals/s");
+    report("rsqrt", tpb, run(k_rsqrt, out, blocks, tpb, iters / 10), thr * (iters / 10) * 8, "Gevals/s");
   }
   return 0;
 }

@@ -15,9 +15,26 @@ keys = ["Kernel Name", "gpu__time_duration.sum", "launch__grid_size", "launch__b
 for k in keys:
     if k in d:
         print(f"{k:80s} {d[k]} {units[hdr.index(k)]}")
-st = [(h, v) for h, v in d.items() if h.startswith("smsp__average_warp_latency_issue_stalled_") or
-      (h.startswith("smsp__warp_issue_stalled_") and h.endswith("_per_warp_active.pct"))]
-st = sorted(((h, float(v)) for h, v in st if v.replace('.', '', 1).isdigit()), key=lambda x: -x[1])[:10]
-print("top stalls:")
+def num(v):
+    try:
+        return float(v.replace(",", ""))
+    except ValueError:
+        return None
+
+
+# stall reasons: average warps stalled per issued instruction (the ratio ncu's
+# "Warp State Statistics" section plots), largest first
+pre, suf = "smsp__average_warps_issue_stalled_", "_per_issue_active.ratio"
+st = [(h[len(pre):-len(suf)], num(v)) for h, v in d.items() if h.startswith(pre) and h.endswith(suf)]
+st = sorted((x for x in st if x[1] is not None), key=lambda x: -x[1])[:10]
+print("top stalls (warps stalled per issued instruction):")
 for h, v in st:
-    print(f"  {h:78s} {v:.2f}")
+    print(f"  {h:40s} {v:.3f}")
+samp = [(h[len("smsp__pcsamp_warps_issue_stalled_"):], num(v)) for h, v in d.items()
+        if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("_not_issued")]
+samp = [x for x in samp if x[1] is not None]
+tot = sum(v for _, v in samp)
+if tot > 0:
+    print("pc-sampling stall share:")
+    for h, v in sorted(samp, key=lambda x: -x[1])[:8]:
+        print(f"  {h:40s} {100 * v / tot:.1f} %")
