@@ -162,7 +162,8 @@ int ublr_block_qr_pair(const double* Y, const double* Z, int64_t ld_y, const dou
 /* K6 — coupling (ref/reconstruction.py:185-198, direct_core):
  * core[roff[i]:, roff[j]:] = U_i^T A_ij V_j for block rows i0 <= i < i1 and all
  * j (U and core indexed by absolute rows: a block-row shard passes shifted
- * pointers). */
+ * pointers). Any block size; effective ranks up to 96 (blocks above 256
+ * points or ranks above 64 take the general kernel). */
 int ublr_coupling(const ublr_op_t* op, const int32_t* off, const int32_t* roff, int b, int k,
                   const double* U, const double* V, int64_t ld_uv, double* core, int64_t ld_c,
                   void* stream, int m_max, int i0, int i1);
@@ -282,6 +283,12 @@ int ublr_scale_rows(double* X, int64_t ldx, int64_t s_x, const double* d, int64_
  * out is n_pairs x m_max x gc. */
 int ublr_tag_combine_pairs(const double* Y, int64_t ld_y, int gc, int ell, const double* w, const int32_t* pair_i,
                            const int32_t* off, int n_pairs, int m_max, double* out, void* stream);
+/* Near blocks between the flat neighbour-CSR layout (block p at b_off[p],
+ * m_i x m_j row-major) and a padded per-pair layout (block p at
+ * p * m_max * m_max, row stride m_max): to_padded = 1 copies flat -> padded,
+ * 0 copies padded -> flat. Used by the type-B solves on ragged tessellations. */
+int ublr_pairs_pad(double* flat, const int64_t* b_off, const int32_t* pair_i, const int32_t* nidx, const int32_t* off,
+                   int n_pairs, int m_max, double* padded, int to_padded, void* stream);
 /* Explicit tagged test matrix Omega[r, c*gc + q] = T[block(r), c] G[r, q]
  * (ref/bases.py:126-137), permuted rows. */
 int ublr_assemble_tagged(const double* T, int ell, const double* G, int64_t ld_g, int gc, const int32_t* off, int b,

@@ -72,6 +72,7 @@ SIGNATURES = {
     "ublr_scale_rows": (INT, [P, I64, I64, P, I64, INT, INT, INT, P]),
     "ublr_assemble_gram": (INT, [P, P, INT, INT, P, INT, P]),
     "ublr_tag_combine_pairs": (INT, [P, I64, INT, INT, P, P, P, INT, INT, P, P]),
+    "ublr_pairs_pad": (INT, [P, P, P, P, P, INT, INT, P, INT, P]),
     "ublr_assemble_tagged": (INT, [P, INT, P, I64, INT, P, INT, P, I64, I64, P]),
     "ublr_blr_apply": (INT, [P, P, I64, P, I64, P, P, P, P, P, P, P, INT, P, I64, INT, INT, P, I64, P, P]),
     "ublr_frob_error": (INT, [C.POINTER(OpDesc), P, P, P, P, INT, P, INT, P, P, I64, P, I64, P, INT, INT, P, P, P]),
@@ -124,7 +125,7 @@ LAUNCHES = {"ublr_rng_normals": 8, "ublr_sketch_tagged": 1, "ublr_sketch_tagged_
             "ublr_blr_apply": 3, "ublr_gemm_batched": 1, "ublr_potrf_diag": 1, "ublr_lu_sign_diag": 1,
             "ublr_lu_sign_diag_r": 1, "ublr_syrk_upper_batched": 1, "ublr_add_scaled_rows": 1,
             "ublr_gather": 1, "ublr_scale_rows": 1, "ublr_tag_combine_pairs": 1, "ublr_assemble_tagged": 1, "ublr_tag_aspect": 1, "ublr_null_vectors_device": 1,
-            "ublr_frob_error": 1, "ublr_frob_diff": 1}
+            "ublr_frob_error": 1, "ublr_frob_diff": 1, "ublr_pairs_pad": 1}
 launch_count = 0
 
 

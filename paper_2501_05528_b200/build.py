@@ -21,7 +21,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "--expt-relaxed-constexpr", f"-I{GEN}", f"-I{os.path.join(ROOT, 'include')}"]
-SOURCES = ["capi.cu", "rng.cu", "sketch.cu", "qr.cu", "coupling.cu", "coupling_small.cu", "blr.cu", "dense.cu", "typeb.cu", "tagaspect.cu", "frob.cu"]
+SOURCES = ["capi.cu", "rng.cu", "sketch.cu", "qr.cu", "coupling.cu", "coupling_small.cu", "blr.cu", "dense.cu", "typeb.cu", "tagaspect.cu", "frob.cu", "coupling_gen.cu"]
 
 
 def _gen_tables():

@@ -810,6 +810,16 @@ __global__ void __launch_bounds__(256, 2) k_nf_B3(ublr_op_t op, const int32_t* _
 
 using namespace ublr;
 
+namespace ublr {
+int coupling_generic(const ublr_op_t* op, const int32_t* off, const int32_t* roff, int b, int k, const double* U,
+                     const double* V, int64_t ld_uv, double* core, int64_t ld_c, cudaStream_t st, int m_max, int i0,
+                     int i1);
+int nearfield_generic(const ublr_op_t* op, const int32_t* off, const int32_t* roff, int k, const double* U,
+                      const double* V, int64_t ld_uv, const double* core, int64_t ld_c, const int32_t* colour,
+                      const int32_t* cptr, const int32_t* cidx, int m_max, const int32_t* pair_i, const int32_t* nidx,
+                      int n_pairs, const int64_t* b_off, double* B, double* S, int KA, cudaStream_t st);
+}  // namespace ublr
+
 static size_t coupling_smem(int MR, int NJ) {
   size_t stage = (size_t)2 * CP_BK * (MR + 4) + (size_t)2 * CP_BK * (8 * NJ + 4);
   size_t w = (size_t)MR * (8 * NJ + 1);
@@ -823,11 +833,12 @@ extern "C" int ublr_coupling(const ublr_op_t* op, const int32_t* off, const int3
   if (rc) return rc;
   UBLR_REQUIRE(b > 0 && off && roff && U && V && core && k >= 1 && ld_uv >= k, UBLR_ERR_VALUE,
                "ublr_coupling: bad arguments");
-  UBLR_REQUIRE(m_max <= 256 && k <= 64, UBLR_ERR_VALUE, "ublr_coupling: supports m <= 256, k <= 64");
-  UBLR_REQUIRE(b <= 65535, UBLR_ERR_VALUE, "ublr_coupling: b <= 65535");
   cudaStream_t st = (cudaStream_t)stream;
   UBLR_REQUIRE(0 <= i0 && i0 < i1 && i1 <= b, UBLR_ERR_VALUE, "ublr_coupling: bad block-row range");
   int kk = k < m_max ? k : m_max;  // effective ranks never exceed min(k, m)
+  // blocks above 256 points or ranks above 64: the general kernel (coupling_gen.cu)
+  if (m_max > 256 || kk > 64) return coupling_generic(op, off, roff, b, k, U, V, ld_uv, core, ld_c, st, m_max, i0, i1);
+  UBLR_REQUIRE(b <= 65535, UBLR_ERR_VALUE, "ublr_coupling: b <= 65535");
   int vec2 = ((ld_uv % 2) == 0 && ((uintptr_t)V) % 16 == 0) ? 1 : 0;
   static const int cp_ver = [] {
     const char* e = getenv("UBLR_COUPLING_VERSION");
@@ -882,7 +893,7 @@ extern "C" int ublr_coupling(const ublr_op_t* op, const int32_t* off, const int3
   return UBLR_OK;
 }
 
-static int ka_of(int k) { return (k <= 8) ? 8 : (k <= 16) ? 16 : (k <= 32) ? 32 : 64; }
+static int ka_of(int k) { return (k <= 8) ? 8 : (k <= 16) ? 16 : (k <= 32) ? 32 : (k <= 64) ? 64 : (k + 7) / 8 * 8; }
 
 extern "C" int64_t ublr_nearfield_workspace_bytes(int n_pairs, int k, int m_max) {
   return (int64_t)n_pairs * ka_of(k) * m_max * (int64_t)sizeof(double);
@@ -899,12 +910,14 @@ extern "C" int ublr_nearfield_colour(const ublr_op_t* op, const int32_t* off, co
   UBLR_REQUIRE(b > 0 && n_colours > 0 && n_pairs > 0 && off && roff && U && V && core && colour && cptr && cidx &&
                    pair_i && nidx && b_off && B && workspace,
                UBLR_ERR_VALUE, "ublr_nearfield_colour: bad arguments");
-  UBLR_REQUIRE(m_max <= 256 && k <= 64, UBLR_ERR_VALUE, "ublr_nearfield_colour: supports m <= 256, k <= 64");
   UBLR_REQUIRE(workspace_bytes >= ublr_nearfield_workspace_bytes(n_pairs, k, m_max), UBLR_ERR_VALUE,
                "ublr_nearfield_colour: workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
   double* S = (double*)workspace;
   const int KA = ka_of(k);
+  if (m_max > 256 || k > 64)   // the general kernels (coupling_gen.cu)
+    return nearfield_generic(op, off, roff, k, U, V, ld_uv, core, ld_c, colour, cptr, cidx, m_max, pair_i, nidx, n_pairs,
+                             b_off, B, S, KA, st);
   static const int nf_ver = [] {
     const char* e = getenv("UBLR_NEARFIELD_VERSION");
     return e ? atoi(e) : 3;

@@ -54,10 +54,41 @@ __global__ void __launch_bounds__(CT) k_assemble_tagged(const double* __restrict
   }
 }
 
+// Near blocks between the flat neighbour-CSR layout (block p at b_off[p],
+// m_i x m_j row-major) and a padded per-pair layout (p * m_max * m_max,
+// row stride m_max) used by the batched solves of ragged tessellations.
+__global__ void __launch_bounds__(CT) k_pairs_pad(double* __restrict__ flat, const int64_t* __restrict__ b_off,
+                                                  const int32_t* __restrict__ pair_i, const int32_t* __restrict__ nidx,
+                                                  const int32_t* __restrict__ off, int m_max,
+                                                  double* __restrict__ padded, int to_padded) {
+  const int p = blockIdx.x;
+  const int i = pair_i[p], j = nidx[p];
+  const int mi = off[i + 1] - off[i], mj = off[j + 1] - off[j];
+  double* pd = padded + (int64_t)p * m_max * m_max;
+  double* fl = flat + b_off[p];
+  for (int e = blockIdx.y * CT + threadIdx.x; e < mi * mj; e += gridDim.y * CT) {
+    const int r = e / mj, c = e - r * mj;
+    if (to_padded) pd[(int64_t)r * m_max + c] = fl[e];
+    else fl[e] = pd[(int64_t)r * m_max + c];
+  }
+}
+
 }  // namespace
 }  // namespace ublr
 
 using namespace ublr;
+
+extern "C" int ublr_pairs_pad(double* flat, const int64_t* b_off, const int32_t* pair_i, const int32_t* nidx,
+                              const int32_t* off, int n_pairs, int m_max, double* padded, int to_padded, void* stream) {
+  UBLR_REQUIRE(flat && b_off && pair_i && nidx && off && padded && n_pairs >= 0 && m_max > 0, UBLR_ERR_VALUE,
+               "ublr_pairs_pad: bad arguments");
+  if (!n_pairs) return UBLR_OK;
+  int gy = (m_max * m_max + CT * 4 - 1) / (CT * 4);
+  dim3 grid(n_pairs, gy < 1 ? 1 : gy);
+  k_pairs_pad<<<grid, CT, 0, (cudaStream_t)stream>>>(flat, b_off, pair_i, nidx, off, m_max, padded, to_padded);
+  UBLR_LAUNCH_CHECK();
+  return UBLR_OK;
+}
 
 extern "C" int ublr_tag_combine_pairs(const double* Y, int64_t ld_y, int gc, int ell, const double* w,
                                       const int32_t* pair_i, const int32_t* off, int n_pairs, int m_max, double* out,

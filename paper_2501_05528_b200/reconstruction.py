@@ -288,6 +288,73 @@ def frobenius_distance(rep1: UniformBLR, rep2: UniformBLR, i0: int = 0, i1: int 
 # Type A
 # ---------------------------------------------------------------------------
 
+def _groups(dt, k):
+    """Blocks grouped by (m_i, k_i) for the batched blockwise GEMMs:
+    [(m, ki, blocks)]."""
+    ranks = dt.ranks(k)
+    out = {}
+    for i in range(dt.b):
+        out.setdefault((int(dt.sizes[i]), int(ranks[i])), []).append(i)
+    return [(m, ki, np.asarray(bl)) for (m, ki), bl in sorted(out.items())]
+
+
+def _rows_map(starts, width):
+    torch = _torch()
+    rows = np.asarray(starts, dtype=np.int64)[:, None] + np.arange(width)[None, :]
+    return torch.from_numpy(rows.astype(np.int32)).cuda()
+
+
+def blockwise_lt_x(dt, L, k, X, out):
+    """out[roff_i : roff_i + k_i, :] = L_i^T X[rows_i, :] for every block
+    (L = U or V, N x ld; X N x w; out K x w), batched per (m_i, k_i) group on
+    ublr_gemm_batched with row maps (ragged blocks supported)."""
+    from . import dense as D
+    roff_h, _ = dt.roff(k)
+    w = X.shape[1]
+    for m, ki, bl in _groups(dt, k):
+        if ki == 0:
+            continue
+        rmap = _rows_map(dt.off_h[bl], m)
+        D.gemm(1, 0, ki, w, m, 1.0, D.addr(L), L.stride(0), 0, D.addr(X), X.stride(0), 0, 0.0, D.addr(out),
+               out.stride(0), 0, len(bl), amap=D.addr(rmap), sAm=m, bmap=D.addr(rmap), sBm=m,
+               cmap=D.addr(_rows_map(roff_h[bl], ki)), sCm=ki)
+
+
+def blockwise_l_y(dt, L, k, Yk, out, alpha=1.0, beta=0.0):
+    """out[rows_i, :] = alpha L_i Yk[roff_i : roff_i + k_i, :] + beta out[rows_i, :]."""
+    from . import dense as D
+    roff_h, _ = dt.roff(k)
+    w = Yk.shape[1]
+    for m, ki, bl in _groups(dt, k):
+        rmap = _rows_map(dt.off_h[bl], m)
+        if ki == 0:
+            if beta != 1.0:
+                for i in bl:
+                    out[dt.off_h[i]:dt.off_h[i + 1]].mul_(beta)
+            continue
+        D.gemm(0, 0, m, w, ki, alpha, D.addr(L), L.stride(0), 0, D.addr(Yk), Yk.stride(0), 0, beta, D.addr(out),
+               out.stride(0), 0, len(bl), amap=D.addr(rmap), sAm=m, bmap=D.addr(_rows_map(roff_h[bl], ki)), sBm=ki,
+               cmap=D.addr(rmap), sCm=m)
+
+
+def _direct_core_host_op(inner, dt, bases, core):
+    """direct_core for a black-box host operator: V_dense (N x K, block
+    diagonal) goes through op.apply as in ref/reconstruction.py:189-197; the
+    projections C_i = U_i^T (A V)[rows_i] run on the device."""
+    torch = _torch()
+    k = bases.rank
+    roff_h, _ = dt.roff(k)
+    K = int(roff_h[-1])
+    Vd = torch.zeros((dt.n, K), dtype=torch.float64, device=dt.device)
+    ranks = dt.ranks(k)
+    for j in range(dt.b):
+        Vd[dt.off_h[j]:dt.off_h[j + 1], roff_h[j]:roff_h[j] + ranks[j]] = bases.V[dt.off_h[j]:dt.off_h[j + 1], :ranks[j]]
+    AV = dt.to_perm_rows(np.asarray(inner.apply(dt.from_perm_rows(Vd)), dtype=np.float64))
+    del Vd
+    blockwise_lt_x(dt, bases.U, k, AV, core)
+    return core
+
+
 def direct_core(op, tess: Tessellation, bases: BlockBases):
     """C = U^T (A V) (ref/reconstruction.py:185-198); device K x K tensor."""
     torch = _torch()
@@ -302,7 +369,7 @@ def direct_core(op, tess: Tessellation, bases: BlockBases):
     if K == 0:
         return core
     if not hasattr(inner, "device_op"):
-        raise NotImplementedError("direct_core needs a GPU operator (DenseOperator / KernelOperator)")
+        return _direct_core_host_op(inner, dt, bases, core)
     if dt.m_max <= FUSED_NEAR_M_MAX and min(k, dt.m_max) <= FUSED_NEAR_K_MAX and dt.pair_of is not None:
         # small blocks: the colour-probe near field (phase III) comes out of the
         # same pass over A (ublr_coupling_nearfield); structured_identity_discrepancy
@@ -343,6 +410,61 @@ def _check_coloring(tess, colors):
                 raise ValueError(f"invalid coloring: two same-color probes collide in the neighborhood of block {i}")
 
 
+def _colour_layout(dt, cols):
+    """Device colour arrays (colour per block, member CSR) of a caller-supplied
+    colouring, cached per colouring on the device tessellation."""
+    torch = _torch()
+    key = ("colours", cols.tobytes())
+    hit = dt.rng_records.get(key)
+    if hit is None:
+        n = int(cols.max()) + 1
+        order = np.argsort(cols, kind="stable")
+        cptr = np.concatenate(([0], np.cumsum(np.bincount(cols, minlength=n)))).astype(np.int32)
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dt.device)  # noqa: E731
+        hit = (t(cols.astype(np.int32)), t(cptr), t(order.astype(np.int32)), n)
+        dt.rng_records[key] = hit
+    return hit
+
+
+def _structured_identity_host_op(inner, tess, bases, core, cols):
+    """structured_identity_discrepancy for a black-box host operator: one
+    identity probe per colour through op.apply (ref/reconstruction.py:227-243);
+    V^T probe, C (V^T probe) and the subtraction of U_i (C V^T probe)[rows_i]
+    run on the device, and the near blocks are cut out of the residual
+    (including the same-colour leak)."""
+    from . import dense as D
+    torch = _torch()
+    dt = bases.dt
+    k = bases.rank
+    K = bases.total_rank
+    sizes = dt.sizes
+    B = torch.empty(max(int(dt.b_off_h[-1]), 1), dtype=torch.float64, device=dt.device)
+    pair = {(int(i), int(j)): q for q, (i, j) in enumerate(zip(dt.pair_i_h, dt.nidx_h))}
+    for c in range(int(cols.max()) + 1):
+        members = np.flatnonzero(cols == c)
+        if members.size == 0:
+            continue
+        mc = int(sizes[members].max())
+        probe = np.zeros((dt.n, mc))
+        for j in members:
+            probe[tess.blocks[j], np.arange(sizes[j])] = 1.0
+        R = dt.to_perm_rows(np.asarray(inner.apply(probe), dtype=np.float64))
+        if K > 0:
+            P = dt.to_perm_rows(probe)
+            VtP = torch.empty((K, mc), dtype=torch.float64, device=dt.device)
+            blockwise_lt_x(dt, bases.V, k, P, VtP)
+            CV = torch.empty((K, mc), dtype=torch.float64, device=dt.device)
+            D.gemm(0, 0, K, mc, K, 1.0, D.addr(core), core.stride(0), 0, D.addr(VtP), mc, 0, 0.0, D.addr(CV), mc, 0,
+                   1)
+            blockwise_l_y(dt, bases.U, k, CV, R, alpha=-1.0, beta=1.0)
+        for j in members:
+            for i in tess.neighbor_lists[j]:
+                q = pair[(int(i), int(j))]
+                B[int(dt.b_off_h[q]):int(dt.b_off_h[q + 1])].view(int(sizes[i]), int(sizes[j])).copy_(
+                    R[dt.off_h[i]:dt.off_h[i + 1], :sizes[j]])
+    return B[:int(dt.b_off_h[-1])]
+
+
 def structured_identity_discrepancy(op, tess: Tessellation, bases: BlockBases, core, coloring: BoxColoring):
     """Near blocks from colour probes, with the reference's same-colour leak
     (ref/reconstruction.py:201-244). Returns a flat device buffer
@@ -354,19 +476,19 @@ def structured_identity_discrepancy(op, tess: Tessellation, bases: BlockBases, c
     if checked is None or not np.array_equal(checked, cols):
         _check_coloring(tess, cols)          # pure function of (tess, colours): validated once
         tess._device["coloring_checked"] = cols.copy()
-    if not np.array_equal(cols, dt.colours_h):
-        raise NotImplementedError("custom colourings: only color_boxes(tess) is supported on the GPU path")
     k = bases.rank
     K = bases.total_rank
     roff_h, roff = dt.roff(k)
     sizes = dt.sizes
+    ncol = int(cols.max()) + 1 if cols.size else 0
     if isinstance(op, CountingOperator):
-        op.ledger.record_apply(int(sum(sizes[dt.colours_h == c].max() for c in range(dt.n_colours))))
+        op.ledger.record_apply(int(sum(sizes[cols == c].max() for c in range(ncol) if (cols == c).any())))
     inner = unwrap(op)
     if not hasattr(inner, "device_op"):
-        raise NotImplementedError("structured_identity_discrepancy needs a GPU operator")
+        return _structured_identity_host_op(inner, tess, bases, core, cols)
+    custom = not np.array_equal(cols, dt.colours_h)
     fused = getattr(bases, "fused_near", None)
-    if fused is not None and fused[0] is core and fused[1] == _versions(core, bases) and fused[2] is inner:
+    if not custom and fused is not None and fused[0] is core and fused[1] == _versions(core, bases) and fused[2] is inner:
         return fused[3]   # computed with this core by direct_core's fused pass
     B = torch.empty(int(dt.b_off_h[-1]), dtype=torch.float64, device=dt.device)
     lib = _lib.load()
@@ -374,9 +496,11 @@ def structured_identity_discrepancy(op, tess: Tessellation, bases: BlockBases, c
     ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device=dt.device)
     if K == 0:
         core = torch.zeros((1, 1), dtype=torch.float64, device=dt.device)
+    colours_d, cptr_d, cidx_d, n_colours = (_colour_layout(dt, cols) if custom else
+                                            (dt.colours, dt.cptr, dt.cidx, dt.n_colours))
     _lib.call("ublr_nearfield_colour", inner.device_op(dt.perm), _lib.ptr(dt.off), _lib.ptr(roff), dt.b, k,
               _lib.ptr(bases.U), _lib.ptr(bases.V), bases.U.stride(0), _lib.ptr(core), max(K, 1),
-              _lib.ptr(dt.colours), _lib.ptr(dt.cptr), _lib.ptr(dt.cidx), dt.n_colours, dt.m_max,
+              _lib.ptr(colours_d), _lib.ptr(cptr_d), _lib.ptr(cidx_d), n_colours, dt.m_max,
               _lib.ptr(dt.pair_i), _lib.ptr(dt.nidx), dt.n_pairs, _lib.ptr(dt.b_off), _lib.ptr(B),
               _lib.ptr(ws), ws_bytes, _lib.stream_handle())
     return B

@@ -49,7 +49,7 @@ def ahat_error_vs_golden(rep, g, ncols=3):
 
 
 @pytest.mark.parametrize("name", ["c1s_A2", "log1k_A2", "rand500_A2", "c1_A2", "c2_A2",
-                                  "log1k_A1", "rand500_A1", "log1k_A3", "log1k_B1", "log1k_B2"])
+                                  "log1k_A1", "rand500_A1", "log1k_A3", "log1k_B1", "log1k_B2", "rand500_B2"])
 def test_compress_matches_reference(name):
     tess, op, _ = gpu_problem(name)
     _, _, k, p, mid, seed = build_case(name)
@@ -139,7 +139,8 @@ def test_exact_rank_recovery_all_methods(mid):
 
 
 @pytest.mark.parametrize("per,b,kind,k,mid", [(64, 16, "inv", 48, "A2"), (50, 16, "log", 20, "A2"),
-                                              (48, 9, "log", 30, "A1")])
+                                              (48, 9, "log", 30, "A1"), (50, 16, "log", 20, "B2"),
+                                              (50, 16, "log", 16, "B1"), (40, 16, "inv", 12, "B2")])
 def test_large_blocks_vs_oracle(per, b, kind, k, mid):
     """m > 64 blocks (the warp-specialised coupling and the v3 near-field
     kernels), uniform m = 256 and ragged 144-169-point blocks, GPU vs the
@@ -231,3 +232,121 @@ def test_compress_on_a_side_stream_matches_default_stream():
     torch.cuda.synchronize()
     for key in ("U", "V", "core", "B"):
         assert np.array_equal(h0[key], h1[key]), key
+
+
+class HostMatrixOperator:
+    """A plain-Python black-box operator: shape / apply / apply_adjoint on
+    numpy arrays only (ref/operators.py:24-35, "any object with..." at
+    pkg/README.md:113-115). No device descriptor: every operator product of
+    the pipeline goes through these host calls."""
+
+    def __init__(self, A):
+        self.A = np.asarray(A, dtype=float)
+        self.shape = self.A.shape
+        self.calls = 0
+
+    def apply(self, X):
+        self.calls += 1
+        return self.A @ X
+
+    def apply_adjoint(self, X):
+        self.calls += 1
+        return self.A.T @ X
+
+
+@pytest.mark.parametrize("name", ["log1k_A1", "log1k_A2", "log1k_A3", "log1k_B1", "log1k_B2", "rand500_A1",
+                                  "rand500_A2", "rand500_B2", "c1s_A2"])
+def test_black_box_host_operator_matches_reference(name):
+    """Phases I-III with a plain-Python operator (sketch, direct_core through
+    op.apply(V_dense), one identity probe per colour) against the reference's
+    goldens and ledger."""
+    tess, dev_op, A = gpu_problem(name)
+    Ad = A if A is not None else dev_op.dense()
+    op = HostMatrixOperator(Ad)
+    _, _, k, p, mid, seed = build_case(name)
+    rep, report = P.compress(op, tess, k, mid, p=p, stream=P.RandomStream(seed), compute_error=True)
+    g = golden(name)
+    assert ahat_error_vs_golden(rep, g) <= TOL
+    mv = np.array([[report.matvecs.get(ph, {"A": 0})["A"], report.matvecs.get(ph, {"Astar": 0})["Astar"]]
+                   for ph in ("I", "II", "III")])
+    assert np.array_equal(mv, g["matvecs"])
+    assert op.calls > 0
+
+
+def test_custom_colouring_matches_oracle():
+    """A caller-supplied valid colouring (not color_boxes) gives the
+    reference's colour-probe near field for that colouring (device operator
+    and black-box operator alike)."""
+    import paper_2501_05528_b200.reconstruction as R
+    from paper_2501_05528_b200.bases import tagging_bases
+    from paper_2501_05528_b200.tessellation import BoxColoring
+    tess, op, _ = gpu_problem("log1k_A2")
+    Ad = op.dense()
+    # greedy distance-2 colouring in reverse block order: valid, different from color_boxes
+    nb = [set(x) for x in tess.neighbor_lists]
+    cols = np.full(tess.b, -1)
+    for i in reversed(range(tess.b)):
+        used = {cols[j] for j in range(tess.b) if cols[j] >= 0 and j != i and nb[i] & nb[j]}
+        c = 0
+        while c in used:
+            c += 1
+        cols[i] = c
+    assert not np.array_equal(cols, P.color_boxes(tess).colors)
+    colouring = BoxColoring(colors=cols, num_colors=int(cols.max()) + 1)
+    plan = P.plan_tagging(tess, 0, "gaussian", P.RandomStream(7).child(1))
+    bases, _ = tagging_bases(op, tess, 10, 5, plan, P.RandomStream(7).child(0))
+    core = R.direct_core(op, tess, bases)
+    B_dev = R.structured_identity_discrepancy(op, tess, bases, core, colouring).cpu().numpy()
+    B_host = R.structured_identity_discrepancy(HostMatrixOperator(Ad), tess, bases, core, colouring).cpu().numpy()
+    # oracle: the reference's probe loop on the same bases and core
+    bx = O.partition(O.cell_centres(32, 2), 16)
+    dt = bases.dt
+    Ub = [bases.U[dt.off_h[i]:dt.off_h[i + 1], :10].cpu().numpy() for i in range(tess.b)]
+    Vb = [bases.V[dt.off_h[i]:dt.off_h[i + 1], :10].cpu().numpy() for i in range(tess.b)]
+    bs = O.Bases(Ub, Vb, np.full(tess.b, 10), "tag")
+    Bref = O.near_colour_probes(O.Dense(Ad), bx, bs, core.cpu().numpy(), cols)
+    want = np.concatenate([Bref[(int(i), int(j))].ravel() for i, j in zip(dt.pair_i_h, dt.nidx_h)])
+    scale = np.linalg.norm(Ad)
+    assert np.linalg.norm(B_dev - want) <= 1e-12 * scale
+    assert np.linalg.norm(B_host - want) <= 1e-12 * scale
+
+
+@pytest.mark.parametrize("per,b,k,mid", [(100, 16, 30, "A2"), (64, 16, 80, "A2"), (50, 16, 70, "A1")])
+def test_generic_block_sizes_and_ranks_vs_oracle(per, b, k, mid):
+    """Blocks above 256 points (625) and ranks above 64: the general coupling /
+    near-field kernels (csrc/coupling_gen.cu), GPU vs the oracle's dense
+    compression of the same -log kernel matrix."""
+    pts = P.grid_points(per, 2)
+    tess = P.build_tessellation(pts, b)
+    diag = -np.log(0.5 / per)
+    rep, _ = P.compress(P.KernelOperator(pts, "log", diag), tess, k, mid, p=10, stream=P.RandomStream(5),
+                        compute_error=False)
+    coords = O.cell_centres(per, 2)
+    bx = O.partition(coords, b)
+    n = per * per
+    A = O.kernel_block(coords, np.arange(n), np.arange(n), "log", diag)
+    orep, _ = O.compress(O.Dense(A), bx, k, mid, p=10, stream=O.Stream(5), compute_error=False)
+    nA = np.linalg.norm(A)
+    D_gpu, D_ref = rep.to_dense(), orep.to_dense()
+    assert np.linalg.norm(D_gpu - D_ref) / nA <= TOL
+    assert np.linalg.norm(A - D_gpu) / nA <= 1.05 * np.linalg.norm(A - D_ref) / nA + 1e-15
+
+
+def test_paper_scale_suggested_blocks():
+    """The paper's own setting: N ~ 100k, k = 30,
+    b = suggest_block_count(N, k, d) (ref/tessellation.py:127-140) gives
+    169 boxes of 576-625 points. Runs through A2 end to end; the exact
+    blockwise Frobenius error is small and the near / far structure holds."""
+    per = 316
+    n = per * per
+    b = P.suggest_block_count(n, 30, 2)
+    assert b == 169
+    pts = P.grid_points(per, 2)
+    tess = P.build_tessellation(pts, b)
+    assert tess.max_block_size > 256
+    op = P.KernelOperator(pts, "log", -np.log(0.5 / per))
+    rep, report = P.compress(op, tess, 30, "A2", p=10, stream=P.RandomStream(7), compute_error=False)
+    fr = P.frobenius_error(op, rep)
+    print(f"N={n} b={b} m_max={tess.max_block_size}: ||A - A_hat||_F / ||A||_F = {fr.relative:.3e}")
+    assert fr.relative < 1e-5
+    assert report.matvecs["II"]["A"] == 30 * b
