@@ -74,10 +74,111 @@ UBLR_HD double u64_to_unit(uint64_t v) { return (double)(v >> 11) * (1.0 / 90071
 #ifdef __CUDA_ARCH__
 #define UBLR_MUL(a, b) __dmul_rn((a), (b))
 #define UBLR_ADD(a, b) __dadd_rn((a), (b))
+#define UBLR_SUB(a, b) __dsub_rn((a), (b))
+#define UBLR_DIV(a, b) __ddiv_rn((a), (b))
 #else
 #define UBLR_MUL(a, b) ((a) * (b))
 #define UBLR_ADD(a, b) ((a) + (b))
+#define UBLR_SUB(a, b) ((a) - (b))
+#define UBLR_DIV(a, b) ((a) / (b))
 #endif
+
+UBLR_HD int32_t hi_word(double x) {
+#ifdef __CUDA_ARCH__
+  return __double2hiint(x);
+#else
+  uint64_t b;
+  __builtin_memcpy(&b, &x, 8);
+  return (int32_t)(b >> 32);
+#endif
+}
+
+UBLR_HD double with_hi_word(double x, int32_t h) {
+#ifdef __CUDA_ARCH__
+  return __hiloint2double(h, __double2loint(x));
+#else
+  uint64_t b;
+  __builtin_memcpy(&b, &x, 8);
+  b = (b & 0xffffffffULL) | ((uint64_t)(uint32_t)h << 32);
+  __builtin_memcpy(&x, &b, 8);
+  return x;
+#endif
+}
+
+// log(1 + x), bit for bit as the host C library computes it for numpy's
+// ziggurat tail (npy_log1p -> glibc 2.39 log1p, whose x86-64 build with FMA
+// is selected on the hosts of this image). The algorithm is the published
+// fdlibm one: 1 + x = 2^k (1 + f) with a rounding correction c,
+// log(1 + f) = f - (hfsq - s (hfsq + R(s^2))), s = f / (2 + f), R a degree-7
+// minimax polynomial in s^2 evaluated in Estrin form; the fused
+// multiply-adds are placed where that build fuses them (checked against the
+// host log1p over 6e7 arguments, tests/test_host.py). Used for -1 < x <= 0
+// (x = -u, u a 53-bit uniform) but valid for every finite x > -1.
+UBLR_HD double log1p_host_exact(double x) {
+  constexpr double LN2_HI = 6.93147180369123816490e-01, LN2_LO = 1.90821492927058770002e-10;
+  constexpr double P1 = 6.666666666666735130e-01, P2 = 3.999999999940941908e-01, P3 = 2.857142874366239149e-01,
+                   P4 = 2.222219843214978396e-01, P5 = 1.818357216161805012e-01, P6 = 1.531383769920937332e-01,
+                   P7 = 1.479819860511658591e-01;
+  const int32_t hx = hi_word(x), ax = hx & 0x7fffffff;
+  int k = 1, hu = 0;
+  double f = 0.0, c = 0.0;
+  if (hx < 0x3FDA827A) {                         // x < 0.41422 (every negative x)
+    if (ax >= 0x3ff00000) return x == -1.0 ? -INFINITY : NAN;
+    if (ax < 0x3e200000) {                       // |x| < 2^-29
+      if (ax < 0x3c900000) return x;             // |x| < 2^-54
+      return fma(-UBLR_MUL(x, x), 0.5, x);
+    }
+    if (hx > 0 || hx <= (int32_t)0xbfd2bec3) {   // -0.2929 < x < 0.41422: no reduction
+      k = 0;
+      f = x;
+      hu = 1;
+    }
+  }
+  if (hx >= 0x7ff00000) return UBLR_ADD(x, x);
+  if (k != 0) {
+    double u;
+    if (hx < 0x43400000) {
+      u = UBLR_ADD(1.0, x);
+      hu = hi_word(u);
+      k = (hu >> 20) - 1023;
+      c = k > 0 ? UBLR_SUB(1.0, UBLR_SUB(u, x)) : UBLR_SUB(x, UBLR_SUB(u, 1.0));
+      c = UBLR_DIV(c, u);
+    } else {
+      u = x;
+      hu = hi_word(u);
+      k = (hu >> 20) - 1023;
+      c = 0.0;
+    }
+    hu &= 0x000fffff;
+    if (hu < 0x6a09e) {                           // 1 + f in [1, sqrt 2)
+      u = with_hi_word(u, hu | 0x3ff00000);
+    } else {                                      // halve: 1 + f in [sqrt 2 / 2, 1)
+      k += 1;
+      u = with_hi_word(u, hu | 0x3fe00000);
+      hu = (0x00100000 - hu) >> 2;
+    }
+    f = UBLR_SUB(u, 1.0);
+  }
+  const double hfsq = UBLR_MUL(UBLR_MUL(f, 0.5), f);
+  const double kd = (double)k;
+  if (hu == 0) {                                  // |f| < 2^-20
+    if (f == 0.0) {
+      if (k == 0) return 0.0;
+      c = fma(kd, LN2_LO, c);
+      return fma(kd, LN2_HI, c);
+    }
+    const double R = UBLR_MUL(fma(-f, 0.66666666666666666, 1.0), hfsq);
+    if (k == 0) return UBLR_SUB(f, R);
+    return fma(kd, LN2_HI, -UBLR_SUB(UBLR_SUB(R, fma(kd, LN2_LO, c)), f));
+  }
+  const double s = UBLR_DIV(f, UBLR_ADD(f, 2.0));
+  const double z = UBLR_MUL(s, s), z2 = UBLR_MUL(z, z), z4 = UBLR_MUL(z2, z2), z6 = UBLR_MUL(z2, z4);
+  const double R2 = fma(z, P3, P2), R3 = fma(z, P5, P4), R4 = fma(z, P7, P6);
+  const double R = fma(z6, R4, fma(z4, R3, fma(z, P1, UBLR_MUL(z2, R2))));
+  const double t = UBLR_MUL(s, UBLR_ADD(hfsq, R));
+  if (k == 0) return UBLR_SUB(f, UBLR_SUB(hfsq, t));
+  return fma(kd, LN2_HI, -UBLR_SUB(UBLR_SUB(hfsq, UBLR_ADD(fma(kd, LN2_LO, c), t)), f));
+}
 
 // One ziggurat attempt starting at word position p of a word source `ws`
 // (ws(q) returns word q). Returns the number of words consumed and sets
@@ -103,8 +204,8 @@ UBLR_HD int zig_token(WordSource& ws, int64_t p, const uint64_t* ki, const doubl
       double u1 = u64_to_unit(ws(q));
       double u2 = u64_to_unit(ws(q + 1));
       q += 2;
-      double xx = UBLR_MUL(-ZIG_INV_R, log1p(-u1));
-      double yy = -log1p(-u2);
+      double xx = UBLR_MUL(-ZIG_INV_R, log1p_host_exact(-u1));
+      double yy = -log1p_host_exact(-u2);
       if (UBLR_ADD(yy, yy) > UBLR_MUL(xx, xx)) {
         val = ((rabs >> 8) & 0x1) ? -UBLR_ADD(ZIG_R, xx) : UBLR_ADD(ZIG_R, xx);
         ok = true;

@@ -105,6 +105,10 @@ def torch_allgather(group=None):
 
     def gather(local, total_rows):
         world = dist.get_world_size(group)
+        if local.is_cuda and dist.get_backend(group) == "gloo":
+            # gloo collectives run on host tensors: V is staged through host memory
+            host = gather(local.cpu(), total_rows)
+            return host.to(local.device)
         tail = tuple(local.shape[1:])
         sizes = torch.zeros(world, dtype=torch.int64, device=local.device)
         mine = torch.tensor([local.shape[0]], dtype=torch.int64, device=local.device)
@@ -171,42 +175,85 @@ def phase1_local(op, tess, k, p, stream, shard, plan=None, keep_sketch=False):
     return plan, U, V, dt
 
 
-def phase23_local(op, k, shard, dt, U, V_all):
-    """Steps 4: own core rows (coupling) and own near blocks (colour probes)."""
+def phase23_local(op, k, shard, dt, U, V_all, core_out=None, panel_blocks=None):
+    """Step 4: own core rows (coupling) and own near blocks (colour probes).
+
+    The core rows land in `core_out` when given — a (K1 - K0) x K tensor on
+    the device, or in PINNED HOST memory: the 1- and 2-GPU config-5 core
+    (309 GB in total) does not fit in HBM, so block-row panels
+    of `panel_blocks` rows are computed into two device panel buffers and
+    copied out on a copy stream while the next panel is computed (the near
+    field of a panel reads only that panel's core rows). Returns (core, B)."""
     torch = _torch()
     inner = unwrap(op)
     roff_h, roff = dt.roff(k)
     K = int(roff_h[-1])
     kloc = shard.K1 - shard.K0
     f64 = dict(dtype=torch.float64, device=dt.device)
-    core = torch.empty((kloc, K), **f64)
     st = _lib.stream_handle()
     desc = inner.device_op(dt.perm)
-    npairs = shard.p1 - shard.p0
     bbase = int(dt.b_off_h[shard.p0])
     B = torch.empty(int(dt.b_off_h[shard.p1]) - bbase, **f64)
-    if dt.m_max <= FUSED_NEAR_M_MAX and min(k, dt.m_max) <= FUSED_NEAR_K_MAX and dt.pair_of is not None:
-        # small blocks: core rows and near blocks from one pass over A (as direct_core)
-        _lib.call("ublr_coupling_nearfield", desc, _lib.ptr(dt.off), _lib.ptr(roff), dt.b, k,
-                  _lib.ptr(U) - 8 * shard.r0 * k, _lib.ptr(V_all), k, _lib.ptr(core) - 8 * shard.K0 * K, K,
-                  _lib.ptr(dt.cptr), _lib.ptr(dt.cidx), dt.n_colours, dt.m_max, _lib.ptr(dt.pair_of),
-                  _lib.ptr(dt.nidx), _lib.ptr(dt.b_off), _lib.ptr(B) - 8 * bbase, st, shard.i0, shard.i1)
-        return core, B
-    _lib.call("ublr_coupling", desc, _lib.ptr(dt.off), _lib.ptr(roff), dt.b, k, _lib.ptr(U) - 8 * shard.r0 * k,
-              _lib.ptr(V_all), k, _lib.ptr(core) - 8 * shard.K0 * K, K, st, dt.m_max, shard.i0, shard.i1)
-    lib = _lib.load()
-    ws_bytes = int(lib.ublr_nearfield_workspace_bytes(npairs, max(k, 1), dt.m_max))
-    ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device=dt.device)
-    _lib.call("ublr_nearfield_colour", desc, _lib.ptr(dt.off), _lib.ptr(roff), dt.b, k,
-              _lib.ptr(U) - 8 * shard.r0 * k, _lib.ptr(V_all), k, _lib.ptr(core) - 8 * shard.K0 * K, K,
-              _lib.ptr(dt.colours), _lib.ptr(dt.cptr), _lib.ptr(dt.cidx), dt.n_colours, dt.m_max,
-              _lib.ptr(dt.pair_i) + 4 * shard.p0, _lib.ptr(dt.nidx) + 4 * shard.p0, npairs,
-              _lib.ptr(dt.b_off) + 8 * shard.p0, _lib.ptr(B) - 8 * bbase, _lib.ptr(ws), ws_bytes, st)
-    return core, B
+    host = core_out is not None and not core_out.is_cuda
+    if core_out is None:
+        core_out = torch.empty((kloc, K), **f64)
+    nblk = shard.i1 - shard.i0
+    pb = nblk if not host else max(1, min(nblk, panel_blocks or nblk))
+    fused = dt.m_max <= FUSED_NEAR_M_MAX and min(k, dt.m_max) <= FUSED_NEAR_K_MAX and dt.pair_of is not None
+    ws = None
+    if not fused:
+        lib = _lib.load()
+        pmax = max(int(dt.nptr_h[min(a + pb, shard.i1)] - dt.nptr_h[a]) for a in range(shard.i0, shard.i1, pb))
+        ws_bytes = int(lib.ublr_nearfield_workspace_bytes(pmax, max(k, 1), dt.m_max))
+        ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device=dt.device)
+    Up = _lib.ptr(U) - 8 * shard.r0 * U.stride(0)
+    Bp = _lib.ptr(B) - 8 * bbase
+    if host:
+        rows_max = max(int(roff_h[min(a + pb, shard.i1)] - roff_h[a]) for a in range(shard.i0, shard.i1, pb))
+        panels = [torch.empty((rows_max, K), **f64) for _ in range(2)]
+        done = [None, None]
+        copy_stream = torch.cuda.Stream(device=dt.device)
+    for n_, a in enumerate(range(shard.i0, shard.i1, pb)):
+        e = min(a + pb, shard.i1)
+        if host:
+            slot = n_ % 2
+            if done[slot] is not None:
+                _lib.current_stream().wait_event(done[slot])     # the panel's previous copy has drained
+            cbase = _lib.ptr(panels[slot]) - 8 * int(roff_h[a]) * K
+        else:
+            cbase = _lib.ptr(core_out) - 8 * shard.K0 * K
+        if fused:
+            # small blocks: core rows and near blocks from one pass over A (as direct_core)
+            _lib.call("ublr_coupling_nearfield", desc, _lib.ptr(dt.off), _lib.ptr(roff), dt.b, k, Up,
+                      _lib.ptr(V_all), V_all.stride(0), cbase, K, _lib.ptr(dt.cptr), _lib.ptr(dt.cidx), dt.n_colours,
+                      dt.m_max, _lib.ptr(dt.pair_of), _lib.ptr(dt.nidx), _lib.ptr(dt.b_off), Bp, st, a, e)
+        else:
+            p0, p1 = int(dt.nptr_h[a]), int(dt.nptr_h[e])
+            _lib.call("ublr_coupling", desc, _lib.ptr(dt.off), _lib.ptr(roff), dt.b, k, Up, _lib.ptr(V_all),
+                      V_all.stride(0), cbase, K, st, dt.m_max, a, e)
+            _lib.call("ublr_nearfield_colour", desc, _lib.ptr(dt.off), _lib.ptr(roff), dt.b, k, Up,
+                      _lib.ptr(V_all), V_all.stride(0), cbase, K, _lib.ptr(dt.colours), _lib.ptr(dt.cptr),
+                      _lib.ptr(dt.cidx), dt.n_colours, dt.m_max, _lib.ptr(dt.pair_i) + 4 * p0,
+                      _lib.ptr(dt.nidx) + 4 * p0, p1 - p0, _lib.ptr(dt.b_off) + 8 * p0, Bp, _lib.ptr(ws),
+                      ws.numel(), st)
+        if host:
+            r0, r1 = int(roff_h[a]) - shard.K0, int(roff_h[e]) - shard.K0
+            ready = torch.cuda.Event()
+            ready.record(_lib.current_stream())
+            copy_stream.wait_event(ready)
+            with torch.cuda.stream(copy_stream):
+                core_out[r0:r1].copy_(panels[slot][:r1 - r0], non_blocking=True)
+            done[slot] = torch.cuda.Event()
+            done[slot].record(copy_stream)
+    if host:
+        _lib.current_stream().wait_stream(copy_stream)
+    return core_out, B
 
 
-def compress_sharded(op, tess, k, p=10, stream=None, rank=0, world=1, allgather=None, plan=None):
-    """One rank's share of a type-A tagging (A2) compression."""
+def compress_sharded(op, tess, k, p=10, stream=None, rank=0, world=1, allgather=None, plan=None, core_out=None,
+                     panel_blocks=None):
+    """One rank's share of a type-A tagging (A2) compression. `core_out` /
+    `panel_blocks`: see phase23_local (pinned-host core rows)."""
     stream = stream or RandomStream(0)
     cop = counting_wrapper(op)
     shard = shard_ranges(tess, world, k)[rank]
@@ -218,7 +265,7 @@ def compress_sharded(op, tess, k, p=10, stream=None, rank=0, world=1, allgather=
         cop.ledger.record_apply(int(dt.roff(k)[0][-1]))
     with cop.ledger.phase("III"):
         cop.ledger.record_apply(int(sum(dt.sizes[dt.colours_h == c].max() for c in range(dt.n_colours))))
-    core, B = phase23_local(op, k, shard, dt, U, V_all)
+    core, B = phase23_local(op, k, shard, dt, U, V_all, core_out, panel_blocks)
     return ShardResult(shard, U, V_all, core, B, plan, cop.ledger.to_dict())
 
 

@@ -29,3 +29,12 @@ extern "C" int64_t host_normals(uint64_t k0, uint64_t k1, int64_t n, double* out
   }
   return p;  // words consumed
 }
+
+extern "C" void host_log1p(const double* x, int64_t n, double* out) {
+  for (int64_t i = 0; i < n; ++i) out[i] = ublr::rng::log1p_host_exact(x[i]);
+}
+
+// the host C library's log1p (what numpy's ziggurat calls through npy_log1p)
+extern "C" void host_libm_log1p(const double* x, int64_t n, double* out) {
+  for (int64_t i = 0; i < n; ++i) out[i] = log1p(x[i]);
+}

@@ -73,3 +73,68 @@ def test_emulated_shards_match_single_gpu(world):
     assert torch.equal(parts[0].V, rep.V[:, :20])
     assert torch.equal(core, rep.core_d)
     assert torch.equal(B, rep.B_d)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("per,b,k,kind", [(64, 64, 10, "inv"), (128, 64, 16, "inv"), (96, 36, 12, "log")])
+def test_host_core_panels_match_device(per, b, k, kind):
+    """Core rows streamed to pinned host memory in block-row panels (the
+    1-2 GPU config-5 layout) equal the device-resident result."""
+    from paper_2501_05528_b200.distributed import compress_emulated, compress_sharded
+    pts = P.grid_points(per, 2)
+    tess = P.build_tessellation(pts, b)
+    op = P.KernelOperator(pts, kind, 2.0 * per if kind == "inv" else -np.log(0.5 / per))
+    world = 2
+    ref = compress_emulated(op, tess, k, 8, P.RandomStream(3), world=world)
+    V_all = ref[0].V
+    for r in range(world):
+        sh = ref[r].shard
+        host = torch.empty(ref[r].core.shape, dtype=torch.float64, pin_memory=True)
+        res = compress_sharded(op, tess, k, 8, P.RandomStream(3), rank=r, world=world,
+                               allgather=lambda V, n: V_all, core_out=host, panel_blocks=3)
+        torch.cuda.synchronize()
+        assert res.core is host
+        assert torch.equal(host, ref[r].core.cpu())
+        assert torch.equal(res.B, ref[r].B)
+        assert res.shard == sh
+
+
+def _sharded_worker(rank, world, port, outdir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2501_05528_b200.distributed import compress_sharded
+    pts = P.grid_points(64, 2)
+    tess = P.build_tessellation(pts, 64)
+    op = P.KernelOperator(pts, "inv", 128.0)
+    res = compress_sharded(op, tess, 10, 6, P.RandomStream(11), rank=rank, world=world)
+    np.savez(os.path.join(outdir, f"r{rank}.npz"), U=res.U.cpu().numpy(), V=res.V.cpu().numpy(),
+             core=res.core.cpu().numpy(), B=res.B.cpu().numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_multiprocess_sharded_gloo_matches_emulated(tmp_path):
+    """Two ranks as two processes (gloo; V staged through host memory — the
+    NCCL path of bench.py on an 8-GPU box), each computing its shard on the
+    device, against the in-process emulation of the same ranks."""
+    from paper_2501_05528_b200.distributed import compress_emulated
+    ctx = mp.get_context("spawn")
+    port = 29700 + (os.getpid() % 500)
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, str(tmp_path))) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(timeout=300)
+        assert pr.exitcode == 0
+    pts = P.grid_points(64, 2)
+    tess = P.build_tessellation(pts, 64)
+    ref = compress_emulated(P.KernelOperator(pts, "inv", 128.0), tess, 10, 6, P.RandomStream(11), world=2)
+    for r in range(2):
+        got = np.load(tmp_path / f"r{r}.npz")
+        assert np.array_equal(got["U"], ref[r].U.cpu().numpy())
+        assert np.array_equal(got["V"], ref[r].V.cpu().numpy())
+        assert np.array_equal(got["core"], ref[r].core.cpu().numpy())
+        assert np.array_equal(got["B"], ref[r].B.cpu().numpy())

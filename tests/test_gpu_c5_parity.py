@@ -72,12 +72,13 @@ def c5():
                 V=V_all.cpu().numpy(), om=om, ps=ps)
 
 
-def _oracle_row(c5, i):
+def _oracle_row(c5, i, coords=None):
     """Reference formulas for block row i (original index order within blocks):
     sketch rows, U_i and V_i from the oracle; the core row and near blocks with
-    the oracle's U_i and the device's V_j of the column blocks."""
+    the oracle's U_i and the device's V_j of the column blocks. `coords`
+    replaces the operator's coordinates (the 1-ulp sensitivity run)."""
     tess, plan = c5["tess"], c5["plan"]
-    coords = c5["pts"].coords
+    coords = c5["pts"].coords if coords is None else coords
     Zv = plan.Z
     gc = K + PP
     rows = tess.blocks[i]
@@ -93,8 +94,6 @@ def _oracle_row(c5, i):
         z += A @ ps[cols]     # A symmetric: A^* Psi rows = A(I_i, :) Psi
     U = O.leading_q(np.tensordot(y.reshape(m, -1, gc), Zv[i], axes=(1, 0)), K)
     Vi = O.leading_q(np.tensordot(z.reshape(m, -1, gc), Zv[i], axes=(1, 0)), K)
-    # core row and colour-probe near blocks, with the device's V_j (checked on
-    # the sampled rows through Vi) for the column blocks
     Vh = c5["V"]
     colours = dt.colours_h
     C = np.zeros((K, tess.b * K))
@@ -116,14 +115,39 @@ def _oracle_row(c5, i):
     return y, z, U, Vi, C, Bn
 
 
+def _ahat_row_distance(c5, i, Ua, Ca, Ba, Ub, Cb, Bb):
+    """||A_hat_a(I_i, :) - A_hat_b(I_i, :)||_F for two (U_i, core row, near
+    blocks) triples on the device's V."""
+    dt = c5["dt"]
+    Vh = c5["V"]
+    d2 = 0.0
+    for j in range(dt.b):
+        Vj = Vh[dt.off_h[j]:dt.off_h[j + 1]]
+        d = (Ua @ Ca[:, j * K:(j + 1) * K] - Ub @ Cb[:, j * K:(j + 1) * K]) @ Vj.T
+        if j in Ba:
+            d = d + Ba[j] - Bb[j]
+        d2 += np.linalg.norm(d) ** 2
+    return np.sqrt(d2)
+
+
 def test_c5_block_rows_match_oracle(c5):
+    """Sketch rows at 1e-12; bases as subspaces; the assembled rows of A_hat
+    within max(1e-10, 2 x the oracle's own 1-ulp sensitivity on that row) of
+    ||A(I_i, :)||_F. The sensitivity matters at c5: the tagging plan keeps a
+    worst aspect ratio of ~1e8 after six draws, and the rows of
+    such blocks move by ~1e-7 when A moves by one ulp — in the reference's
+    arithmetic as in ours."""
     dt, shards = c5["dt"], c5["shards"]
-    sh3, sh4 = shards[3], shards[4]
+    sh4 = shards[4]
     b0 = sh4.i0                          # first block row of shard 4
     rows = [b0 - 64, b0 - 63, b0 - 2, b0 - 1, b0, b0 + 1, b0 + 63, b0 + 64 + 17]
-    with ThreadPoolExecutor(min(len(rows), os.cpu_count() or 1)) as ex:
+    pert = np.nextafter(c5["pts"].coords, 2.0)
+    with ThreadPoolExecutor(min(2 * len(rows), os.cpu_count() or 1)) as ex:
         refs = list(ex.map(lambda i: _oracle_row(c5, i), rows))
-    for i, (y, z, U, Vi, C, Bn) in zip(rows, refs):
+        refs2 = list(ex.map(lambda i: _oracle_row(c5, i, pert), rows))
+    rho = c5["plan"].rho_base
+    report = []
+    for i, (y, z, U, Vi, C, Bn), (_, _, U2, _, C2, Bn2) in zip(rows, refs, refs2):
         r = 3 if i < b0 else 4
         res, Yg, Zg = c5["res"][r]
         sh = res.shard
@@ -131,8 +155,8 @@ def test_c5_block_rows_match_oracle(c5):
         assert np.linalg.norm(Yg[lo:hi] - y) <= 1e-12 * np.linalg.norm(y)
         assert np.linalg.norm(Zg[lo:hi] - z) <= 1e-12 * np.linalg.norm(z)
         # the bases are compared as subspaces: the trailing columns of a
-        # Householder basis rotate with rounding-level changes of the sample
-        # (by ~eps * sigma_1 / sigma_k); A_hat below is the gate
+        # Householder basis rotate with rounding-level changes of an
+        # ill-conditioned sample
         Ug = res.U[lo:hi].cpu().numpy()
         Vg = c5["V"][dt.off_h[i]:dt.off_h[i + 1]]
         assert np.linalg.norm(Ug @ Ug.T - U @ U.T, 2) <= 1e-5
@@ -141,23 +165,20 @@ def test_c5_block_rows_match_oracle(c5):
         Cg = res.core[kr:kr + K].cpu().numpy()
         Bflat = res.B.cpu().numpy()
         bbase = dt.b_off_h[sh.p0]
-        arow = 0.0
-        dA2 = 0.0
+        Bg = {}
         for q in range(dt.nptr_h[i], dt.nptr_h[i + 1]):
             j = int(dt.nidx_h[q])
-            mj = int(dt.sizes[j])
-            Bg = Bflat[dt.b_off_h[q] - bbase:dt.b_off_h[q + 1] - bbase].reshape(hi - lo, mj)
-            dA2 += np.linalg.norm(Bg - Bn[j]) ** 2
-            arow += np.linalg.norm(Bn[j]) ** 2
-        # A_hat(I_i, :) = U_i C_i blockdiag(V)^T + B_i: far part through the core rows
-        Vh = c5["V"]
-        for j in range(dt.b):
-            Vj = Vh[dt.off_h[j]:dt.off_h[j + 1]]
-            d = Ug @ Cg[:, j * K:(j + 1) * K] @ Vj.T - U @ C[:, j * K:(j + 1) * K] @ Vj.T
-            dA2 += np.linalg.norm(d) ** 2
+            Bg[j] = Bflat[dt.b_off_h[q] - bbase:dt.b_off_h[q + 1] - bbase].reshape(hi - lo, int(dt.sizes[j]))
         A_row = np.linalg.norm(O.kernel_block(c5["pts"].coords, c5["tess"].blocks[i],
                                               np.arange(c5["tess"].n_points), "inv", DIAG))
-        assert np.sqrt(dA2) <= 1e-10 * A_row, (i, np.sqrt(dA2) / A_row)
+        dist = _ahat_row_distance(c5, i, Ug, Cg, Bg, U, C, Bn) / A_row
+        sens = _ahat_row_distance(c5, i, U, C, Bn, U2, C2, Bn2) / A_row
+        report.append((i, float(rho[i]), dist, sens))
+    for i, rh, dist, sens in report:
+        print(f"c5 row {i}: aspect ratio {rh:.2e}  ||dA_hat||/||A_row|| = {dist:.2e}  "
+              f"oracle 1-ulp sensitivity {sens:.2e}")
+    for i, rh, dist, sens in report:
+        assert dist <= max(1e-10, 2.0 * sens), (i, dist, sens)
 
 
 def test_c5_exact_frobenius_error_of_shards(c5):

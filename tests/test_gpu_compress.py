@@ -329,7 +329,9 @@ def test_generic_block_sizes_and_ranks_vs_oracle(per, b, k, mid):
     nA = np.linalg.norm(A)
     D_gpu, D_ref = rep.to_dense(), orep.to_dense()
     assert np.linalg.norm(D_gpu - D_ref) / nA <= TOL
-    assert np.linalg.norm(A - D_gpu) / nA <= 1.05 * np.linalg.norm(A - D_ref) / nA + 1e-15
+    # (k = 70 on 144-169-point blocks is exact to rounding: both errors sit
+    # near 1e-15, where the 1.05x ratio is not meaningful; floor 1e-13)
+    assert np.linalg.norm(A - D_gpu) / nA <= max(1.05 * np.linalg.norm(A - D_ref) / nA, 1e-13)
 
 
 def test_paper_scale_suggested_blocks():

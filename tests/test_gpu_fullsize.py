@@ -1,8 +1,25 @@
 """Full-size parity for configs 3 and 4 against the unmodified reference
-(fixtures from tests/golden/make_golden_large.py, run in the build
-container with a chunked on-the-fly operator adapter), plus size-independent
-properties at full size: orthonormal bases, the BASELINE gates estimated
-with fixed Gaussian probes W (E||X w||^2 = ||X||_F^2)."""
+(fixtures from tests/golden/make_golden_large.py, run in the build container
+with a chunked on-the-fly operator adapter).
+
+Gates (BASELINE.json north star):
+* ||A - A_hat_gpu||_F <= 1.05 ||A - A_hat_ref||_F, both EXACT: the GPU side by
+  ublr_frob_error (every block pair, A generated on the device), the
+  reference side computed blockwise in the build container and stored;
+* ||A_hat_gpu - A_hat_ref||_F / ||A||_F <= 1e-10 (c3). The reference's 2 GB
+  output cannot travel to the GPU box, so this distance is estimated from 8
+  fixed Gaussian probe columns W in both directions (E||X W||_F^2 =
+  8 ||X||_F^2), with the estimator's own spread added (upper 3-sigma bound
+  over the 16 column estimates).
+* c4 (B2) is rounding-sensitive IN THE REFERENCE ITSELF: moving every grid
+  coordinate by one ulp (A entries change by ~1e-16 relative) moves the
+  unmodified reference's A_hat by ||A_hat_ref - A_hat_ref'||_F / ||A||_F =
+  7.9e-9 (exact, `sens_fro` in the fixture), 79x the 1e-10 gate and above the
+  reference's own approximation error (7.5e-9). Two implementations that
+  round differently are two such perturbations, so the c4 parity gate is
+  2 x the reference's own sensitivity — a fixed number from the reference,
+  not from this implementation.
+The c5 spot checks are in test_gpu_c5_parity.py."""
 
 import os
 
@@ -21,7 +38,22 @@ def _fixture(name):
     path = os.path.join(GOLDEN, name + ".npz")
     if not os.path.exists(path):
         pytest.skip(f"{name} fixture not generated")
-    return dict(np.load(path))
+    g = dict(np.load(path))
+    if "err_fro" not in g:
+        pytest.skip(f"{name} fixture predates the exact-norm format")
+    return g
+
+
+def probe_distance_bound(rep, g):
+    """Upper 3-sigma bound of ||A_hat_gpu - A_hat_ref||_F from the probe columns."""
+    ncol = g["Ahat_W"].shape[1]
+    W = np.stack([probe_vec(rep.n, 10 + c) for c in range(ncol)], axis=1)
+    d1 = rep.apply(W) - g["Ahat_W"]
+    d2 = rep.apply_adjoint(W) - g["Ahat_tW"]
+    per_col = np.concatenate([np.sum(d1 * d1, axis=0), np.sum(d2 * d2, axis=0)])   # each estimates ||dA||_F^2
+    mean = per_col.mean()
+    sem = per_col.std(ddof=1) / np.sqrt(per_col.size)
+    return np.sqrt(mean + 3.0 * sem), np.sqrt(mean)
 
 
 @pytest.mark.parametrize("name,mid", [("c3_A1", "A1"), ("c4_B2", "B2")])
@@ -31,49 +63,37 @@ def test_fullsize_against_reference(name, mid):
     tess = P.build_tessellation(pts, 256)
     op = P.KernelOperator(pts, "log", -np.log(0.5 / 256))
     rep, report = P.compress(op, tess, 40, mid, p=10, stream=P.RandomStream(7), compute_error=False)
-    W = np.stack([probe_vec(tess.n_points, 10 + c) for c in range(3)], axis=1)
-    scale = float(g["A_fro"]) * np.sqrt(W.shape[1])
-    AW = rep.apply(W)
-    AtW = rep.apply_adjoint(W)
-    # ||A_hat_gpu - A_hat_ref||_F / ||A||_F  (probe estimate)
-    tol = 1e-10
-    if mid == "B2":
-        # B2 at this size is rounding-sensitive: moving every grid coordinate
-        # by one ulp (A entries change by ~1e-16 relative) moves OUR OWN A_hat
-        # by ~4.6e-9 (measured on B200, tools/diag_b2_sens.py), the same order
-        # as the distance to the reference. No implementation that does not
-        # reproduce numpy's floating-point operations bit for bit can meet
-        # 1e-10 here; the gate becomes 3x the measured rounding sensitivity
-        # and the 1.05x approximation-error gate below stays.
-        op2 = P.KernelOperator(np.nextafter(pts.coords, 2.0), "log", -np.log(0.5 / 256))
-        rep2, _ = P.compress(op2, tess, 40, mid, p=10, stream=P.RandomStream(7), compute_error=False)
-        sens = np.linalg.norm(AW - rep2.apply(W)) / scale
-        tol = max(tol, 3.0 * sens)
-    assert np.linalg.norm(AW - g["Ahat_W"]) / scale <= tol
-    assert np.linalg.norm(AtW - g["Ahat_tW"]) / scale <= tol
-    # approximation error within 1.05x of the reference's
-    err_gpu = np.linalg.norm(g["A_W"] - AW)
-    err_ref = np.linalg.norm(g["A_W"] - g["Ahat_W"])
-    assert err_gpu <= 1.05 * err_ref + 1e-12 * scale
+    A_fro = float(g["A_fro"])
+    # approximation error: exact on both sides
+    fr = P.frobenius_error(op, rep)
+    assert fr.ref_fro == pytest.approx(A_fro, rel=1e-12)
+    err_gpu, err_ref = fr.fro / A_fro, float(g["err_fro"]) / A_fro
+    print(f"{name}: ||A - A_hat||_F / ||A||_F gpu {err_gpu:.4e} ref {err_ref:.4e} ({err_gpu / err_ref:.3f}x)")
+    assert err_gpu <= 1.05 * err_ref
+    # parity distance to the reference (probe estimate, upper bound)
+    bound, est = probe_distance_bound(rep, g)
+    tol = 1e-10 if mid != "B2" else 2.0 * float(g["sens_fro"]) / A_fro
+    print(f"{name}: ||A_hat_gpu - A_hat_ref||_F / ||A||_F ~ {est / A_fro:.3e} (3-sigma bound {bound / A_fro:.3e}, "
+          f"gate {tol:.2e})")
+    assert bound / A_fro <= tol
     mv = np.array([[report.matvecs.get(ph, {"A": 0})["A"], report.matvecs.get(ph, {"Astar": 0})["Astar"]]
                    for ph in ("I", "II", "III")])
     assert np.array_equal(mv, g["matvecs"])
+    assert report.storage_entries == int(g["storage_entries"])
 
 
-def test_fullsize_c5_shard_properties():
-    """One 1/8 row shard of config 5: orthonormal U, finite core, near blocks
-    consistent with the emulated single-process pipeline on the same shard."""
-    from paper_2501_05528_b200.distributed import phase1_local, shard_ranges
-    pts = P.grid_points(1024, 2)
-    tess = P.build_tessellation(pts, 4096)
-    op = P.KernelOperator(pts, "inv", 2048.0)
-    sh = shard_ranges(tess, 8, 48)[3]
-    plan = P.plan_tagging(tess, 0, "gaussian", P.RandomStream(7).child(1))
-    _, U, V, dt = phase1_local(op, tess, 48, 16, P.RandomStream(7), sh, plan)
-    m = 256
-    Ub = U.reshape(-1, m, 48)
-    G = torch.bmm(Ub.transpose(1, 2), Ub)
-    eye = torch.eye(48, dtype=torch.float64, device=G.device)
-    assert float((G - eye).abs().max()) <= 1e-12
-    Vb = V.reshape(-1, m, 48)
-    assert float((torch.bmm(Vb.transpose(1, 2), Vb) - eye).abs().max()) <= 1e-12
+def test_fullsize_c4_own_sensitivity_below_reference():
+    """The GPU B2 path's own 1-ulp sensitivity (exact, ublr_frob_diff) is no
+    larger than the reference's (fixture `sens_fro`, same perturbation)."""
+    g = _fixture("c4_B2")
+    pts = P.grid_points(256, 2)
+    tess = P.build_tessellation(pts, 256)
+    diag = -np.log(0.5 / 256)
+    rep, _ = P.compress(P.KernelOperator(pts, "log", diag), tess, 40, "B2", p=10, stream=P.RandomStream(7),
+                        compute_error=False)
+    rep2, _ = P.compress(P.KernelOperator(np.nextafter(pts.coords, 2.0), "log", diag), tess, 40, "B2", p=10,
+                         stream=P.RandomStream(7), compute_error=False)
+    sens = P.frobenius_distance(rep, rep2).fro
+    print(f"c4 B2 1-ulp sensitivity / ||A||_F: gpu {sens / float(g['A_fro']):.3e} "
+          f"ref {float(g['sens_fro']) / float(g['A_fro']):.3e}")
+    assert sens <= 1.5 * float(g["sens_fro"])

@@ -42,9 +42,9 @@ def test_rng_long_stream_with_rowmap():
     device_normals([(st, rows, cols, 0, cols, rowmap)], out)
     want = st.normal(rows, cols)
     got = out.cpu().numpy()[perm]
-    mism = np.flatnonzero(got.ravel() != want.ravel())
-    assert len(mism) <= 5, len(mism)
-    assert np.allclose(got, want, rtol=4e-15, atol=0)
+    # bit for bit, tail samples included (log1p restated as the host libm
+    # computes it, csrc/philox_zig.cuh)
+    assert np.array_equal(got, want)
 
 
 def test_rng_many_small_streams():
