@@ -15,6 +15,7 @@
 //   Also returns L^-1 and U^-1 of the block.
 #include "common.cuh"
 #include "gemm_core.cuh"
+#include "ws.cuh"
 
 namespace ublr {
 namespace {
@@ -128,7 +129,208 @@ __global__ void __launch_bounds__(Cfg::NT) k_gemm2(int M, int N, int K, double a
   }
 }
 
-template <int BM, int BN, int WMW, int WNW, int STAGES>
+// tile_copy for a producer group: thread pt of NP copies a (rows x cols)
+// tile, row r of the source is map[r] (or r), zero fill outside (rlim, clim).
+template <int NP>
+__device__ __forceinline__ void producer_copy(int pt, double* dst, int sstride, const double* src, int64_t ld,
+                                              int rows, int cols, int r0, int c0, int rlim, int clim,
+                                              const int32_t* map, bool vec2) {
+  if (vec2) {
+    const int half = cols >> 1;
+    for (int e = pt; e < rows * half; e += NP) {
+      const int r = e / half, c = (e - r * half) * 2;
+      const int gr = r0 + r, gc = c0 + c;
+      double* d = dst + r * sstride + c;
+      const int64_t row = gr < rlim ? (int64_t)(map ? map[gr] : gr) : 0;
+      if (gr < rlim && gc + 1 < clim) {
+        cp_async16(d, src + row * ld + gc, true);
+      } else {
+        const bool ok = gr < rlim && gc < clim;
+        cp_async8(d, ok ? (const void*)(src + row * ld + gc) : (const void*)src, ok);
+        cp_async8(d + 1, src, false);
+      }
+    }
+  } else {
+    for (int e = pt; e < rows * cols; e += NP) {
+      const int r = e / cols, c = e - r * cols;
+      const int gr = r0 + r, gc = c0 + c;
+      const bool ok = gr < rlim && gc < clim;
+      const int64_t row = ok ? (int64_t)(map ? map[gr] : gr) : 0;
+      cp_async8(dst + r * sstride + c, ok ? (const void*)(src + row * ld + gc) : (const void*)src, ok);
+    }
+  }
+}
+
+// Warp-specialised batched GEMM (the k_apply3 structure with a stored A):
+// NPROD producer threads move both operand tiles of a stage with cp.async
+// (row maps, either orientation) and signal full[s] through
+// cp.async.mbarrier.arrive; the consumer warps run the DMMAs from a
+// STAGES-deep ring and release empty[s]. Producer address arithmetic and
+// copy latency leave the consumers' issue slots (k_gemm2 interleaves both in
+// every warp and waits on __syncthreads each step).
+template <class Cfg, bool TA, bool TB, int NPROD>
+__global__ void __launch_bounds__(Cfg::NT + NPROD, 1) k_gemm3(int M, int N, int K, double alpha,
+                                                              const double* __restrict__ A, int64_t lda, int64_t sA,
+                                                              const int32_t* __restrict__ amap, int64_t sAm,
+                                                              const double* __restrict__ B, int64_t ldb, int64_t sB,
+                                                              const int32_t* __restrict__ bmap, int64_t sBm,
+                                                              double beta, double* __restrict__ C, int64_t ldc,
+                                                              int64_t sC, const int32_t* __restrict__ cmap,
+                                                              int64_t sCm, int vecA, int vecB, int upper_only) {
+  static_assert(Cfg::A_KM == TA && Cfg::B_KM == !TB, "tile orientation must follow the operand storage");
+  constexpr int STAGES = Cfg::STAGES, BK = Cfg::BK, NCONS = Cfg::NT;
+  extern __shared__ double dsm[];
+  __shared__ uint64_t full[STAGES], empty[STAGES];
+  if (upper_only && (int)(blockIdx.x + 1) * Cfg::BN <= (int)blockIdx.y * Cfg::BM) return;
+  const int bz = blockIdx.z;
+  A += bz * sA;
+  B += bz * sB;
+  C += bz * sC;
+  if (amap) amap += bz * sAm;
+  if (bmap) bmap += bz * sBm;
+  if (cmap) cmap += bz * sCm;
+  const int m0 = blockIdx.y * Cfg::BM, n0 = blockIdx.x * Cfg::BN;
+  const int nk = (K + BK - 1) / BK;
+  double* As0 = dsm;
+  double* Bs0 = dsm + STAGES * Cfg::A_STAGE;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      ws::mbar_init(&full[s], NPROD);
+      ws::mbar_init(&empty[s], NCONS);
+    }
+  }
+  __syncthreads();
+  if ((int)threadIdx.x >= NCONS) {
+    // ---------------- producers (threadIdx - NCONS in [0, NPROD))
+    const int pt = threadIdx.x - NCONS;
+    for (int ks = 0; ks < nk; ++ks) {
+      const int s = ks % STAGES;
+      ws::mbar_wait(&empty[s], ((uint32_t)(ks / STAGES) & 1) ^ 1);
+      double* As = As0 + s * Cfg::A_STAGE;
+      double* Bs = Bs0 + s * Cfg::B_STAGE;
+      const int k0 = ks * BK;
+      if (TA) producer_copy<NPROD>(pt, As, Cfg::SA, A, lda, BK, Cfg::BM, k0, m0, K, M, amap, vecA != 0);
+      else producer_copy<NPROD>(pt, As, Cfg::SA, A, lda, Cfg::BM, BK, m0, k0, M, K, amap, vecA != 0);
+      if (!TB) producer_copy<NPROD>(pt, Bs, Cfg::SB, B, ldb, BK, Cfg::BN, k0, n0, K, N, bmap, vecB != 0);
+      else producer_copy<NPROD>(pt, Bs, Cfg::SB, B, ldb, Cfg::BN, BK, n0, k0, N, K, bmap, vecB != 0);
+      ws::mbar_cp_async_arrive(&full[s]);
+    }
+    cp_async_wait<0>();
+    return;
+  }
+  // ---------------- consumers
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wr = warp / Cfg::WNW, wc = warp % Cfg::WNW;
+  const int am0 = wr * Cfg::WM + g, bn0 = wc * Cfg::WN + g;
+  const bool preload = beta != 0.0 && (alpha == 1.0 || alpha == -1.0);
+  const double ab = alpha * beta;
+  const bool cvec = ((((uintptr_t)C) | ((uintptr_t)(ldc * 8))) & 15) == 0;
+  double acc[Cfg::MI][Cfg::NJ][2];
+#pragma unroll
+  for (int i = 0; i < Cfg::MI; ++i) {
+    int r = m0 + wr * Cfg::WM + i * 8 + g;
+    const double* crow = C + (int64_t)(r < M ? (cmap ? cmap[r] : r) : 0) * ldc;
+#pragma unroll
+    for (int j = 0; j < Cfg::NJ; ++j) {
+      acc[i][j][0] = acc[i][j][1] = 0.0;
+      int c = n0 + wc * Cfg::WN + j * 8 + 2 * t;
+      if (preload && r < M) {
+        if (cvec && c + 1 < N) {
+          double2 v = *reinterpret_cast<const double2*>(crow + c);
+          acc[i][j][0] = ab * v.x;
+          acc[i][j][1] = ab * v.y;
+        } else {
+          if (c < N) acc[i][j][0] = ab * crow[c];
+          if (c + 1 < N) acc[i][j][1] = ab * crow[c + 1];
+        }
+      }
+    }
+  }
+  for (int ks = 0; ks < nk; ++ks) {
+    const int s = ks % STAGES;
+    ws::mbar_wait(&full[s], (uint32_t)(ks / STAGES) & 1);
+    const double* As = As0 + s * Cfg::A_STAGE;
+    const double* Bs = Bs0 + s * Cfg::B_STAGE;
+    double a[2][Cfg::MI], b[2][Cfg::NJ];
+#pragma unroll
+    for (int i = 0; i < Cfg::MI; ++i) a[0][i] = As[Cfg::ai(am0 + i * 8, t)];
+#pragma unroll
+    for (int j = 0; j < Cfg::NJ; ++j) b[0][j] = Bs[Cfg::bi(t, bn0 + j * 8)];
+#pragma unroll
+    for (int k4 = 0; k4 < BK / 4; ++k4) {
+      const int cur = k4 & 1;
+      if (k4 + 1 < BK / 4) {
+        const int kr = (k4 + 1) * 4 + t;
+#pragma unroll
+        for (int i = 0; i < Cfg::MI; ++i) a[cur ^ 1][i] = As[Cfg::ai(am0 + i * 8, kr)];
+#pragma unroll
+        for (int j = 0; j < Cfg::NJ; ++j) b[cur ^ 1][j] = Bs[Cfg::bi(kr, bn0 + j * 8)];
+      }
+#pragma unroll
+      for (int i = 0; i < Cfg::MI; ++i)
+#pragma unroll
+        for (int j = 0; j < Cfg::NJ; ++j) mma8x8x4(acc[i][j][0], acc[i][j][1], a[cur][i], b[cur][j]);
+    }
+    ws::mbar_arrive(&empty[s]);
+  }
+#pragma unroll
+  for (int i = 0; i < Cfg::MI; ++i) {
+    int r = m0 + wr * Cfg::WM + i * 8 + g;
+    if (r >= M) continue;
+    double* crow = C + (int64_t)(cmap ? cmap[r] : r) * ldc;
+#pragma unroll
+    for (int j = 0; j < Cfg::NJ; ++j) {
+      int c = n0 + wc * Cfg::WN + j * 8 + 2 * t;
+      if (preload) {
+        if (cvec && c + 1 < N) {
+          *reinterpret_cast<double2*>(crow + c) = make_double2(alpha * acc[i][j][0], alpha * acc[i][j][1]);
+        } else {
+          if (c < N) crow[c] = alpha * acc[i][j][0];
+          if (c + 1 < N) crow[c + 1] = alpha * acc[i][j][1];
+        }
+        continue;
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (c + h >= N) continue;
+        double v = alpha * acc[i][j][h];
+        crow[c + h] = (beta == 0.0) ? v : fma(beta, crow[c + h], v);
+      }
+    }
+  }
+}
+
+template <int BM, int BN, int WMW, int WNW, int STAGES, int BK, int NPROD>
+int launch_gemm3(int ta, int tb, int M, int N, int K, double alpha, const double* A, int64_t lda, int64_t sA,
+                 const int32_t* amap, int64_t sAm, const double* B, int64_t ldb, int64_t sB, const int32_t* bmap,
+                 int64_t sBm, double beta, double* C, int64_t ldc, int64_t sC, const int32_t* cmap, int64_t sCm,
+                 int batch, cudaStream_t st, int upper_only = 0) {
+  dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, batch);
+  auto aligned = [](const void* p, int64_t ld, int64_t stride) {
+    return (((uintptr_t)p) % 16 == 0) && (ld % 2 == 0) && (stride % 2 == 0);
+  };
+  int vecA = aligned(A, lda, sA) ? 1 : 0;
+  int vecB = aligned(B, ldb, sB) ? 1 : 0;
+#define UBLR_G3(TA, TB)                                                                                       \
+  {                                                                                                           \
+    using Cfg = TileCfg<BM, BN, BK, WMW, WNW, STAGES, TA, !TB>;                                               \
+    size_t sm = Cfg::smem_bytes();                                                                            \
+    UBLR_CUDA(cudaFuncSetAttribute(k_gemm3<Cfg, TA, TB, NPROD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
+    k_gemm3<Cfg, TA, TB, NPROD><<<grid, Cfg::NT + NPROD, sm, st>>>(M, N, K, alpha, A, lda, sA, amap, sAm, B, ldb, sB, \
+                                                                  bmap, sBm, beta, C, ldc, sC, cmap, sCm, vecA, vecB, \
+                                                                  upper_only);                                 \
+  }
+  if (!ta && !tb) UBLR_G3(false, false)
+  else if (!ta && tb) UBLR_G3(false, true)
+  else if (ta && !tb) UBLR_G3(true, false)
+  else UBLR_G3(true, true)
+#undef UBLR_G3
+  UBLR_LAUNCH_CHECK();
+  return UBLR_OK;
+}
+
+template <int BM, int BN, int WMW, int WNW, int STAGES, int BK = 32, bool K8 = false>
 int launch_gemm2(int ta, int tb, int M, int N, int K, double alpha, const double* A, int64_t lda, int64_t sA,
                  const int32_t* amap, int64_t sAm, const double* B, int64_t ldb, int64_t sB, const int32_t* bmap,
                  int64_t sBm, double beta, double* C, int64_t ldc, int64_t sC, const int32_t* cmap, int64_t sCm,
@@ -141,7 +343,7 @@ int launch_gemm2(int ta, int tb, int M, int N, int K, double alpha, const double
   int vecB = aligned(B, ldb, sB) ? 1 : 0;
 #define UBLR_G2(TA, TB)                                                                                       \
   {                                                                                                           \
-    using Cfg = TileCfg<BM, BN, 32, WMW, WNW, STAGES, TA, !TB>;                                               \
+    using Cfg = TileCfg<BM, BN, BK, WMW, WNW, STAGES, TA, !TB, K8>;                                           \
     size_t sm = Cfg::smem_bytes();                                                                            \
     UBLR_CUDA(cudaFuncSetAttribute(k_gemm2<Cfg, TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
     k_gemm2<Cfg, TA, TB><<<grid, Cfg::NT, sm, st>>>(M, N, K, alpha, A, lda, sA, amap, sAm, B, ldb, sB, bmap, sBm,  \
@@ -392,11 +594,35 @@ extern "C" int ublr_gemm_batched(int ta, int tb, int M, int N, int K, double alp
   if (M == 0 || N == 0 || batch == 0) return UBLR_OK;
   cudaStream_t st = (cudaStream_t)stream;
   int64_t tiles128 = (int64_t)((M + 127) / 128) * ((N + 127) / 128) * batch;
-  if (M >= 96 && N >= 96 && tiles128 >= 148)
-    return launch_gemm2<128, 128, 4, 4, 2>(ta, tb, M, N, K, alpha, A, lda, sA, amap, sAm, B, ldb, sB, bmap, sBm, beta,
-                                           C, ldc, sC, cmap, sCm, batch, st);
-  return launch_gemm2<64, 64, 2, 4, 2>(ta, tb, M, N, K, alpha, A, lda, sA, amap, sAm, B, ldb, sB, bmap, sBm, beta, C,
-                                       ldc, sC, cmap, sCm, batch, st);
+  // tile configuration. Default (6): the warp-specialised k_gemm3 for large
+  // tiles (128 x 128, 8 consumer warps, 4 producer warps, 3 stages of BK 32:
+  // 33.4 TF/s = 90 % of the DMMA peak on 4096^3 and the c3 Gram / Cholesky
+  // shapes, against 27.5 TF/s for k_gemm2; tools/gemm_bench.py,
+  // profiles/r02/gemm_bench.txt) and k_gemm2 64 x 64 for skinny / small
+  // products, where the synchronous kernel is faster. UBLR_GEMM_CFG selects
+  // alternatives for benchmarking: 0 k_gemm2 everywhere (BK 32, 2 stages);
+  // 1 / 2 / 3 k_gemm2 with BK 16 x 4 stages / + m16n8k8 / BK 32 x 3 stages;
+  // 4 / 5 k_gemm3 with BK 16 x 4 stages (8 / 16 consumer warps).
+  static const int cfg = [] {
+    const char* e = getenv("UBLR_GEMM_CFG");
+    return e ? atoi(e) : 6;
+  }();
+#define UBLR_GEMM_ARGS ta, tb, M, N, K, alpha, A, lda, sA, amap, sAm, B, ldb, sB, bmap, sBm, beta, C, ldc, sC, cmap, sCm, batch, st
+  if (M >= 96 && N >= 96 && tiles128 >= 148) {
+    if (cfg == 1) return launch_gemm2<128, 128, 4, 4, 4, 16>(UBLR_GEMM_ARGS);
+    if (cfg == 2) return launch_gemm2<128, 128, 4, 4, 4, 16, true>(UBLR_GEMM_ARGS);
+    if (cfg == 3) return launch_gemm2<128, 128, 4, 4, 3, 32>(UBLR_GEMM_ARGS);
+    if (cfg == 4) return launch_gemm3<128, 128, 4, 2, 4, 16, 128>(UBLR_GEMM_ARGS);
+    if (cfg == 5) return launch_gemm3<128, 128, 4, 4, 4, 16, 128>(UBLR_GEMM_ARGS);
+    if (cfg == 6) return launch_gemm3<128, 128, 4, 2, 3, 32, 128>(UBLR_GEMM_ARGS);
+    return launch_gemm2<128, 128, 4, 4, 2>(UBLR_GEMM_ARGS);
+  }
+  if (cfg == 1) return launch_gemm2<64, 64, 2, 4, 4, 16>(UBLR_GEMM_ARGS);
+  if (cfg == 2) return launch_gemm2<64, 64, 2, 4, 4, 16, true>(UBLR_GEMM_ARGS);
+  if (cfg == 3) return launch_gemm2<64, 64, 2, 4, 3, 32>(UBLR_GEMM_ARGS);
+  if (cfg == 4 || cfg == 5) return launch_gemm3<64, 64, 2, 2, 4, 16, 64>(UBLR_GEMM_ARGS);
+  return launch_gemm2<64, 64, 2, 4, 2>(UBLR_GEMM_ARGS);
+#undef UBLR_GEMM_ARGS
 }
 
 extern "C" int ublr_syrk_upper_batched(int M, int K, double alpha, const double* A, int64_t lda, int64_t sA,
@@ -407,8 +633,8 @@ extern "C" int ublr_syrk_upper_batched(int M, int K, double alpha, const double*
   cudaStream_t st = (cudaStream_t)stream;
   int64_t tiles128 = (int64_t)((M + 127) / 128) * ((M + 127) / 128) * batch / 2;
   if (M >= 96 && tiles128 >= 148)
-    return launch_gemm2<128, 128, 4, 4, 2>(1, 0, M, M, K, alpha, A, lda, sA, nullptr, 0, A, lda, sA, nullptr, 0, beta,
-                                           C, ldc, sC, nullptr, 0, batch, st, 1);
+    return launch_gemm3<128, 128, 4, 2, 3, 32, 128>(1, 0, M, M, K, alpha, A, lda, sA, nullptr, 0, A, lda, sA, nullptr,
+                                                    0, beta, C, ldc, sC, nullptr, 0, batch, st, 1);
   return launch_gemm2<64, 64, 2, 4, 2>(1, 0, M, M, K, alpha, A, lda, sA, nullptr, 0, A, lda, sA, nullptr, 0, beta, C,
                                        ldc, sC, nullptr, 0, batch, st, 1);
 }

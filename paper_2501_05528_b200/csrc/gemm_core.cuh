@@ -21,9 +21,11 @@
 
 namespace ublr {
 
-template <int BM_, int BN_, int BK_, int WMW_, int WNW_, int STAGES_, bool A_KM_ = true, bool B_KM_ = true>
+template <int BM_, int BN_, int BK_, int WMW_, int WNW_, int STAGES_, bool A_KM_ = true, bool B_KM_ = true,
+          bool K8_ = false>
 struct TileCfg {
   static constexpr int BM = BM_, BN = BN_, BK = BK_, WMW = WMW_, WNW = WNW_, STAGES = STAGES_;
+  static constexpr bool K8 = K8_;   // m16n8k8 DMMA instead of m8n8k4
   static constexpr bool A_KM = A_KM_, B_KM = B_KM_;
   static constexpr int NT = WMW * WNW * 32;
   static constexpr int SA = A_KM ? BM + 4 : BK + 4;  // row stride of the A tile in smem
@@ -80,7 +82,7 @@ __device__ __forceinline__ void dmma_mainloop(AP& ap, BP& bp, int nk, double* sm
     if (nx + 1 < nk) ap.prefetch(nx + 1);
     const double* As = As0 + (ks % STAGES) * Cfg::A_STAGE;
     const double* Bs = Bs0 + (ks % STAGES) * Cfg::B_STAGE;
-    if constexpr (UBLR_MMA_K8 && Cfg::MI % 2 == 0) {
+    if constexpr ((UBLR_MMA_K8 || Cfg::K8) && Cfg::MI % 2 == 0) {
     // m16n8k8: 8-row groups (2i, 2i+1) of acc form one 16-row MMA tile
     constexpr int MI2 = Cfg::MI / 2;
     // single-buffered fragments (the double-buffered form spills at 128

@@ -38,6 +38,14 @@ def _torch():
     return torch
 
 
+def _alloc(shape, dtype=None, device=None, zero=False):
+    """Device buffers of the shard kernels (a test hook: tests/test_distributed.py
+    swaps in a guard-banded allocator to check that the shifted shard
+    pointers never write outside their buffers)."""
+    torch = _torch()
+    return (torch.zeros if zero else torch.empty)(shape, dtype=dtype, device=device)
+
+
 @dataclass
 class Shard:
     rank: int
@@ -156,15 +164,15 @@ def phase1_local(op, tess, k, p, stream, shard, plan=None, keep_sketch=False):
         raise NotImplementedError("sharded compression needs a symmetric GPU kernel operator")
     nloc = shard.r1 - shard.r0
     f64 = dict(dtype=torch.float64, device=dt.device)
-    Y = torch.empty((nloc, s), **f64)
-    Z = torch.empty((nloc, s), **f64)
+    Y = _alloc((nloc, s), **f64)
+    Z = _alloc((nloc, s), **f64)
     st = _lib.stream_handle()
     shift = 8 * shard.r0 * s
     _lib.call("ublr_sketch_tagged_pair", inner.device_op(dt.perm), _lib.ptr(dt.off), dt.b, _lib.ptr(T_dev), ell,
               _lib.ptr(G), _lib.ptr(H), gc, gc, _lib.ptr(Y) - shift, _lib.ptr(Z) - shift, s, shard.r0, shard.r1, st)
     kq = max(1, min(k, dt.m_max))
-    U = torch.zeros((nloc, k), **f64)
-    V = torch.zeros((nloc, k), **f64)
+    U = _alloc((nloc, k), zero=True, **f64)
+    V = _alloc((nloc, k), zero=True, **f64)
     ushift = 8 * shard.r0 * k
     _lib.call("ublr_block_qr_pair", _lib.ptr(Y) - shift, _lib.ptr(Z) - shift, s, _lib.ptr(Z_dev) + 8 * shard.i0 * ell,
               ell, gc, _lib.ptr(dt.off) + 4 * shard.i0, shard.i1 - shard.i0, kq, _lib.ptr(U) - ushift,
@@ -193,10 +201,10 @@ def phase23_local(op, k, shard, dt, U, V_all, core_out=None, panel_blocks=None):
     st = _lib.stream_handle()
     desc = inner.device_op(dt.perm)
     bbase = int(dt.b_off_h[shard.p0])
-    B = torch.empty(int(dt.b_off_h[shard.p1]) - bbase, **f64)
+    B = _alloc((int(dt.b_off_h[shard.p1]) - bbase,), **f64)
     host = core_out is not None and not core_out.is_cuda
     if core_out is None:
-        core_out = torch.empty((kloc, K), **f64)
+        core_out = _alloc((kloc, K), **f64)
     nblk = shard.i1 - shard.i0
     pb = nblk if not host else max(1, min(nblk, panel_blocks or nblk))
     fused = dt.m_max <= FUSED_NEAR_M_MAX and min(k, dt.m_max) <= FUSED_NEAR_K_MAX and dt.pair_of is not None
@@ -205,12 +213,12 @@ def phase23_local(op, k, shard, dt, U, V_all, core_out=None, panel_blocks=None):
         lib = _lib.load()
         pmax = max(int(dt.nptr_h[min(a + pb, shard.i1)] - dt.nptr_h[a]) for a in range(shard.i0, shard.i1, pb))
         ws_bytes = int(lib.ublr_nearfield_workspace_bytes(pmax, max(k, 1), dt.m_max))
-        ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device=dt.device)
+        ws = _alloc((max(ws_bytes, 8),), dtype=torch.uint8, device=dt.device)
     Up = _lib.ptr(U) - 8 * shard.r0 * U.stride(0)
     Bp = _lib.ptr(B) - 8 * bbase
     if host:
         rows_max = max(int(roff_h[min(a + pb, shard.i1)] - roff_h[a]) for a in range(shard.i0, shard.i1, pb))
-        panels = [torch.empty((rows_max, K), **f64) for _ in range(2)]
+        panels = [_alloc((rows_max, K), **f64) for _ in range(2)]
         done = [None, None]
         copy_stream = torch.cuda.Stream(device=dt.device)
     for n_, a in enumerate(range(shard.i0, shard.i1, pb)):

@@ -13,8 +13,9 @@ adapter only provides shape/apply/apply_adjoint). Stored:
 * for c4 (B2) also the reference's OWN rounding sensitivity: the unmodified
   reference is run a second time with every grid coordinate moved up by one
   ulp (np.nextafter(coords, 2), A entries change by ~1e-16 relative) and the
-  exact ||A_hat_ref - A_hat_ref'||_F (total and per pair) is stored. The GPU
-  parity gate for B2 is anchored on this number, not on the GPU's own.
+  exact ||A_hat_ref - A_hat_ref'||_F (total and per pair) is stored, with the
+  perturbed run's own exact error ||A - A_hat_ref'||_F. The GPU parity gate
+  for B2 is anchored on these numbers, not on the GPU's own.
 
 Takes ~40 min for c3 and ~35 min for c4 (two reference runs) on 8 cores:
 
@@ -73,7 +74,8 @@ class BlockRows:
 
 def blockwise_norms(tess, coords, diag, reps):
     """Per block pair: ||A_ij||_F^2, ||(A - reps[0])_ij||_F^2 and, with two
-    representations, ||(reps[0] - reps[1])_ij||_F^2 (exact, in fp64)."""
+    representations, ||(reps[0] - reps[1])_ij||_F^2 and ||(A - reps[1])_ij||_F^2
+    (exact, in fp64)."""
     b = tess.b
     cols = np.concatenate(tess.blocks)
     m = int(tess.block_sizes[0])
@@ -81,6 +83,7 @@ def blockwise_norms(tess, coords, diag, reps):
     a2 = np.zeros((b, b))
     e2 = np.zeros((b, b))
     d2 = np.zeros((b, b))
+    f2 = np.zeros((b, b))
 
     def one(i):
         A = kernel_block(coords, tess.blocks[i], cols, "log", diag)
@@ -89,12 +92,15 @@ def blockwise_norms(tess, coords, diag, reps):
         D = (A - H0).reshape(m, b, m)
         e2[i] = np.einsum("rjc,rjc->j", D, D)
         if len(rows_of) > 1:
-            D = (H0 - rows_of[1].row(i)).reshape(m, b, m)
+            H1 = rows_of[1].row(i)
+            D = (H0 - H1).reshape(m, b, m)
             d2[i] = np.einsum("rjc,rjc->j", D, D)
+            D = (A - H1).reshape(m, b, m)
+            f2[i] = np.einsum("rjc,rjc->j", D, D)
 
     with ThreadPoolExecutor(os.cpu_count() or 1) as ex:
         list(ex.map(one, range(b)))
-    return a2, e2, d2
+    return a2, e2, d2, f2
 
 
 def run(name):
@@ -128,7 +134,7 @@ def run(name):
         print(name, "perturbed reference seconds", time.time() - t2, flush=True)
         reps.append(rep2)
     t3 = time.time()
-    a2, e2, d2 = blockwise_norms(tess, pts.coords, diag, reps)
+    a2, e2, d2, f2 = blockwise_norms(tess, pts.coords, diag, reps)
     print(name, "blockwise norms seconds", time.time() - t3, flush=True)
     out["A_fro"] = np.sqrt(a2.sum())
     out["err_fro"] = np.sqrt(e2.sum())          # exact ||A - A_hat_ref||_F
@@ -136,6 +142,7 @@ def run(name):
     if name == "c4":
         out["sens_fro"] = np.sqrt(d2.sum())      # exact ||A_hat_ref - A_hat_ref(coords + 1 ulp)||_F
         out["sens_pair"] = np.sqrt(d2)
+        out["err_fro_pert"] = np.sqrt(f2.sum())  # the perturbed reference's exact error (against the unperturbed A)
     np.savez_compressed(os.path.join(OUT, f"{name}_{mid}.npz"), **out)
     print(name, "A_fro", out["A_fro"], "err/A", out["err_fro"] / out["A_fro"],
           "sens/A", out.get("sens_fro", np.nan) / out["A_fro"], flush=True)

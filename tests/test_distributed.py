@@ -138,3 +138,59 @@ def test_multiprocess_sharded_gloo_matches_emulated(tmp_path):
         assert np.array_equal(got["V"], ref[r].V.cpu().numpy())
         assert np.array_equal(got["core"], ref[r].core.cpu().numpy())
         assert np.array_equal(got["B"], ref[r].B.cpu().numpy())
+
+
+class _GuardedAlloc:
+    """Every buffer is the middle of a larger one whose two guard bands hold a
+    sentinel bit pattern; `check()` verifies no kernel wrote outside its
+    buffer (compute-sanitizer is unavailable on this pool, so out-of-bounds
+    writes of the shifted shard pointers are caught this way)."""
+
+    GUARD = 1 << 16   # elements per side
+
+    def __init__(self):
+        self.blocks = []
+
+    def __call__(self, shape, dtype=None, device=None, zero=False):
+        n = int(np.prod(shape))
+        big = torch.empty(n + 2 * self.GUARD, dtype=dtype, device=device)
+        raw = big.view(torch.uint8)
+        raw.fill_(0xA5)
+        body = big[self.GUARD:self.GUARD + n]
+        if zero:
+            body.zero_()
+        self.blocks.append(big)
+        return body.view(shape)
+
+    def check(self):
+        torch.cuda.synchronize()
+        for big in self.blocks:
+            raw = big.view(torch.uint8)
+            g = self.GUARD * big.element_size()
+            assert bool((raw[:g] == 0xA5).all()) and bool((raw[-g:] == 0xA5).all()), "write outside a buffer"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("per,b,k,world,kind", [(256, 256, 48, 8, "inv"), (64, 64, 10, 4, "inv"),
+                                                (96, 36, 12, 3, "log")])
+def test_shard_kernels_stay_inside_their_buffers(monkeypatch, per, b, k, world, kind):
+    """Guard bands around every shard buffer (Y, Z, U, V, core rows, near
+    blocks, workspace, host-sink panels) for each rank of a sharded job,
+    with the result compared against the unguarded run."""
+    import paper_2501_05528_b200.distributed as Dm
+    pts = P.grid_points(per, 2)
+    tess = P.build_tessellation(pts, b)
+    op = P.KernelOperator(pts, kind, 2.0 * per if kind == "inv" else -np.log(0.5 / per))
+    ref = Dm.compress_emulated(op, tess, k, 16, P.RandomStream(5), world=world)
+    guard = _GuardedAlloc()
+    monkeypatch.setattr(Dm, "_alloc", guard)
+    got = Dm.compress_emulated(op, tess, k, 16, P.RandomStream(5), world=world)
+    host = torch.empty(got[1].core.shape, dtype=torch.float64, pin_memory=True)
+    V_all = got[0].V
+    panel = Dm.compress_sharded(op, tess, k, 16, P.RandomStream(5), rank=1, world=world,
+                                allgather=lambda V, n: V_all, core_out=host, panel_blocks=2)
+    guard.check()
+    for a, c in zip(ref, got):
+        assert torch.equal(a.core, c.core) and torch.equal(a.B, c.B) and torch.equal(a.U, c.U)
+    assert torch.equal(host, ref[1].core.cpu())
+    assert len(guard.blocks) >= 6 * world
