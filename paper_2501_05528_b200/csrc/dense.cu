@@ -502,6 +502,274 @@ __global__ void __launch_bounds__(FT) k_lu_sign_diag(double* W, int64_t ldw, int
   for (int e = threadIdx.x; e < nb * nb; e += FT) Ub[e] = I[e];
 }
 
+// ------------------------------------------------- register-tile leaves
+// 64 x 64 diagonal-block factorisations for nb <= 64 with the block held in
+// registers: 256 threads in a 16 x 16 grid, thread (tr, tc) owns rows
+// 4 tr .. 4 tr + 3 and columns 4 tc .. 4 tc + 3. Step j broadcasts the pivot
+// row (and column) through a double-buffered shared-memory vector, so each
+// elimination step costs one barrier; the 16 threads of a row group are one
+// half-warp and read the pivot by shuffle. Rows / columns past nb are padded
+// with the identity and never stored. The triangular inverses are
+// Gauss-Jordan sweeps in the same layout. (The shared-memory kernels above,
+// one barrier-separated phase per step with an integer division per entry
+// and a thread per column in the inverses, stay for 64 < nb <= 96.)
+struct RegTile {
+  int tr, tc;
+  __device__ __forceinline__ RegTile() : tr(threadIdx.x >> 4), tc(threadIdx.x & 15) {}
+  __device__ __forceinline__ unsigned half_mask() const { return (tr & 1) ? 0xffff0000u : 0x0000ffffu; }
+  // lane of thread (row group tr, column group c) inside this thread's warp
+  __device__ __forceinline__ int lane_of(int c) const { return ((tr & 1) << 4) + c; }
+};
+
+// backward Gauss-Jordan: x <- U^-1 (x starts as the identity), U upper
+// triangular held in u (only the upper part is read); rinv[a] = 1 / U[r][r]
+// for the thread's rows r = 4 tr + a (kept from the factorisation: the
+// serial chain of each step carries no division)
+__device__ __forceinline__ void regtile_inv_upper(const RegTile& T, const double (&u)[4][4], const double (&rinv)[4],
+                                                  double (&x)[4][4], double (*rowb)[64], double (*colb)[64]) {
+  for (int jb = 15; jb >= 0; --jb) {
+#pragma unroll
+    for (int jj = 3; jj >= 0; --jj) {
+      const int j = 4 * jb + jj, buf = j & 1;
+      if (T.tr == jb) {
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          x[jj][b] = x[jj][b] * rinv[jj];
+          rowb[buf][4 * T.tc + b] = x[jj][b];
+        }
+      }
+      if (T.tc == jb) {
+#pragma unroll
+        for (int a = 0; a < 4; ++a) colb[buf][4 * T.tr + a] = u[a][jj];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        if (4 * T.tr + a >= j) continue;
+        const double m = colb[buf][4 * T.tr + a];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) x[a][b] = fma(-m, rowb[buf][4 * T.tc + b], x[a][b]);
+      }
+    }
+  }
+}
+
+// forward Gauss-Jordan: x <- L^-1 (x starts as the identity), L unit lower
+// triangular held in the strictly lower part of l
+__device__ __forceinline__ void regtile_inv_unit_lower(const RegTile& T, const double (&l)[4][4], double (&x)[4][4],
+                                                       double (*rowb)[64], double (*colb)[64]) {
+  for (int jb = 0; jb < 16; ++jb) {
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const int j = 4 * jb + jj, buf = j & 1;
+      if (T.tr == jb) {
+#pragma unroll
+        for (int b = 0; b < 4; ++b) rowb[buf][4 * T.tc + b] = x[jj][b];
+      }
+      if (T.tc == jb) {
+#pragma unroll
+        for (int a = 0; a < 4; ++a) colb[buf][4 * T.tr + a] = l[a][jj];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        if (4 * T.tr + a <= j) continue;
+        const double m = colb[buf][4 * T.tr + a];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) x[a][b] = fma(-m, rowb[buf][4 * T.tc + b], x[a][b]);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_potrf64(double* A, int64_t lda, int64_t sA, int j0, int nb, double* R,
+                                                 int64_t ldr, int64_t sR, double* Rinv, int* status) {
+  __shared__ double rowb[2][64], colb[2][64];
+  const RegTile T;
+  const int bz = blockIdx.x;
+  const double* Ab = A + bz * sA + (int64_t)j0 * lda + j0;
+  double v[4][4], x[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int r = 4 * T.tr + a, c = 4 * T.tc + b;
+      v[a][b] = (r < nb && c < nb) ? Ab[(int64_t)r * lda + c] : (r == c ? 1.0 : 0.0);
+      x[a][b] = r == c ? 1.0 : 0.0;
+    }
+  bool bad = false;
+  double rinv[4] = {1.0, 1.0, 1.0, 1.0};   // 1 / R[r][r] of this thread's rows
+  // upper Cholesky, right-looking by rows: R[j, j:] = S[j, j:] / sqrt(S[j, j]),
+  // S[r, c] -= R[j, r] R[j, c] for j < r <= c
+  for (int jb = 0; jb < 16; ++jb) {
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const int j = 4 * jb + jj, buf = j & 1;
+      if (T.tr == jb) {
+        double s2 = __shfl_sync(T.half_mask(), v[jj][jj], T.lane_of(jb));
+        if (!(s2 > 0.0)) {
+          bad = true;
+          s2 = 1.0;
+        }
+        const double rs = rsqrt(s2);          // 1 / R[j][j]
+        const double d = s2 * rs;             // R[j][j]
+        rinv[jj] = rs;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int c = 4 * T.tc + b;
+          v[jj][b] = c > j ? v[jj][b] * rs : (c == j ? d : 0.0);
+          rowb[buf][c] = v[jj][b];
+        }
+      }
+      __syncthreads();
+      double rc[4];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) rc[b] = rowb[buf][4 * T.tc + b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int r = 4 * T.tr + a;
+        if (r <= j) continue;
+        const double rr = rowb[buf][r];
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          if (4 * T.tc + b >= r) v[a][b] = fma(-rr, rc[b], v[a][b]);
+      }
+    }
+  }
+  if (bad) atomicExch(status, 1);
+  __syncthreads();   // the last step's broadcast vectors are read before the inverse reuses them
+  regtile_inv_upper(T, v, rinv, x, rowb, colb);
+  double* Rb = R + bz * sR + (int64_t)j0 * ldr + j0;
+  double* Ib = Rinv + (int64_t)bz * nb * nb;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int r = 4 * T.tr + a, c = 4 * T.tc + b;
+      if (r < nb && c < nb) {
+        Rb[(int64_t)r * ldr + c] = r > c ? 0.0 : v[a][b];
+        Ib[r * nb + c] = x[a][b];
+      }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_lu_sign64(double* W, int64_t ldw, int64_t sW, int j0, int nb, double* LU,
+                                                   int64_t ldlu, int64_t sLU, double* Linv, double* Uinv, double* D,
+                                                   int64_t sD, int* status, const double* __restrict__ R, int64_t ldr,
+                                                   int64_t sR, int n) {
+  __shared__ double rowb[2][64], colb[2][64];
+  const RegTile T;
+  const int bz = blockIdx.x;
+  double* Wb = W + bz * sW + (int64_t)j0 * ldw + j0;
+  const double* Rb = R ? R + bz * sR + (int64_t)j0 * ldr + j0 : nullptr;
+  double v[4][4], rt[4][4];   // W tile; R tile (row j of D R joins at step j: loaded up front)
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int r = 4 * T.tr + a, c = 4 * T.tc + b;
+      v[a][b] = (r < nb && c < nb) ? Wb[(int64_t)r * ldw + c] : (r == c ? 1.0 : 0.0);
+      rt[a][b] = Rb ? ((r < nb && c < nb) ? Rb[(int64_t)r * ldr + c] : (r == c ? 1.0 : 0.0)) : 0.0;
+    }
+  bool bad = false;
+  __shared__ double rpivb[2];
+  double rinv[4] = {1.0, 1.0, 1.0, 1.0};   // 1 / U[r][r] of this thread's rows
+  for (int jb = 0; jb < 16; ++jb) {
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const int j = 4 * jb + jj, buf = j & 1;
+      if (T.tr == jb) {
+        // D_jj = sign(w_jj) (the working matrix is -Q eliminated so far);
+        // plain form: pivot w + D_jj; R-scaled form: row j of D R joins now
+        const double w = __shfl_sync(T.half_mask(), v[jj][jj], T.lane_of(jb));
+        const double d = (w > 0.0) ? 1.0 : -1.0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int c = 4 * T.tc + b;
+          if (Rb) {
+            if (c >= j) v[jj][b] = fma(d, rt[jj][b], v[jj][b]);
+          } else if (c == j) {
+            v[jj][b] = w + d;
+          }
+          rowb[buf][c] = v[jj][b];
+        }
+        // the pivot's reciprocal, from its owner (correctly rounded)
+        const double pv = __shfl_sync(T.half_mask(), v[jj][jj], T.lane_of(jb));
+        rinv[jj] = __drcp_rn(pv);
+        if (T.tc == jb) {
+          rpivb[buf] = rinv[jj];
+          if (j < nb) D[bz * sD + j0 + j] = d;
+        }
+      }
+      if (T.tc == jb) {
+#pragma unroll
+        for (int a = 0; a < 4; ++a) colb[buf][4 * T.tr + a] = v[a][jj];
+      }
+      __syncthreads();
+      if (rowb[buf][j] == 0.0) bad = true;
+      const double rpiv = rpivb[buf];
+      double rc[4];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) rc[b] = rowb[buf][4 * T.tc + b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int r = 4 * T.tr + a;
+        if (r <= j) continue;
+        const double m = colb[buf][r] * rpiv;
+        if (T.tc == jb) v[a][jj] = m;                 // L multiplier, stored in place
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          if (4 * T.tc + b > j) v[a][b] = fma(-m, rc[b], v[a][b]);
+      }
+    }
+  }
+  if (bad && T.tr == 0 && T.tc == 0) atomicExch(status, 1);
+  double* LUb = LU + bz * sLU + (int64_t)j0 * ldlu + j0;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int r = 4 * T.tr + a, c = 4 * T.tc + b;
+      if (r < nb && c < nb) LUb[(int64_t)r * ldlu + c] = v[a][b];
+    }
+  if (Rb && n > j0 + nb) {
+    // the panel rows' D R to the right of the block, before U12 = L11^-1 W12
+    __syncthreads();   // D of the panel written
+    const int rest = n - j0 - nb;
+    for (int r = 0; r < nb; ++r) {
+      const double d = D[bz * sD + j0 + r];
+      for (int c = threadIdx.x; c < rest; c += blockDim.x)
+        Wb[(int64_t)r * ldw + nb + c] = fma(d, Rb[(int64_t)r * ldr + nb + c], Wb[(int64_t)r * ldw + nb + c]);
+    }
+  }
+  double x[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) x[a][b] = (4 * T.tr + a == 4 * T.tc + b) ? 1.0 : 0.0;
+  __syncthreads();   // the last elimination step's broadcast vectors are read
+  regtile_inv_unit_lower(T, v, x, rowb, colb);
+  double* Lb = Linv + (int64_t)bz * nb * nb;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int r = 4 * T.tr + a, c = 4 * T.tc + b;
+      if (r < nb && c < nb) Lb[r * nb + c] = x[a][b];
+      x[a][b] = r == c ? 1.0 : 0.0;
+    }
+  __syncthreads();
+  regtile_inv_upper(T, v, rinv, x, rowb, colb);
+  double* Ub = Uinv + (int64_t)bz * nb * nb;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int r = 4 * T.tr + a, c = 4 * T.tc + b;
+      if (r < nb && c < nb) Ub[r * nb + c] = x[a][b];
+    }
+}
+
 // out[b][r][c] = src[b*s_src + map[b*s_map + r] * ld + col0 + c]   (transpose: out[b][c][r])
 __global__ void k_gather(const double* __restrict__ src, int64_t ld, int64_t s_src, const int32_t* __restrict__ map,
                          int64_t s_map, int rows, int cols, int col0, int transpose, double* __restrict__ out,
@@ -639,12 +907,26 @@ extern "C" int ublr_syrk_upper_batched(int M, int K, double alpha, const double*
                                        ldc, sC, nullptr, 0, batch, st, 1);
 }
 
+// leaf kernels: 2 = register-tile (nb <= 64, default), 1 = shared-memory
+static int leaf_version() {
+  static const int v = [] {
+    const char* e = getenv("UBLR_LEAF_VERSION");
+    return e ? atoi(e) : 2;
+  }();
+  return v;
+}
+
 extern "C" int ublr_potrf_diag(double* A, int64_t lda, int64_t sA, int j0, int nb, double* R, int64_t ldr,
                                int64_t sR, double* Rinv, int* status, int batch, void* stream) {
   UBLR_REQUIRE(A && R && Rinv && status && nb >= 1 && nb <= 96 && batch >= 1, UBLR_ERR_VALUE,
                "ublr_potrf_diag: bad arguments");
-  size_t sm = (size_t)(nb * (nb + 1) + nb * nb) * sizeof(double);
   cudaStream_t st = (cudaStream_t)stream;
+  if (nb <= 64 && leaf_version() == 2) {
+    k_potrf64<<<batch, 256, 0, st>>>(A, lda, sA, j0, nb, R, ldr, sR, Rinv, status);
+    UBLR_LAUNCH_CHECK();
+    return UBLR_OK;
+  }
+  size_t sm = (size_t)(nb * (nb + 1) + nb * nb) * sizeof(double);
   UBLR_CUDA(cudaFuncSetAttribute(k_potrf_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   k_potrf_diag<<<batch, FT, sm, st>>>(A, lda, sA, j0, nb, R, ldr, sR, Rinv, status);
   UBLR_LAUNCH_CHECK();
@@ -664,8 +946,13 @@ extern "C" int ublr_lu_sign_diag_r(double* W, int64_t ldw, int64_t sW, int j0, i
   UBLR_REQUIRE(W && LU && Linv && Uinv && D && status && nb >= 1 && nb <= 96 && batch >= 1, UBLR_ERR_VALUE,
                "ublr_lu_sign_diag: bad arguments");
   UBLR_REQUIRE(!R || n >= j0 + nb, UBLR_ERR_VALUE, "ublr_lu_sign_diag_r: n < j0 + nb");
-  size_t sm = (size_t)(nb * (nb + 1) + nb * nb) * sizeof(double);
   cudaStream_t st = (cudaStream_t)stream;
+  if (nb <= 64 && leaf_version() == 2) {
+    k_lu_sign64<<<batch, 256, 0, st>>>(W, ldw, sW, j0, nb, LU, ldlu, sLU, Linv, Uinv, D, sD, status, R, ldr, sR, n);
+    UBLR_LAUNCH_CHECK();
+    return UBLR_OK;
+  }
+  size_t sm = (size_t)(nb * (nb + 1) + nb * nb) * sizeof(double);
   UBLR_CUDA(cudaFuncSetAttribute(k_lu_sign_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   k_lu_sign_diag<<<batch, FT, sm, st>>>(W, ldw, sW, j0, nb, LU, ldlu, sLU, Linv, Uinv, D, sD, status, R, ldr, sR,
                                          n);
