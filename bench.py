@@ -328,9 +328,26 @@ def run_sharded(args, rank, world, local):
     def gather_emulated(V, n):
         return torch.cat([V if p_ is None else p_ for p_ in other_V], 0)
 
+    # core rows of this rank: 309 GB / S. When they do not fit next to the
+    # working set in HBM (S <= 2), they stream to pinned host memory in
+    # block-row panels (distributed.phase23_local)
+    sh = shards[me]
+    K = int(np.minimum(wl.k, wl.tess.block_sizes).sum())
+    core_bytes = (sh.K1 - sh.K0) * K * 8
+    free, _ = torch.cuda.mem_get_info(dev)
+    core_out, panel_blocks, sink = None, None, "device"
+    if core_bytes > free - 24 * 2 ** 30:
+        import psutil
+        if core_bytes > psutil.virtual_memory().available - 16 * 2 ** 30:
+            raise SystemExit(f"c5 on {S} rank(s): {core_bytes / 1e9:.0f} GB of core rows per rank fit neither in "
+                             f"HBM ({free / 1e9:.0f} GB free) nor in host memory")
+        core_out = torch.empty((sh.K1 - sh.K0, K), dtype=torch.float64, pin_memory=True)
+        panel_blocks, sink = 64, "pinned host (block-row panels of 64)"
+
     def step(op=None):
         return compress_sharded(op or wl.op, wl.tess, wl.k, wl.p, P.RandomStream(W.COMPRESS_SEED), rank=me,
-                                world=S, allgather=gather_emulated if emulate else None)
+                                world=S, allgather=gather_emulated if emulate else None, core_out=core_out,
+                                panel_blocks=panel_blocks)
 
     for _ in range(args.warmup):
         step()
@@ -359,7 +376,6 @@ def run_sharded(args, rank, world, local):
     roof = roofline_of(ev, _lib.work, "c5", wl.describe().get("operator", ""))
 
     # e2e: operator from host coordinates (H2D), the rank's result to pinned host memory (D2H)
-    sh = shards[me]
     e2e_times, h2d, d2h = [], 0, 0
     host = None
     for it in range(3):
@@ -371,13 +387,13 @@ def run_sharded(args, rank, world, local):
         op = P.KernelOperator(wl.points, wl.op.kind, wl.op.diag)
         h2d = wl.points.coords.nbytes
         res = step(op)
-        parts = (res.U, res.core, res.B)
+        parts = tuple(x for x in (res.U, res.core, res.B) if x.is_cuda)   # a host-sink core is already on the host
         if host is None:
             host = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in parts]
         for h, x in zip(host, parts):
             h.copy_(x, non_blocking=True)
         torch.cuda.synchronize()
-        d2h = sum(x.numel() * 8 for x in parts)
+        d2h = sum(x.numel() * 8 for x in (res.U, res.core, res.B))
         res = parts = None
         if it > 0:
             e2e_times.append(time.perf_counter() - t0)
@@ -393,7 +409,7 @@ def run_sharded(args, rank, world, local):
             "config": bench_config(wl, world, "c5", S if emulate else None),
             "measured": ("one rank's share of a %d-way sharded job on 1 GPU (all-gather emulated)" % S)
             if emulate else "all ranks, NCCL all-gather of V; max over ranks",
-            "shard_rank": me, "rows_per_shard": sh.r1 - sh.r0,
+            "shard_rank": me, "rows_per_shard": sh.r1 - sh.r0, "core_rows_in": sink,
             "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(launches),
             "roofline": roof,
