@@ -426,7 +426,7 @@ def block_nullification_width(tess: Tessellation, r: int) -> int:
     return max(r + widest, 3 ** tess.dim * r)
 
 
-def nullspace_samples(dt, Om, ld_om, col_om, Ysrc, ld_y, s, r, k, S_out, chunk_bytes=12 << 30):
+def nullspace_samples(dt, Om, ld_om, col_om, Ysrc, ld_y, s, r, k, S_out, chunk_bytes=40 << 30, nside=1):
     """S_i = Y_i P_k^(i) for every block, P_k^(i) the first k of the r trailing
     null-space columns that null_basis(Omega[nbr(i)], r) returns
     (ref/bases.py:102-110, ref/linalg.py:72-94), without a Householder QR:
@@ -439,12 +439,31 @@ def nullspace_samples(dt, Om, ld_om, col_om, Ysrc, ld_y, s, r, k, S_out, chunk_b
 
     where B = Omega[nbr(i)] (n x s), Qt = B^T R^-1 and E selects columns
     s-r .. s-r+k-1 (DESIGN.md §bn null space). Blocks with equal
-    neighbourhood size n are batched; Omega rows are gathered in place."""
+    neighbourhood size n are batched; Omega rows are gathered in place.
+
+    nside = 2 runs both sides of block nullification in the same launches
+    (twice the batch, half the launches): Om = [Omega | Psi] and
+    Ysrc = [Y | Z] are N x 2s (ld 2s, col_om = 0) and S_out is N x 2 x k.
+    Side sigma's row q of a side-by-side pair is the virtual row
+    nside * q + sigma of a matrix with leading dimension s (k for S_out), so
+    the row maps address both sides without copies."""
     import torch
 
     from . import dense as D
 
     dev = dt.device
+    if nside == 2 and (ld_om != 2 * s or ld_y != 2 * s or col_om != 0):
+        raise ValueError("nullspace_samples(nside=2) needs [Omega | Psi] and [Y | Z] side by side")
+    vl_om = s if nside == 2 else ld_om          # leading dimension of the virtual row space
+    vl_y = s if nside == 2 else ld_y
+    vl_s = k if nside == 2 else S_out.stride(0)
+
+    def vrows(rows, sides):
+        """virtual rows (len(sides) * len(blocks), width): side-major batch order."""
+        rows = np.asarray(rows, dtype=np.int64)
+        return np.concatenate([nside * rows + sg for sg in sides], axis=0)
+
+    sides = list(range(nside))
     om0 = D.addr(Om, col_om)      # Omega side: column offset inside the fused buffer
     sizes = dt.sizes
     nbr_n = np.array([int(sizes[dt.nidx_h[dt.nptr_h[i]:dt.nptr_h[i + 1]]].sum()) for i in range(dt.b)])
@@ -457,33 +476,35 @@ def nullspace_samples(dt, Om, ld_om, col_om, Ysrc, ld_y, s, r, k, S_out, chunk_b
         pairs = sorted({(min(a, c), max(a, c)) for i in range(dt.b)
                         for a in dt.nidx_h[dt.nptr_h[i]:dt.nptr_h[i + 1]].tolist()
                         for c in dt.nidx_h[dt.nptr_h[i]:dt.nptr_h[i + 1]].tolist()})
-        if len(pairs) <= 65535:
+        if len(pairs) * nside <= 65535:
             pid = {pq: t for t, pq in enumerate(pairs)}
             pa = np.array(pairs, dtype=np.int64)
-            amap_p = torch.from_numpy((dt.off_h[pa[:, 0]][:, None] + np.arange(m0)[None, :]).astype(np.int32)).to(dev)
-            bmap_p = torch.from_numpy((dt.off_h[pa[:, 1]][:, None] + np.arange(m0)[None, :]).astype(np.int32)).to(dev)
-            P_all = torch.empty((len(pairs), m0, m0), dtype=torch.float64, device=dev)
-            D.gemm(0, 1, m0, m0, s, 1.0, om0, ld_om, 0, om0, ld_om, 0, 0.0, D.addr(P_all), m0, m0 * m0, len(pairs),
-                   amap=D.addr(amap_p), sAm=m0, bmap=D.addr(bmap_p), sBm=m0)
-            shared = (P_all, pid)
+            ra = dt.off_h[pa[:, 0]][:, None] + np.arange(m0)[None, :]
+            rb = dt.off_h[pa[:, 1]][:, None] + np.arange(m0)[None, :]
+            amap_p = torch.from_numpy(vrows(ra, sides).astype(np.int32)).to(dev)
+            bmap_p = torch.from_numpy(vrows(rb, sides).astype(np.int32)).to(dev)
+            P_all = torch.empty((nside * len(pairs), m0, m0), dtype=torch.float64, device=dev)
+            D.gemm(0, 1, m0, m0, s, 1.0, om0, vl_om, 0, om0, vl_om, 0, 0.0, D.addr(P_all), m0, m0 * m0,
+                   nside * len(pairs), amap=D.addr(amap_p), sAm=m0, bmap=D.addr(bmap_p), sBm=m0)
+            shared = (P_all, pid, len(pairs))
     for n, m in keys:
         n, m = int(n), int(m)
         if s - r < n:
             raise ValueError("block-nullification width too small for a neighbourhood")
         members = np.flatnonzero((nbr_n == n) & (sizes == m))
-        per_block = 3 * n * n * 8 + (s + 3 * n) * k * 8
-        ch = max(1, min(len(members), int(chunk_bytes // per_block), 65535))
+        per_block = nside * (3 * n * n * 8 + (s + 3 * n) * k * 8)
+        ch = max(1, min(len(members), int(chunk_bytes // per_block), 65535 // nside))
         eb = np.zeros((s - n, k))
         eb[np.arange(s - r - n, s - r - n + k), np.arange(k)] = 1.0
         Ebot = torch.from_numpy(eb).to(dev)
         for c0 in range(0, len(members), ch):
             blk = members[c0:c0 + ch]
-            nb_ = len(blk)
+            nb_ = nside * len(blk)        # batch entries: side-major
             maps = np.stack([np.concatenate([np.arange(dt.off_h[j], dt.off_h[j + 1])
                                              for j in dt.nidx_h[dt.nptr_h[i]:dt.nptr_h[i + 1]]]) for i in blk])
-            amap = torch.from_numpy(maps.astype(np.int32)).to(dev)
-            rows = np.stack([np.arange(dt.off_h[i], dt.off_h[i + 1]) for i in blk]).astype(np.int32)
-            rmap = torch.from_numpy(rows).to(dev)
+            amap = torch.from_numpy(vrows(maps, sides).astype(np.int32)).to(dev)
+            rows = np.stack([np.arange(dt.off_h[i], dt.off_h[i + 1]) for i in blk])
+            rmap = torch.from_numpy(vrows(rows, sides).astype(np.int32)).to(dev)
             f64 = dict(dtype=torch.float64, device=dev)
             G = torch.empty((nb_, n, n), **f64)
             R = torch.zeros((nb_, n, n), **f64)
@@ -493,32 +514,34 @@ def nullspace_samples(dt, Om, ld_om, col_om, Ysrc, ld_y, s, r, k, S_out, chunk_b
             # G = B B^T  (B = Omega[nbr]): from the shared neighbour-pair products
             # when blocks are uniform, else gathered in place
             if shared is not None:
-                P_all, pid = shared
+                P_all, pid, npairs = shared
                 nbl = n // m
                 gm = np.empty((nb_, nbl, nbl), dtype=np.int32)
-                for c, i in enumerate(blk):
-                    L = dt.nidx_h[dt.nptr_h[i]:dt.nptr_h[i + 1]]
-                    for a in range(nbl):
-                        for bq in range(nbl):
-                            ja, jb = int(L[a]), int(L[bq])
-                            gm[c, a, bq] = pid[(ja, jb)] if ja <= jb else -pid[(jb, ja)] - 1
+                for sg in sides:
+                    for c, i in enumerate(blk):
+                        L = dt.nidx_h[dt.nptr_h[i]:dt.nptr_h[i + 1]]
+                        for a in range(nbl):
+                            for bq in range(nbl):
+                                ja, jb = int(L[a]), int(L[bq])
+                                t = sg * npairs + (pid[(ja, jb)] if ja <= jb else pid[(jb, ja)])
+                                gm[sg * len(blk) + c, a, bq] = t if ja <= jb else -t - 1
                 gmap = torch.from_numpy(gm).to(dev)
                 _lib.call("ublr_assemble_gram", D.addr(P_all), D.addr(gmap), nbl, m, D.addr(G), nb_,
                           _lib.stream_handle())
             else:
-                D.gemm(0, 1, n, n, s, 1.0, om0, ld_om, 0, om0, ld_om, 0, 0.0, D.addr(G), n, nn, nb_,
+                D.gemm(0, 1, n, n, s, 1.0, om0, vl_om, 0, om0, vl_om, 0, 0.0, D.addr(G), n, nn, nb_,
                        amap=D.addr(amap), sAm=n, bmap=D.addr(amap), sBm=n)
             fC = D.cholesky_upper(G, R)
             # LU of D R - B1^T = (D - Q_top) R  (B1 = B[:, :n]; G is free again)
             W = G
-            _lib.call("ublr_gather", om0, ld_om, 0, D.addr(amap), n, n, n, 0, 1, D.addr(W), n, nn, nb_,
+            _lib.call("ublr_gather", om0, vl_om, 0, D.addr(amap), n, n, n, 0, 1, D.addr(W), n, nn, nb_,
                       _lib.stream_handle())
             neg = torch.full((n,), -1.0, **f64)
             _lib.call("ublr_scale_rows", D.addr(W), n, nn, D.addr(neg), 0, n, n, nb_, _lib.stream_handle())
             fL = D.lu_sign(W, LU, Dg, R=R)
             # M = L^-T U^-T R^-T B[:, E] = L^-T U'^-T B[:, E]   (U' = U R)
             Mm = torch.empty((nb_, n, k), **f64)
-            _lib.call("ublr_gather", om0, ld_om, 0, D.addr(amap), n, n, k, s - r, 0, D.addr(Mm), k, n * k, nb_,
+            _lib.call("ublr_gather", om0, vl_om, 0, D.addr(amap), n, n, k, s - r, 0, D.addr(Mm), k, n * k, nb_,
                       _lib.stream_handle())
             tk = torch.empty((nb_, D.NB, k), **f64)
             D.trsm_left(LU, Mm, fL, fL.inv2, upper=True, trans=True, tmp=tk)
@@ -530,10 +553,10 @@ def nullspace_samples(dt, Om, ld_om, col_om, Ysrc, ld_y, s, r, k, S_out, chunk_b
             DM = Mm
             _lib.call("ublr_scale_rows", D.addr(DM), k, n * k, D.addr(Dg), n, n, k, nb_, _lib.stream_handle())
             D.trsm_left(R, DM, fC, fC.inv, upper=True, trans=False, tmp=tk)
-            D.gemm(1, 0, s, k, n, -1.0, om0, ld_om, 0, D.addr(DM), k, n * k, 1.0, D.addr(P), k, s * k, nb_,
+            D.gemm(1, 0, s, k, n, -1.0, om0, vl_om, 0, D.addr(DM), k, n * k, 1.0, D.addr(P), k, s * k, nb_,
                    amap=D.addr(amap), sAm=n)
             # S_i = Y_i P  (rows of block i scattered into S_out)
-            D.gemm(0, 0, m, k, s, 1.0, D.addr(Ysrc), ld_y, 0, D.addr(P), k, s * k, 0.0, D.addr(S_out), k, 0, nb_,
+            D.gemm(0, 0, m, k, s, 1.0, D.addr(Ysrc), vl_y, 0, D.addr(P), k, s * k, 0.0, D.addr(S_out), vl_s, 0, nb_,
                    amap=D.addr(rmap), sAm=m, cmap=D.addr(rmap), sCm=m)
             D.check_status(fC, "Cholesky of Omega[nbr] Omega[nbr]^T")
             D.check_status(fL, "sign-selected LU")
@@ -569,13 +592,14 @@ def block_nullification_bases(op, tess: Tessellation, k: int, p: int, stream: Ra
     kq = max(1, min(k, dt.m_max))
     U = torch.zeros((n, max(k, 1)), dtype=torch.float64, device=dt.device)
     V = torch.zeros_like(U)
-    Sbuf = torch.zeros((n, kq), dtype=torch.float64, device=dt.device)
+    Sbuf = torch.zeros((n, 2, kq), dtype=torch.float64, device=dt.device)    # [S_U | S_V] per row
     col0 = torch.zeros(dt.b, dtype=torch.int32, device=dt.device)
+    if k < dt.m_max:
+        # both sides in the same launches (doubled batches, half the launches)
+        nullspace_samples(dt, OP, 2 * s, 0, YZ, 2 * s, s, r, kq, Sbuf, nside=2)
     for side, dst in ((0, U), (1, V)):
-        if k < dt.m_max:
-            nullspace_samples(dt, OP, 2 * s, side * s, YZ[:, side * s:], 2 * s, s, r, kq, Sbuf)
-        _lib.call("ublr_block_qr", _lib.ptr(Sbuf), kq, 1, None, 0, 0, _lib.ptr(col0), _lib.ptr(dt.off), dt.b, kq,
-                  _lib.ptr(dst), dst.stride(0), st, dt.m_max)
+        _lib.call("ublr_block_qr", _lib.ptr(Sbuf) + 8 * side * kq, 2 * kq, 1, None, 0, 0, _lib.ptr(col0),
+                  _lib.ptr(dt.off), dt.b, kq, _lib.ptr(dst), dst.stride(0), st, dt.m_max)
     bases = BlockBases(dt, U, V, k, "bn", (s, s))
     bundle = SketchBundle("bn", dt, s, YZ[:, :s], YZ[:, s:], omega_d=OP[:, :s], psi_d=OP[:, s:])
     return bases, bundle

@@ -272,6 +272,28 @@ def test_nullspace_samples_match_reference_null_basis():
         assert np.abs(got - want).max() <= 1e-11 * np.abs(want).max(), i
 
 
+@pytest.mark.parametrize("per,b", [(32, 16), (48, 9)])
+def test_nullspace_samples_both_sides_in_one_batch(per, b):
+    """nside = 2 (both block-nullification sides in the same launches, virtual
+    row maps into [Omega | Psi] and [Y | Z]) equals two one-side calls."""
+    from paper_2501_05528_b200.bases import nullspace_samples
+    tess = P.build_tessellation(P.grid_points(per, 2), b)
+    dt = device_tess(tess, torch.device(DEV))
+    k, p = 8, 4
+    r = k + p
+    s = P.block_nullification_width(tess, r)
+    rng = np.random.default_rng(5)
+    OP = torch.from_numpy(rng.standard_normal((dt.n, 2 * s))).to(DEV)
+    YZ = torch.from_numpy(rng.standard_normal((dt.n, 2 * s))).to(DEV)
+    both = torch.zeros((dt.n, 2, k), dtype=torch.float64, device=DEV)
+    nullspace_samples(dt, OP, 2 * s, 0, YZ, 2 * s, s, r, k, both, nside=2)
+    for side in (0, 1):
+        one = torch.zeros((dt.n, k), dtype=torch.float64, device=DEV)
+        nullspace_samples(dt, OP, 2 * s, side * s, YZ[:, side * s:], 2 * s, s, r, k, one)
+        d = (both[:, side] - one).abs().max().item()
+        assert d <= 1e-12 * one.abs().max().item(), (side, d)
+
+
 @pytest.mark.parametrize("kind,k,per,nb", [("inv", 48, 64, 16), ("log", 40, 64, 16), ("log", 33, 50, 16)])
 def test_coupling_matches_numpy(kind, k, per, nb):
     """C_ij = U_i^T A_ij V_j for every block pair (the m = 256 warp-specialised
