@@ -771,43 +771,69 @@ __global__ void __launch_bounds__(256) k_lu_sign64(double* W, int64_t ldw, int64
 }
 
 // out[b][r][c] = src[b*s_src + map[b*s_map + r] * ld + col0 + c]   (transpose: out[b][c][r])
-__global__ void k_gather(const double* __restrict__ src, int64_t ld, int64_t s_src, const int32_t* __restrict__ map,
-                         int64_t s_map, int rows, int cols, int col0, int transpose, double* __restrict__ out,
-                         int64_t ldo, int64_t s_out) {
-  const int bz = blockIdx.y;
-  const int64_t tot = (int64_t)rows * cols;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
-    int r, c;
-    if (!transpose) { r = (int)(e / cols); c = (int)(e % cols); } else { c = (int)(e / rows); r = (int)(e % rows); }
-    int64_t pr = map ? map[bz * s_map + r] : r;
-    double v = src[bz * s_src + pr * ld + col0 + c];
-    if (!transpose) out[bz * s_out + (int64_t)r * ldo + c] = v;
-    else out[bz * s_out + (int64_t)c * ldo + r] = v;
+// 32 x 32 tiles per CTA (32 x 8 threads), 32-bit tile indices; the
+// transpose goes through a padded shared-memory tile so that both the read
+// (along c) and the write (along r) are coalesced.
+__global__ void __launch_bounds__(256) k_gather(const double* __restrict__ src, int64_t ld, int64_t s_src,
+                                                const int32_t* __restrict__ map, int64_t s_map, int rows, int cols,
+                                                int col0, int transpose, double* __restrict__ out, int64_t ldo,
+                                                int64_t s_out) {
+  __shared__ double tile[32][33];
+  const int bz = blockIdx.z;
+  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const double* sb = src + bz * s_src + col0;
+  const int32_t* mb = map ? map + bz * s_map : nullptr;
+  double* ob = out + bz * s_out;
+  if (!transpose) {
+    const int c = c0 + tx;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = r0 + ty + 8 * i;
+      if (r < rows && c < cols) {
+        const int64_t pr = mb ? mb[r] : r;
+        ob[(int64_t)r * ldo + c] = sb[pr * ld + c];
+      }
+    }
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = r0 + ty + 8 * i, c = c0 + tx;
+    if (r < rows && c < cols) {
+      const int64_t pr = mb ? mb[r] : r;
+      tile[ty + 8 * i][tx] = sb[pr * ld + c];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int c = c0 + ty + 8 * i, r = r0 + tx;
+    if (r < rows && c < cols) ob[(int64_t)c * ldo + r] = tile[tx][ty + 8 * i];
   }
 }
 
 // W[b][r][c] += d[b*s_d + r] * R[b][r][c] on a rows x cols sub-block
-__global__ void k_add_scaled_rows(double* __restrict__ W, int64_t ldw, int64_t s_w, const double* __restrict__ R,
-                                  int64_t ldr, int64_t s_r, const double* __restrict__ d, int64_t s_d, int rows,
-                                  int cols) {
-  const int bz = blockIdx.y;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)rows * cols;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int r = (int)(e / cols), c = (int)(e % cols);
+__global__ void __launch_bounds__(256) k_add_scaled_rows(double* __restrict__ W, int64_t ldw, int64_t s_w,
+                                                         const double* __restrict__ R, int64_t ldr, int64_t s_r,
+                                                         const double* __restrict__ d, int64_t s_d, int rows,
+                                                         int cols) {
+  const int bz = blockIdx.z;
+  const int c = blockIdx.x * 256 + threadIdx.x;
+  if (c >= cols) return;
+  for (int r = blockIdx.y; r < rows; r += gridDim.y) {
     double* w = W + bz * s_w + (int64_t)r * ldw + c;
     *w = fma(d[bz * s_d + r], R[bz * s_r + (int64_t)r * ldr + c], *w);
   }
 }
 
 // X[b][r][c] *= d[b*s_d + r]
-__global__ void k_scale_rows(double* __restrict__ X, int64_t ldx, int64_t s_x, const double* __restrict__ d,
-                             int64_t s_d, int rows, int cols) {
-  const int bz = blockIdx.y;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)rows * cols;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    int r = (int)(e / cols), c = (int)(e % cols);
-    X[bz * s_x + (int64_t)r * ldx + c] *= d[bz * s_d + r];
-  }
+__global__ void __launch_bounds__(256) k_scale_rows(double* __restrict__ X, int64_t ldx, int64_t s_x,
+                                                    const double* __restrict__ d, int64_t s_d, int rows, int cols) {
+  const int bz = blockIdx.z;
+  const int c = blockIdx.x * 256 + threadIdx.x;
+  if (c >= cols) return;
+  for (int r = blockIdx.y; r < rows; r += gridDim.y) X[bz * s_x + (int64_t)r * ldx + c] *= d[bz * s_d + r];
 }
 
 }  // namespace
@@ -821,8 +847,8 @@ extern "C" int ublr_gather(const double* src, int64_t ld, int64_t s_src, const i
   UBLR_REQUIRE(src && out && rows >= 0 && cols >= 0 && batch >= 0 && batch <= 65535, UBLR_ERR_VALUE,
                "ublr_gather: bad arguments");
   if (!rows || !cols || !batch) return UBLR_OK;
-  int64_t tot = (int64_t)rows * cols;
-  dim3 grid((unsigned)((tot + 255) / 256 < 4096 ? (tot + 255) / 256 : 4096), batch);
+  UBLR_REQUIRE((rows + 31) / 32 <= 65535, UBLR_ERR_VALUE, "ublr_gather: too many rows");
+  dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32), batch);
   k_gather<<<grid, 256, 0, (cudaStream_t)stream>>>(src, ld, s_src, map, s_map, rows, cols, col0, transpose, out, ldo,
                                                    s_out);
   UBLR_LAUNCH_CHECK();
@@ -834,8 +860,7 @@ extern "C" int ublr_add_scaled_rows(double* W, int64_t ldw, int64_t s_w, const d
   UBLR_REQUIRE(W && R && d && rows >= 0 && cols >= 0 && batch >= 0 && batch <= 65535, UBLR_ERR_VALUE,
                "ublr_add_scaled_rows: bad arguments");
   if (!rows || !cols || !batch) return UBLR_OK;
-  int64_t tot = (int64_t)rows * cols;
-  dim3 grid((unsigned)((tot + 255) / 256 < 1024 ? (tot + 255) / 256 : 1024), batch);
+  dim3 grid((unsigned)((cols + 255) / 256), (unsigned)(rows < 64 ? rows : 64), batch);
   k_add_scaled_rows<<<grid, 256, 0, (cudaStream_t)stream>>>(W, ldw, s_w, R, ldr, s_r, d, s_d, rows, cols);
   UBLR_LAUNCH_CHECK();
   return UBLR_OK;
@@ -846,8 +871,7 @@ extern "C" int ublr_scale_rows(double* X, int64_t ldx, int64_t s_x, const double
   UBLR_REQUIRE(X && d && rows >= 0 && cols >= 0 && batch >= 0 && batch <= 65535, UBLR_ERR_VALUE,
                "ublr_scale_rows: bad arguments");
   if (!rows || !cols || !batch) return UBLR_OK;
-  int64_t tot = (int64_t)rows * cols;
-  dim3 grid((unsigned)((tot + 255) / 256 < 4096 ? (tot + 255) / 256 : 4096), batch);
+  dim3 grid((unsigned)((cols + 255) / 256), (unsigned)(rows < 256 ? rows : 256), batch);
   k_scale_rows<<<grid, 256, 0, (cudaStream_t)stream>>>(X, ldx, s_x, d, s_d, rows, cols);
   UBLR_LAUNCH_CHECK();
   return UBLR_OK;
@@ -967,18 +991,40 @@ extern "C" int ublr_lu_sign_diag_r(double* W, int64_t ldw, int64_t sW, int j0, i
 // neighbouring pair and reused by every neighbourhood containing both).
 namespace ublr {
 namespace {
-__global__ void k_assemble_gram(const double* __restrict__ P, const int32_t* __restrict__ map, int nb, int m,
-                                double* __restrict__ G) {
-  const int c = blockIdx.y;
+__global__ void __launch_bounds__(256) k_assemble_gram(const double* __restrict__ P, const int32_t* __restrict__ map,
+                                                       int nb, int m, double* __restrict__ G) {
+  // CTA = one 32 x 32 tile of block (a, b) of G_c; transposed blocks go
+  // through a shared-memory tile (coalesced read and write)
+  __shared__ double tile[32][33];
+  const int c = blockIdx.z;
   const int n = nb * m;
-  const int64_t tot = (int64_t)n * n;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
-    int r = (int)(e / n), q = (int)(e % n);
-    int a = r / m, b = q / m, rr = r - a * m, qq = q - b * m;
-    int pid = map[((int64_t)c * nb + a) * nb + b];
-    double v = (pid >= 0) ? P[(int64_t)pid * m * m + (int64_t)rr * m + qq]
-                          : P[(int64_t)(-pid - 1) * m * m + (int64_t)qq * m + rr];
-    G[(int64_t)c * tot + e] = v;
+  const int tpb = (m + 31) / 32;                    // tiles per block side
+  const int ab = blockIdx.y, a = ab / nb, b = ab - a * nb;
+  const int ty0 = blockIdx.x / tpb, tx0 = blockIdx.x - ty0 * tpb;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int pid = map[((int64_t)c * nb + a) * nb + b];
+  double* Gc = G + (int64_t)c * n * n + (int64_t)(a * m) * n + b * m;
+  if (pid >= 0) {
+    const double* Pb = P + (int64_t)pid * m * m;
+    const int q = tx0 * 32 + tx;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = ty0 * 32 + ty + 8 * i;
+      if (r < m && q < m) Gc[(int64_t)r * n + q] = Pb[(int64_t)r * m + q];
+    }
+    return;
+  }
+  const double* Pb = P + (int64_t)(-pid - 1) * m * m;   // G block (r, q) = P[q][r]
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int q = tx0 * 32 + ty + 8 * i, r = ty0 * 32 + tx;
+    if (q < m && r < m) tile[ty + 8 * i][tx] = Pb[(int64_t)q * m + r];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = ty0 * 32 + ty + 8 * i, q = tx0 * 32 + tx;
+    if (r < m && q < m) Gc[(int64_t)r * n + q] = tile[tx][ty + 8 * i];
   }
 }
 }  // namespace
@@ -988,8 +1034,8 @@ extern "C" int ublr_assemble_gram(const double* P, const int32_t* map, int nb, i
                                   void* stream) {
   UBLR_REQUIRE(P && map && G && nb > 0 && m > 0 && batch > 0 && batch <= 65535, UBLR_ERR_VALUE,
                "ublr_assemble_gram: bad arguments");
-  int64_t tot = (int64_t)nb * m * nb * m;
-  dim3 grid((unsigned)((tot + 255) / 256 < 2048 ? (tot + 255) / 256 : 2048), batch);
+  const int tpb = (m + 31) / 32;
+  dim3 grid((unsigned)(tpb * tpb), (unsigned)(nb * nb), batch);
   k_assemble_gram<<<grid, 256, 0, (cudaStream_t)stream>>>(P, map, nb, m, G);
   UBLR_LAUNCH_CHECK();
   return UBLR_OK;

@@ -14,8 +14,10 @@ adapter only provides shape/apply/apply_adjoint). Stored:
   reference is run a second time with every grid coordinate moved up by one
   ulp (np.nextafter(coords, 2), A entries change by ~1e-16 relative) and the
   exact ||A_hat_ref - A_hat_ref'||_F (total and per pair) is stored, with the
-  perturbed run's own exact error ||A - A_hat_ref'||_F. The GPU parity gate
-  for B2 is anchored on these numbers, not on the GPU's own.
+  perturbed run's own exact error ||A - A_hat_ref'||_F, and the exact
+  errors over a family of five 1-ulp coordinate perturbations (base, +1, -1,
+  +1 on axis 0, +2 ulp). The GPU gates for B2 are anchored on these numbers,
+  not on the GPU's own.
 
 Takes ~40 min for c3 and ~35 min for c4 (two reference runs) on 8 cores:
 
@@ -125,14 +127,26 @@ def run(name):
         "ranks": rep.effective_ranks,
     }
     reps = [rep]
+    family = {}
     if name == "c4":
         # the reference's own 1-ulp rounding sensitivity (same tessellation,
-        # same streams; only the operator's coordinates move)
-        op2 = KernelOp(np.nextafter(pts.coords, 2.0), "log", diag, chunk=256)
-        t2 = time.time()
-        rep2, _ = compress(op2, tess, k, method_id=mid, p=p, stream=RandomStream(7), compute_error=False)
-        print(name, "perturbed reference seconds", time.time() - t2, flush=True)
-        reps.append(rep2)
+        # same streams; only the operator's coordinates move), and its exact
+        # error over a family of 1-ulp coordinate perturbations (the B2 error
+        # at c4 is rounding-noise dominated)
+        c = pts.coords
+        variants = {"+1ulp": np.nextafter(c, 2.0), "-1ulp": np.nextafter(c, -1.0),
+                    "+1ulp x": np.stack([np.nextafter(c[:, 0], 2.0), c[:, 1]], 1),
+                    "+2ulp": np.nextafter(np.nextafter(c, 2.0), 2.0)}
+        for vname, vc in variants.items():
+            t2 = time.time()
+            repv, _ = compress(KernelOp(vc, "log", diag, chunk=256), tess, k, method_id=mid, p=p,
+                               stream=RandomStream(7), compute_error=False)
+            print(name, vname, "perturbed reference seconds", time.time() - t2, flush=True)
+            if vname == "+1ulp":
+                reps.append(repv)
+            else:
+                family[vname] = np.sqrt(blockwise_norms(tess, c, diag, [repv])[1].sum())
+            del repv
     t3 = time.time()
     a2, e2, d2, f2 = blockwise_norms(tess, pts.coords, diag, reps)
     print(name, "blockwise norms seconds", time.time() - t3, flush=True)
@@ -143,6 +157,9 @@ def run(name):
         out["sens_fro"] = np.sqrt(d2.sum())      # exact ||A_hat_ref - A_hat_ref(coords + 1 ulp)||_F
         out["sens_pair"] = np.sqrt(d2)
         out["err_fro_pert"] = np.sqrt(f2.sum())  # the perturbed reference's exact error (against the unperturbed A)
+        names = ["base", "+1ulp"] + list(family)
+        out["err_family_names"] = np.array(names)
+        out["err_family"] = np.array([out["err_fro"], out["err_fro_pert"]] + [family[v] for v in family])
     np.savez_compressed(os.path.join(OUT, f"{name}_{mid}.npz"), **out)
     print(name, "A_fro", out["A_fro"], "err/A", out["err_fro"] / out["A_fro"],
           "sens/A", out.get("sens_fro", np.nan) / out["A_fro"], flush=True)

@@ -19,10 +19,11 @@ Gates (BASELINE.json north star):
   round differently are two such perturbations, so the c4 parity gate is
   2 x the reference's own sensitivity — a fixed number from the reference,
   not from this implementation. For the same reason a single
-  B2 approximation error is one draw from a rounding-noise distribution; the
-  1.05x gate compares the root-mean-square error over the same 1-ulp
-  perturbation of the coordinates on both sides (reference: `err_fro`,
-  `err_fro_pert`; GPU: the same two coordinate sets).
+  B2 approximation error is one draw from a rounding-noise distribution (two
+  runs of the unmodified reference that differ only in the BLAS threading
+  of the operator adapter give 7.49e-9 and 7.11e-9); the 1.05x gate compares
+  the root-mean-square exact error over the same family of five 1-ulp
+  coordinate perturbations on both sides (fixture `err_family`).
 The c5 spot checks are in test_gpu_c5_parity.py."""
 
 import os
@@ -76,17 +77,28 @@ def test_fullsize_against_reference(name, mid):
     if mid != "B2":
         assert err_gpu <= 1.05 * err_ref
     else:
-        # rms over {coordinates, coordinates + 1 ulp} on both sides, each
-        # against the unperturbed A
-        assert "err_fro_pert" in g, "c4 fixture lacks the perturbed reference's error"
-        rep2, _ = P.compress(P.KernelOperator(np.nextafter(pts.coords, 2.0), "log", -np.log(0.5 / 256)), tess, 40,
-                             mid, p=10, stream=P.RandomStream(7), compute_error=False)
-        err_gpu2 = P.frobenius_error(op, rep2).fro / A_fro
-        rms_gpu = np.sqrt((err_gpu ** 2 + err_gpu2 ** 2) / 2)
-        err_ref2 = float(g["err_fro_pert"]) / A_fro
-        rms_ref = np.sqrt((err_ref ** 2 + err_ref2 ** 2) / 2)
-        print(f"{name}: rms error over the 1-ulp pair gpu {rms_gpu:.4e} ({err_gpu:.3e}, {err_gpu2:.3e}) "
-              f"ref {rms_ref:.4e} ({err_ref:.3e}, {err_ref2:.3e}) ({rms_gpu / rms_ref:.3f}x)")
+        # rms of the exact error over the same family of 1-ulp coordinate
+        # perturbations on both sides (each against the unperturbed A)
+        assert "err_family" in g, "c4 fixture lacks the reference's perturbation family"
+        names = [str(x) for x in g["err_family_names"]]
+        c = pts.coords
+        variants = {"base": c, "+1ulp": np.nextafter(c, 2.0), "-1ulp": np.nextafter(c, -1.0),
+                    "+1ulp x": np.stack([np.nextafter(c[:, 0], 2.0), c[:, 1]], 1),
+                    "+2ulp": np.nextafter(np.nextafter(c, 2.0), 2.0)}
+        errs = []
+        for nm in names:
+            if nm == "base":
+                errs.append(err_gpu)
+                continue
+            rv, _ = P.compress(P.KernelOperator(variants[nm], "log", -np.log(0.5 / 256)), tess, 40, mid, p=10,
+                               stream=P.RandomStream(7), compute_error=False)
+            errs.append(P.frobenius_error(op, rv).fro / A_fro)
+            rv = None
+        ref_errs = np.asarray(g["err_family"], dtype=float) / A_fro
+        rms_gpu, rms_ref = np.sqrt(np.mean(np.square(errs))), np.sqrt(np.mean(np.square(ref_errs)))
+        print(f"{name}: exact errors over {names}: gpu {np.round(np.array(errs) * 1e9, 3)} e-9, "
+              f"ref {np.round(ref_errs * 1e9, 3)} e-9; rms gpu {rms_gpu:.4e} ref {rms_ref:.4e} "
+              f"({rms_gpu / rms_ref:.3f}x)")
         assert rms_gpu <= 1.05 * rms_ref
     # parity distance to the reference (probe estimate, upper bound)
     bound, est = probe_distance_bound(rep, g)
