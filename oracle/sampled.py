@@ -20,7 +20,13 @@ stage's independent units, and the stage time is scaled by
 * sequential stream draws: a sample of rows of the same stream;
 * one of the nine colour probes (ref/reconstruction.py:227-243), x 9;
 * the dense K x (K + p) SVD of type-B's pinv_core (ref/reconstruction.py:420)
-  at a reduced size, scaled by the cube of the size ratio.
+  at a reduced size, scaled by the size ratio to the power measured between
+  two reduced sizes (at most 3).
+
+Operator applies are sampled as two waves of the adapter's thread pool (a
+cold and a warm chunk per thread, as in the full apply). Checked against
+full runs of the oracle port at N = 16384 on the GPU box's 16 host threads
+(`tools/validate_sampled.py`, profiles/r02/validate_sampled.txt).
 
 The estimate is labelled as such wherever it is reported; `Estimate.stages`
 keeps every (measured seconds, sampled units, total units) triple.
@@ -85,7 +91,7 @@ def _tic():
     return time.perf_counter()
 
 
-def _apply_sample(op: KernelOp, X, waves=1, col_scale=1.0):
+def _apply_sample(op: KernelOp, X, waves=2, col_scale=1.0):
     """Time `waves` rounds of op.threads row chunks of op.apply(X) on the
     adapter's thread pool (the chunks a full apply runs, spread over the
     matrix). Returns (seconds, chunks timed, chunks in a full apply).
@@ -205,7 +211,7 @@ def estimate_a1(op: KernelOp, bx, k, p, label="c3", row_frac=16, blocks_per_size
     return est
 
 
-def estimate_b2(op: KernelOp, bx, k, p, label="c4", row_frac=16, block_frac=16, svd_scale=4):
+def estimate_b2(op: KernelOp, bx, k, p, label="c4", row_frac=16, sample_blocks=32, svd_scale=4):
     """compress_type_b(method="tag") (ref/reconstruction.py:586-677 with
     ref/bases.py:140-204, :326-421) at full size, sampled."""
     wall0 = _tic()
@@ -230,14 +236,14 @@ def estimate_b2(op: KernelOp, bx, k, p, label="c4", row_frac=16, block_frac=16, 
     U = [_basis(_combine(y[rows], plan.Z[i], gc), k) for i, rows in enumerate(bx.blocks)]
     est.add("I: combine + col_basis (both sides)", _tic() - t0, 1, 2)
     # phase III: near_b2 — pinvs of every G_j, H_i and the per-pair solves
-    npinv = max(1, b // block_frac)
+    npinv = max(1, min(b, sample_blocks))
     t0 = _tic()
     Gp = [svd_pinv(G[j]) for j in range(npinv)]
     est.add("III: svd pseudo-inverses of G_j, H_i", _tic() - t0, npinv, 2 * b)
     Gp = Gp + [Gp[0]] * (b - npinv)
     T = plan.T
     lim = 1e-10 * max(1.0, np.linalg.norm(T))
-    sample = list(range(0, b, block_frac))
+    sample = _block_sample(b, sample_blocks)
     t0 = _tic()
     npairs = 0
     for i in sample:
@@ -283,19 +289,31 @@ def estimate_b2(op: KernelOp, bx, k, p, label="c4", row_frac=16, block_frac=16, 
     est.add("II: V^T Omega, U^T (Y - B Omega)", _tic() - t0, len(sample), b)
     del omega, BOm, VtO, LHS
     # dense SVD pseudo-inverse of V^T Omega (K x L) and the core product,
-    # timed at K / svd_scale and scaled by svd_scale^3
-    Ks, Ls = K // svd_scale, L // svd_scale
-    M = np.random.default_rng(3).standard_normal((Ks, Ls))
-    t0 = _tic()
-    Pm = svd_pinv(M)
-    np.full((Ks, Ls), 0.5) @ Pm
-    est.add(f"II: svd pinv of V^T Omega + core product, at {Ks} x {Ls} (x {svd_scale}^3)", _tic() - t0, 1,
-            svd_scale ** 3)
+    # timed at K / svd_scale and K / (2 svd_scale); the growth exponent between
+    # the two sizes (at most 3: LAPACK's efficiency rises with the size)
+    # extrapolates to K
+    def svd_time(div):
+        Ks, Ls = K // div, L // div
+        M = np.random.default_rng(3).standard_normal((Ks, Ls))
+        t0 = _tic()
+        Pm = svd_pinv(M)
+        np.full((Ks, Ls), 0.5) @ Pm
+        return _tic() - t0
+    t_small, t_big = svd_time(2 * svd_scale), svd_time(svd_scale)
+    alpha = min(3.0, max(2.0, np.log2(t_big / t_small))) if t_small > 0 else 3.0
+    est.add(f"II: svd pinv of V^T Omega + core product, at K/{svd_scale} (x {svd_scale}^{alpha:.2f}, exponent "
+            f"fitted between K/{2 * svd_scale} and K/{svd_scale})", t_big, 1, svd_scale ** alpha)
     est.wall = _tic() - wall0
     return est
 
 
-def estimate_a2(op: KernelOp, bx, k, p, label="c5", block_frac=64, col_blocks=32, attempts=None):
+def _block_sample(b, count):
+    """`count` (at most b) evenly spaced block indices."""
+    count = max(1, min(b, count))
+    return sorted({(i * b) // count for i in range(count)})
+
+
+def estimate_a2(op: KernelOp, bx, k, p, label="c5", sample_blocks=64, col_blocks=32, attempts=None):
     """compress_type_a(method="tag") (ref/reconstruction.py:498-583 with
     ref/tagging.py:306-379, ref/bases.py:140-210, ref/reconstruction.py:185-244)
     at full size, sampled. Config 5 is infeasible on a CPU (phase II pushes a
@@ -309,7 +327,7 @@ def estimate_a2(op: KernelOp, bx, k, p, label="c5", block_frac=64, col_blocks=32
     gc = k + p
     stream = Stream(7)
     rng = np.random.default_rng(5)
-    sample = list(range(0, b, block_frac))
+    sample = _block_sample(b, sample_blocks)
     # plan: ref/tagging.py:355-379 per block, `attempts` draws (6 at c5)
     if attempts is None:
         attempts = plan_tags(bx, stream.child(1)).attempts if b <= 1024 else 6

@@ -11,7 +11,7 @@ from paper_2501_05528_b200 import dense as D
 
 SHAPES = [  # (ta, tb, M, N, K, batch)
     (0, 1, 256, 256, 2354, 1433), (0, 0, 1152, 1152, 1152, 98), (0, 0, 1728, 576, 576, 98),
-    (1, 0, 576, 1152, 576, 98), (1, 0, 2354, 40, 2304, 98), (0, 0, 64, 1152, 64, 98), (0, 0, 64, 40, 64, 98),
+    (1, 0, 576, 1152, 576, 98), (1, 0, 2354, 40, 2304, 98), (0, 0, 2304, 40, 2304, 98), (1, 0, 1152, 40, 1152, 98), (0, 0, 64, 1152, 64, 98), (0, 0, 64, 40, 64, 98),
     (0, 0, 4096, 4096, 4096, 1), (1, 0, 10240, 10250, 10250, 1)]
 out = []
 for ta, tb, M, N, K, b in SHAPES:
