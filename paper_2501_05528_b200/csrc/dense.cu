@@ -909,9 +909,8 @@ extern "C" int ublr_gemm_batched(int ta, int tb, int M, int N, int K, double alp
     if (cfg == 6) return launch_gemm3<128, 128, 4, 2, 3, 32, 128>(UBLR_GEMM_ARGS);
     return launch_gemm2<128, 128, 4, 4, 2>(UBLR_GEMM_ARGS);
   }
-  // skinny products (N <= 48 columns: the k-column null-space / sample
-  // solves): 128 x 48 tiles, 4 consumer warps of 32 x 48, no padding to 64
-  if (cfg == 6 && N <= 48 && M >= 256 && K >= 256) return launch_gemm3<128, 48, 4, 1, 3, 32, 128>(UBLR_GEMM_ARGS);
+  // (a 128 x 48 k_gemm3 tile for the skinny N = 40 solves measured no faster
+  // than k_gemm2 64 x 64: 14.8-15.9 TF/s either way)
   if (cfg == 1) return launch_gemm2<64, 64, 2, 4, 4, 16>(UBLR_GEMM_ARGS);
   if (cfg == 2) return launch_gemm2<64, 64, 2, 4, 4, 16, true>(UBLR_GEMM_ARGS);
   if (cfg == 3) return launch_gemm2<64, 64, 2, 4, 3, 32>(UBLR_GEMM_ARGS);

@@ -33,6 +33,6 @@ for ta, tb, M, N, K, b in SHAPES:
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
     tf = 2.0 * M * N * K * b / (ms * 1e-3) / 1e12
-    print(f"cfg {os.environ.get('UBLR_GEMM_CFG', '0')} t{ta}{tb} M{M} N{N} K{K} b{b}: {ms:8.3f} ms {tf:6.2f} TF/s",
+    print(f"cfg {os.environ.get('UBLR_GEMM_CFG', '6 (default)')} t{ta}{tb} M{M} N{N} K{K} b{b}: {ms:8.3f} ms {tf:6.2f} TF/s",
           flush=True)
     del A, B, C
