@@ -1267,9 +1267,11 @@ int sketch_common_v4(const ublr_op_t* op, const int32_t* off, int b, const doubl
     k_sketch_tagged4<KIND, DIM, L, C><<<grid, C::NT, sm, st>>>(*op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y,   \
                                                                row_begin, row_end);                              \
   }
-  // (a 96-column tile for c4's 532 columns — 6 x 96 = 576 padded columns
-  // instead of 5 x 128 = 640 — measured no faster on B200, 266.6 vs 262.7 ms:
-  // the sixth regeneration of the A tile costs what the padding saved)
+  // (measured no faster on B200 and dropped: a 96-column tile for c4's 532
+  // columns — 6 x 96 = 576 padded columns instead of 5 x 128 = 640 — 266.6 vs
+  // 262.7 ms, the sixth regeneration of the A tile costs what the padding
+  // saved; BK = 32 with 4 stages — c4 278 vs 263 ms, c5 shard 1662 vs
+  // 1573 ms, the 56-register producers spill)
 #define UBLR_TS4_L(KIND, DIM)                                                                                    \
   {                                                                                                              \
     if (ncols <= 64) {                                                                                           \
