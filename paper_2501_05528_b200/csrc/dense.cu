@@ -909,8 +909,18 @@ extern "C" int ublr_gemm_batched(int ta, int tb, int M, int N, int K, double alp
     if (cfg == 6) return launch_gemm3<128, 128, 4, 2, 3, 32, 128>(UBLR_GEMM_ARGS);
     return launch_gemm2<128, 128, 4, 4, 2>(UBLR_GEMM_ARGS);
   }
-  // (a 128 x 48 k_gemm3 tile for the skinny N = 40 solves measured no faster
-  // than k_gemm2 64 x 64: 14.8-15.9 TF/s either way)
+  // skinny products (N <= 48: the k-column null-space solves and sample
+  // products of block nullification): 128 x 40 / 128 x 48 k_gemm2 tiles,
+  // 8 warps of 16 x N, instead of the 64 x 64 tile whose last columns are
+  // padding: 15.8 -> 26.5 TF/s on M 2354 x N 40 x K 2304 (batch 98), 18.1 ->
+  // 28.3 on 2304 x 40 x 2304 (a 3-stage ring: 19.6 / 21.1; a 128 x 48
+  // k_gemm3: 15.8). UBLR_GEMM_SKINNY=0 restores the 64 x 64 tile.
+  static const int skinny = [] {
+    const char* e = getenv("UBLR_GEMM_SKINNY");
+    return e ? atoi(e) : 1;
+  }();
+  if (skinny && N <= 40 && M >= 128) return launch_gemm2<128, 40, 8, 1, 2>(UBLR_GEMM_ARGS);
+  if (skinny && N <= 48 && M >= 128) return launch_gemm2<128, 48, 8, 1, 2>(UBLR_GEMM_ARGS);
   if (cfg == 1) return launch_gemm2<64, 64, 2, 4, 4, 16>(UBLR_GEMM_ARGS);
   if (cfg == 2) return launch_gemm2<64, 64, 2, 4, 4, 16, true>(UBLR_GEMM_ARGS);
   if (cfg == 3) return launch_gemm2<64, 64, 2, 4, 3, 32>(UBLR_GEMM_ARGS);
