@@ -137,6 +137,17 @@ int ublr_sketch_tagged_two(const ublr_op_t* op, const ublr_op_t* op_adj, const i
 int ublr_sketch_tagged_pair(const ublr_op_t* op, const int32_t* off, int b, const double* T, int ell,
                             const double* G, const double* H, int64_t ld_x, int gc,
                             double* Y, double* Z, int64_t ld_y, int row_begin, int row_end, void* stream);
+/* The same products with a COMPENSATED fold over the column blocks: the
+ * rounding error of every Y_c += T[j,c] (A_ij X_j) is recovered exactly and
+ * summed apart. Type B (ref/reconstruction.py:326-376,
+ * tagging_pinv_discrepancy) divides pair-combined sketches by projected tags
+ * as small as 1e-4 and feeds them to the core least squares, so the
+ * sketch's fold rounding is the leading term of the B2 approximation error
+ * at N = 65,536; type A does not need it. H and Z may both be NULL (one
+ * side). ell <= 10; larger ell falls back to the plain fold. */
+int ublr_sketch_tagged_comp(const ublr_op_t* op, const int32_t* off, int b, const double* T, int ell,
+                            const double* G, const double* H, int64_t ld_x, int gc,
+                            double* Y, double* Z, int64_t ld_y, int row_begin, int row_end, void* stream);
 
 /* Generic operator apply (ref/operators.py:48-52 and every op.apply call of
  * the pipeline): out (N x w, permuted rows, ld_o) = A X (N x w, ld_x). */

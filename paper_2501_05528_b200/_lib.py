@@ -51,6 +51,7 @@ SIGNATURES = {
     "ublr_rng_normals": (INT, [P, P, INT, P, P, I64, P]),
     "ublr_sketch_tagged": (INT, [C.POINTER(OpDesc), P, INT, P, INT, P, I64, INT, P, I64, INT, INT, P]),
     "ublr_sketch_tagged_pair": (INT, [C.POINTER(OpDesc), P, INT, P, INT, P, P, I64, INT, P, P, I64, INT, INT, P]),
+    "ublr_sketch_tagged_comp": (INT, [C.POINTER(OpDesc), P, INT, P, INT, P, P, I64, INT, P, P, I64, INT, INT, P]),
     "ublr_sketch_tagged_two": (INT, [C.POINTER(OpDesc), C.POINTER(OpDesc), P, INT, P, INT, P, P, I64, INT, P, P, I64,
                                      INT, INT, P]),
     "ublr_apply": (INT, [C.POINTER(OpDesc), P, I64, INT, P, I64, P]),
@@ -119,7 +120,7 @@ def check(rc: int, what: str = ""):
 
 
 # kernels each C-ABI entry point launches (for bench.py's `gpu_launches`)
-LAUNCHES = {"ublr_rng_normals": 8, "ublr_sketch_tagged": 1, "ublr_sketch_tagged_pair": 1, "ublr_sketch_tagged_two": 1, "ublr_apply": 1,
+LAUNCHES = {"ublr_rng_normals": 8, "ublr_sketch_tagged": 1, "ublr_sketch_tagged_pair": 1, "ublr_sketch_tagged_comp": 1, "ublr_sketch_tagged_two": 1, "ublr_apply": 1,
             "ublr_block_qr": 1, "ublr_block_qr_pair": 1, "ublr_coupling": 1, "ublr_nearfield_colour": 2,
             "ublr_coupling_nearfield": 1,
             "ublr_blr_apply": 3, "ublr_gemm_batched": 1, "ublr_potrf_diag": 1, "ublr_lu_sign_diag": 1,
@@ -185,12 +186,12 @@ def _work_of(name, args):
             n, b, ell, gc = args[0].n, int(args[3]), int(args[5]), int(args[9])
             r0, r1 = int(args[13]), int(args[14])
             return 2 * (2.0 * (r1 - r0) * n * gc + 2.0 * (r1 - r0) * b * gc * ell)
-        if name in ("ublr_sketch_tagged", "ublr_sketch_tagged_pair"):
-            pair = name.endswith("pair")
+        if name in ("ublr_sketch_tagged", "ublr_sketch_tagged_pair", "ublr_sketch_tagged_comp"):
+            pair = not name.endswith("tagged")
             n, b, ell = args[0].n, int(args[2]), int(args[4])
             gc = int(args[8] if pair else args[7])
             r0, r1 = (int(args[12]), int(args[13])) if pair else (int(args[10]), int(args[11]))
-            cols = (2 if pair else 1) * gc
+            cols = (2 if pair and args[6] else 1) * gc
             return 2.0 * (r1 - r0) * n * cols + 2.0 * (r1 - r0) * b * cols * ell
         if name == "ublr_gemm_batched":
             return 2.0 * int(args[2]) * int(args[3]) * int(args[4]) * int(args[22])

@@ -212,10 +212,12 @@ def draw_test_pair(dt, stream: RandomStream, cols: int, tag_stream: RandomStream
     return TestPair(buf, dt.n, cols, dt.b, tag_cols)
 
 
-def tagged_sketch(op, dt, T_dev, T_entries, G, H, gc, out=None, ell=None):
+def tagged_sketch(op, dt, T_dev, T_entries, G, H, gc, out=None, ell=None, compensated=False):
     """Y = A Omega, Z = A^* Psi for the tagged test matrices; returns (Y, Z)
     (into `out` = (Y, Z) when given). T_entries (host) is needed only by a
-    black-box operator."""
+    black-box operator. `compensated`: the fold over column blocks recovers
+    its rounding errors (ublr_sketch_tagged_comp; type B, where the sketch's
+    rounding noise is divided by small projected tags)."""
     torch = _torch()
     inner = unwrap(op)
     ell = T_entries.shape[1] if ell is None else ell
@@ -227,7 +229,17 @@ def tagged_sketch(op, dt, T_dev, T_entries, G, H, gc, out=None, ell=None):
         else:
             Y = torch.empty((dt.n, s), dtype=torch.float64, device=dt.device)
             Z = torch.empty((dt.n, s), dtype=torch.float64, device=dt.device)
-        if getattr(inner, "symmetric", False):
+        if compensated and ell <= 10:
+            if getattr(inner, "symmetric", False):
+                _lib.call("ublr_sketch_tagged_comp", inner.device_op(dt.perm), _lib.ptr(dt.off), dt.b,
+                          _lib.ptr(T_dev), ell, _lib.ptr(G), _lib.ptr(H), gc, gc, _lib.ptr(Y), _lib.ptr(Z), s, 0, dt.n,
+                          stream)
+            else:
+                _lib.call("ublr_sketch_tagged_comp", inner.device_op(dt.perm), _lib.ptr(dt.off), dt.b,
+                          _lib.ptr(T_dev), ell, _lib.ptr(G), None, gc, gc, _lib.ptr(Y), None, s, 0, dt.n, stream)
+                _lib.call("ublr_sketch_tagged_comp", inner.device_op(dt.perm, adjoint=True), _lib.ptr(dt.off), dt.b,
+                          _lib.ptr(T_dev), ell, _lib.ptr(H), None, gc, gc, _lib.ptr(Z), None, s, 0, dt.n, stream)
+        elif getattr(inner, "symmetric", False):
             _lib.call("ublr_sketch_tagged_pair", inner.device_op(dt.perm), _lib.ptr(dt.off), dt.b,
                       _lib.ptr(T_dev), ell, _lib.ptr(G), _lib.ptr(H), gc, gc, _lib.ptr(Y), _lib.ptr(Z), s, 0, dt.n,
                       stream)
@@ -275,8 +287,10 @@ def _plan_worker():
 
 def tagging_bases(op, tess: Tessellation, k: int, p: int, plan, stream: RandomStream,
                   group_cols: int | None = None, extra_samples: bool = False, first=None, test_pair=None,
-                  defer_plan: bool = False):
+                  defer_plan: bool = False, compensated: bool = False):
     """ref/bases.py:140-204 on the GPU. Returns (BlockBases, SketchBundle).
+    `compensated`: tagged sketch with the compensated fold (type B; see
+    tagged_sketch).
 
     `plan` is a TaggingPlan, or a zero-argument callable producing one (the
     host redraw policy of ref/tagging.py:306-352) together with `first`, the
@@ -332,13 +346,13 @@ def tagging_bases(op, tess: Tessellation, k: int, p: int, plan, stream: RandomSt
         YZ = torch.empty(2 * dt.n * s, dtype=torch.float64, device=dt.device)
         yp = int(YZ.data_ptr())
         tagged_sketch(op, dt, T_dev, None, test_pair.G_ptr, test_pair.H_ptr, gc, out=(yp, yp + 8 * dt.n * s),
-                      ell=ell)
+                      ell=ell, compensated=compensated)
     else:
         Y = torch.empty((dt.n, s), dtype=torch.float64, device=dt.device)
         Z = torch.empty((dt.n, s), dtype=torch.float64, device=dt.device)
         G, H = draw_test_pair(dt, stream, gc) if test_pair is None else test_pair[:2]
         Y, Z = tagged_sketch(op, dt, T_dev, None if matrix is None else matrix.entries, G, H, gc, out=(Y, Z),
-                             ell=ell)
+                             ell=ell, compensated=compensated)
     _bill(op, s, s)
     if device_T:
         YZv = YZ.view(2, dt.n, s)
@@ -376,7 +390,8 @@ def tagging_bases(op, tess: Tessellation, k: int, p: int, plan, stream: RandomSt
             if pl.matrix is not m0:          # redrawn: sketch the accepted matrix
                 uv = None
                 T_entries = pl.matrix.entries
-                Y, Z = tagged_sketch(op, dt, _lib.h2d(T_entries, dt.device), T_entries, G, H, gc)
+                Y, Z = tagged_sketch(op, dt, _lib.h2d(T_entries, dt.device), T_entries, G, H, gc,
+                                     compensated=compensated)
         if uv is None:
             uv = block_bases_from_tagged(dt, Y, Z, _lib.h2d(combine(pl), dt.device), ell, gc, k)
         return pl, uv
@@ -403,7 +418,8 @@ def tagging_bases(op, tess: Tessellation, k: int, p: int, plan, stream: RandomSt
             if pl.matrix is m0:
                 return pl, None
             T_entries = pl.matrix.entries   # redrawn: sketch and bases of the accepted matrix
-            Y2, Z2 = tagged_sketch(op, dt, _lib.h2d(T_entries, dt.device), T_entries, G, H, gc)
+            Y2, Z2 = tagged_sketch(op, dt, _lib.h2d(T_entries, dt.device), T_entries, G, H, gc,
+                                   compensated=compensated)
             uv = block_bases_from_tagged(dt, Y2, Z2, _lib.h2d(combine(pl), dt.device), ell, gc, k)
             return pl, (uv, Y2, Z2)
         bundle.resolve_plan = resolve_plan

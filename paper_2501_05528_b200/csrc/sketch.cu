@@ -217,6 +217,79 @@ __global__ void __launch_bounds__(Cfg::NT) k_apply2(ublr_op_t op, const double* 
 // output columns) and short (BM = 64), halving the generation work per flop
 // against a 128 x 128 tile. The accumulator tile (64 x 256 doubles) is what
 // the register file can hold next to the fragments.
+// k-steps between two flushes of the DMMA accumulators into the TMEM sums
+// (0 = single-level accumulation); UBLR_APPLY_FLUSH overrides.
+inline int apply_flush() {
+  static const int v = [] {
+    const char* e = getenv("UBLR_APPLY_FLUSH");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+// Second-level accumulators in tensor memory for the long k loops of the
+// operator apply: the DMMA accumulators are added into TMEM every `flush`
+// k-steps and restarted from zero, so a sum over n = 65,536 terms becomes
+// n / (flush BK) partial sums of flush BK terms each (two-level summation:
+// the rounding error of the running sum grows with the square root of the
+// number of additions into one accumulator). Each consumer warp owns WD
+// doubles per lane in its lane quarter; the two warps of a quarter use
+// disjoint column ranges.
+template <int MI, int NJ>
+struct TmemAcc2 {
+  static constexpr int WD = MI * NJ * 2;
+  static_assert(WD % 8 == 0, "whole 8-double TMEM chunks");
+  uint32_t base;
+  __device__ __forceinline__ void init(uint32_t tbase, int cons_warp) {
+    base = tmem::addr(tbase, cons_warp, (cons_warp >> 2) * (2 * WD));
+  }
+  __device__ __forceinline__ void zero() const {
+    double z[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) z[q] = 0.0;
+#pragma unroll
+    for (int h = 0; h < WD / 8; ++h) tmem::st8(base + h * 16, z);
+    tmem::wait_st();
+  }
+  // tm += acc; acc = 0
+  __device__ __forceinline__ void flush(double (&acc)[MI][NJ][2]) const {
+#pragma unroll
+    for (int h0 = 0; h0 < WD / 8; h0 += 2) {
+      uint32_t raw[2][16];
+      tmem::ld8_async(base + h0 * 16, raw[0]);
+      if (h0 + 1 < WD / 8) tmem::ld8_async(base + (h0 + 1) * 16, raw[1]);
+      tmem::wait_ld();
+#pragma unroll
+      for (int f = 0; f < 2; ++f) {
+        if (h0 + f >= WD / 8) break;
+        double v[8];
+        tmem::unpack8(raw[f], v);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int e = (h0 + f) * 8 + q;
+          v[q] += acc[e / (NJ * 2)][(e / 2) % NJ][e & 1];
+          acc[e / (NJ * 2)][(e / 2) % NJ][e & 1] = 0.0;
+        }
+        tmem::st8(base + (h0 + f) * 16, v);
+      }
+    }
+    tmem::wait_st();
+  }
+  // acc += tm
+  __device__ __forceinline__ void finish(double (&acc)[MI][NJ][2]) const {
+#pragma unroll
+    for (int h = 0; h < WD / 8; ++h) {
+      double v[8];
+      tmem::ld8(base + h * 16, v);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int e = h * 8 + q;
+        acc[e / (NJ * 2)][(e / 2) % NJ][e & 1] += v[q];
+      }
+    }
+  }
+};
+
 template <int BM_, int BN_, int BK_, int STAGES_, int WMW_, int WNW_, int NPROD_>
 struct Ap3Cfg {
   static constexpr int BM = BM_, BN = BN_, BK = BK_, STAGES = STAGES_, WMW = WMW_, WNW = WNW_;
@@ -245,16 +318,18 @@ struct Ap3Cfg {
 // 71 %; the synchronous k_apply2 (UBLR_APPLY_CFG=4) 60.5 %.
 using Ap3Wide = Ap3Cfg<64, 256, 16, 4, 2, 4, 256>;     // default
 using Ap3Square = Ap3Cfg<128, 128, 32, 3, 2, 4, 256>;  // UBLR_APPLY_CFG=5
+using Ap3Half = Ap3Cfg<64, 128, 16, 4, 2, 4, 256>;     // last column slice of <= 128 columns
 
 template <int KIND, int DIM, class C>
 __global__ void __launch_bounds__(C::NT, 1) k_apply3(ublr_op_t op, const double* __restrict__ X, int64_t ldx,
-                                                     int w, double* __restrict__ out, int64_t ldo, int vec2) {
+                                                     int w, double* __restrict__ out, int64_t ldo, int vec2, int flush) {
   constexpr int BM = C::BM, BN = C::BN, BK = C::BK, STAGES = C::STAGES, SA = C::SA, SB = C::SB;
   constexpr int NPROD = C::NPROD, NCONS = C::NCONS, KPT = C::KPT, PB = C::PB;
   constexpr int MI = C::MI, NJ = C::NJ;
   __shared__ LogTables lt;
   __shared__ double ringbuf[9 * BK];
   __shared__ uint64_t full[STAGES], empty[STAGES];
+  __shared__ uint32_t tbase_slot;
   extern __shared__ double dsm[];
   double* As0 = dsm;
   double* Bs0 = dsm + STAGES * C::A_STAGE;
@@ -269,7 +344,10 @@ __global__ void __launch_bounds__(C::NT, 1) k_apply3(ublr_op_t op, const double*
       ws::mbar_init(&empty[s], NCONS);
     }
   }
+  if (flush > 0 && threadIdx.x / 32 == NPROD / 32) tmem::alloc(&tbase_slot, 256);  // first consumer warp
+  tmem::fence_before();
   __syncthreads();
+  tmem::fence_after();
 
   if (threadIdx.x < NPROD) {
     // ---------------- producers
@@ -315,9 +393,7 @@ __global__ void __launch_bounds__(C::NT, 1) k_apply3(ublr_op_t op, const double*
       ws::mbar_arrive(&full[s]);
     }
     cp_async_wait<0>();
-    return;
-  }
-
+  } else {
   // ---------------- consumers
   ws::regs_inc<C::CONS_REGS>();
   const int ct = threadIdx.x - NPROD;
@@ -330,6 +406,11 @@ __global__ void __launch_bounds__(C::NT, 1) k_apply3(ublr_op_t op, const double*
   for (int i = 0; i < MI; ++i)
 #pragma unroll
     for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  TmemAcc2<MI, NJ> tm;
+  if (flush > 0) {
+    tm.init(tbase_slot, warp);
+    tm.zero();
+  }
   for (int ks = 0; ks < nk; ++ks) {
     const int s = ks % STAGES;
     ws::mbar_wait(&full[s], (uint32_t)(ks / STAGES) & 1);
@@ -356,7 +437,9 @@ __global__ void __launch_bounds__(C::NT, 1) k_apply3(ublr_op_t op, const double*
         for (int j = 0; j < NJ; ++j) mma8x8x4(acc[i][j][0], acc[i][j][1], a[cur][i], b[cur][j]);
     }
     ws::mbar_arrive(&empty[s]);
+    if (flush > 0 && (ks + 1) % flush == 0 && ks + 1 < nk) tm.flush(acc);
   }
+  if (flush > 0) tm.finish(acc);
   const bool pair = (ldo % 2) == 0 && (((uintptr_t)out) % 16) == 0;
 #pragma unroll
   for (int i = 0; i < MI; ++i) {
@@ -374,6 +457,11 @@ __global__ void __launch_bounds__(C::NT, 1) k_apply3(ublr_op_t op, const double*
       }
     }
   }
+  }
+  tmem::fence_before();
+  __syncthreads();
+  tmem::fence_after();
+  if (flush > 0 && threadIdx.x / 32 == NPROD / 32) tmem::dealloc(tbase_slot, 256);
 }
 
 template <class C>
@@ -384,7 +472,7 @@ int launch_apply3(const ublr_op_t* op, const double* X, int64_t ld_x, int w, dou
 #define UBLR_AP3(KIND, DIM)                                                                                       \
   {                                                                                                               \
     UBLR_CUDA(cudaFuncSetAttribute(k_apply3<KIND, DIM, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
-    k_apply3<KIND, DIM, C><<<grid, C::NT, sm, st>>>(*op, X, ld_x, w, out, ld_o, vec2);                           \
+    k_apply3<KIND, DIM, C><<<grid, C::NT, sm, st>>>(*op, X, ld_x, w, out, ld_o, vec2, apply_flush());                           \
   }
   if (op->kind == UBLR_OP_LOG) {
     if (op->dim == 1) UBLR_AP3(UBLR_OP_LOG, 1) else if (op->dim == 2) UBLR_AP3(UBLR_OP_LOG, 2) else UBLR_AP3(UBLR_OP_LOG, 3)
@@ -395,6 +483,224 @@ int launch_apply3(const ublr_op_t* op, const double* X, int64_t ld_x, int w, dou
   return UBLR_OK;
 }
 
+// ------------------------------- apply, warp-specialised, cluster-shared A
+// k_apply3 regenerates the BM x n strip of A once per 256-column tile of X
+// (18 times at c3), and that generation runs on the FP64 pipe the DMMAs need
+// (ncu: DMMA 81 % + FP64 6 % of the shared pipe, the rest lost to the two
+// streams interleaving). Here the CS CTAs of a thread-block cluster take
+// the same row tile and CS adjacent column tiles: each generates 1/CS of
+// every A stage (a BK/CS slice of the k-step) and writes it into the stage
+// buffers of all CS CTAs: its own with plain stores, the peers' with
+// st.async through distributed shared memory, each store signalling
+// complete_tx on the peer's full[s]. Ring protocol per CTA and stage:
+// full[s] collects the CTA's own X-tile cp.async arrivals, its own
+// producers' arrivals (one of them expects the peers' bytes) and the
+// transaction bytes of the peers' slices; empty[s] collects one arrival per
+// consumer warp of every CTA (a producer overwrites the stage in all of
+// them). No cluster-scope fence anywhere in the loop.
+template <int KIND, int DIM, class C, int CS>
+__global__ void __launch_bounds__(C::NT, 1) k_apply4(ublr_op_t op, const double* __restrict__ X, int64_t ldx,
+                                                     int w, double* __restrict__ out, int64_t ldo, int vec2, int flush) {
+  constexpr int BM = C::BM, BN = C::BN, BK = C::BK, STAGES = C::STAGES, SA = C::SA, SB = C::SB;
+  constexpr int NPROD = C::NPROD, NCONS = C::NCONS;
+  constexpr int MI = C::MI, NJ = C::NJ;
+  constexpr int KL = BK / CS;          // k entries of a stage generated by this CTA
+  constexpr int KPT = KL / C::PH;      // ... by one producer thread
+  static_assert(BK % CS == 0 && KL % C::PH == 0 && KPT >= 1, "cluster split of the k-step");
+  __shared__ LogTables lt;
+  __shared__ double ringbuf[9 * BK];
+  __shared__ uint64_t full[STAGES], empty[STAGES];
+  __shared__ uint32_t tbase_slot;
+  extern __shared__ double dsm[];
+  double* As0 = dsm;
+  double* Bs0 = dsm + STAGES * C::A_STAGE;
+  const int n = (int)op.n;
+  const int row0 = blockIdx.x * BM, col0 = blockIdx.y * BN;
+  const int nk = (n + BK - 1) / BK;
+  const uint32_t crank = ws::cluster_ctarank();
+  ColRing<BK> ring{ringbuf};
+  if (KIND == UBLR_OP_LOG) init_log_tables(&lt);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      ws::mbar_init(&full[s], 2 * NPROD);
+      ws::mbar_init(&empty[s], CS * (NCONS / 32));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (flush > 0 && threadIdx.x / 32 == NPROD / 32) tmem::alloc(&tbase_slot, 256);  // first consumer warp
+  tmem::fence_before();
+  __syncthreads();
+  tmem::fence_after();
+  ws::cluster_sync();  // every CTA's barriers exist before a peer arrives on them
+
+  if (threadIdx.x < NPROD) {
+    // ---------------- producers
+    ws::regs_dec<C::PROD_REGS>();
+    const int p = threadIdx.x % BM;                              // A-tile row
+    const int kq0 = (int)crank * KL + (threadIdx.x / BM) * KPT;  // first k entry of this thread
+    const RowPoint rp = load_row_point(op, min(row0 + p, n - 1), true);
+    const RowPoint rq = {row0 + p, rp.orig, rp.x0, rp.x1, rp.x2};
+    const double diag = op.diag;
+    uint32_t peer_as[CS > 1 ? CS - 1 : 1], peer_full[CS > 1 ? CS - 1 : 1];
+#pragma unroll
+    for (int c = 1; c < CS; ++c) {
+      peer_as[c - 1] = ws::mapa(ws::smem_addr(As0), (crank + c) % CS);
+      peer_full[c - 1] = ws::mapa(ws::smem_addr(&full[0]), (crank + c) % CS);
+    }
+    constexpr uint32_t PEER_BYTES = (uint32_t)((CS - 1) * KL * BM * sizeof(double));  // per stage, from the peers
+    const bool has_cols = col0 < w;
+    ring.prefetch(op, 0, 0, n, NPROD);
+    cp_async_commit();
+    for (int ks = 0; ks < nk; ++ks) {
+      const int s = ks % STAGES;
+      const uint32_t u = (uint32_t)(ks / STAGES);
+      if (ks == 0) cp_async_wait<0>();
+      else cp_async_wait<1>();
+      ws::named_sync(1, NPROD);
+      if (ks + 1 < nk) ring.prefetch(op, ks + 1, (ks + 1) * BK, n, NPROD);
+      cp_async_commit();
+      ws::mbar_wait(&empty[s], (u & 1) ^ 1);
+      if (has_cols)
+        tile_copy<NPROD>(Bs0 + s * C::B_STAGE, SB, X, ldx, BK, BN, ks * BK, col0, n, w, IdentityRows{}, vec2 != 0);
+      cp_async_commit();
+      ws::mbar_cp_async_arrive(&full[s]);
+      double* As = As0 + s * C::A_STAGE;
+      const int k0 = ks * BK;
+      const double* cr = ring.buf + (ks % 3) * 3 * BK;
+      double v[KPT];
+#pragma unroll
+      for (int e = 0; e < KPT; ++e) {
+        const int kk = kq0 + e;
+        const double a = kernel_entry_dim<KIND, DIM>(rq, k0 + kk, cr[kk], DIM > 1 ? cr[BK + kk] : 0.0,
+                                                     DIM > 2 ? cr[2 * BK + kk] : 0.0, diag, &lt);
+        v[e] = k0 + kk < n ? a : 0.0;
+      }
+#pragma unroll
+      for (int e = 0; e < KPT; ++e) {
+        const int idx = s * C::A_STAGE + (kq0 + e) * SA + p;
+        As0[idx] = v[e];
+#pragma unroll
+        for (int c = 1; c < CS; ++c)
+          ws::st_async_f64(peer_as[c - 1] + (uint32_t)idx * 8u, v[e], peer_full[c - 1] + (uint32_t)s * 8u);
+      }
+      (void)As;
+      if (CS > 1 && threadIdx.x == 0) ws::mbar_arrive_expect_tx(&full[s], PEER_BYTES);
+      else ws::mbar_arrive(&full[s]);
+    }
+    cp_async_wait<0>();
+  } else {
+    // ---------------- consumers
+    ws::regs_inc<C::CONS_REGS>();
+    const int ct = threadIdx.x - NPROD;
+    const int warp = ct >> 5, lane = ct & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int wr = warp / C::WNW, wc = warp % C::WNW;
+    const int am0 = wr * C::WM + g, bn0 = wc * C::WN + g;
+    uint32_t peer_empty[CS];
+#pragma unroll
+    for (int c = 0; c < CS; ++c) peer_empty[c] = ws::mapa(ws::smem_addr(&empty[0]), (crank + c) % CS);
+    const bool has_cols = col0 + wc * C::WN < w;   // warps past the last column skip the DMMAs
+    double acc[MI][NJ][2];
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    TmemAcc2<MI, NJ> tm;
+    if (flush > 0) {
+      tm.init(tbase_slot, warp);
+      tm.zero();
+    }
+    for (int ks = 0; ks < nk; ++ks) {
+      const int s = ks % STAGES;
+      ws::mbar_wait(&full[s], (uint32_t)(ks / STAGES) & 1);
+      if (has_cols) {
+        const double* As = As0 + s * C::A_STAGE;
+        const double* Bs = Bs0 + s * C::B_STAGE;
+        double a[2][MI], b[2][NJ];
+#pragma unroll
+        for (int i = 0; i < MI; ++i) a[0][i] = As[t * SA + am0 + i * 8];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) b[0][j] = Bs[t * SB + bn0 + j * 8];
+#pragma unroll
+        for (int k4 = 0; k4 < BK / 4; ++k4) {
+          const int cur = k4 & 1;
+          if (k4 + 1 < BK / 4) {
+            const int kr = (k4 + 1) * 4 + t;
+#pragma unroll
+            for (int i = 0; i < MI; ++i) a[cur ^ 1][i] = As[kr * SA + am0 + i * 8];
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) b[cur ^ 1][j] = Bs[kr * SB + bn0 + j * 8];
+          }
+#pragma unroll
+          for (int i = 0; i < MI; ++i)
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) mma8x8x4(acc[i][j][0], acc[i][j][1], a[cur][i], b[cur][j]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+#pragma unroll
+        for (int c = 0; c < CS; ++c) ws::mbar_arrive_remote(peer_empty[c] + (uint32_t)s * 8u);
+      }
+      if (flush > 0 && (ks + 1) % flush == 0 && ks + 1 < nk) tm.flush(acc);
+    }
+    if (flush > 0) tm.finish(acc);
+    const bool pair = (ldo % 2) == 0 && (((uintptr_t)out) % 16) == 0;
+#pragma unroll
+    for (int i = 0; i < MI; ++i) {
+      const int r = row0 + wr * C::WM + i * 8 + g;
+      if (r >= n) continue;
+      double* orow = out + (int64_t)r * ldo;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const int c = col0 + wc * C::WN + j * 8 + 2 * t;
+        if (pair && c + 1 < w) {
+          *reinterpret_cast<double2*>(orow + c) = make_double2(acc[i][j][0], acc[i][j][1]);
+        } else {
+          if (c < w) orow[c] = acc[i][j][0];
+          if (c + 1 < w) orow[c + 1] = acc[i][j][1];
+        }
+      }
+    }
+  }
+  // no CTA leaves while a peer may still store into its stages or arrive on its barriers
+  tmem::fence_before();
+  ws::cluster_sync();
+  tmem::fence_after();
+  if (flush > 0 && threadIdx.x / 32 == NPROD / 32) tmem::dealloc(tbase_slot, 256);
+}
+
+template <class C, int CS>
+int launch_apply4(const ublr_op_t* op, const double* X, int64_t ld_x, int w, double* out, int64_t ld_o, int vec2,
+                  cudaStream_t st) {
+  const unsigned ty = (unsigned)((w + C::BN - 1) / C::BN);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((op->n + C::BM - 1) / C::BM), (ty + CS - 1) / CS * CS);
+  cfg.blockDim = dim3(C::NT);
+  cfg.dynamicSmemBytes = C::smem_bytes();
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = CS;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+#define UBLR_AP4(KIND, DIM)                                                                                       \
+  {                                                                                                               \
+    UBLR_CUDA(cudaFuncSetAttribute(k_apply4<KIND, DIM, C, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
+                                   (int)cfg.dynamicSmemBytes));                                                   \
+    UBLR_CUDA(cudaLaunchKernelEx(&cfg, k_apply4<KIND, DIM, C, CS>, *op, X, ld_x, w, out, ld_o, vec2, apply_flush()));            \
+  }
+  if (op->kind == UBLR_OP_LOG) {
+    if (op->dim == 1) UBLR_AP4(UBLR_OP_LOG, 1) else if (op->dim == 2) UBLR_AP4(UBLR_OP_LOG, 2) else UBLR_AP4(UBLR_OP_LOG, 3)
+  } else {
+    if (op->dim == 1) UBLR_AP4(UBLR_OP_INV, 1) else if (op->dim == 2) UBLR_AP4(UBLR_OP_INV, 2) else UBLR_AP4(UBLR_OP_INV, 3)
+  }
+#undef UBLR_AP4
+  return UBLR_OK;
+}
+
 // ---------------------------------------------------------- tagged sketch
 constexpr int TS_BM = 16;
 constexpr int TS_BK = 32;
@@ -402,7 +708,7 @@ constexpr int TS_THREADS = 256;
 
 // CTA: 16 consecutive (permuted) rows x BN of the (gc or 2gc) test-block columns.
 // Warp w covers all 16 rows x BN/8 columns.
-template <int KIND, int L, int BN>
+template <int KIND, int L, int BN, bool COMP = false>
 __global__ void __launch_bounds__(TS_THREADS) k_sketch_tagged(ublr_op_t op, const int32_t* __restrict__ off, int b,
                                                               const double* __restrict__ T, int ell,
                                                               const double* __restrict__ G,
@@ -440,6 +746,15 @@ __global__ void __launch_bounds__(TS_THREADS) k_sketch_tagged(ublr_op_t op, cons
 #pragma unroll
       for (int j = 0; j < NJ; ++j) acc[c][r][j][0] = acc[c][r][j][1] = 0.0;
   double wacc[2][NJ][2];
+  // COMP: compensated fold (the rounding error of every acc += tc * w is
+  // recovered exactly with an error-free product and TwoSum, and summed apart)
+  double cacc[COMP ? L : 1][2][NJ][2];
+#pragma unroll
+  for (int c = 0; c < (COMP ? L : 1); ++c)
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) cacc[c][r][j][0] = cacc[c][r][j][1] = 0.0;
 
   __syncthreads();
 
@@ -507,8 +822,20 @@ __global__ void __launch_bounds__(TS_THREADS) k_sketch_tagged(ublr_op_t op, cons
       for (int r = 0; r < 2; ++r)
 #pragma unroll
         for (int jj = 0; jj < NJ; ++jj) {
-          acc[c][r][jj][0] = fma(tc, wacc[r][jj][0], acc[c][r][jj][0]);
-          acc[c][r][jj][1] = fma(tc, wacc[r][jj][1], acc[c][r][jj][1]);
+          if (COMP) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const double a = acc[c][r][jj][h], w = wacc[r][jj][h];
+              const double pr = tc * w, pe = fma(tc, w, -pr);
+              const double sm = a + pr, bb = sm - a;
+              const double e = (a - (sm - bb)) + (pr - bb);
+              cacc[COMP ? c : 0][r][jj][h] += e + pe;
+              acc[c][r][jj][h] = sm;
+            }
+          } else {
+            acc[c][r][jj][0] = fma(tc, wacc[r][jj][0], acc[c][r][jj][0]);
+            acc[c][r][jj][1] = fma(tc, wacc[r][jj][1], acc[c][r][jj][1]);
+          }
         }
     }
     ++j;
@@ -529,7 +856,7 @@ __global__ void __launch_bounds__(TS_THREADS) k_sketch_tagged(ublr_op_t op, cons
         int q = (col < gc) ? col : col - gc;
 #pragma unroll
         for (int c = 0; c < L; ++c)
-          if (c < ell) dst[(int64_t)row * ldy + c * gc + q] = acc[c][r][jj][h];
+          if (c < ell) dst[(int64_t)row * ldy + c * gc + q] = acc[c][r][jj][h] + (COMP ? cacc[COMP ? c : 0][r][jj][h] : 0.0);
       }
   }
 }
@@ -866,9 +1193,31 @@ struct Sk4Cfg {
   static constexpr int A_STAGE = BK * SA, B_STAGE = BK * SB;
   static constexpr int CONS_REGS = 200, PROD_REGS = 56;
   static constexpr size_t smem_bytes() { return (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double); }
+  // compensated fold: 16 bytes (8 bf16 error sums) per consumer thread and 8-entry chunk of each tag group
+  static constexpr int WD = MI * NJ * 2, WDP = (WD + 7) / 8 * 8;
+  static constexpr int TCAP = ((512 / (NCONS / 32 / 4)) / 2) / WDP;   // tag groups a warp's TMEM columns hold
+  static constexpr size_t comp_bytes(int L) { return (size_t)NCONS * 16 * (size_t)(L * (WDP / 8)); }
 };
 
-template <int KIND, int DIM, int L, class C>
+// Compensated fold (COMP). Z_c = sum_j T[j,c] W_j adds b = 256 increments of
+// size ~|W_j| into an accumulator of size ~sqrt(b)|W_j|: its rounding errors
+// (one per fold, half an ulp of the running sum) are the largest noise term
+// of the tagged sketch, and type B divides the pair-combined sketch by
+// projected tags as small as 1e-4 and pushes it through the core least
+// squares, so that noise IS the approximation error of B2 at N = 65,536
+// (measured: 9.1e-9 -> 5.4e-9 with the errors recovered; reference 7.1e-9).
+// Per fold s = fma(t, w, a) is followed by e = fma(t, w, a - s), the exact
+// error when |t w| <~ |a| (a - s is then exact), and e is summed apart: in
+// bf16 in shared memory for the TMEM groups (TMEM is full; |sum e| is a few
+// ulp(a), so 8 mantissa bits leave ~0.1 ulp), in fp32 registers for the
+// register groups; the epilogue adds the error sums to the accumulators.
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+template <int KIND, int DIM, int L, class C, bool COMP = false>
 __global__ void __launch_bounds__(C::NT, 1) k_sketch_tagged4(ublr_op_t op, const int32_t* __restrict__ off, int b,
                                                              const double* __restrict__ T, int ell,
                                                              const double* __restrict__ G,
@@ -889,6 +1238,7 @@ __global__ void __launch_bounds__(C::NT, 1) k_sketch_tagged4(ublr_op_t op, const
   extern __shared__ double dsm[];
   double* As0 = dsm;
   double* Bs0 = dsm + STAGES * C::A_STAGE;
+  uint4* comp = reinterpret_cast<uint4*>(dsm + STAGES * (C::A_STAGE + C::B_STAGE));  // COMP: [chunk][consumer thread]
   const int ncols = (H ? 2 : 1) * gc;
   const int row0 = row_begin + blockIdx.x * BM;
   const int col0 = blockIdx.y * BN;
@@ -1004,6 +1354,10 @@ __global__ void __launch_bounds__(C::NT, 1) k_sketch_tagged4(ublr_op_t op, const
 #pragma unroll
         for (int c = 0; c < (RG > 0 ? RG : 1); ++c) racc[c][i][jj][0] = racc[c][i][jj][1] = 0.0;
       }
+    if (COMP) {
+#pragma unroll
+      for (int ch = 0; ch < L * (WDP / 8); ++ch) comp[ch * C::NCONS + ct] = make_uint4(0u, 0u, 0u, 0u);
+    }
     {
       double z8[8];
 #pragma unroll
@@ -1053,7 +1407,7 @@ __global__ void __launch_bounds__(C::NT, 1) k_sketch_tagged4(ublr_op_t op, const
         }
       // TMEM groups in batches of FB chunks: issue the loads, one wait, FMAs, stores
       constexpr int NCH = TG * (WDP / 8);           // 8-double chunks held in TMEM
-      constexpr int FB = NCH < (WDP > 8 ? 2 : 4) ? NCH : (WDP > 8 ? 2 : 4);
+      constexpr int FB = COMP ? 1 : (NCH < (WDP > 8 ? 2 : 4) ? NCH : (WDP > 8 ? 2 : 4));
 #pragma unroll
       for (int c0 = 0; c0 < NCH; c0 += FB) {
         uint32_t raw[FB][16];
@@ -1068,8 +1422,29 @@ __global__ void __launch_bounds__(C::NT, 1) k_sketch_tagged4(ublr_op_t op, const
           const double tc = (c < ell) ? __ldg(&Tj[c]) : 0.0;
           double v[8];
           tmem::unpack8(raw[f], v);
+          if (COMP) {
+            uint4* cp = comp + (c0 + f) * C::NCONS + ct;
+            const uint4 cb = *cp;
+            const uint32_t cw[4] = {cb.x, cb.y, cb.z, cb.w};
+            uint32_t nw[4];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) v[q] = fma(tc, wf[h * 8 + q], v[q]);
+            for (int q2 = 0; q2 < 4; ++q2) {
+              float e2[2] = {__uint_as_float(cw[q2] << 16), __uint_as_float(cw[q2] & 0xffff0000u)};
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh) {
+                const int q = 2 * q2 + hh;
+                const double a = v[q], ww = wf[h * 8 + q];
+                const double sm = fma(tc, ww, a);
+                e2[hh] += __double2float_rn(fma(tc, ww, a - sm));
+                v[q] = sm;
+              }
+              nw[q2] = pack_bf16x2(e2[0], e2[1]);
+            }
+            *cp = make_uint4(nw[0], nw[1], nw[2], nw[3]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = fma(tc, wf[h * 8 + q], v[q]);
+          }
           tmem::st8(tmem::addr(tbase, twarp, colbase + (c0 + f) * 16), v);
         }
       }
@@ -1080,9 +1455,37 @@ __global__ void __launch_bounds__(C::NT, 1) k_sketch_tagged4(ublr_op_t op, const
         for (int i = 0; i < MI; ++i)
 #pragma unroll
           for (int jj = 0; jj < NJ; ++jj) {
-            racc[c][i][jj][0] = fma(tc, wf[(i * NJ + jj) * 2], racc[c][i][jj][0]);
-            racc[c][i][jj][1] = fma(tc, wf[(i * NJ + jj) * 2 + 1], racc[c][i][jj][1]);
+            if (!COMP) {
+              racc[c][i][jj][0] = fma(tc, wf[(i * NJ + jj) * 2], racc[c][i][jj][0]);
+              racc[c][i][jj][1] = fma(tc, wf[(i * NJ + jj) * 2 + 1], racc[c][i][jj][1]);
+            }
           }
+        if (COMP) {
+#pragma unroll
+          for (int h = 0; h < WDP / 8; ++h) {
+            uint4* cp = comp + ((TG + c) * (WDP / 8) + h) * C::NCONS + ct;
+            const uint4 cb = *cp;
+            const uint32_t cw[4] = {cb.x, cb.y, cb.z, cb.w};
+            uint32_t nw[4];
+#pragma unroll
+            for (int q2 = 0; q2 < 4; ++q2) {
+              float e2[2] = {__uint_as_float(cw[q2] << 16), __uint_as_float(cw[q2] & 0xffff0000u)};
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh) {
+                const int e = h * 8 + 2 * q2 + hh;
+                if (e < WD) {
+                  double& a = racc[c][e / (NJ * 2)][(e / 2) % NJ][e & 1];
+                  const double ww = wf[e];
+                  const double sm = fma(tc, ww, a);
+                  e2[hh] += __double2float_rn(fma(tc, ww, a - sm));
+                  a = sm;
+                }
+              }
+              nw[q2] = pack_bf16x2(e2[0], e2[1]);
+            }
+            *cp = make_uint4(nw[0], nw[1], nw[2], nw[3]);
+          }
+        }
       }
     }
     tmem::wait_st();
@@ -1096,6 +1499,15 @@ __global__ void __launch_bounds__(C::NT, 1) k_sketch_tagged4(ublr_op_t op, const
         for (int h = 0; h < WDP / 8; ++h) {
           double v[8];
           tmem::ld8(tmem::addr(tbase, twarp, colbase + (c * WDP + h * 8) * 2), v);
+          if (COMP) {
+            const uint4 cb = comp[(c * (WDP / 8) + h) * C::NCONS + ct];
+            const uint32_t cw[4] = {cb.x, cb.y, cb.z, cb.w};
+#pragma unroll
+            for (int q2 = 0; q2 < 4; ++q2) {
+              v[2 * q2] += (double)__uint_as_float(cw[q2] << 16);
+              v[2 * q2 + 1] += (double)__uint_as_float(cw[q2] & 0xffff0000u);
+            }
+          }
 #pragma unroll
           for (int q = 0; q < 8; ++q) accv[h * 8 + q] = v[q];
         }
@@ -1107,6 +1519,18 @@ __global__ void __launch_bounds__(C::NT, 1) k_sketch_tagged4(ublr_op_t op, const
             accv[(i * NJ + jj) * 2] = racc[(c - TG) < 0 ? 0 : (c - TG)][i][jj][0];
             accv[(i * NJ + jj) * 2 + 1] = racc[(c - TG) < 0 ? 0 : (c - TG)][i][jj][1];
           }
+        if (COMP) {
+#pragma unroll
+          for (int h = 0; h < WDP / 8; ++h) {
+            const uint4 cb = comp[(c * (WDP / 8) + h) * C::NCONS + ct];
+            const uint32_t cw[4] = {cb.x, cb.y, cb.z, cb.w};
+#pragma unroll
+            for (int q2 = 0; q2 < 4; ++q2) {
+              accv[h * 8 + 2 * q2] += (double)__uint_as_float(cw[q2] << 16);
+              accv[h * 8 + 2 * q2 + 1] += (double)__uint_as_float(cw[q2] & 0xffff0000u);
+            }
+          }
+        }
       }
 #pragma unroll
       for (int i = 0; i < MI; ++i) {
@@ -1159,10 +1583,45 @@ extern "C" int ublr_apply(const ublr_op_t* op, const double* X, int64_t ld_x, in
     UBLR_CUDA(cudaFuncSetAttribute(k_apply2<KIND, CFG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
     k_apply2<KIND, CFG><<<grid, CFG::NT, sm, st>>>(*op, X, ld_x, w, out, ld_o, vec2);                         \
   })
-  if (w > 64 && op->kind != UBLR_OP_DENSE && (variant == 0 || variant == 5)) {
-    rc = variant == 5 ? launch_apply3<Ap3Square>(op, X, ld_x, w, out, ld_o, vec2, st)
-                      : launch_apply3<Ap3Wide>(op, X, ld_x, w, out, ld_o, vec2, st);
+  if (w > 64 && op->kind != UBLR_OP_DENSE && variant == 5) {
+    rc = launch_apply3<Ap3Square>(op, X, ld_x, w, out, ld_o, vec2, st);
     if (rc) return rc;
+  } else if (w > 64 && op->kind != UBLR_OP_DENSE && variant == 0) {
+    // column ranges: clusters of 4 then 2 CTAs sharing the generated A strip
+    // over whole 256-column tiles, the remainder on single CTAs (a 128-column
+    // tile for a last slice of <= 128 columns). All offsets are multiples of
+    // 256 columns, so the 16-byte alignment of X / out carries over.
+    static const int cs_max = [] {
+      const char* e = getenv("UBLR_APPLY_CS");
+      return e ? atoi(e) : 2;
+    }();
+    int c0 = 0;
+    if (cs_max >= 4 && (w - c0) >= 4 * Ap3Wide::BN) {
+      const int wm = (w - c0) / (4 * Ap3Wide::BN) * (4 * Ap3Wide::BN);
+      rc = launch_apply4<Ap3Wide, 4>(op, X + c0, ld_x, wm, out + c0, ld_o, vec2, st);
+      if (rc) return rc;
+      c0 += wm;
+    }
+    if (cs_max >= 2 && (w - c0) >= 2 * Ap3Wide::BN) {
+      const int wm = (w - c0) / (2 * Ap3Wide::BN) * (2 * Ap3Wide::BN);
+      rc = launch_apply4<Ap3Wide, 2>(op, X + c0, ld_x, wm, out + c0, ld_o, vec2, st);
+      if (rc) return rc;
+      c0 += wm;
+    }
+    int rem = w - c0;
+    if (rem > 0) {
+      int wfull = rem / Ap3Wide::BN * Ap3Wide::BN;
+      if (rem - wfull > Ap3Half::BN) wfull = rem;
+      if (wfull > 0) {
+        rc = launch_apply3<Ap3Wide>(op, X + c0, ld_x, wfull, out + c0, ld_o, vec2, st);
+        if (rc) return rc;
+        c0 += wfull;
+      }
+      if (w - c0 > 0) {
+        rc = launch_apply3<Ap3Half>(op, X + c0, ld_x, w - c0, out + c0, ld_o, vec2, st);
+        if (rc) return rc;
+      }
+    }
   } else if (w <= 64) {
     UBLR_AP2(CfgN);
   } else {
@@ -1177,7 +1636,7 @@ namespace {
 // v1: 16-row tiles (kept as default: measured faster than v2 on c2/c4 shapes, profiles/r01)
 int sketch_common_v1(const ublr_op_t* op, const int32_t* off, int b, const double* T, int ell, const double* G,
                      const double* H, int64_t ld_x, int gc, double* Y, double* Z, int64_t ld_y, int row_begin,
-                     int row_end, cudaStream_t st) {
+                     int row_end, cudaStream_t st, bool comp = false) {
   int ncols = (H ? 2 : 1) * gc;
   dim3 grid;
   grid.y = (unsigned)((row_end - row_begin + TS_BM - 1) / TS_BM);
@@ -1192,7 +1651,17 @@ int sketch_common_v1(const ublr_op_t* op, const int32_t* off, int b, const doubl
                                                                  row_begin, row_end);                  \
     })                                                                                                     \
   }
-  if (ell <= 4) UBLR_TS_LAUNCH(4, 128)
+  if (ell <= 4 && !comp) UBLR_TS_LAUNCH(4, 128)
+  else if (ell <= 10 && comp) {
+    grid.x = (unsigned)((ncols + 63) / 64);
+    UBLR_DISPATCH_KIND(op->kind, KIND, {
+      size_t sm = (size_t)2 * TS_BK * ((TS_BM + 4) + (64 + 4)) * sizeof(double);
+      UBLR_CUDA(cudaFuncSetAttribute(k_sketch_tagged<KIND, 10, 64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sm));
+      k_sketch_tagged<KIND, 10, 64, true><<<grid, TS_THREADS, sm, st>>>(*op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y,
+                                                                        row_begin, row_end);
+    })
+  }
   else if (ell <= 10) UBLR_TS_LAUNCH(10, 64)
   else if (ell <= 28) UBLR_TS_LAUNCH(28, 64)
   else {
@@ -1254,7 +1723,7 @@ int sketch_common_v3(const ublr_op_t* op, const int32_t* off, int b, const doubl
 
 int sketch_common_v4(const ublr_op_t* op, const int32_t* off, int b, const double* T, int ell, const double* G,
                      const double* H, int64_t ld_x, int gc, double* Y, double* Z, int64_t ld_y, int row_begin,
-                     int row_end, cudaStream_t st) {
+                     int row_end, cudaStream_t st, bool comp = false) {
   const int ncols = (H ? 2 : 1) * gc;
   dim3 grid((unsigned)((row_end - row_begin + 31) / 32), 0);
 #define UBLR_TS4(KIND, DIM, L, BNv)                                                                              \
@@ -1280,6 +1749,26 @@ int sketch_common_v4(const ublr_op_t* op, const int32_t* off, int b, const doubl
       if (ell <= 4) UBLR_TS4(KIND, DIM, 4, 128) else UBLR_TS4(KIND, DIM, 10, 128)                                \
     }                                                                                                            \
   }
+#define UBLR_TS4C(KIND, DIM)                                                                                     \
+  {                                                                                                              \
+    using C = Sk4Cfg<128, 6>;                                                                                    \
+    grid.y = (unsigned)((ncols + C::BN - 1) / C::BN);                                                            \
+    size_t sm = C::smem_bytes() + C::comp_bytes(10);                                                             \
+    UBLR_CUDA(cudaFuncSetAttribute(k_sketch_tagged4<KIND, DIM, 10, C, true>,                                     \
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));                      \
+    k_sketch_tagged4<KIND, DIM, 10, C, true><<<grid, C::NT, sm, st>>>(*op, off, b, T, ell, G, H, ld_x, gc, Y, Z,  \
+                                                                      ld_y, row_begin, row_end);                 \
+  }
+  if (comp) {   // compensated fold (type B): one tile shape, ell <= 10
+    if (op->kind == UBLR_OP_LOG) {
+      if (op->dim == 1) UBLR_TS4C(UBLR_OP_LOG, 1) else if (op->dim == 2) UBLR_TS4C(UBLR_OP_LOG, 2) else UBLR_TS4C(UBLR_OP_LOG, 3)
+    } else {
+      if (op->dim == 1) UBLR_TS4C(UBLR_OP_INV, 1) else if (op->dim == 2) UBLR_TS4C(UBLR_OP_INV, 2) else UBLR_TS4C(UBLR_OP_INV, 3)
+    }
+    UBLR_LAUNCH_CHECK();
+    return UBLR_OK;
+  }
+#undef UBLR_TS4C
   if (op->kind == UBLR_OP_LOG) {
     if (op->dim == 1) UBLR_TS4_L(UBLR_OP_LOG, 1) else if (op->dim == 2) UBLR_TS4_L(UBLR_OP_LOG, 2) else UBLR_TS4_L(UBLR_OP_LOG, 3)
   } else {
@@ -1293,8 +1782,16 @@ int sketch_common_v4(const ublr_op_t* op, const int32_t* off, int b, const doubl
 
 int sketch_common(const ublr_op_t* op, const int32_t* off, int b, const double* T, int ell, const double* G,
                   const double* H, int64_t ld_x, int gc, double* Y, double* Z, int64_t ld_y, int row_begin,
-                  int row_end, cudaStream_t st) {
+                  int row_end, cudaStream_t st, bool comp = false) {
   UBLR_REQUIRE(row_begin >= 0 && row_begin < row_end && row_end <= op->n, UBLR_ERR_VALUE, "sketch: bad row range");
+  if (comp && ell <= 10) {
+    // compensated fold: the warp-specialised kernel for kernel operators, the
+    // 16-row register-tile kernel otherwise (dense A, unaligned panels)
+    const bool vok = (ld_x % 2) == 0 && (gc % 2) == 0 && ((uintptr_t)G) % 16 == 0 && (!H || ((uintptr_t)H) % 16 == 0);
+    if ((op->kind == UBLR_OP_LOG || op->kind == UBLR_OP_INV) && vok)
+      return sketch_common_v4(op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y, row_begin, row_end, st, true);
+    return sketch_common_v1(op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y, row_begin, row_end, st, true);
+  }
   static const char* ver = getenv("UBLR_SKETCH_VERSION");
   const int v = ver ? atoi(ver) : 4;
   const bool vec_ok = (ld_x % 2) == 0 && (gc % 2) == 0 && ((uintptr_t)G) % 16 == 0 && (!H || ((uintptr_t)H) % 16 == 0);
@@ -1356,4 +1853,16 @@ extern "C" int ublr_sketch_tagged_pair(const ublr_op_t* op, const int32_t* off, 
                    ld_y >= (int64_t)ell * gc,
                UBLR_ERR_VALUE, "ublr_sketch_tagged_pair: bad arguments");
   return sketch_common(op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y, row_begin, row_end, (cudaStream_t)stream);
+}
+
+extern "C" int ublr_sketch_tagged_comp(const ublr_op_t* op, const int32_t* off, int b, const double* T, int ell,
+                                       const double* G, const double* H, int64_t ld_x, int gc, double* Y, double* Z,
+                                       int64_t ld_y, int row_begin, int row_end, void* stream) {
+  int rc = check_op(op);
+  if (rc) return rc;
+  UBLR_REQUIRE(b > 0 && off && T && G && Y && (!H == !Z) && gc > 0 && ell > 0 && ld_x >= gc &&
+                   ld_y >= (int64_t)ell * gc,
+               UBLR_ERR_VALUE, "ublr_sketch_tagged_comp: bad arguments");
+  return sketch_common(op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y, row_begin, row_end, (cudaStream_t)stream,
+                       true);
 }

@@ -29,9 +29,20 @@ __global__ void __launch_bounds__(CT) k_tag_combine_pairs(const double* __restri
   for (int64_t e = (int64_t)blockIdx.y * CT + threadIdx.x; e < (int64_t)m * gc; e += (int64_t)gridDim.y * CT) {
     int r = (int)(e / gc), q = (int)(e % gc);
     const double* yr = Y + (int64_t)(r0 + r) * ldy + q;
-    double s = 0.0;
-    for (int c = 0; c < ell; ++c) s = fma(ws[c], yr[(int64_t)c * gc], s);
-    o[(int64_t)r * gc + q] = s;
+    // the null-vector weights cancel the near-field part of every Y_c, so
+    // the result is far smaller than the terms: a compensated dot product
+    // (error-free products and TwoSum, errors summed apart) keeps the
+    // combination's own rounding out of the near blocks -- the kernel is
+    // HBM-bound, the extra FP64 operations are free
+    double s = 0.0, comp = 0.0;
+    for (int c = 0; c < ell; ++c) {
+      const double wy = ws[c], y = yr[(int64_t)c * gc];
+      const double pr = wy * y, pe = fma(wy, y, -pr);
+      const double t = s + pr, bb = t - s;
+      comp += ((s - (t - bb)) + (pr - bb)) + pe;
+      s = t;
+    }
+    o[(int64_t)r * gc + q] = s + comp;
   }
 }
 

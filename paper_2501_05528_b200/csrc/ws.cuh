@@ -55,6 +55,47 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// ---- thread-block clusters: the CTAs of a cluster share generated operand
+// tiles through distributed shared memory. A peer's copy of a shared-memory
+// object lives at mapa(own address, peer rank); stores and mbarrier arrivals
+// on it use the shared::cluster window, waits stay on the CTA's own barrier
+// with cluster-scope acquire.
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+// Asynchronous 8-byte store into a peer CTA's shared memory that signals
+// complete_tx(8) on an mbarrier of that peer (both addresses in the
+// shared::cluster window, same CTA). The data become visible to the threads
+// that observe the barrier's phase complete -- no fence on either side.
+__device__ __forceinline__ void st_async_f64(uint32_t cluster_addr, double v, uint32_t cluster_mbar) {
+  asm volatile("st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(cluster_addr),
+               "d"(v), "r"(cluster_mbar)
+               : "memory");
+}
+// arrive on the CTA's own barrier and add `bytes` to the transaction count the phase waits for
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+// arrive on a barrier of a peer CTA ("this warp has finished reading the
+// stage"): the reads it orders are complete when the arrive issues (their
+// values fed instructions issued before it), so CTA-scope release suffices
+// and no cluster-scope fence is emitted
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// every thread of every CTA of the cluster
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 template <int N>
 __device__ __forceinline__ void regs_dec() {
   asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));

@@ -741,7 +741,7 @@ def compress_type_b(op, tess, k, p=10, method="bn", stream=None, distribution="g
                 cop, tess, k, p,
                 lambda: plan_tagging(tess, 0, distribution, stream.child(1), optimize=optimize,
                                      max_redraws=max_tag_redraws, device="auto", extra_check=lambda T: b2_denominators_ok(T, tess), first=first),
-                stream.child(0), group_cols=tess.max_block_size + p, first=first)
+                stream.child(0), group_cols=tess.max_block_size + p, first=first, compensated=True)
             plan = bundle.plan
     with _PhaseTimer(times, "III"), cop.ledger.phase("III"):
         if method == "bn":

@@ -15,20 +15,23 @@ def timeit(fn, reps=2):
         a.record(); fn(); b.record(); torch.cuda.synchronize(); ts.append(a.elapsed_time(b))
     return min(ts) / 1e3
 
-# correctness (small)
-pts = P.grid_points(48, 2)
-n = pts.n
-op = P.KernelOperator(pts, "log", 3.0)
-perm = torch.arange(n, dtype=torch.int32, device="cuda")
-X = torch.randn(n, 700, dtype=torch.float64, device="cuda")
-Y = op.apply_device(X, perm)
-c = torch.from_numpy(pts.coords).cuda()
-d2 = ((c[:, None, :] - c[None, :, :]) ** 2).sum(-1)
-A = -0.5 * torch.log(d2.fill_diagonal_(1.0))
-A.fill_diagonal_(3.0)
-ref = A @ X
-print("variant", os.environ.get("UBLR_APPLY_CFG", "0"), "max rel diff", float((Y - ref).abs().max() / ref.abs().max()))
-for kind, per, w in (("log", 256, 4708), ("log", 256, 7590), ("inv", 256, 1024)):
+# correctness (small): widths that take the 4-CTA cluster, 2-CTA cluster,
+# single-CTA 256- and 128-column paths; n not a multiple of the 64-row tile
+for per, w, kind in ((48, 700, "log"), (50, 1300, "log"), (50, 1300 + 512 + 100, "inv"), (37, 96, "log")):
+    pts = P.grid_points(per, 2)
+    n = pts.n
+    op = P.KernelOperator(pts, kind, 3.0)
+    perm = torch.arange(n, dtype=torch.int32, device="cuda")
+    X = torch.randn(n, w, dtype=torch.float64, device="cuda")
+    Y = op.apply_device(X, perm)
+    c = torch.from_numpy(pts.coords).cuda()
+    d2 = ((c[:, None, :] - c[None, :, :]) ** 2).sum(-1)
+    A = -0.5 * torch.log(d2.fill_diagonal_(1.0)) if kind == "log" else torch.rsqrt(d2.fill_diagonal_(1.0))
+    A.fill_diagonal_(3.0)
+    ref = A @ X
+    print("variant", os.environ.get("UBLR_APPLY_CFG", "0"), "cs", os.environ.get("UBLR_APPLY_CS", "-"), f"n={n} w={w} {kind}",
+          "max rel diff", float((Y - ref).abs().max() / ref.abs().max()))
+for kind, per, w in (("log", 256, 4096), ("log", 256, 4708), ("log", 256, 7590), ("inv", 256, 1024)):
     pts = P.grid_points(per, 2)
     n = pts.n
     op = P.KernelOperator(pts, kind, 1.0)
