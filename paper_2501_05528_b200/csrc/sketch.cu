@@ -1587,21 +1587,20 @@ extern "C" int ublr_apply(const ublr_op_t* op, const double* X, int64_t ld_x, in
     rc = launch_apply3<Ap3Square>(op, X, ld_x, w, out, ld_o, vec2, st);
     if (rc) return rc;
   } else if (w > 64 && op->kind != UBLR_OP_DENSE && variant == 0) {
-    // column ranges: clusters of 4 then 2 CTAs sharing the generated A strip
-    // over whole 256-column tiles, the remainder on single CTAs (a 128-column
-    // tile for a last slice of <= 128 columns). All offsets are multiples of
-    // 256 columns, so the 16-byte alignment of X / out carries over.
+    // column ranges: clusters of 2 CTAs sharing the generated A strip over
+    // whole pairs of 256-column tiles, the remainder on single CTAs (a
+    // 128-column tile for a last slice of <= 128 columns). All offsets are
+    // multiples of 256 columns, so the 16-byte alignment of X / out carries
+    // over. Measured on B200 (N = 65,536, w = 4096): single CTAs 79.4 %,
+    // 2-CTA clusters 80.1 %; clusters of 4 51 % (a 4-CTA cluster strands 16 of
+    // the 148 SMs) and are not built. UBLR_APPLY_CS=1 turns clusters off.
+    // Also measured and dropped: fetching the next stage's first fragments
+    // during a stage's last k4 slice (test_wait one slice early): 78.5 %.
     static const int cs_max = [] {
       const char* e = getenv("UBLR_APPLY_CS");
       return e ? atoi(e) : 2;
     }();
     int c0 = 0;
-    if (cs_max >= 4 && (w - c0) >= 4 * Ap3Wide::BN) {
-      const int wm = (w - c0) / (4 * Ap3Wide::BN) * (4 * Ap3Wide::BN);
-      rc = launch_apply4<Ap3Wide, 4>(op, X + c0, ld_x, wm, out + c0, ld_o, vec2, st);
-      if (rc) return rc;
-      c0 += wm;
-    }
     if (cs_max >= 2 && (w - c0) >= 2 * Ap3Wide::BN) {
       const int wm = (w - c0) / (2 * Ap3Wide::BN) * (2 * Ap3Wide::BN);
       rc = launch_apply4<Ap3Wide, 2>(op, X + c0, ld_x, wm, out + c0, ld_o, vec2, st);
