@@ -1344,6 +1344,11 @@ __global__ void __launch_bounds__(C::NT, 1) k_sketch_tagged4(ublr_op_t op, const
     const int am0 = wr * C::WM + g, bn0 = wc * C::WN + g;
     const int twarp = warp;                       // lane quarter = warp & 3
     const int colbase = (warp >> 2) * WCOLS;
+    // 8-column groups of this warp's slice that hold columns of [G | H]: the
+    // last column tile is mostly padding (c4: 20 of 128 columns), and its
+    // DMMAs on zero-filled panel columns would cost what real ones do
+    const int ncol_w = ncols - (col0 + wc * C::WN);
+    const int nj_valid = ncol_w <= 0 ? 0 : (ncol_w >= C::WN ? NJ : (ncol_w + 7) / 8);
     double w[MI][NJ][2];
     double racc[RG > 0 ? RG : 1][MI][NJ][2];
 #pragma unroll
@@ -1379,19 +1384,36 @@ __global__ void __launch_bounds__(C::NT, 1) k_sketch_tagged4(ublr_op_t op, const
         static_assert(MI == 2, "the m16n8k8 fragments cover the warp's two 8-row blocks");
         // m16n8k8 DMMA: a0..a3 = A[g][t], A[g+8][t], A[g][t+4], A[g+8][t+4];
         // b0, b1 = B[t][g], B[t+4][g]; d = (w[0][jj], w[1][jj]) -- the m8n8k4 layout
+        if (nj_valid == NJ) {
 #pragma unroll
-        for (int k8 = 0; k8 < BK / 8; ++k8) {
-          const int kr = k8 * 8 + t;
-          const double a0 = As[kr * SA + am0], a1 = As[kr * SA + am0 + 8];
-          const double a2 = As[(kr + 4) * SA + am0], a3 = As[(kr + 4) * SA + am0 + 8];
+          for (int k8 = 0; k8 < BK / 8; ++k8) {
+            const int kr = k8 * 8 + t;
+            const double a0 = As[kr * SA + am0], a1 = As[kr * SA + am0 + 8];
+            const double a2 = As[(kr + 4) * SA + am0], a3 = As[(kr + 4) * SA + am0 + 8];
 #pragma unroll
-          for (int jj = 0; jj < NJ; ++jj) {
-            const double b0 = Bs[kr * SB + bn0 + jj * 8], b1 = Bs[(kr + 4) * SB + bn0 + jj * 8];
-            mma16x8x8(w[0][jj][0], w[0][jj][1], w[1][jj][0], w[1][jj][1], a0, a1, a2, a3, b0, b1);
+            for (int jj = 0; jj < NJ; ++jj) {
+              const double b0 = Bs[kr * SB + bn0 + jj * 8], b1 = Bs[(kr + 4) * SB + bn0 + jj * 8];
+              mma16x8x8(w[0][jj][0], w[0][jj][1], w[1][jj][0], w[1][jj][1], a0, a1, a2, a3, b0, b1);
+            }
+          }
+        } else if (nj_valid > 0) {   // last column tile: only the 8-column groups that hold columns
+#pragma unroll
+          for (int k8 = 0; k8 < BK / 8; ++k8) {
+            const int kr = k8 * 8 + t;
+            const double a0 = As[kr * SA + am0], a1 = As[kr * SA + am0 + 8];
+            const double a2 = As[(kr + 4) * SA + am0], a3 = As[(kr + 4) * SA + am0 + 8];
+#pragma unroll
+            for (int jj = 0; jj < NJ; ++jj) {
+              if (jj < nj_valid) {
+                const double b0 = Bs[kr * SB + bn0 + jj * 8], b1 = Bs[(kr + 4) * SB + bn0 + jj * 8];
+                mma16x8x8(w[0][jj][0], w[0][jj][1], w[1][jj][0], w[1][jj][1], a0, a1, a2, a3, b0, b1);
+              }
+            }
           }
         }
         ws::mbar_arrive(&empty[s]);
       }
+      if (nj_valid == 0) continue;   // a warp past the last column has nothing to fold
       // block j complete: acc_c += T[j, c] W
       const double* Tj = T + (int64_t)j * ell;
       double wf[WDP];
