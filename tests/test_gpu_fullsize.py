@@ -18,11 +18,18 @@ Gates (BASELINE.json north star):
   reference's own approximation error (7.5e-9). Two implementations that
   round differently are two such perturbations, so the c4 parity gate is
   2 x the reference's own sensitivity — a fixed number from the reference,
-  not from this implementation. For the same reason a single
-  B2 approximation error is one draw from a rounding-noise distribution (two
-  runs of the unmodified reference that differ only in the BLAS threading
-  of the operator adapter give 7.49e-9 and 7.11e-9); the 1.05x gate compares
-  the root-mean-square exact error over the same family of five 1-ulp
+  not from this implementation. What the reference's B2
+  error consists of: 95 % of its ||A - A_hat||_F^2 sits in three block rows
+  of the core (fixture `err_pair`), the rows of near pairs whose projected
+  tag (the type-B denominator) is ~1e-4 -- the sketch's rounding noise
+  divided by that denominator and pushed through the core least squares. It
+  is a rounding-noise level, not a truncation error, so a single run is one
+  draw (two runs of the unmodified reference that differ only in the BLAS
+  threading of the operator adapter give 7.49e-9 and 7.11e-9). The GPU path
+  removes the largest noise term (compensated fold of the tagged sketch,
+  compensated pair combination) and must meet BOTH forms of the 1.05x gate:
+  the unperturbed run against the reference's unperturbed run, and the
+  root-mean-square exact error over the same family of five 1-ulp
   coordinate perturbations on both sides (fixture `err_family`).
 The c5 spot checks are in test_gpu_c5_parity.py."""
 
@@ -74,9 +81,8 @@ def test_fullsize_against_reference(name, mid):
     assert fr.ref_fro == pytest.approx(A_fro, rel=1e-12)
     err_gpu, err_ref = fr.fro / A_fro, float(g["err_fro"]) / A_fro
     print(f"{name}: ||A - A_hat||_F / ||A||_F gpu {err_gpu:.4e} ref {err_ref:.4e} ({err_gpu / err_ref:.3f}x)")
-    if mid != "B2":
-        assert err_gpu <= 1.05 * err_ref
-    else:
+    assert err_gpu <= 1.05 * err_ref
+    if mid == "B2":
         # rms of the exact error over the same family of 1-ulp coordinate
         # perturbations on both sides (each against the unperturbed A)
         assert "err_family" in g, "c4 fixture lacks the reference's perturbation family"
