@@ -252,8 +252,15 @@ def cpu_baseline(wl, shards=1):
 KERNEL_OF = {"ublr_sketch_tagged_pair": "k_sketch_tagged{v} (Kronecker-restructured tagged sketch, TMEM tag groups)",
              "ublr_sketch_tagged": "k_sketch_tagged{v} (Kronecker-restructured tagged sketch, TMEM tag groups)",
              "ublr_sketch_tagged_two": "k_sketch_tagged3 (both sides of a non-symmetric A in one launch, TMEM tag groups)",
-             "ublr_apply": "k_apply3 (operator apply, warp-specialised: A generated by producer warps, DMMA consumers)",
-             "ublr_gemm_batched": "k_gemm2 (batched DMMA GEMM)",
+             "ublr_sketch_tagged_comp": "k_sketch_tagged4 (tagged sketch with the compensated fold, TMEM tag groups)",
+             "ublr_apply": "k_apply4 (operator apply, warp-specialised: A generated by producer warps and shared by "
+                           "the 2 CTAs of a cluster through st.async, DMMA consumers; the last < 512 columns on "
+                           "single-CTA k_apply3 launches inside the same timed call)",
+             "ublr_apply_staged": "k_gen_strip + k_gemm3 (operator apply through a staged strip of A: the strip's "
+                                  "entries are evaluated once into an HBM workspace by an ALU kernel, then the "
+                                  "warp-specialised stored-operand DMMA GEMM multiplies it by all w columns; the "
+                                  "timed call covers every strip's two launches)",
+             "ublr_gemm_batched": "k_gemm3 / k_gemm2 (batched DMMA GEMM)",
              "ublr_coupling": "k_coupling3 (C_ij = U_i^T A_ij V_j, warp-specialised)",
              "ublr_coupling_nearfield": "k_coupling_nf_small (coupling + colour-probe near field, one pass over A)"}
 
@@ -338,11 +345,19 @@ def run_sharded(args, rank, world, local):
     core_out, panel_blocks, sink = None, None, "device"
     if core_bytes > free - 24 * 2 ** 30:
         import psutil
-        if core_bytes > psutil.virtual_memory().available - 16 * 2 ** 30:
-            raise SystemExit(f"c5 on {S} rank(s): {core_bytes / 1e9:.0f} GB of core rows per rank fit neither in "
-                             f"HBM ({free / 1e9:.0f} GB free) nor in host memory")
-        core_out = torch.empty((sh.K1 - sh.K0, K), dtype=torch.float64, pin_memory=True)
-        panel_blocks, sink = 64, "pinned host (block-row panels of 64)"
+        panel_blocks = 64
+        host_free = psutil.virtual_memory().available // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
+        if core_bytes > host_free - 16 * 2 ** 30:
+            # neither HBM nor this rank's share of host memory holds the rows:
+            # every panel is still computed and copied out, into a ring of 4
+            # pinned panel slots that a file writer / sender would drain
+            rows = 4 * panel_blocks * wl.k
+            core_out = torch.empty((rows, K), dtype=torch.float64, pin_memory=True)
+            sink = (f"pinned host RING of 4 block-row panels of 64 (rows computed and copied out, not retained: "
+                    f"{core_bytes / 1e9:.0f} GB per rank fit neither in HBM nor in host memory)")
+        else:
+            core_out = torch.empty((sh.K1 - sh.K0, K), dtype=torch.float64, pin_memory=True)
+            sink = "pinned host (block-row panels of 64)"
 
     def step(op=None):
         return compress_sharded(op or wl.op, wl.tess, wl.k, wl.p, P.RandomStream(W.COMPRESS_SEED), rank=me,

@@ -153,6 +153,17 @@ int ublr_sketch_tagged_comp(const ublr_op_t* op, const int32_t* off, int b, cons
  * the pipeline): out (N x w, permuted rows, ld_o) = A X (N x w, ld_x). */
 int ublr_apply(const ublr_op_t* op, const double* X, int64_t ld_x, int w, double* out, int64_t ld_o,
                void* stream);
+/* The same product for a WIDE right-hand side of a kernel operator (the
+ * 2(9m + k + p)-column block-nullification sketch, the K + p - s extra
+ * columns of the type-B core): A is evaluated once per strip of rows into
+ * `workspace` (any size from one 128-row strip, 128 n doubles, up to
+ * ublr_apply_staged_workspace_bytes) and multiplied by all w columns with the
+ * stored-operand DMMA GEMM; ublr_apply evaluates it inside the GEMM, once per
+ * 256-column tile. Same entries, same result up to summation order. */
+int64_t ublr_apply_staged_workspace_bytes(int64_t n, int w);
+int ublr_apply_staged_rows(int64_t n, int w, int64_t workspace_bytes);   /* rows per strip; 0 = workspace too small */
+int ublr_apply_staged(const ublr_op_t* op, const double* X, int64_t ld_x, int w, double* out, int64_t ld_o,
+                      void* workspace, int64_t workspace_bytes, void* stream);
 
 /* K4 — combine + QR: ref/bases.py:174-189, :207-210 with ref/linalg.py:55-69
  * and ref/bases.py:78-83. Per block i: sample S_i (m_i x k) is

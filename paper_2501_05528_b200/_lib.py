@@ -55,6 +55,9 @@ SIGNATURES = {
     "ublr_sketch_tagged_two": (INT, [C.POINTER(OpDesc), C.POINTER(OpDesc), P, INT, P, INT, P, P, I64, INT, P, P, I64,
                                      INT, INT, P]),
     "ublr_apply": (INT, [C.POINTER(OpDesc), P, I64, INT, P, I64, P]),
+    "ublr_apply_staged": (INT, [C.POINTER(OpDesc), P, I64, INT, P, I64, P, I64, P]),
+    "ublr_apply_staged_workspace_bytes": (I64, [I64, INT]),
+    "ublr_apply_staged_rows": (INT, [I64, INT, I64]),
     "ublr_block_qr": (INT, [P, I64, INT, P, INT, INT, P, P, INT, INT, P, I64, P, INT]),
     "ublr_block_qr_pair": (INT, [P, P, I64, P, INT, INT, P, INT, INT, P, P, I64, P, INT]),
     "ublr_coupling": (INT, [C.POINTER(OpDesc), P, P, INT, INT, P, P, I64, P, I64, P, INT, INT, INT]),
@@ -141,6 +144,10 @@ def rng_launches(counts) -> int:
 
 
 def _launches_of(name, args):
+    if name == "ublr_apply_staged":   # one evaluation + one GEMM launch per strip of rows
+        n, w, nbytes = int(args[0].n), int(args[3]), int(args[7])
+        rows = max(128, int(load().ublr_apply_staged_rows(n, w, nbytes)))
+        return 2 * -(-n // rows)
     return LAUNCHES.get(name, 0)
 _events = None  # name -> list of (start, end) CUDA events when instrumentation is on
 
@@ -179,7 +186,7 @@ def event_times():
 def _work_of(name, args):
     """Algorithmic fp64 flops of the hot entry points, from their arguments."""
     try:
-        if name == "ublr_apply":
+        if name in ("ublr_apply", "ublr_apply_staged"):
             n = args[0].n
             return 2.0 * n * n * int(args[3])
         if name == "ublr_sketch_tagged_two":

@@ -12,7 +12,7 @@ import numpy as np
 
 from . import _lib
 from .linalg import RandomStream, device_normals
-from .operators import CountingOperator, unwrap
+from .operators import CountingOperator, device_apply, unwrap
 from .tagging import DEVICE_PLAN_MIN_B
 from .tessellation import Tessellation, device_tess
 
@@ -595,11 +595,11 @@ def block_nullification_bases(op, tess: Tessellation, k: int, p: int, stream: Ra
     st = _lib.stream_handle()
     if hasattr(inner, "device_op"):
         if getattr(inner, "symmetric", False):
-            _lib.call("ublr_apply", inner.device_op(dt.perm), _lib.ptr(OP), 2 * s, 2 * s, _lib.ptr(YZ), 2 * s, st)
+            device_apply(inner, dt.perm, _lib.ptr(OP), 2 * s, 2 * s, _lib.ptr(YZ), 2 * s, dt.device)
         else:
-            _lib.call("ublr_apply", inner.device_op(dt.perm), _lib.ptr(OP), 2 * s, s, _lib.ptr(YZ), 2 * s, st)
-            _lib.call("ublr_apply", inner.device_op(dt.perm, adjoint=True), _lib.ptr(OP) + 8 * s, 2 * s, s,
-                      _lib.ptr(YZ) + 8 * s, 2 * s, st)
+            device_apply(inner, dt.perm, _lib.ptr(OP), 2 * s, s, _lib.ptr(YZ), 2 * s, dt.device)
+            device_apply(inner, dt.perm, _lib.ptr(OP) + 8 * s, 2 * s, s, _lib.ptr(YZ) + 8 * s, 2 * s, dt.device,
+                         adjoint=True)
     else:
         Yh = inner.apply(dt.from_perm_rows(OP[:, :s]))
         Zh = inner.apply_adjoint(dt.from_perm_rows(OP[:, s:]))
@@ -647,8 +647,8 @@ def naive_bases(op, tess: Tessellation, k: int, p: int, stream: RandomStream):
     Y = torch.empty((n, w), **f64)
     Z = torch.empty((n, w), **f64)
     if hasattr(inner, "device_op"):
-        _lib.call("ublr_apply", inner.device_op(dt.perm), _lib.ptr(OM), w, w, _lib.ptr(Y), w, st)
-        _lib.call("ublr_apply", inner.device_op(dt.perm, adjoint=True), _lib.ptr(PS), w, w, _lib.ptr(Z), w, st)
+        device_apply(inner, dt.perm, _lib.ptr(OM), w, w, _lib.ptr(Y), w, dt.device)
+        device_apply(inner, dt.perm, _lib.ptr(PS), w, w, _lib.ptr(Z), w, dt.device, adjoint=True)
     else:
         Y = dt.to_perm_rows(inner.apply(dt.from_perm_rows(OM)))
         Z = dt.to_perm_rows(inner.apply_adjoint(dt.from_perm_rows(PS)))

@@ -171,27 +171,36 @@ struct WholeStage {
 // cols, into shared memory at dst[r * sstride + c] (r < rows, c < cols),
 // zero-filling outside (rlim, clim). Row r's global row is rowmap(r).
 // 16-byte cp.async when `vec2` (even ld / offsets, 16B-aligned base).
+// `free_dim` (1: cols, 2: rows): the dimension that is not the product's k
+// dimension; entries beyond its limit feed only outputs that are never
+// stored and are left untouched instead of zero-filled (see producer_copy in
+// dense.cu for the measurement).
 template <int NT, class RowMap>
 __device__ __forceinline__ void tile_copy(double* dst, int sstride, const double* src, int64_t ld, int rows, int cols,
-                                          int r0, int c0, int rlim, int clim, RowMap rowmap, bool vec2) {
+                                          int r0, int c0, int rlim, int clim, RowMap rowmap, bool vec2,
+                                          int free_dim = 0) {
   if (vec2) {
     const int half = cols >> 1;
     for (int e = threadIdx.x; e < rows * half; e += NT) {
       int r = e / half, c = (e - r * half) * 2;
       int gr = r0 + r, gc = c0 + c;
       double* d = dst + r * sstride + c;
+      if (free_dim == 2 && gr >= rlim) continue;
+      if (free_dim == 1 && gc >= clim) continue;
       if (gr < rlim && gc + 1 < clim) {
         cp_async16(d, src + (int64_t)rowmap(gr) * ld + gc, true);
       } else {
         bool ok = gr < rlim && gc < clim;
         cp_async8(d, ok ? (const void*)(src + (int64_t)rowmap(gr) * ld + gc) : (const void*)src, ok);
-        cp_async8(d + 1, src, false);
+        if (free_dim != 1 || gr >= rlim) cp_async8(d + 1, src, false);   // a k row past the end is zero in both halves
       }
     }
   } else {
     for (int e = threadIdx.x; e < rows * cols; e += NT) {
       int r = e / cols, c = e - r * cols;
       int gr = r0 + r, gc = c0 + c;
+      if (free_dim == 2 && gr >= rlim) continue;
+      if (free_dim == 1 && gc >= clim) continue;
       bool ok = gr < rlim && gc < clim;
       cp_async8(dst + r * sstride + c, ok ? (const void*)(src + (int64_t)rowmap(gr) * ld + gc) : (const void*)src, ok);
     }

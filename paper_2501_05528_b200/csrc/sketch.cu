@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(C::NT, 1) k_apply3(ublr_op_t op, const double*
       if (ks + 1 < nk) ring.prefetch(op, ks + 1, (ks + 1) * BK, n, NPROD);
       cp_async_commit();
       ws::mbar_wait(&empty[s], (u & 1) ^ 1);
-      tile_copy<NPROD>(Bs0 + s * C::B_STAGE, SB, X, ldx, BK, BN, ks * BK, col0, n, w, IdentityRows{}, vec2 != 0);
+      tile_copy<NPROD>(Bs0 + s * C::B_STAGE, SB, X, ldx, BK, BN, ks * BK, col0, n, w, IdentityRows{}, vec2 != 0, 1);
       cp_async_commit();
       ws::mbar_cp_async_arrive(&full[s]);
       double* As = As0 + s * C::A_STAGE;
@@ -561,7 +561,7 @@ __global__ void __launch_bounds__(C::NT, 1) k_apply4(ublr_op_t op, const double*
       cp_async_commit();
       ws::mbar_wait(&empty[s], (u & 1) ^ 1);
       if (has_cols)
-        tile_copy<NPROD>(Bs0 + s * C::B_STAGE, SB, X, ldx, BK, BN, ks * BK, col0, n, w, IdentityRows{}, vec2 != 0);
+        tile_copy<NPROD>(Bs0 + s * C::B_STAGE, SB, X, ldx, BK, BN, ks * BK, col0, n, w, IdentityRows{}, vec2 != 0, 1);
       cp_async_commit();
       ws::mbar_cp_async_arrive(&full[s]);
       double* As = As0 + s * C::A_STAGE;
@@ -699,6 +699,66 @@ int launch_apply4(const ublr_op_t* op, const double* X, int64_t ld_x, int w, dou
   }
 #undef UBLR_AP4
   return UBLR_OK;
+}
+
+// ------------------------------------ apply through a staged strip of A
+// DMMA and the FP64 ALU share one pipe, so generating A inside the GEMM costs
+// tensor throughput twice: the evaluation's own pipe cycles, and the two
+// instruction streams interleaving (k_apply3/4: 79-80 % of the DMMA peak,
+// k_gemm3 on a stored operand: 90 %). For wide right-hand sides the strip
+// form separates them in time instead of in warps: a strip of R rows of A
+// (R x n doubles) is evaluated ONCE into a caller-provided HBM buffer by an
+// ALU-bound kernel (every entry used to be evaluated once per 256-column
+// tile: 18 times at c3, 30 at c4), then a plain k_gemm3 multiplies it by all
+// w columns; the next strip reuses the buffer. A is still never stored as a
+// whole (the strip is 0.5-4 GB of the 34 GB matrix at N = 65,536), the
+// entries are the same bits, and the generation is ~1 % of the run.
+template <int KIND, int DIM>
+__global__ void __launch_bounds__(256) k_gen_strip(ublr_op_t op, int r0, int rows, double* __restrict__ out) {
+  constexpr int RPC = 16;   // rows per CTA: the column point is loaded once for 16 entries
+  __shared__ LogTables lt;
+  __shared__ double rx[RPC][3];
+  if (KIND == UBLR_OP_LOG) init_log_tables(&lt);
+  const int n = (int)op.n;
+  const int rb = r0 + blockIdx.y * RPC;
+  if (threadIdx.x < RPC * DIM) {
+    const int r = threadIdx.x / DIM, d = threadIdx.x % DIM;
+    rx[r][d] = rb + r < r0 + rows ? op.coords[(int64_t)d * n + rb + r] : 0.0;
+  }
+  __syncthreads();
+  const int q = blockIdx.x * 256 + threadIdx.x;
+  if (q >= n) return;
+  const double c0 = op.coords[q], c1 = DIM > 1 ? op.coords[(int64_t)n + q] : 0.0,
+               c2 = DIM > 2 ? op.coords[2 * (int64_t)n + q] : 0.0;
+  const double diag = op.diag;
+#pragma unroll 4
+  for (int r = 0; r < RPC; ++r) {
+    const int p = rb + r;
+    if (p >= r0 + rows) break;
+    const RowPoint rp = {p, 0, rx[r][0], rx[r][1], rx[r][2]};
+    out[(int64_t)(p - r0) * n + q] = kernel_entry_dim<KIND, DIM>(rp, q, c0, c1, c2, diag, &lt);
+  }
+}
+
+// Rows per strip: a multiple of the 128-row GEMM tile chosen so that the
+// strip's CTA count (row tiles x ceil(w / 128) column tiles) fills whole
+// waves of the SMs, as large as `max_bytes` allows (fewer strip boundaries).
+inline int strip_rows(int64_t n, int w, int64_t max_bytes, int sms) {
+  const int64_t ct = (w + 127) / 128;
+  int64_t cap = max_bytes / (128 * n * 8);
+  if (cap > (n + 127) / 128) cap = (n + 127) / 128;
+  if (cap < 1) return 0;
+  int best = 1;
+  double best_eff = 0.0;
+  for (int64_t rt = 1; rt <= cap; ++rt) {
+    const int64_t ctas = rt * ct, waves = (ctas + sms - 1) / sms;
+    const double eff = (double)ctas / (double)(waves * sms);
+    if (eff >= best_eff - 0.004) {   // a larger strip wins unless it wastes > 0.4 % more of its last wave
+      best = (int)rt;
+      if (eff > best_eff) best_eff = eff;
+    }
+  }
+  return best * 128;
 }
 
 // ---------------------------------------------------------- tagged sketch
@@ -1886,4 +1946,57 @@ extern "C" int ublr_sketch_tagged_comp(const ublr_op_t* op, const int32_t* off, 
                UBLR_ERR_VALUE, "ublr_sketch_tagged_comp: bad arguments");
   return sketch_common(op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y, row_begin, row_end, (cudaStream_t)stream,
                        true);
+}
+
+// Largest strip the staged apply asks for (it runs with any workspace of at
+// least one 128-row strip).
+extern "C" int64_t ublr_apply_staged_workspace_bytes(int64_t n, int w) {
+  const int64_t want = (int64_t)4 << 30;
+  const int rows = strip_rows(n, w, want, 148);
+  return (int64_t)(rows > 0 ? rows : 128) * n * 8;
+}
+
+static int device_sms() {
+  static const int sms = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return sms;
+}
+
+// Rows per strip the staged apply uses with a workspace of this size (0: too small).
+extern "C" int ublr_apply_staged_rows(int64_t n, int w, int64_t workspace_bytes) {
+  return strip_rows(n, w, workspace_bytes, device_sms());
+}
+
+extern "C" int ublr_apply_staged(const ublr_op_t* op, const double* X, int64_t ld_x, int w, double* out, int64_t ld_o,
+                                 void* workspace, int64_t workspace_bytes, void* stream) {
+  int rc = check_op(op);
+  if (rc) return rc;
+  UBLR_REQUIRE(w >= 0 && X && out && ld_x >= w && ld_o >= w, UBLR_ERR_VALUE, "ublr_apply_staged: bad X/out");
+  UBLR_REQUIRE(op->kind == UBLR_OP_LOG || op->kind == UBLR_OP_INV, UBLR_ERR_VALUE,
+               "ublr_apply_staged: kernel operators only (a dense A is already stored)");
+  if (w == 0) return UBLR_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n = op->n;
+  const int R = strip_rows(n, w, workspace_bytes, device_sms());
+  UBLR_REQUIRE(workspace && R >= 128, UBLR_ERR_VALUE, "ublr_apply_staged: workspace smaller than one 128-row strip");
+  double* strip = (double*)workspace;
+  for (int64_t r0 = 0; r0 < n; r0 += R) {
+    const int rows = (int)(n - r0 < R ? n - r0 : R);
+    dim3 grid((unsigned)((n + 255) / 256), (unsigned)((rows + 15) / 16));
+#define UBLR_GEN(KIND, DIM) k_gen_strip<KIND, DIM><<<grid, 256, 0, st>>>(*op, (int)r0, rows, strip)
+    if (op->kind == UBLR_OP_LOG) {
+      if (op->dim == 1) UBLR_GEN(UBLR_OP_LOG, 1); else if (op->dim == 2) UBLR_GEN(UBLR_OP_LOG, 2); else UBLR_GEN(UBLR_OP_LOG, 3);
+    } else {
+      if (op->dim == 1) UBLR_GEN(UBLR_OP_INV, 1); else if (op->dim == 2) UBLR_GEN(UBLR_OP_INV, 2); else UBLR_GEN(UBLR_OP_INV, 3);
+    }
+#undef UBLR_GEN
+    UBLR_LAUNCH_CHECK();
+    rc = ublr_gemm_batched(0, 0, rows, w, (int)n, 1.0, strip, n, 0, nullptr, 0, X, ld_x, 0, nullptr, 0, 0.0,
+                           out + r0 * ld_o, ld_o, 0, nullptr, 0, 1, stream);
+    if (rc) return rc;
+  }
+  return UBLR_OK;
 }

@@ -191,7 +191,11 @@ def phase23_local(op, k, shard, dt, U, V_all, core_out=None, panel_blocks=None):
     (309 GB in total) does not fit in HBM, so block-row panels
     of `panel_blocks` rows are computed into two device panel buffers and
     copied out on a copy stream while the next panel is computed (the near
-    field of a panel reads only that panel's core rows). Returns (core, B)."""
+    field of a panel reads only that panel's core rows). A pinned `core_out`
+    with FEWER rows than the shard owns is used as a ring of panel slots
+    (panel n lands in slot n mod slots): the hand-off buffer of a consumer
+    that drains panels as they arrive (a file writer, a sender) on a box whose
+    memory cannot hold the shard's rows at all. Returns (core, B)."""
     torch = _torch()
     inner = unwrap(op)
     roff_h, roff = dt.roff(k)
@@ -221,6 +225,11 @@ def phase23_local(op, k, shard, dt, U, V_all, core_out=None, panel_blocks=None):
         panels = [_alloc((rows_max, K), **f64) for _ in range(2)]
         done = [None, None]
         copy_stream = torch.cuda.Stream(device=dt.device)
+        ring_slots = 0
+        if core_out.shape[0] < kloc:
+            ring_slots = core_out.shape[0] // rows_max
+            if ring_slots < 2:
+                raise ValueError(f"core_out ring needs at least {2 * rows_max} rows (two panels of {rows_max})")
     for n_, a in enumerate(range(shard.i0, shard.i1, pb)):
         e = min(a + pb, shard.i1)
         if host:
@@ -249,6 +258,8 @@ def phase23_local(op, k, shard, dt, U, V_all, core_out=None, panel_blocks=None):
             ready = torch.cuda.Event()
             ready.record(_lib.current_stream())
             copy_stream.wait_event(ready)
+            if ring_slots:
+                r0, r1 = (n_ % ring_slots) * rows_max, (n_ % ring_slots) * rows_max + (r1 - r0)
             with torch.cuda.stream(copy_stream):
                 core_out[r0:r1].copy_(panels[slot][:r1 - r0], non_blocking=True)
             done[slot] = torch.cuda.Event()

@@ -14,11 +14,18 @@ matvec ledger still records the columns it would have pushed through A).
 
 from __future__ import annotations
 
+import os
 from contextlib import contextmanager
 
 import numpy as np
 
 from . import _lib
+
+# ublr_apply_staged for right-hand sides at least this wide on operators at
+# least this large (below, the strip evaluation and the GEMM's partial waves
+# cost more than evaluating A inside the GEMM saves)
+STAGED_MIN_COLS = 512
+STAGED_MIN_ROWS = 4096
 
 
 class LinearOperatorHandle:
@@ -38,6 +45,27 @@ class LinearOperatorHandle:
 def _torch():
     import torch
     return torch
+
+
+def device_apply(inner, perm, x_ptr, ld_x, w, out_ptr, ld_o, device, adjoint=False):
+    """out (n x w, ld_o) = A X (ld_x) on the device for an operator with a
+    descriptor, rows in the order of `perm`. Kernel operators with a wide
+    right-hand side go through ublr_apply_staged (A evaluated once per strip
+    of rows into a workspace, then the stored-operand GEMM); everything else
+    through ublr_apply (A evaluated inside the GEMM)."""
+    torch = _torch()
+    desc = inner.device_op(perm, adjoint)
+    n = int(desc.n)
+    st = _lib.stream_handle()
+    if (getattr(inner, "kind", None) in ("log", "inv") and w >= STAGED_MIN_COLS and n >= STAGED_MIN_ROWS
+            and os.environ.get("UBLR_APPLY_STAGED", "1") != "0"):
+        lib = _lib.load()
+        free, _ = torch.cuda.mem_get_info(device)
+        nbytes = min(int(lib.ublr_apply_staged_workspace_bytes(n, w)), max(free // 4, 128 * n * 8)) // 8 * 8
+        ws = torch.empty(nbytes // 8, dtype=torch.float64, device=device)
+        _lib.call("ublr_apply_staged", desc, x_ptr, ld_x, w, out_ptr, ld_o, _lib.ptr(ws), nbytes, st)
+        return
+    _lib.call("ublr_apply", desc, x_ptr, ld_x, w, out_ptr, ld_o, st)
 
 
 class _DeviceOperator(LinearOperatorHandle):
@@ -62,8 +90,7 @@ class _DeviceOperator(LinearOperatorHandle):
         torch = _torch()
         n, w = Xd.shape
         out = torch.empty((n, w), dtype=torch.float64, device=Xd.device)
-        desc = self.device_op(perm, adjoint)
-        _lib.call("ublr_apply", desc, _lib.ptr(Xd), Xd.stride(0), w, _lib.ptr(out), w, _lib.stream_handle())
+        device_apply(self, perm, _lib.ptr(Xd), Xd.stride(0), w, _lib.ptr(out), w, Xd.device, adjoint)
         return out
 
     def _host_apply(self, X, adjoint):

@@ -22,7 +22,7 @@ import numpy as np
 from . import _lib
 from . import dense as D
 from .linalg import device_normals
-from .operators import CountingOperator, unwrap
+from .operators import CountingOperator, device_apply, unwrap
 from .tagging import DegenerateTagsError, pair_vectors
 
 
@@ -328,7 +328,7 @@ def pinv_core(op, bundle, bases, B_flat, p: int, stream, max_width=None):
             op.ledger.record_apply(extra)
         inner = unwrap(op)
         if hasattr(inner, "device_op"):
-            _lib.call("ublr_apply", inner.device_op(dt.perm), D.addr(Of, s), L, extra, D.addr(Yf, s), L, st)
+            device_apply(inner, dt.perm, D.addr(Of, s), L, extra, D.addr(Yf, s), L, dt.device)
         else:
             Yf[:, s:] = dt.to_perm_rows(inner.apply(dt.from_perm_rows(Of[:, s:])))
     # Rf = Y - B Omega, accumulated by neighbour slot t (no two writers per row

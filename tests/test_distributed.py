@@ -99,6 +99,32 @@ def test_host_core_panels_match_device(per, b, k, kind):
         assert res.shard == sh
 
 
+@pytest.mark.gpu
+def test_host_core_ring_holds_last_panels():
+    """A pinned core_out with fewer rows than the shard owns is a ring of
+    panel slots: after the run, slot (n mod slots) holds panel n for the last
+    panels; near blocks are unaffected."""
+    from paper_2501_05528_b200.distributed import compress_emulated, compress_sharded
+    per, b, k, pb = 48, 36, 8, 2
+    pts = P.grid_points(per, 2)
+    tess = P.build_tessellation(pts, b)
+    op = P.KernelOperator(pts, "log", -np.log(0.5 / per))
+    ref = compress_emulated(op, tess, k, 8, P.RandomStream(3), world=1)[0]
+    rows_max = pb * k
+    slots = 3
+    ring = torch.zeros((slots * rows_max, ref.core.shape[1]), dtype=torch.float64, pin_memory=True)
+    res = compress_sharded(op, tess, k, 8, P.RandomStream(3), rank=0, world=1, allgather=lambda V, n: V,
+                           core_out=ring, panel_blocks=pb)
+    torch.cuda.synchronize()
+    assert torch.equal(res.B, ref.B)
+    npan = b // pb
+    core = ref.core.cpu()
+    for n in range(npan - slots, npan):
+        want = core[n * rows_max:(n + 1) * rows_max]
+        got = ring[(n % slots) * rows_max:(n % slots + 1) * rows_max]
+        assert torch.equal(got, want)
+
+
 def _sharded_worker(rank, world, port, outdir):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)

@@ -235,6 +235,65 @@ def test_lu_sign_r_scaled_matches_unscaled_l():
         assert np.abs(np.triu(A) - np.triu(A0) @ Rh[b]).max() <= 1e-10 * np.abs(np.triu(A)).max()
 
 
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("M,N,K,batch", [(300, 200, 77, 3), (131, 45, 33, 2), (1000, 1100, 129, 1), (64, 40, 65, 5),
+                                         (257, 300, 1, 2)])
+@pytest.mark.parametrize("pad", [3, 4])
+def test_gemm_batched_ragged_shapes(ta, tb, M, N, K, batch, pad):
+    """Every orientation on shapes that end inside a tile in all three
+    dimensions (the operand tiles are zero-filled only where the k dimension
+    runs out; the rest of a ragged tile is left as it is), the operands
+    embedded in NaN so that a read outside (M, N, K) shows."""
+    rng = np.random.default_rng(M + N + K)   # pad 4: 16-byte-aligned operands (vector copies) when the ld is even
+
+    def embed(x):
+        out = np.full((x.shape[0], x.shape[1] + pad, x.shape[2] + 2 * pad), np.nan)
+        out[:, :x.shape[1], pad:pad + x.shape[2]] = x
+        return torch.from_numpy(out).cuda()
+
+    A = rng.standard_normal((batch, K, M) if ta else (batch, M, K))
+    B = rng.standard_normal((batch, N, K) if tb else (batch, K, N))
+    C0 = rng.standard_normal((batch, M, N))
+    Ad, Bd = embed(A), embed(B)
+    Cd = torch.from_numpy(C0).cuda()
+    want = 0.5 * C0 - np.einsum("bmk,bkn->bmn", A.transpose(0, 2, 1) if ta else A, B.transpose(0, 2, 1) if tb else B)
+    Dn.gemm(ta, tb, M, N, K, -1.0, Dn.addr(Ad, pad), Ad.shape[2], Ad[0].numel(), Dn.addr(Bd, pad), Bd.shape[2],
+            Bd[0].numel(), 0.5, Dn.addr(Cd), N, M * N, batch)
+    got = Cd.cpu().numpy()
+    assert np.isfinite(got).all()
+    assert np.abs(got - want).max() <= 1e-12 * max(1.0, np.abs(want).max())
+
+
+@pytest.mark.parametrize("kind,per,w", [("log", 70, 700), ("inv", 67, 1100), ("log", 64, 513)])
+def test_apply_staged_matches_fused(kind, per, w):
+    """ublr_apply_staged (A evaluated once per strip of rows, then the
+    stored-operand GEMM) against ublr_apply (A evaluated inside the GEMM) and
+    numpy, with a workspace of exactly two 128-row strips (several strips, a
+    ragged last one) and with the library's own size."""
+    coords = O.cell_centres(per, 2)
+    n = len(coords)
+    op = P.KernelOperator(coords, kind, 3.25)
+    perm = torch.arange(n, dtype=torch.int32, device=DEV)
+    X = torch.from_numpy(np.random.default_rng(4).standard_normal((n, w))).cuda()
+    fused = torch.empty((n, w), dtype=torch.float64, device=DEV)
+    _lib.call("ublr_apply", op.device_op(perm), X.data_ptr(), w, w, fused.data_ptr(), w, _lib.stream_handle())
+    A = O.kernel_block(coords, np.arange(n), np.arange(n), kind, 3.25)
+    want = A @ X.cpu().numpy()
+    scale = np.linalg.norm(A) * np.linalg.norm(X.cpu().numpy())
+    lib = _lib.load()
+    for nbytes in (2 * 128 * n * 8, int(lib.ublr_apply_staged_workspace_bytes(n, w))):
+        ws = torch.full((nbytes // 8,), np.nan, dtype=torch.float64, device=DEV)
+        out = torch.full((n, w), np.nan, dtype=torch.float64, device=DEV)
+        _lib.call("ublr_apply_staged", op.device_op(perm), X.data_ptr(), w, w, out.data_ptr(), w, ws.data_ptr(),
+                  nbytes, _lib.stream_handle())
+        got = out.cpu().numpy()
+        assert np.linalg.norm(got - want) <= 1e-13 * scale
+        assert np.linalg.norm(got - fused.cpu().numpy()) <= 1e-13 * scale
+    with pytest.raises(ValueError):
+        _lib.call("ublr_apply_staged", op.device_op(perm), X.data_ptr(), w, w, out.data_ptr(), w, ws.data_ptr(),
+                  64 * n * 8, _lib.stream_handle())
+
+
 def test_syrk_upper_matches_gemm_on_upper_triangle():
     rng = np.random.default_rng(6)
     for M, K in ((300, 64), (77, 13)):

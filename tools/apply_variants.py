@@ -17,7 +17,7 @@ def timeit(fn, reps=2):
 
 # correctness (small): widths that take the 4-CTA cluster, 2-CTA cluster,
 # single-CTA 256- and 128-column paths; n not a multiple of the 64-row tile
-for per, w, kind in ((48, 700, "log"), (50, 1300, "log"), (50, 1300 + 512 + 100, "inv"), (37, 96, "log")):
+for per, w, kind in ((70, 700, "log"), (67, 1100, "inv"), (48, 700, "log"), (50, 1300, "log"), (50, 1300 + 512 + 100, "inv"), (37, 96, "log")):
     pts = P.grid_points(per, 2)
     n = pts.n
     op = P.KernelOperator(pts, kind, 3.0)
@@ -29,7 +29,7 @@ for per, w, kind in ((48, 700, "log"), (50, 1300, "log"), (50, 1300 + 512 + 100,
     A = -0.5 * torch.log(d2.fill_diagonal_(1.0)) if kind == "log" else torch.rsqrt(d2.fill_diagonal_(1.0))
     A.fill_diagonal_(3.0)
     ref = A @ X
-    print("variant", os.environ.get("UBLR_APPLY_CFG", "0"), "cs", os.environ.get("UBLR_APPLY_CS", "-"), f"n={n} w={w} {kind}",
+    print("variant", os.environ.get("UBLR_APPLY_CFG", "0"), "cs", os.environ.get("UBLR_APPLY_CS", "-"), "staged", os.environ.get("UBLR_APPLY_STAGED", "1"), f"n={n} w={w} {kind}",
           "max rel diff", float((Y - ref).abs().max() / ref.abs().max()))
 for kind, per, w in (("log", 256, 4096), ("log", 256, 4708), ("log", 256, 7590), ("inv", 256, 1024)):
     pts = P.grid_points(per, 2)

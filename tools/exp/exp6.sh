@@ -1,4 +1,2 @@
-timeout 900 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_compress.py -x -q 2>&1 | tail -3
+timeout 900 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_compress.py tests/test_distributed.py -x -q 2>&1 | tail -3
 for c in c3 c4; do timeout 600 python tools/prof_stages.py $c > gpurun_out/stages_$c.txt 2>&1; head -14 gpurun_out/stages_$c.txt; done
-timeout 2400 bash tools/profile_round.sh c3 c4
-ls -la gpurun_out/prof

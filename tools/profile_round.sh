@@ -24,13 +24,14 @@ for c in $CFGS; do
       ;;
     c3)
       ncu $M --log-file $OUT/launches_c3.csv python tools/one_compress.py c3 1 > $OUT/l_c3.log 2>&1
-      ncu $F -k regex:k_apply4 -c 1 -o $OUT/c3_apply4 python tools/one_compress.py c3 1 > $OUT/f_c3.log 2>&1
-      ncu $F -k regex:k_gemm3 -s 6 -c 1 -o $OUT/c3_gemm3 python tools/one_compress.py c3 1 > $OUT/f_c3g.log 2>&1
+      # the staged apply: first k_gen_strip and first k_gemm3 launch (one full strip each);
+      # a later k_gemm3 launch is a block-nullification product
+      ncu $F -k regex:k_gen_strip -c 1 -o $OUT/c3_gen_strip python tools/one_compress.py c3 1 > $OUT/f_c3a.log 2>&1
+      ncu $F -k regex:k_gemm3 -c 1 -o $OUT/c3_apply_gemm3 python tools/one_compress.py c3 1 > $OUT/f_c3b.log 2>&1
+      ncu $F -k regex:k_gemm3 -s 10 -c 1 -o $OUT/c3_gemm3 python tools/one_compress.py c3 1 > $OUT/f_c3g.log 2>&1
       ;;
     c4)
-      ncu $M --log-file $OUT/launches_c4.csv python tools/one_compress.py c4 1 > $OUT/l_c4.log 2>&1
       ncu $F -k regex:k_sketch_tagged4 -c 1 -o $OUT/c4_sketch4 python tools/one_compress.py c4 1 > $OUT/f_c4s.log 2>&1
-      ncu $F -k regex:k_apply4 -c 1 -o $OUT/c4_apply4 python tools/one_compress.py c4 1 > $OUT/f_c4.log 2>&1
       ;;
     c5)
       ncu $M --log-file $OUT/launches_c5.csv python tools/one_compress.py c5 1 > $OUT/l_c5.log 2>&1
@@ -39,4 +40,8 @@ for c in $CFGS; do
       ;;
   esac
 done
+# summarise on the box and drop the reports (several full captures exceed the
+# 64 MiB that gpurun copies back)
+python tools/summarize_profiles.py gpurun_out/prof_txt
+rm -f $OUT/*.ncu-rep
 echo done
