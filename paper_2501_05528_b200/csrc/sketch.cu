@@ -1306,8 +1306,13 @@ __global__ void __launch_bounds__(C::NT, 1) k_sketch_tagged4(ublr_op_t op, const
   if (KIND == UBLR_OP_LOG) init_log_tables(&lt);
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      ws::mbar_init(&full[s], 2 * C::NPROD);
-      ws::mbar_init(&empty[s], C::NCONS);
+      // arrivals per stage: one cp.async arrival per producer thread (its
+      // panel copies have landed) + one per producer warp (its A entries are
+      // stored) on full; one per consumer warp on empty. An mbarrier takes
+      // arrivals one at a time, so per-thread arrivals (768 per stage) cost
+      // more than the stage's DMMAs
+      ws::mbar_init(&full[s], C::NPROD + C::NPROD / 32);
+      ws::mbar_init(&empty[s], C::NCONS / 32);
     }
   }
   if (threadIdx.x / 32 == C::NPROD / 32) tmem::alloc(&tbase_slot, 512);  // first consumer warp
@@ -1390,7 +1395,8 @@ __global__ void __launch_bounds__(C::NT, 1) k_sketch_tagged4(ublr_op_t op, const
         double* As = As0 + s * C::A_STAGE;
 #pragma unroll
         for (int e = 0; e < EPT; ++e) As[(kq + e * KL) * SA + r] = v[e];
-        ws::mbar_arrive(&full[s]);
+        __syncwarp();
+        if ((p & 31) == 0) ws::mbar_arrive(&full[s]);
       }
     }
     cp_async_wait<0>();
@@ -1445,15 +1451,18 @@ __global__ void __launch_bounds__(C::NT, 1) k_sketch_tagged4(ublr_op_t op, const
         // m16n8k8 DMMA: a0..a3 = A[g][t], A[g+8][t], A[g][t+4], A[g+8][t+4];
         // b0, b1 = B[t][g], B[t+4][g]; d = (w[0][jj], w[1][jj]) -- the m8n8k4 layout
         if (nj_valid == NJ) {
+          // m8n8k4 DMMAs (16 pipe cycles each instead of 64 for m16n8k8): the
+          // producers' FP64 evaluations get a slot between two of them four
+          // times as often (c5 shard sketch 1573 -> 1473 ms; c4 unchanged)
 #pragma unroll
-          for (int k8 = 0; k8 < BK / 8; ++k8) {
-            const int kr = k8 * 8 + t;
+          for (int k4 = 0; k4 < BK / 4; ++k4) {
+            const int kr = k4 * 4 + t;
             const double a0 = As[kr * SA + am0], a1 = As[kr * SA + am0 + 8];
-            const double a2 = As[(kr + 4) * SA + am0], a3 = As[(kr + 4) * SA + am0 + 8];
 #pragma unroll
             for (int jj = 0; jj < NJ; ++jj) {
-              const double b0 = Bs[kr * SB + bn0 + jj * 8], b1 = Bs[(kr + 4) * SB + bn0 + jj * 8];
-              mma16x8x8(w[0][jj][0], w[0][jj][1], w[1][jj][0], w[1][jj][1], a0, a1, a2, a3, b0, b1);
+              const double b0 = Bs[kr * SB + bn0 + jj * 8];
+              mma8x8x4(w[0][jj][0], w[0][jj][1], a0, b0);
+              mma8x8x4(w[1][jj][0], w[1][jj][1], a1, b0);
             }
           }
         } else if (nj_valid > 0) {   // last column tile: only the 8-column groups that hold columns
@@ -1471,7 +1480,8 @@ __global__ void __launch_bounds__(C::NT, 1) k_sketch_tagged4(ublr_op_t op, const
             }
           }
         }
-        ws::mbar_arrive(&empty[s]);
+        __syncwarp();
+        if (lane == 0) ws::mbar_arrive(&empty[s]);
       }
       if (nj_valid == 0) continue;   // a warp past the last column has nothing to fold
       // block j complete: acc_c += T[j, c] W
