@@ -191,7 +191,23 @@ __global__ void __launch_bounds__(Cfg::NT + NPROD, 1) k_gemm3(int M, int N, int 
   constexpr int STAGES = Cfg::STAGES, BK = Cfg::BK, NCONS = Cfg::NT;
   extern __shared__ double dsm[];
   __shared__ uint64_t full[STAGES], empty[STAGES];
-  if (upper_only && (int)(blockIdx.x + 1) * Cfg::BN <= (int)blockIdx.y * Cfg::BM) return;
+  // CTAs are dispatched in launch order (x fastest), so a wave of 148 CTAs on
+  // the natural (column tile, row tile) grid is a 148 / nx x nx slab that
+  // streams nx column tiles of B for a few row tiles of A. Column tiles are
+  // taken in groups of RASTER_GW instead, rows fastest inside a group: a wave
+  // is then a ~12 x 12 block of tiles and reads 24 operand strips from DRAM
+  // instead of nx + 148 / nx (the c3 strip GEMM, nx = 37: 41).
+  constexpr int RASTER_GW = 12;
+  int tile_n = blockIdx.x, tile_m = blockIdx.y;
+  if ((int)gridDim.x > RASTER_GW && (int)gridDim.y > 1) {
+    const int nx = gridDim.x, ny = gridDim.y;
+    const int lin = blockIdx.y * nx + blockIdx.x;
+    const int grp = lin / (RASTER_GW * ny), rem = lin - grp * (RASTER_GW * ny);
+    const int gw = min(RASTER_GW, nx - grp * RASTER_GW);
+    tile_m = rem / gw;
+    tile_n = grp * RASTER_GW + rem - tile_m * gw;
+  }
+  if (upper_only && (tile_n + 1) * Cfg::BN <= tile_m * Cfg::BM) return;
   const int bz = blockIdx.z;
   A += bz * sA;
   B += bz * sB;
@@ -199,7 +215,7 @@ __global__ void __launch_bounds__(Cfg::NT + NPROD, 1) k_gemm3(int M, int N, int 
   if (amap) amap += bz * sAm;
   if (bmap) bmap += bz * sBm;
   if (cmap) cmap += bz * sCm;
-  const int m0 = blockIdx.y * Cfg::BM, n0 = blockIdx.x * Cfg::BN;
+  const int m0 = tile_m * Cfg::BM, n0 = tile_n * Cfg::BN;
   const int nk = (K + BK - 1) / BK;
   double* As0 = dsm;
   double* Bs0 = dsm + STAGES * Cfg::A_STAGE;
