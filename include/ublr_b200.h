@@ -149,6 +149,20 @@ int ublr_sketch_tagged_comp(const ublr_op_t* op, const int32_t* off, int b, cons
                             const double* G, const double* H, int64_t ld_x, int gc,
                             double* Y, double* Z, int64_t ld_y, int row_begin, int row_end, void* stream);
 
+/* The tagged sketch through a staged strip of A (kernel operators; n and
+ * every off[j] even): rows [r0, r0 + R) of A are evaluated once into
+ * `workspace` and the sketch kernel's producers only copy tiles, so no FP64
+ * evaluation shares the pipe with the DMMAs and A is evaluated once per strip
+ * instead of once per 128-column tile. R = ublr_sketch_tagged_staged_rows(n,
+ * columns (gc, or 2 gc with H), rows, workspace_bytes); 0 means no strip of
+ * that size fills the SMs -- use the entry points above. `compensated` as
+ * ublr_sketch_tagged_comp. Same products as the fused entry points. */
+int ublr_sketch_tagged_staged_rows(int64_t n, int ncols, int rows, int64_t workspace_bytes);
+int ublr_sketch_tagged_staged(const ublr_op_t* op, const int32_t* off, int b, const double* T, int ell,
+                              const double* G, const double* H, int64_t ld_x, int gc,
+                              double* Y, double* Z, int64_t ld_y, int row_begin, int row_end,
+                              int compensated, void* workspace, int64_t workspace_bytes, void* stream);
+
 /* Generic operator apply (ref/operators.py:48-52 and every op.apply call of
  * the pipeline): out (N x w, permuted rows, ld_o) = A X (N x w, ld_x). */
 int ublr_apply(const ublr_op_t* op, const double* X, int64_t ld_x, int w, double* out, int64_t ld_o,

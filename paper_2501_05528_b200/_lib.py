@@ -52,6 +52,9 @@ SIGNATURES = {
     "ublr_sketch_tagged": (INT, [C.POINTER(OpDesc), P, INT, P, INT, P, I64, INT, P, I64, INT, INT, P]),
     "ublr_sketch_tagged_pair": (INT, [C.POINTER(OpDesc), P, INT, P, INT, P, P, I64, INT, P, P, I64, INT, INT, P]),
     "ublr_sketch_tagged_comp": (INT, [C.POINTER(OpDesc), P, INT, P, INT, P, P, I64, INT, P, P, I64, INT, INT, P]),
+    "ublr_sketch_tagged_staged": (INT, [C.POINTER(OpDesc), P, INT, P, INT, P, P, I64, INT, P, P, I64, INT, INT, INT,
+                                        P, I64, P]),
+    "ublr_sketch_tagged_staged_rows": (INT, [I64, INT, INT, I64]),
     "ublr_sketch_tagged_two": (INT, [C.POINTER(OpDesc), C.POINTER(OpDesc), P, INT, P, INT, P, P, I64, INT, P, P, I64,
                                      INT, INT, P]),
     "ublr_apply": (INT, [C.POINTER(OpDesc), P, I64, INT, P, I64, P]),
@@ -144,6 +147,10 @@ def rng_launches(counts) -> int:
 
 
 def _launches_of(name, args):
+    if name == "ublr_sketch_tagged_staged":   # one evaluation + one sketch launch per strip of rows
+        n, gc, r0, r1, nbytes = int(args[0].n), int(args[8]), int(args[12]), int(args[13]), int(args[16])
+        rows = int(load().ublr_sketch_tagged_staged_rows(n, (2 if args[6] else 1) * gc, r1 - r0, nbytes))
+        return 2 * -(-(r1 - r0) // rows) if rows >= 32 else 2
     if name == "ublr_apply_staged":   # one evaluation + one GEMM launch per strip of rows
         n, w, nbytes = int(args[0].n), int(args[3]), int(args[7])
         rows = max(128, int(load().ublr_apply_staged_rows(n, w, nbytes)))
@@ -193,7 +200,8 @@ def _work_of(name, args):
             n, b, ell, gc = args[0].n, int(args[3]), int(args[5]), int(args[9])
             r0, r1 = int(args[13]), int(args[14])
             return 2 * (2.0 * (r1 - r0) * n * gc + 2.0 * (r1 - r0) * b * gc * ell)
-        if name in ("ublr_sketch_tagged", "ublr_sketch_tagged_pair", "ublr_sketch_tagged_comp"):
+        if name in ("ublr_sketch_tagged", "ublr_sketch_tagged_pair", "ublr_sketch_tagged_comp",
+                    "ublr_sketch_tagged_staged"):
             pair = not name.endswith("tagged")
             n, b, ell = args[0].n, int(args[2]), int(args[4])
             gc = int(args[8] if pair else args[7])

@@ -8,6 +8,8 @@ lazily, only when a caller asks for them.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from . import _lib
@@ -212,6 +214,38 @@ def draw_test_pair(dt, stream: RandomStream, cols: int, tag_stream: RandomStream
     return TestPair(buf, dt.n, cols, dt.b, tag_cols)
 
 
+STAGED_SKETCH_MIN_ROWS = 16384   # below, one fused launch beats per-strip launches
+
+
+def staged_sketch_workspace(inner, dt, gc, nrows, ell):
+    """(tensor, bytes) for ublr_sketch_tagged_staged, or None when the fused
+    entry points should be used: symmetric kernel operators with even n and
+    even block offsets (16-byte aligned A chunks), ell <= 10, and a strip that
+    fills the SMs within a third of the free memory (capped at 4 GB unless a
+    single column tile needs a whole wave of row tiles, as a c5 shard does)."""
+    torch = _torch()
+    if os.environ.get("UBLR_SKETCH_STAGED", "1") == "0":
+        return None
+    if getattr(inner, "kind", None) not in ("log", "inv") or not getattr(inner, "symmetric", False):
+        return None
+    if ell > 10 or dt.n % 2 or gc % 2 or nrows < STAGED_SKETCH_MIN_ROWS or (dt.off_h % 2).any():
+        return None
+    lib = _lib.load()
+    free, _ = torch.cuda.mem_get_info(dt.device)
+    ncols = 2 * gc
+    ct = -(-ncols // (64 if ncols <= 64 else 128))
+    if ct < 2:
+        # one column tile (a c5 shard: 128 columns): every entry of A is used
+        # once, and writing + reading the strip costs more HBM time than the
+        # evaluation inside the kernel does (measured 1,771 against 1,448 ms)
+        return None
+    want = max(4 << 30, -(-148 // ct) * 32 * dt.n * 8)
+    nbytes = min(want, free // 3) // 16 * 16
+    if int(lib.ublr_sketch_tagged_staged_rows(dt.n, ncols, nrows, nbytes)) < 32:
+        return None
+    return torch.empty(nbytes // 8, dtype=torch.float64, device=dt.device), nbytes
+
+
 def tagged_sketch(op, dt, T_dev, T_entries, G, H, gc, out=None, ell=None, compensated=False):
     """Y = A Omega, Z = A^* Psi for the tagged test matrices; returns (Y, Z)
     (into `out` = (Y, Z) when given). T_entries (host) is needed only by a
@@ -229,7 +263,12 @@ def tagged_sketch(op, dt, T_dev, T_entries, G, H, gc, out=None, ell=None, compen
         else:
             Y = torch.empty((dt.n, s), dtype=torch.float64, device=dt.device)
             Z = torch.empty((dt.n, s), dtype=torch.float64, device=dt.device)
-        if compensated and ell <= 10:
+        staged = staged_sketch_workspace(inner, dt, gc, dt.n, ell)
+        if staged is not None:
+            _lib.call("ublr_sketch_tagged_staged", inner.device_op(dt.perm), _lib.ptr(dt.off), dt.b, _lib.ptr(T_dev),
+                      ell, _lib.ptr(G), _lib.ptr(H), gc, gc, _lib.ptr(Y), _lib.ptr(Z), s, 0, dt.n,
+                      1 if compensated else 0, _lib.ptr(staged[0]), staged[1], stream)
+        elif compensated and ell <= 10:
             if getattr(inner, "symmetric", False):
                 _lib.call("ublr_sketch_tagged_comp", inner.device_op(dt.perm), _lib.ptr(dt.off), dt.b,
                           _lib.ptr(T_dev), ell, _lib.ptr(G), _lib.ptr(H), gc, gc, _lib.ptr(Y), _lib.ptr(Z), s, 0, dt.n,

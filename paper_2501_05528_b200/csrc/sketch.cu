@@ -1250,7 +1250,8 @@ struct Sk4Cfg {
   static constexpr int NPROD = 256, NCONS = 256, NT = NPROD + NCONS;
   static constexpr int WMW = 2, WNW = 4, WM = BM / WMW, WN = BN / WNW, MI = WM / 8, NJ = WN / 8;
   static constexpr int SA = BM + 4, SB = BN + 4;
-  static constexpr int A_STAGE = BK * SA, B_STAGE = BK * SB;
+  static constexpr int SAM = BK + 4;   // STAGED: the A stage is copied m-major (As[m][k], as its source is stored)
+  static constexpr int A_STAGE = BK * SA > BM * SAM ? BK * SA : BM * SAM, B_STAGE = BK * SB;
   static constexpr int CONS_REGS = 200, PROD_REGS = 56;
   static constexpr size_t smem_bytes() { return (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double); }
   // compensated fold: 16 bytes (8 bf16 error sums) per consumer thread and 8-entry chunk of each tag group
@@ -1277,13 +1278,22 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return r;
 }
 
-template <int KIND, int DIM, int L, class C, bool COMP = false>
+// STAGED: the rows [strip_r0, ...) of A have been evaluated into `strip`
+// (row-major, ld = n) by k_gen_strip, and the producers only copy: A tiles
+// with 16-byte cp.async into an m-major stage, next to the panel. No FP64
+// work competes with the DMMAs (the evaluation inside the kernel holds the
+// DMMA pipe at 43-57 %: the consumers own the pipe while they have a stage,
+// the producers' chains advance when they wait), and A is evaluated once per
+// strip instead of once per column tile. Needs n and every off[j] even.
+template <int KIND, int DIM, int L, class C, bool COMP = false, bool STAGED = false>
 __global__ void __launch_bounds__(C::NT, 1) k_sketch_tagged4(ublr_op_t op, const int32_t* __restrict__ off, int b,
                                                              const double* __restrict__ T, int ell,
                                                              const double* __restrict__ G,
                                                              const double* __restrict__ H, int64_t ldx, int gc,
                                                              double* __restrict__ Y, double* __restrict__ Z,
-                                                             int64_t ldy, int row_begin, int row_end) {
+                                                             int64_t ldy, int row_begin, int row_end,
+                                                             const double* __restrict__ strip = nullptr,
+                                                             int strip_r0 = 0) {
   constexpr int BM = C::BM, BN = C::BN, BK = C::BK, STAGES = C::STAGES, SA = C::SA, SB = C::SB;
   constexpr int MI = C::MI, NJ = C::NJ;
   constexpr int WD = MI * NJ * 2;                       // W doubles per consumer thread
@@ -1303,7 +1313,7 @@ __global__ void __launch_bounds__(C::NT, 1) k_sketch_tagged4(ublr_op_t op, const
   const int row0 = row_begin + blockIdx.x * BM;
   const int col0 = blockIdx.y * BN;
   const int n = (int)op.n;
-  if (KIND == UBLR_OP_LOG) init_log_tables(&lt);
+  if (KIND == UBLR_OP_LOG && !STAGED) init_log_tables(&lt);
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       // arrivals per stage: one cp.async arrival per producer thread (its
@@ -1347,6 +1357,41 @@ __global__ void __launch_bounds__(C::NT, 1) k_sketch_tagged4(ublr_op_t op, const
       bmeta[z] = (kk * SB + c) | (kk << 16) | (valid ? (1 << 30) : 0);
     }
     int it = 0;
+    if (STAGED) {
+      // copy-only producers: thread p moves the 16-byte pair (row p / 8, k pair p % 8) of the A tile
+      static_assert(!STAGED || (C::NPROD == BM * BK / 2), "one 16-byte A chunk per producer thread");
+      const int pr = p >> 3, pk2 = (p & 7) * 2;
+      const int prow = row0 + pr < row_end ? row0 + pr : row_begin;      // rows past the end: any valid row
+      const double* arow = strip + (int64_t)(prow - strip_r0) * n;
+      for (int j = 0; j < b; ++j) {
+        const int qe = off[j + 1];
+        for (int q0 = off[j]; q0 < qe; q0 += BK, ++it) {
+          const int s = it % STAGES;
+          ws::mbar_wait(&empty[s], ((uint32_t)(it / STAGES) & 1) ^ 1);
+          double* Bs = Bs0 + s * C::B_STAGE;
+          const int64_t roff = (int64_t)q0 * ldx;
+#pragma unroll
+          for (int z = 0; z < PPT; ++z) {
+            const int meta = bmeta[z];
+            const bool ok = (meta >> 30) && q0 + ((meta >> 16) & 0x3fff) < qe;
+            cp_async16(Bs + (meta & 0xffff), ok ? (const void*)(bsrc[z] + roff) : (const void*)G, ok);
+          }
+          double* Ad = As0 + s * C::A_STAGE + pr * C::SAM + pk2;
+          const int k = q0 + pk2;
+          if (k + 1 < qe) {
+            cp_async16(Ad, arow + k, true);
+          } else {                       // the k dimension ends inside this pair: zeros past the end
+            cp_async8(Ad, k < qe ? (const void*)(arow + k) : (const void*)strip, k < qe);
+            cp_async8(Ad + 1, strip, false);
+          }
+          cp_async_commit();
+          ws::mbar_cp_async_arrive(&full[s]);
+          __syncwarp();
+          if ((p & 31) == 0) ws::mbar_arrive(&full[s]);
+        }
+      }
+      cp_async_wait<0>();
+    } else {
     // column coordinates are loaded one stage ahead (software pipelining: the
     // global-load latency of stage it + 1 hides behind the evaluations of it)
     double cn[EPT][DIM];
@@ -1400,6 +1445,7 @@ __global__ void __launch_bounds__(C::NT, 1) k_sketch_tagged4(ublr_op_t op, const
       }
     }
     cp_async_wait<0>();
+    }
   } else {
     // ---------------- consumers
     ws::regs_inc<C::CONS_REGS>();
@@ -1457,7 +1503,8 @@ __global__ void __launch_bounds__(C::NT, 1) k_sketch_tagged4(ublr_op_t op, const
 #pragma unroll
           for (int k4 = 0; k4 < BK / 4; ++k4) {
             const int kr = k4 * 4 + t;
-            const double a0 = As[kr * SA + am0], a1 = As[kr * SA + am0 + 8];
+            const double a0 = STAGED ? As[am0 * C::SAM + kr] : As[kr * SA + am0];
+            const double a1 = STAGED ? As[(am0 + 8) * C::SAM + kr] : As[kr * SA + am0 + 8];
 #pragma unroll
             for (int jj = 0; jj < NJ; ++jj) {
               const double b0 = Bs[kr * SB + bn0 + jj * 8];
@@ -1469,8 +1516,10 @@ __global__ void __launch_bounds__(C::NT, 1) k_sketch_tagged4(ublr_op_t op, const
 #pragma unroll
           for (int k8 = 0; k8 < BK / 8; ++k8) {
             const int kr = k8 * 8 + t;
-            const double a0 = As[kr * SA + am0], a1 = As[kr * SA + am0 + 8];
-            const double a2 = As[(kr + 4) * SA + am0], a3 = As[(kr + 4) * SA + am0 + 8];
+            const double a0 = STAGED ? As[am0 * C::SAM + kr] : As[kr * SA + am0];
+            const double a1 = STAGED ? As[(am0 + 8) * C::SAM + kr] : As[kr * SA + am0 + 8];
+            const double a2 = STAGED ? As[am0 * C::SAM + kr + 4] : As[(kr + 4) * SA + am0];
+            const double a3 = STAGED ? As[(am0 + 8) * C::SAM + kr + 4] : As[(kr + 4) * SA + am0 + 8];
 #pragma unroll
             for (int jj = 0; jj < NJ; ++jj) {
               if (jj < nj_valid) {
@@ -1871,6 +1920,66 @@ int sketch_common_v4(const ublr_op_t* op, const int32_t* off, int b, const doubl
   return UBLR_OK;
 }
 
+// Rows per strip of the staged tagged sketch: a multiple of the 32-row tile
+// such that rt x ct CTAs (ct column tiles) fill whole waves of the SMs; 0 if
+// no strip within `max_bytes` reaches 85 % of its last wave (a c5 shard has one
+// column tile: 148 row tiles = 4,736 rows = 40 GB of strip at N = 2^20).
+inline int sketch_strip_rows(int64_t n, int ncols, int64_t rows_total, int64_t max_bytes, int sms,
+                             bool require_eff = true) {
+  const int64_t ct = (ncols + (ncols <= 64 ? 63 : 127)) / (ncols <= 64 ? 64 : 128);
+  int64_t cap = max_bytes / (32 * n * 8);
+  if (cap > (rows_total + 31) / 32) cap = (rows_total + 31) / 32;
+  int best = 0;
+  double best_eff = 0.0;
+  for (int64_t rt = 1; rt <= cap; ++rt) {
+    const int64_t ctas = rt * ct, waves = (ctas + sms - 1) / sms;
+    const double eff = (double)ctas / (double)(waves * sms);
+    if (eff >= best_eff - 0.004) {
+      best = (int)rt;
+      if (eff > best_eff) best_eff = eff;
+    }
+  }
+  if (!require_eff) return best * 32;                                            // the entry point runs with any strip
+  if (cap >= (rows_total + 31) / 32 && best_eff < 0.85) return (int)cap * 32;   // the whole range fits: one strip
+  return best_eff >= 0.85 ? best * 32 : 0;
+}
+
+int sketch_staged(const ublr_op_t* op, const int32_t* off, int b, const double* T, int ell, const double* G,
+                  const double* H, int64_t ld_x, int gc, double* Y, double* Z, int64_t ld_y, int row_begin,
+                  int row_end, bool comp, double* strip, int R, cudaStream_t st) {
+  const int ncols = (H ? 2 : 1) * gc;
+  const int64_t n = op->n;
+  for (int r0 = row_begin; r0 < row_end; r0 += R) {
+    const int r1 = r0 + R < row_end ? r0 + R : row_end;
+    dim3 ggrid((unsigned)((n + 255) / 256), (unsigned)((r1 - r0 + 15) / 16));
+#define UBLR_GEN(KIND, DIM) k_gen_strip<KIND, DIM><<<ggrid, 256, 0, st>>>(*op, r0, r1 - r0, strip)
+    if (op->kind == UBLR_OP_LOG) {
+      if (op->dim == 1) UBLR_GEN(UBLR_OP_LOG, 1); else if (op->dim == 2) UBLR_GEN(UBLR_OP_LOG, 2); else UBLR_GEN(UBLR_OP_LOG, 3);
+    } else {
+      if (op->dim == 1) UBLR_GEN(UBLR_OP_INV, 1); else if (op->dim == 2) UBLR_GEN(UBLR_OP_INV, 2); else UBLR_GEN(UBLR_OP_INV, 3);
+    }
+#undef UBLR_GEN
+    UBLR_LAUNCH_CHECK();
+    dim3 grid((unsigned)((r1 - r0 + 31) / 32), 0);
+#define UBLR_TS5(L, BNv, COMPv)                                                                                  \
+  {                                                                                                              \
+    using C = Sk4Cfg<BNv, 6>;                                                                                    \
+    grid.y = (unsigned)((ncols + C::BN - 1) / C::BN);                                                            \
+    size_t sm = C::smem_bytes() + ((COMPv) ? C::comp_bytes(10) : 0);                                             \
+    UBLR_CUDA(cudaFuncSetAttribute(k_sketch_tagged4<UBLR_OP_INV, 1, L, C, COMPv, true>,                          \
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));                      \
+    k_sketch_tagged4<UBLR_OP_INV, 1, L, C, COMPv, true><<<grid, C::NT, sm, st>>>(                                \
+        *op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y, r0, r1, strip, r0);                                     \
+  }
+    if (comp) UBLR_TS5(10, 128, true)
+    else if (ncols <= 64) { if (ell <= 4) UBLR_TS5(4, 64, false) else UBLR_TS5(10, 64, false) }
+    else { if (ell <= 4) UBLR_TS5(4, 128, false) else UBLR_TS5(10, 128, false) }
+#undef UBLR_TS5
+    UBLR_LAUNCH_CHECK();
+  }
+  return UBLR_OK;
+}
+
 int sketch_common(const ublr_op_t* op, const int32_t* off, int b, const double* T, int ell, const double* G,
                   const double* H, int64_t ld_x, int gc, double* Y, double* Z, int64_t ld_y, int row_begin,
                   int row_end, cudaStream_t st, bool comp = false) {
@@ -2009,4 +2118,31 @@ extern "C" int ublr_apply_staged(const ublr_op_t* op, const double* X, int64_t l
     if (rc) return rc;
   }
   return UBLR_OK;
+}
+
+// Rows per strip of ublr_sketch_tagged_staged with this workspace (0: no
+// strip of that size keeps the SMs busy -- use the fused entry points).
+extern "C" int ublr_sketch_tagged_staged_rows(int64_t n, int ncols, int rows, int64_t workspace_bytes) {
+  return sketch_strip_rows(n, ncols, rows, workspace_bytes, device_sms());
+}
+
+extern "C" int ublr_sketch_tagged_staged(const ublr_op_t* op, const int32_t* off, int b, const double* T, int ell,
+                                         const double* G, const double* H, int64_t ld_x, int gc, double* Y, double* Z,
+                                         int64_t ld_y, int row_begin, int row_end, int compensated, void* workspace,
+                                         int64_t workspace_bytes, void* stream) {
+  int rc = check_op(op);
+  if (rc) return rc;
+  UBLR_REQUIRE(b > 0 && off && T && G && Y && (!H == !Z) && gc > 0 && ell > 0 && ell <= 10 && ld_x >= gc &&
+                   ld_y >= (int64_t)ell * gc && row_begin >= 0 && row_begin < row_end && row_end <= op->n,
+               UBLR_ERR_VALUE, "ublr_sketch_tagged_staged: bad arguments (ell <= 10)");
+  UBLR_REQUIRE((op->kind == UBLR_OP_LOG || op->kind == UBLR_OP_INV) && op->n % 2 == 0, UBLR_ERR_VALUE,
+               "ublr_sketch_tagged_staged: kernel operators with an even number of points");
+  UBLR_REQUIRE((ld_x % 2) == 0 && (gc % 2) == 0 && ((uintptr_t)G) % 16 == 0 && (!H || ((uintptr_t)H) % 16 == 0) &&
+                   workspace && ((uintptr_t)workspace) % 16 == 0,
+               UBLR_ERR_VALUE, "ublr_sketch_tagged_staged: 16-byte aligned panels and workspace, even gc / ld_x");
+  const int ncols = (H ? 2 : 1) * gc;
+  const int R = sketch_strip_rows(op->n, ncols, row_end - row_begin, workspace_bytes, device_sms(), false);
+  UBLR_REQUIRE(R >= 32, UBLR_ERR_VALUE, "ublr_sketch_tagged_staged: workspace smaller than one 32-row strip");
+  return sketch_staged(op, off, b, T, ell, G, H, ld_x, gc, Y, Z, ld_y, row_begin, row_end, compensated != 0,
+                       (double*)workspace, R, (cudaStream_t)stream);
 }

@@ -25,7 +25,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .bases import _bill, draw_test_pair
+from .bases import _bill, draw_test_pair, staged_sketch_workspace
 from .linalg import RandomStream
 from .operators import counting_wrapper, unwrap
 from .reconstruction import FUSED_NEAR_K_MAX, FUSED_NEAR_M_MAX
@@ -168,8 +168,16 @@ def phase1_local(op, tess, k, p, stream, shard, plan=None, keep_sketch=False):
     Z = _alloc((nloc, s), **f64)
     st = _lib.stream_handle()
     shift = 8 * shard.r0 * s
-    _lib.call("ublr_sketch_tagged_pair", inner.device_op(dt.perm), _lib.ptr(dt.off), dt.b, _lib.ptr(T_dev), ell,
-              _lib.ptr(G), _lib.ptr(H), gc, gc, _lib.ptr(Y) - shift, _lib.ptr(Z) - shift, s, shard.r0, shard.r1, st)
+    staged = staged_sketch_workspace(inner, dt, gc, nloc, ell)
+    if staged is not None:   # A evaluated once per strip of the shard's rows, copy-only sketch producers
+        _lib.call("ublr_sketch_tagged_staged", inner.device_op(dt.perm), _lib.ptr(dt.off), dt.b, _lib.ptr(T_dev), ell,
+                  _lib.ptr(G), _lib.ptr(H), gc, gc, _lib.ptr(Y) - shift, _lib.ptr(Z) - shift, s, shard.r0, shard.r1,
+                  0, _lib.ptr(staged[0]), staged[1], st)
+        del staged
+    else:
+        _lib.call("ublr_sketch_tagged_pair", inner.device_op(dt.perm), _lib.ptr(dt.off), dt.b, _lib.ptr(T_dev), ell,
+                  _lib.ptr(G), _lib.ptr(H), gc, gc, _lib.ptr(Y) - shift, _lib.ptr(Z) - shift, s, shard.r0, shard.r1,
+                  st)
     kq = max(1, min(k, dt.m_max))
     U = _alloc((nloc, k), zero=True, **f64)
     V = _alloc((nloc, k), zero=True, **f64)

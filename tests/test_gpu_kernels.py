@@ -153,6 +153,48 @@ def test_tagged_sketch_matches_oracle(case):
     assert np.linalg.norm(dt.from_perm_rows(Zc) - bundle.z) <= 1e-13 * np.linalg.norm(bundle.z)
 
 
+@pytest.mark.parametrize("kind,comp,rows,gc", [("log", 0, (0, 4096), 20), ("inv", 1, (512, 3100), 64),
+                                                ("log", 1, (0, 4096), 30), ("inv", 0, (1000, 4096), 32)])
+def test_tagged_sketch_staged_matches_fused(kind, comp, rows, gc):
+    """ublr_sketch_tagged_staged (A evaluated once per strip of rows, copy-only
+    producers) against the fused entry points on a row range, with a workspace
+    of a few 32-row tiles (several strips, a ragged last one)."""
+    per, nb = 64, 64
+    coords = O.cell_centres(per, 2)
+    n = len(coords)
+    tess = P.build_tessellation(P.grid_points(per, 2), nb)
+    op = P.KernelOperator(coords, kind, 4.0 if kind == "log" else 128.0)
+    dt = device_tess(tess, torch.device(DEV))
+    plan = P.plan_tagging(tess, 0, "gaussian", P.RandomStream(5).child(1))
+    T = plan.matrix.entries
+    ell = T.shape[1]
+    st = P.RandomStream(5).child(0)
+    G = draw_test_blocks(dt, st, 0, gc)
+    H = draw_test_blocks(dt, st, 1, gc)
+    T_dev = torch.from_numpy(T).to(DEV)
+    s = ell * gc
+    r0, r1 = rows
+    outs = []
+    for staged in (False, True):
+        Y = torch.full((n, s), np.nan, dtype=torch.float64, device=DEV)
+        Z = torch.full((n, s), np.nan, dtype=torch.float64, device=DEV)
+        if staged:
+            nbytes = 10 * 32 * n * 8            # ten row tiles per strip
+            ws = torch.full((nbytes // 8,), np.nan, dtype=torch.float64, device=DEV)
+            _lib.call("ublr_sketch_tagged_staged", op.device_op(dt.perm), _lib.ptr(dt.off), dt.b, _lib.ptr(T_dev), ell,
+                      _lib.ptr(G), _lib.ptr(H), gc, gc, _lib.ptr(Y), _lib.ptr(Z), s, r0, r1, comp, _lib.ptr(ws),
+                      nbytes, _lib.stream_handle())
+        else:
+            _lib.call("ublr_sketch_tagged_comp" if comp else "ublr_sketch_tagged_pair", op.device_op(dt.perm),
+                      _lib.ptr(dt.off), dt.b, _lib.ptr(T_dev), ell, _lib.ptr(G), _lib.ptr(H), gc, gc, _lib.ptr(Y),
+                      _lib.ptr(Z), s, r0, r1, _lib.stream_handle())
+        outs.append((Y.cpu().numpy(), Z.cpu().numpy()))
+    for a, b_ in zip(outs[0], outs[1]):
+        assert np.isnan(a[:r0]).all() and np.isnan(a[r1:]).all() and np.isnan(b_[:r0]).all() and np.isnan(b_[r1:]).all()
+        assert np.isfinite(b_[r0:r1]).all()
+        assert np.linalg.norm(a[r0:r1] - b_[r0:r1]) <= 1e-14 * np.linalg.norm(a[r0:r1])
+
+
 @pytest.mark.parametrize("kind", ["log", "dense"])
 def test_tagged_sketch_compensated_fold_is_more_accurate(kind):
     """Against an 80-bit (numpy longdouble) evaluation of Y = A Omega on a
