@@ -404,9 +404,31 @@ def run_sharded(args, rank, world, local):
         res = step(op)
         parts = tuple(x for x in (res.U, res.core, res.B) if x.is_cuda)   # a host-sink core is already on the host
         if host is None:
-            host = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in parts]
-        for h, x in zip(host, parts):
-            h.copy_(x, non_blocking=True)
+            import psutil
+            need = sum(x.numel() * 8 for x in parts)
+            share = psutil.virtual_memory().available // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
+            if need < share - 16 * 2 ** 30:
+                host = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in parts]
+            else:   # the rank's result does not fit in its share of host memory: through two pinned 1 GiB slots
+                host = "ring"
+                ring = [torch.empty(2 ** 27, dtype=torch.float64, pin_memory=True) for _ in range(2)]
+                ring_ev = [None, None]
+        if host == "ring":
+            nslot = 0
+            for x in parts:
+                flat = x.reshape(-1)
+                for o in range(0, flat.numel(), 2 ** 27):
+                    sl = nslot % 2
+                    if ring_ev[sl] is not None:
+                        ring_ev[sl].synchronize()
+                    chunk = flat[o:o + 2 ** 27]
+                    ring[sl][:chunk.numel()].copy_(chunk, non_blocking=True)
+                    ring_ev[sl] = torch.cuda.Event()
+                    ring_ev[sl].record()
+                    nslot += 1
+        else:
+            for h, x in zip(host, parts):
+                h.copy_(x, non_blocking=True)
         torch.cuda.synchronize()
         d2h = sum(x.numel() * 8 for x in (res.U, res.core, res.B))
         res = parts = None
