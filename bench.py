@@ -286,7 +286,8 @@ def roofline_of(ev, work, config, operator):
         if tj.get("entry") == name:
             traffic = tj.get("dram_bytes_per_launch")
     n_launch = len(ev[name])
-    return {"kernel": kernel_label(name, operator), "entry": name, "bound": "fp64", "achieved": achieved,
+    return {"kernel": kernel_label(name, operator), "entry": name, "bound": "tensor", "pipe": "fp64 DMMA (mma.sync m8n8k4.f64)",
+            "achieved": achieved,
             "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
             "peak_source": "measured DMMA m8n8k4 burst (profiles/fp64_peak_r02.txt); MEASURED_PEAKS.json has no "
                            "fp64 entry",
